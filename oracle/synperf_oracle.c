@@ -1,0 +1,644 @@
+/*
+ * oracle/synperf_oracle.c -- plain, slow, fp64 CPU oracle of SynPerf's batched
+ * prediction hot path (arXiv 2601.14910, "SynPerf").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / `--impl reference` legs may load this library.
+ * The product path (paper_2601_14910_b200/) never imports, links or executes
+ * it, and this file shares no code, header, table or constant generator with
+ * the CUDA path: the two meet only at their inputs (workloads/).
+ *
+ * What it computes, per (kernel config X, GPU spec S) pair, step by step in the
+ * paper's order (PAPER.md line numbers "P:n"; readings R1..R22 of SURVEY.md
+ * §8(c), restated in DESIGN.md):
+ *   O1 Kernel Decomposer F, Eq.1: enumerate every task tau_i in the
+ *      kernel's natural order with its per-pipe op counts (Eq.3, P:335-338;
+ *      element-wise counts) and its load bytes B_i.
+ *   O2 Occupancy ("registers, shared memory, warp-slots") and waves
+ *      ceil(T / (N_SM * occ)).
+ *   O3 Scheduling Simulator M, Eq.2: hardware round-robin, task t
+ *      dealt to SM (t mod N_SM) (R5), accumulated into explicit per-SM arrays.
+ *   O4 GPU totals: summed over the task list itself, independently of the
+ *      per-SM arrays, so conservation (sum_j S_j = total) is a real check.
+ *   O5 Max-SM: max_j S_j per quantity independently (R7).
+ *   O6 Theoretical cycles, Eq.4 and Eq.5; memory cycles
+ *      C_mem = B / BW_mem at GPU level (global, L2) and SM level
+ *      (global, L2 per-SM shares BW/N_SM (R8), shared memory).
+ *   O7 t_theory = max over the GPU-level roofs present / f (R9).
+ *   O8-O11 Performance Estimator: Table IV vector in frozen
+ *      order, log1p z-score normalisation (R17), MLP 256-128-64 with
+ *      Linear -> ReLU -> BatchNorm (eval) -> Dropout(identity) (R18, unfused),
+ *      sigmoid efficiency, latency = t_theory / efficiency.
+ *
+ * All floating point is fp64, no fast-math, no reassociation beyond what the
+ * formulas state.  Integers are int64.  Nothing is blocked, fused or reordered.
+ *
+ * Parity pins for every function live in tests/test_oracle_pins.py; the one
+ * function without an independent pin is the MLP's *realism* (no trained
+ * weights exist) -- "parity unpinned" for realism, see DESIGN.md.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---------------- input formats (defined by workloads/, documented in include/synperf.h) */
+
+enum { FAM_GEMM = 0, FAM_ATTENTION = 1, FAM_MOE = 2, FAM_RMSNORM = 3, FAM_SILU = 4 };
+enum { DT_BF16 = 0, DT_FP16 = 1, DT_FP32 = 2, DT_FP8 = 3 };
+
+/* per-pair status codes (include/synperf.h sp_pair_status) */
+enum {
+  ST_OK = 0, ST_DIM = 1, ST_TILE = 2, ST_HEADS = 3, ST_HIST = 4,
+  ST_CAUSAL = 5, ST_RES = 6, ST_DTYPE = 7, ST_RANGE = 8
+};
+
+/* field order of each family (workloads/gen.py FIELDS) */
+enum { G_M, G_N, G_K, G_TM, G_TN, G_BK, G_STAGES, G_WARPS, G_REGS, G_SMEM, G_DTYPE };
+enum { A_BS, A_NH, A_NKV, A_HD, A_BQ, A_BKV, A_CHUNK, A_CAUSAL, A_WARPS, A_REGS, A_SMEM, A_DTYPE };
+enum { E_M, E_E, E_TOPK, E_H, E_N, E_BM, E_BN, E_BK, E_GROUPM, E_STAGES, E_WARPS, E_REGS, E_SMEM, E_DTYPE };
+enum { R_SEQ, R_DIM, R_WARPS, R_REGS, R_SMEM, R_DTYPE };
+
+/* Table II record, byte layout of workloads/specs.py SPEC_DTYPE (112 B) */
+typedef struct {
+  char name[32];
+  int32_t cc_major, cc_minor, num_sms;
+  int32_t th_tensor_bf16, th_tensor_fp16, th_tensor_fp8, th_fma, th_xu;
+  int32_t smem_bw_bytes_per_clk, smem_per_sm_bytes, regfile_per_sm_bytes;
+  int32_t max_warps_per_sm, max_ctas_per_sm, pad_;
+  double sm_clock_mhz, bw_global_gbps, bw_l2_gbps;
+} orc_spec;
+
+/* oracle flags */
+#define ORC_CLAMPED 1 /* SPEC's clamped edge tiles (R2 alternative), oracle-only */
+
+/* output slots (SURVEY §8 uniform record) */
+enum { I_NTASKS, I_OCC, I_WAVES, I_TOT_T, I_TOT_F, I_TOT_X, I_MAX_T, I_MAX_F, I_MAX_X,
+       I_BYTES, I_BYTES_MAX, N_I };
+enum { F_CG_T, F_CG_F, F_CG_X, F_CS_T, F_CS_F, F_CS_X, F_GLOB_G, F_L2_G, F_GLOB_S, F_L2_S,
+       F_SMEM_S, F_TTHEORY, N_F };
+
+#define INT32_LIM 2147483647LL
+#define UINT32_LIM 4294967295LL
+
+static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+static int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+static int bytes_per_elem(int dtype) {
+  switch (dtype) {
+    case DT_BF16: case DT_FP16: return 2;
+    case DT_FP32: return 4;
+    default: return 0;
+  }
+}
+
+/* ---------------- O3/O4 accumulation state for one pair ---------------- */
+
+/* quantity index: 0 = Tensor ops, 1 = FMA ops, 2 = XU ops, 3 = load bytes */
+typedef struct {
+  int64_t n_sm;
+  int64_t t;          /* tasks enumerated so far (= next task index) */
+  int64_t *sm_sum;    /* [n_sm][4] explicit per-SM sums  S_j(X) */
+  int64_t *sm_count;  /* [n_sm] tasks per SM */
+  int64_t total[4];   /* sum over the task list */
+} orc_sched;
+
+/* One task tau_t with demands d[4]: Eq.2 cyclic dealing (R5) + O4 totals. */
+static void emit_task(orc_sched *s, int64_t ops_t, int64_t ops_f, int64_t ops_x, int64_t bytes) {
+  int64_t d[4] = {ops_t, ops_f, ops_x, bytes};
+  int64_t j = s->t % s->n_sm; /* M: task t -> SM (t mod N_SM) */
+  for (int q = 0; q < 4; ++q) {
+    s->sm_sum[j * 4 + q] += d[q];
+    s->total[q] += d[q];
+  }
+  s->sm_count[j] += 1;
+  s->t += 1;
+}
+
+/* ---------------- O1 decomposers (Eq.1, one per family) ---------------- */
+
+/* GEMM (Table V; Eq.3 alpha = 2): output tiles row-major,
+ * i over ceil(M/tm) outer, j over ceil(N/tn) inner (R4).  Padded (R2): every
+ * tile is a full tm x tn x K_pad MMA with K_pad = ceil(K/BK)*BK (R1);
+ * loads = (tm + tn) * K_pad elements (A and B panels). */
+static void decompose_gemm(const int64_t *x, int flags, orc_sched *s) {
+  int64_t M = x[G_M], N = x[G_N], K = x[G_K], tm = x[G_TM], tn = x[G_TN], bk = x[G_BK];
+  int64_t bpe = bytes_per_elem((int)x[G_DTYPE]);
+  int64_t kpad = cdiv(K, bk) * bk;
+  for (int64_t i = 0; i < cdiv(M, tm); ++i) {
+    for (int64_t j = 0; j < cdiv(N, tn); ++j) {
+      if (flags & ORC_CLAMPED) {
+        int64_t ma = imin(tm, M - i * tm), na = imin(tn, N - j * tn);
+        emit_task(s, 2 * ma * na * K, 0, 0, (ma + na) * K * bpe);
+      } else {
+        emit_task(s, 2 * tm * tn * kpad, 0, 0, (tm + tn) * kpad * bpe);
+      }
+    }
+  }
+}
+
+/* Fused MoE (Table V; §V-B; R16): expert e receives t_e
+ * tokens (histogram, or balanced q + [e < r]); tasks are expert-major, then
+ * m-block over ceil(t_e/BM), then n-block over ceil(N/BN); each task is a
+ * padded BM x BN x H_pad GEMM tile, H_pad = ceil(H/BK)*BK. */
+static void decompose_moe(const int64_t *x, const int32_t *hist, int flags, orc_sched *s) {
+  int64_t M = x[E_M], E = x[E_E], topk = x[E_TOPK], H = x[E_H], N = x[E_N];
+  int64_t bm = x[E_BM], bn = x[E_BN], bk = x[E_BK];
+  int64_t bpe = bytes_per_elem((int)x[E_DTYPE]);
+  int64_t hpad = cdiv(H, bk) * bk;
+  int64_t q = (M * topk) / E, r = (M * topk) % E;
+  for (int64_t e = 0; e < E; ++e) {
+    int64_t te = hist ? (int64_t)hist[e] : q + (e < r ? 1 : 0);
+    for (int64_t mb = 0; mb < cdiv(te, bm); ++mb) {
+      for (int64_t nb = 0; nb < cdiv(N, bn); ++nb) {
+        if (flags & ORC_CLAMPED) {
+          int64_t ma = imin(bm, te - mb * bm), na = imin(bn, N - nb * bn);
+          emit_task(s, 2 * ma * na * H, 0, 0, (ma + na) * H * bpe);
+        } else {
+          emit_task(s, 2 * bm * bn * hpad, 0, 0, (bm + bn) * hpad * bpe);
+        }
+      }
+    }
+  }
+}
+
+/* RMSNorm (Table V, FMA+XU; R14): one task per row; per row
+ * FMA = 3*dim (square-accumulate, scale, weight multiply), XU = 1 (rsqrt,
+ * Table III), loads = input row + weight vector = 2*dim elements. */
+static void decompose_rmsnorm(const int64_t *x, orc_sched *s) {
+  int64_t seq = x[R_SEQ], dim = x[R_DIM], bpe = bytes_per_elem((int)x[R_DTYPE]);
+  for (int64_t row = 0; row < seq; ++row) emit_task(s, 0, 3 * dim, 1, 2 * dim * bpe);
+}
+
+/* SiLU&Mul (Table V, FMA+XU; R15): one task per row; dim = output
+ * width; per element FMA 4, XU 2 (ex2 + rcp, Table III); loads = gate +
+ * up halves = 2*dim elements. */
+static void decompose_silu(const int64_t *x, orc_sched *s) {
+  int64_t seq = x[R_SEQ], dim = x[R_DIM], bpe = bytes_per_elem((int)x[R_DTYPE]);
+  for (int64_t row = 0; row < seq; ++row) emit_task(s, 0, 4 * dim, 2 * dim, 2 * dim * bpe);
+}
+
+/* Attention, FlashInfer FA2 (Table V; Eq.3 alpha = 4; P:262
+ * causal non-uniform tasks; R10-R13).  GQA group g = nh/nkv; request b has
+ * R_b = qlen_b * g packed query rows and nqb_b = ceil(R_b/BQ) q-blocks; task
+ * order: kv-head h outermost, then request b, q-block i, kv-chunk c (R4).
+ * For q-block i the last query token is q_last = floor((min((i+1)BQ, R_b)-1)/g);
+ * causal: kv_need = min(kvlen, kvlen - qlen + q_last + 1), else kv_need = kvlen;
+ * split-KV (R12): n_ch = ceil(kv_need/kv_chunk) chunks of
+ * len_c = min(kv_chunk, kv_need - c*kv_chunk) (kv_chunk = 0: one chunk);
+ * kv_eff = ceil(len_c/BKV)*BKV.  Per task: Tensor 4*BQ*kv_eff*hd; XU = one exp2
+ * per score + one rescale exp2 per row per KV block = BQ*kv_eff + BQ*kv_eff/BKV;
+ * loads = Q tile + K and V tiles = (BQ*hd + 2*kv_eff*hd) elements. */
+static void decompose_attention(const int64_t *x, const int32_t *req, int flags, orc_sched *s) {
+  int64_t bs = x[A_BS], nh = x[A_NH], nkv = x[A_NKV], hd = x[A_HD];
+  int64_t bq = x[A_BQ], bkv = x[A_BKV], chunk = x[A_CHUNK], causal = x[A_CAUSAL];
+  int64_t bpe = bytes_per_elem((int)x[A_DTYPE]);
+  int64_t g = nh / nkv;
+  for (int64_t h = 0; h < nkv; ++h) {
+    for (int64_t b = 0; b < bs; ++b) {
+      int64_t qlen = req[2 * b], kvlen = req[2 * b + 1];
+      int64_t rows = qlen * g;
+      for (int64_t i = 0; i < cdiv(rows, bq); ++i) {
+        int64_t q_last = (imin((i + 1) * bq, rows) - 1) / g;
+        int64_t kv_need = causal ? imin(kvlen, kvlen - qlen + q_last + 1) : kvlen;
+        int64_t n_ch = chunk > 0 ? cdiv(kv_need, chunk) : 1;
+        for (int64_t c = 0; c < n_ch; ++c) {
+          int64_t len = chunk > 0 ? imin(chunk, kv_need - c * chunk) : kv_need;
+          if (flags & ORC_CLAMPED) {
+            int64_t qr = imin(bq, rows - i * bq);
+            emit_task(s, 4 * qr * len * hd, 0, qr * len + qr * cdiv(len, bkv),
+                      (qr * hd + 2 * len * hd) * bpe);
+          } else {
+            int64_t kv_eff = cdiv(len, bkv) * bkv;
+            emit_task(s, 4 * bq * kv_eff * hd, 0, bq * kv_eff + bq * (kv_eff / bkv),
+                      (bq * hd + 2 * kv_eff * hd) * bpe);
+          }
+        }
+      }
+    }
+  }
+}
+
+/* ---------------- domain checks (include/synperf.h "per-pair domain") ---- */
+
+static int is_tensor_family(int fam) { return fam == FAM_GEMM || fam == FAM_ATTENTION || fam == FAM_MOE; }
+
+/* Validates one config; also computes its task count T (int64) and, for
+ * attention, the per-kv-head kv-unit sum, to enforce the documented exact
+ * range (T < 2^31, per-head sum of kv_eff/BKV < 2^32).  Returns a status. */
+static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_out) {
+  *T_out = 0;
+  switch (fam) {
+    case FAM_GEMM: {
+      if (x[G_M] < 1 || x[G_N] < 1 || x[G_K] < 1) return ST_DIM;
+      if (x[G_TM] < 1 || x[G_TN] < 1 || x[G_BK] < 1 || x[G_STAGES] < 1) return ST_TILE;
+      if (x[G_WARPS] < 1 || x[G_REGS] < 1 || x[G_SMEM] < 0) return ST_RES;
+      if (x[G_DTYPE] != DT_BF16 && x[G_DTYPE] != DT_FP16) return ST_DTYPE;
+      int64_t T = cdiv(x[G_M], x[G_TM]) * cdiv(x[G_N], x[G_TN]);
+      if (T > INT32_LIM) return ST_RANGE;
+      *T_out = T;
+      return ST_OK;
+    }
+    case FAM_MOE: {
+      if (x[E_M] < 1 || x[E_E] < 1 || x[E_TOPK] < 1 || x[E_H] < 1 || x[E_N] < 1) return ST_DIM;
+      if (x[E_BM] < 1 || x[E_BN] < 1 || x[E_BK] < 1 || x[E_STAGES] < 1) return ST_TILE;
+      if (x[E_WARPS] < 1 || x[E_REGS] < 1 || x[E_SMEM] < 0) return ST_RES;
+      if (x[E_DTYPE] != DT_BF16 && x[E_DTYPE] != DT_FP16) return ST_DTYPE;
+      int64_t mt = x[E_M] * x[E_TOPK];
+      if (mt > INT32_LIM) return ST_RANGE;
+      int64_t T = 0;
+      if (rag) {
+        int64_t sum = 0;
+        for (int64_t e = 0; e < x[E_E]; ++e) {
+          if (rag[e] < 0) return ST_HIST;
+          sum += rag[e];
+        }
+        if (sum != mt) return ST_HIST;
+        for (int64_t e = 0; e < x[E_E]; ++e) T += cdiv(rag[e], x[E_BM]);
+      } else {
+        int64_t q = mt / x[E_E], r = mt % x[E_E];
+        T = r * cdiv(q + 1, x[E_BM]) + (x[E_E] - r) * cdiv(q, x[E_BM]);
+      }
+      T *= cdiv(x[E_N], x[E_BN]);
+      if (T > INT32_LIM) return ST_RANGE;
+      *T_out = T;
+      return ST_OK;
+    }
+    case FAM_RMSNORM: case FAM_SILU: {
+      if (x[R_SEQ] < 1 || x[R_DIM] < 1) return ST_DIM;
+      if (x[R_WARPS] < 1 || x[R_REGS] < 1 || x[R_SMEM] < 0) return ST_RES;
+      if (bytes_per_elem((int)x[R_DTYPE]) == 0) return ST_DTYPE;
+      *T_out = x[R_SEQ];
+      return ST_OK;
+    }
+    case FAM_ATTENTION: {
+      if (x[A_BS] < 1 || x[A_NH] < 1 || x[A_NKV] < 1 || x[A_HD] < 1) return ST_DIM;
+      if (x[A_BQ] < 1 || x[A_BKV] < 1 || x[A_CHUNK] < 0) return ST_TILE;
+      if (x[A_WARPS] < 1 || x[A_REGS] < 1 || x[A_SMEM] < 0) return ST_RES;
+      if (x[A_DTYPE] != DT_BF16 && x[A_DTYPE] != DT_FP16) return ST_DTYPE;
+      if (x[A_NH] % x[A_NKV] != 0) return ST_HEADS;
+      int64_t g = x[A_NH] / x[A_NKV];
+      for (int64_t b = 0; b < x[A_BS]; ++b) {
+        int64_t qlen = rag[2 * b], kvlen = rag[2 * b + 1];
+        if (qlen < 1 || kvlen < 1) return ST_DIM;
+        if (x[A_CAUSAL] && kvlen < qlen) return ST_CAUSAL;
+        if (qlen * g > INT32_LIM) return ST_RANGE;
+      }
+      /* per-head task count L and kv-unit sum U, counted item by item */
+      int64_t L = 0, U = 0;
+      for (int64_t b = 0; b < x[A_BS]; ++b) {
+        int64_t qlen = rag[2 * b], kvlen = rag[2 * b + 1], rows = qlen * g;
+        for (int64_t i = 0; i < cdiv(rows, x[A_BQ]); ++i) {
+          int64_t q_last = (imin((i + 1) * x[A_BQ], rows) - 1) / g;
+          int64_t kv_need = x[A_CAUSAL] ? imin(kvlen, kvlen - qlen + q_last + 1) : kvlen;
+          int64_t chunk = x[A_CHUNK];
+          int64_t n_ch = chunk > 0 ? cdiv(kv_need, chunk) : 1;
+          for (int64_t c = 0; c < n_ch; ++c) {
+            int64_t len = chunk > 0 ? imin(chunk, kv_need - c * chunk) : kv_need;
+            U += cdiv(len, x[A_BKV]);
+          }
+          L += n_ch;
+          if (L > INT32_LIM || U > UINT32_LIM) return ST_RANGE;
+        }
+      }
+      if (L * x[A_NKV] > INT32_LIM) return ST_RANGE;
+      *T_out = L * x[A_NKV];
+      return ST_OK;
+    }
+  }
+  return ST_DIM;
+}
+
+/* O2: per-task resource footprint and occupancy, R6 register units. */
+static int64_t occupancy(int fam, const int64_t *x, const orc_spec *sp) {
+  int64_t smem = 0, warps = 0, regs = 0;
+  switch (fam) {
+    case FAM_GEMM:
+      warps = x[G_WARPS]; regs = x[G_REGS];
+      smem = x[G_SMEM] > 0 ? x[G_SMEM]
+                           : x[G_STAGES] * (x[G_TM] + x[G_TN]) * x[G_BK] * bytes_per_elem((int)x[G_DTYPE]);
+      break;
+    case FAM_MOE:
+      warps = x[E_WARPS]; regs = x[E_REGS];
+      smem = x[E_SMEM] > 0 ? x[E_SMEM]
+                           : x[E_STAGES] * (x[E_BM] + x[E_BN]) * x[E_BK] * bytes_per_elem((int)x[E_DTYPE]);
+      break;
+    case FAM_ATTENTION:
+      warps = x[A_WARPS]; regs = x[A_REGS];
+      smem = x[A_SMEM] > 0 ? x[A_SMEM]
+                           : (x[A_BQ] + 2 * x[A_BKV]) * x[A_HD] * bytes_per_elem((int)x[A_DTYPE]);
+      break;
+    default:
+      warps = x[R_WARPS]; regs = x[R_REGS];
+      smem = x[R_SMEM] > 0 ? x[R_SMEM] : warps * 4;
+      break;
+  }
+  int64_t occ = sp->max_ctas_per_sm;
+  if (smem > 0) occ = imin(occ, sp->smem_per_sm_bytes / smem);
+  occ = imin(occ, (sp->regfile_per_sm_bytes / 4) / (regs * 32 * warps));
+  occ = imin(occ, sp->max_warps_per_sm / warps);
+  return imax(1, occ);
+}
+
+/* Pipes present per family (Table V): bit 0 Tensor, 1 FMA, 2 XU */
+static int pipes_of(int fam) {
+  switch (fam) {
+    case FAM_GEMM: case FAM_MOE: return 1;
+    case FAM_ATTENTION: return 1 | 4;
+    default: return 2 | 4;
+  }
+}
+
+static void set_error(int64_t *ints, double *flts) {
+  for (int k = 0; k < N_I; ++k) ints[k] = -1;
+  for (int k = 0; k < N_F; ++k) flts[k] = NAN;
+}
+
+/* One (config, spec) pair through O1..O7.  ints[N_I], flts[N_F]. */
+static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const orc_spec *sp,
+                          int flags, int64_t *ints, double *flts) {
+  int64_t T = 0;
+  int st = validate(fam, x, rag, &T);
+  int64_t tensor_th = 0;
+  if (st == ST_OK && is_tensor_family(fam)) {
+    int dt = (int)(fam == FAM_GEMM ? x[G_DTYPE] : fam == FAM_MOE ? x[E_DTYPE] : x[A_DTYPE]);
+    tensor_th = dt == DT_BF16 ? sp->th_tensor_bf16 : sp->th_tensor_fp16;
+    if (tensor_th <= 0) st = ST_DTYPE;
+  }
+  if (st != ST_OK) {
+    set_error(ints, flts);
+    return st;
+  }
+
+  orc_sched s;
+  memset(&s, 0, sizeof s);
+  s.n_sm = sp->num_sms;
+  s.sm_sum = (int64_t *)calloc((size_t)s.n_sm * 4, sizeof(int64_t));
+  s.sm_count = (int64_t *)calloc((size_t)s.n_sm, sizeof(int64_t));
+
+  switch (fam) { /* O1 + O3 + O4 */
+    case FAM_GEMM: decompose_gemm(x, flags, &s); break;
+    case FAM_MOE: decompose_moe(x, rag, flags, &s); break;
+    case FAM_RMSNORM: decompose_rmsnorm(x, &s); break;
+    case FAM_SILU: decompose_silu(x, &s); break;
+    case FAM_ATTENTION: decompose_attention(x, rag, flags, &s); break;
+  }
+
+  /* O5: per-quantity max over SMs (R7) */
+  int64_t mx[4] = {0, 0, 0, 0};
+  for (int64_t j = 0; j < s.n_sm; ++j)
+    for (int q = 0; q < 4; ++q) mx[q] = imax(mx[q], s.sm_sum[j * 4 + q]);
+
+  /* O2 */
+  int64_t occ = occupancy(fam, x, sp);
+  ints[I_NTASKS] = s.t;
+  ints[I_OCC] = occ;
+  ints[I_WAVES] = cdiv(s.t, (int64_t)sp->num_sms * occ);
+  ints[I_TOT_T] = s.total[0];
+  ints[I_TOT_F] = s.total[1];
+  ints[I_TOT_X] = s.total[2];
+  ints[I_MAX_T] = mx[0];
+  ints[I_MAX_F] = mx[1];
+  ints[I_MAX_X] = mx[2];
+  ints[I_BYTES] = s.total[3];
+  ints[I_BYTES_MAX] = mx[3];
+
+  /* O6: Eq.4 C_p = N_ops,p / Th_p ; Eq.5 C_p^GPU = N^GPU / (N_SM Th_p) */
+  double nsm = (double)sp->num_sms, f = sp->sm_clock_mhz;
+  double th[3] = {(double)tensor_th, (double)sp->th_fma, (double)sp->th_xu};
+  int pipes = pipes_of(fam);
+  for (int p = 0; p < 3; ++p) {
+    if (pipes & (1 << p)) {
+      flts[F_CG_T + p] = (double)s.total[p] / (nsm * th[p]);
+      flts[F_CS_T + p] = (double)mx[p] / th[p];
+    } else {
+      flts[F_CG_T + p] = 0.0;
+      flts[F_CS_T + p] = 0.0;
+    }
+  }
+  /* C_mem = B / BW in SM-clock cycles: B bytes / (BW GB/s * 1e3 B/us) * f cycles/us (R8) */
+  double B = (double)s.total[3], Bm = (double)mx[3];
+  flts[F_GLOB_G] = B / (sp->bw_global_gbps * 1e3) * f;
+  flts[F_L2_G] = B / (sp->bw_l2_gbps * 1e3) * f;
+  flts[F_GLOB_S] = Bm / (sp->bw_global_gbps * 1e3 / nsm) * f;
+  flts[F_L2_S] = Bm / (sp->bw_l2_gbps * 1e3 / nsm) * f;
+  flts[F_SMEM_S] = Bm / (double)sp->smem_bw_bytes_per_clk;
+
+  /* O7: t_theory = max(GPU-level roofs present) / f (R9) */
+  double roof = fmax(flts[F_GLOB_G], flts[F_L2_G]);
+  for (int p = 0; p < 3; ++p)
+    if (pipes & (1 << p)) roof = fmax(roof, flts[F_CG_T + p]);
+  flts[F_TTHEORY] = roof / f;
+
+  free(s.sm_sum);
+  free(s.sm_count);
+  return ST_OK;
+}
+
+/* Gather config c's fields (int32 SoA [n_fields][ld]) into int64 */
+static void load_config(const int32_t *fields, int64_t ld, int64_t c, int nf, int64_t *x) {
+  for (int k = 0; k < nf; ++k) x[k] = fields[(int64_t)k * ld + c];
+}
+
+static int n_fields_of(int fam) {
+  switch (fam) {
+    case FAM_GEMM: return 11;
+    case FAM_ATTENTION: return 12;
+    case FAM_MOE: return 14;
+    default: return 6;
+  }
+}
+
+/*
+ * Batched featurization.  Pair p uses config cfg_idx[p] and spec spec_idx[p].
+ * Outputs SoA: ints[k * n_pairs + p] (k < 11), flts[k * n_pairs + p] (k < 12),
+ * status[p].  Returns 0, or -1 on a bad family.
+ */
+int orc_featurize(int fam, int64_t n_configs, const int32_t *fields, int64_t field_ld,
+                  const int32_t *ragged, const int64_t *ragged_off, const orc_spec *specs,
+                  int64_t n_pairs, const int64_t *cfg_idx, const int64_t *spec_idx, int flags,
+                  int64_t *ints, double *flts, uint8_t *status, int nthreads) {
+  if (fam < 0 || fam > 4) return -1;
+  (void)n_configs;
+  int nf = n_fields_of(fam);
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+  for (int64_t p = 0; p < n_pairs; ++p) {
+    int64_t x[16], pi[N_I];
+    double pf[N_F];
+    int64_t c = cfg_idx[p];
+    load_config(fields, field_ld, c, nf, x);
+    const int32_t *rag = NULL;
+    if (ragged_off && ragged_off[c] >= 0) rag = ragged + ragged_off[c];
+    if (fam == FAM_ATTENTION && !rag) {
+      set_error(pi, pf);
+      status[p] = ST_DIM;
+    } else {
+      status[p] = (uint8_t)featurize_pair(fam, x, rag, &specs[spec_idx[p]], flags, pi, pf);
+    }
+    for (int k = 0; k < N_I; ++k) ints[(int64_t)k * n_pairs + p] = pi[k];
+    for (int k = 0; k < N_F; ++k) flts[(int64_t)k * n_pairs + p] = pf[k];
+  }
+  return 0;
+}
+
+/* Per-SM arrays of the cyclic schedule for the test suite's partition checks:
+ * sm_of[t] = SM of task t (Eq.2 partition). */
+void orc_schedule_rr(int64_t n_tasks, int64_t n_sm, int64_t *sm_of) {
+  for (int64_t t = 0; t < n_tasks; ++t) sm_of[t] = t % n_sm;
+}
+
+/* Per-task demand list of one config on one spec (tests: conservation,
+ * monotone kv extent, brute-force comparisons).  Writes up to cap tasks as
+ * [ops_T, ops_F, ops_X, bytes] rows; returns the task count, or -status. */
+int64_t orc_task_list(int fam, const int32_t *fields, int64_t field_ld, int64_t c,
+                      const int32_t *rag, int flags, int64_t n_sm, int64_t *out, int64_t cap) {
+  int64_t x[16], T = 0;
+  load_config(fields, field_ld, c, n_fields_of(fam), x);
+  int st = validate(fam, x, rag, &T);
+  if (st != ST_OK) return -st;
+  orc_sched s;
+  memset(&s, 0, sizeof s);
+  /* one "SM" per task slot, so sm_sum rows are the per-task demands in order */
+  s.n_sm = T > 0 ? T : 1;
+  if (s.n_sm > cap) return -(int64_t)100;
+  (void)n_sm;
+  s.sm_sum = (int64_t *)calloc((size_t)s.n_sm * 4, sizeof(int64_t));
+  s.sm_count = (int64_t *)calloc((size_t)s.n_sm, sizeof(int64_t));
+  switch (fam) {
+    case FAM_GEMM: decompose_gemm(x, flags, &s); break;
+    case FAM_MOE: decompose_moe(x, rag, flags, &s); break;
+    case FAM_RMSNORM: decompose_rmsnorm(x, &s); break;
+    case FAM_SILU: decompose_silu(x, &s); break;
+    case FAM_ATTENTION: decompose_attention(x, rag, flags, &s); break;
+  }
+  memcpy(out, s.sm_sum, (size_t)s.t * 4 * sizeof(int64_t));
+  int64_t n = s.t;
+  free(s.sm_sum);
+  free(s.sm_count);
+  return n;
+}
+
+/* ---------------- O8-O11 Performance Estimator ---------------- */
+
+/* Host fp32 model description (same arrays the C-ABI's sp_mlp_desc points at). */
+typedef struct {
+  int32_t family, n_in, precision, pad_;
+  const float *mu, *sigma;          /* [n_in] normalisation stats (R17) */
+  const float *w1, *b1;             /* [256][n_in], [256] */
+  const float *g1, *be1, *m1, *v1;  /* BN1 gamma, beta, running mean, var [256] */
+  const float *w2, *b2;             /* [128][256], [128] */
+  const float *g2, *be2, *m2, *v2;
+  const float *w3, *b3;             /* [64][128], [64] */
+  const float *g3, *be3, *m3, *v3;
+  const float *w4;                  /* [64] */
+  float b4, bn_eps;
+} orc_mlp;
+
+/* O8: Table IV order: per pipe present (Tensor, FMA, XU):
+ * [total ops, C^GPU, max-SM ops, C^SM], then the 7 MIO features. */
+static int build_input(int fam, const int64_t *ints, const double *flts, double *v) {
+  int pipes = pipes_of(fam), n = 0;
+  for (int p = 0; p < 3; ++p) {
+    if (!(pipes & (1 << p))) continue;
+    v[n++] = (double)ints[I_TOT_T + p];
+    v[n++] = flts[F_CG_T + p];
+    v[n++] = (double)ints[I_MAX_T + p];
+    v[n++] = flts[F_CS_T + p];
+  }
+  v[n++] = (double)ints[I_BYTES];
+  v[n++] = flts[F_GLOB_G];
+  v[n++] = flts[F_L2_G];
+  v[n++] = (double)ints[I_BYTES_MAX];
+  v[n++] = flts[F_GLOB_S];
+  v[n++] = flts[F_L2_S];
+  v[n++] = flts[F_SMEM_S];
+  return n;
+}
+
+/* One hidden layer, unfused (O10): a = W h + b; r = max(a,0);
+ * out = gamma (r - mean) / sqrt(var + eps) + beta; dropout = identity (eval). */
+static void hidden_layer(int n_out, int n_in, const float *w, const float *b, const float *g,
+                         const float *be, const float *m, const float *var, double eps,
+                         const double *h, double *out) {
+  for (int o = 0; o < n_out; ++o) {
+    double a = (double)b[o];
+    for (int k = 0; k < n_in; ++k) a += (double)w[(int64_t)o * n_in + k] * h[k];
+    double r = a > 0.0 ? a : 0.0;
+    out[o] = (double)g[o] * (r - (double)m[o]) / sqrt((double)var[o] + eps) + (double)be[o];
+  }
+}
+
+/* O9-O11 for one feature vector v[n_in]; returns the logit z. */
+static double mlp_logit(const orc_mlp *md, const double *v) {
+  double x[16], h1[256], h2[128], h3[64];
+  for (int i = 0; i < md->n_in; ++i) {
+    double sd = (double)md->sigma[i] > 1e-8 ? (double)md->sigma[i] : 1e-8;
+    x[i] = (log1p(v[i]) - (double)md->mu[i]) / sd;
+  }
+  double eps = (double)md->bn_eps;
+  hidden_layer(256, md->n_in, md->w1, md->b1, md->g1, md->be1, md->m1, md->v1, eps, x, h1);
+  hidden_layer(128, 256, md->w2, md->b2, md->g2, md->be2, md->m2, md->v2, eps, h1, h2);
+  hidden_layer(64, 128, md->w3, md->b3, md->g3, md->be3, md->m3, md->v3, eps, h2, h3);
+  double z = (double)md->b4;
+  for (int k = 0; k < 64; ++k) z += (double)md->w4[k] * h3[k];
+  return z;
+}
+
+/*
+ * Batched prediction from oracle features (ints/flts SoA as written by
+ * orc_featurize).  efficiency e = 1/(1+exp(-z)) (sigmoid);
+ * latency_us = t_theory / e.  Status != 0 -> NaN.
+ */
+int orc_predict(const orc_mlp *md, int64_t n_pairs, const int64_t *ints, const double *flts,
+                const uint8_t *status, double *latency_us, double *efficiency, double *logit,
+                int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+  for (int64_t p = 0; p < n_pairs; ++p) {
+    int64_t pi[N_I];
+    double pf[N_F], v[16];
+    for (int k = 0; k < N_I; ++k) pi[k] = ints[(int64_t)k * n_pairs + p];
+    for (int k = 0; k < N_F; ++k) pf[k] = flts[(int64_t)k * n_pairs + p];
+    if (status[p] != ST_OK) {
+      latency_us[p] = NAN;
+      if (efficiency) efficiency[p] = NAN;
+      if (logit) logit[p] = NAN;
+      continue;
+    }
+    build_input(md->family, pi, pf, v);
+    double z = mlp_logit(md, v);
+    double e = 1.0 / (1.0 + exp(-z));
+    latency_us[p] = pf[F_TTHEORY] / e;
+    if (efficiency) efficiency[p] = e;
+    if (logit) logit[p] = z;
+  }
+  return 0;
+}
+
+/* Normalised MLP input of one pair (tests: compare against torch.nn). */
+int orc_mlp_input(const orc_mlp *md, const int64_t *pi, const double *pf, double *x_out) {
+  double v[16];
+  int n = build_input(md->family, pi, pf, v);
+  for (int i = 0; i < n; ++i) {
+    double sd = (double)md->sigma[i] > 1e-8 ? (double)md->sigma[i] : 1e-8;
+    x_out[i] = (log1p(v[i]) - (double)md->mu[i]) / sd;
+  }
+  return n;
+}
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

@@ -1,0 +1,482 @@
+"""Pins of the fp64 CPU oracle against what the paper and mathematics fix.
+
+Each test states what it pins: worked examples printed by the paper/spec or
+derived by hand (tests/golden/worked_examples.json, cited per case), closed
+forms (waves, Eq.5, roofline in physical units), invariants (partition,
+conservation, monotonicity, schedule-independence of totals), brute force on
+tiny shapes (literal element loops written here, sharing nothing with the
+oracle), and a textbook library routine (torch.nn, fp64) for the MLP.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from workloads import gen, models, specs
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+A100 = specs.spec_by_name("A100")
+
+
+def one(family, cfg, requests=None, hist=None):
+    cols = {k: [v] for k, v in cfg.items()}
+    if requests is not None:
+        rag = [x for r in requests for x in r]
+        return gen.make_batch(family, cols, rag, [0])
+    if hist is not None:
+        return gen.make_batch(family, cols, hist, [0])
+    if family == gen.FUSED_MOE:
+        return gen.make_batch(family, cols, [], [-1])
+    return gen.make_batch(family, cols)
+
+
+def spec_with(**kw):
+    s = specs.spec_by_name("A100")
+    for k, v in kw.items():
+        s[0][k] = v
+    return s
+
+
+def feats(orc, batch, spec, **kw):
+    f = orc.featurize(batch, spec, **kw)
+    ints = dict(zip(orc.INT_NAMES, f.ints[:, 0]))
+    flts = dict(zip(orc.FLT_NAMES, f.flts[:, 0]))
+    return ints, flts, int(f.status[0])
+
+
+# --------------------------------------------------------------- worked examples
+
+def test_gemm_4096_tiles(orc):
+    g = GOLD["gemm_4096_tiles"]
+    tl = orc.task_list(one(gen.GEMM, g["config"]))
+    assert len(tl) == g["n_tasks"]
+    assert (tl[:, 0] == g["ops_per_task"]).all()
+
+
+def test_gemm_single_tile_clamped_and_padded(orc):
+    g = GOLD["gemm_single_tile_clamped"]
+    b = one(gen.GEMM, g["config"])
+    assert orc.task_list(b, flags=orc.CLAMPED)[:, 0].tolist() == [g["clamped_ops"]]
+    assert orc.task_list(b)[:, 0].tolist() == [g["padded_ops"]]
+
+
+@pytest.mark.parametrize("case", ["attention_causal_2task", "attention_gqa_causal"])
+def test_attention_task_ops(orc, case):
+    g = GOLD[case]
+    tl = orc.task_list(one(gen.ATTENTION, g["config"], g["requests"]))
+    assert tl[:, 0].tolist() == g["task_tensor_ops"]
+
+
+def test_attention_decode_splitkv(orc):
+    g = GOLD["attention_decode_splitkv_4sm"]
+    ints, _, st = feats(orc, one(gen.ATTENTION, g["config"], g["requests"]), spec_with(num_sms=g["n_sm"]))
+    assert st == 0
+    assert ints["n_tasks"] == g["n_tasks"]
+    assert ints["tot_T"] == g["total_tensor_ops"]
+    assert ints["max_T"] == g["max_sm_tensor_ops"]
+    assert ints["max_X"] == g["max_sm_xu_ops"]
+    assert ints["bytes_max"] == g["max_sm_bytes"]
+
+
+def test_occupancy_corrected_example(orc):
+    g = GOLD["occupancy_corrected"]
+    cfg = dict(SEQ=10, DIM=128, DTYPE=0, **g["footprint"])
+    ints, _, st = feats(orc, one(gen.RMSNORM, cfg), spec_with(**g["sm"]))
+    assert st == 0 and ints["occupancy"] == g["occupancy"]
+
+
+def test_a100_gemm_4096_full_record(orc):
+    g = GOLD["a100_gemm_4096"]
+    ints, flts, st = feats(orc, one(gen.GEMM, g["config"]), specs.spec_by_name(g["gpu"]))
+    assert st == 0
+    for k, v in g["ints"].items():
+        assert ints[k] == v, k
+    for k, v in g["flts"].items():
+        assert flts[k] == pytest.approx(v, rel=g["flt_rtol"]), k
+
+
+def test_analyze_balanced(orc):
+    g = GOLD["analyze_balanced"]
+    ints, flts, st = feats(orc, one(gen.GEMM, g["config"]), spec_with(**g["sm"]))
+    assert st == 0
+    assert ints["tot_T"] == g["tot_T"] and ints["max_T"] == g["max_T"]
+    assert flts["cg_T"] == g["cg_T"] and flts["cs_T"] == g["cs_T"]
+
+
+def test_rr_deal(orc):
+    for n_tasks, n_sm, expect in GOLD["rr_deal"]["cases"]:
+        assert orc.schedule_rr(n_tasks, n_sm).tolist() == expect
+
+
+def test_bytes_to_cycles_corrected(orc):
+    g = GOLD["bytes_to_cycles"]
+    ints, flts, st = feats(orc, one(gen.RMSNORM, g["config"]), specs.spec_by_name(g["gpu"]))
+    assert ints["bytes"] == g["bytes"]
+    assert flts["glob_gpu"] == pytest.approx(g["glob_gpu"], rel=g["rtol"])
+
+
+def test_rmsnorm_brute(orc):
+    g = GOLD["rmsnorm_brute"]
+    ints, _, _ = feats(orc, one(gen.RMSNORM, g["config"]), A100)
+    assert ints["tot_F"] == g["tot_F"] and ints["tot_X"] == g["tot_X"]
+
+
+def test_causal_brute_80(orc):
+    g = GOLD["causal_brute_80"]
+    ints, _, _ = feats(orc, one(gen.ATTENTION, g["config"], g["requests"]), A100)
+    assert ints["tot_T"] == g["tot_T"]
+
+
+# ------------------------------------------------------- brute force, tiny shapes
+
+def brute_gemm_macs(M, N, K, tm, tn, bk, padded):
+    """Literal (row, col, k) loops over every tile's iteration space."""
+    count = 0
+    Mp = -(-M // tm) * tm if padded else M
+    Np = -(-N // tn) * tn if padded else N
+    Kp = -(-K // bk) * bk if padded else K
+    for _row in range(Mp):
+        for _col in range(Np):
+            for _k in range(Kp):
+                count += 1
+    return 2 * count
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_gemm_brute(orc, seed):
+    rng = np.random.default_rng(seed)
+    M, N, K = (int(x) for x in rng.integers(1, 20, 3))
+    tm, tn, bk = (int(x) for x in rng.choice([1, 2, 4, 8, 16], 3))
+    cfg = dict(M=M, N=N, K=K, TM=tm, TN=tn, BK=bk, STAGES=2, WARPS=4, REGS=64, SMEM=0, DTYPE=0)
+    b = one(gen.GEMM, cfg)
+    for padded, flags in ((True, 0), (False, orc.CLAMPED)):
+        ints, _, st = feats(orc, b, A100, flags=flags)
+        assert st == 0
+        assert ints["tot_T"] == brute_gemm_macs(M, N, K, tm, tn, bk, padded)
+
+
+def brute_attention_scores(requests, nh, nkv, causal):
+    """Literal loop over (query head, query token, key position) of every
+    request, counting scores not removed by the causal mask (a query at token
+    q of a length-qlen chunk whose cache holds kvlen keys sees keys
+    0..kvlen-qlen+q)."""
+    count = 0
+    for _kvh in range(nkv):
+        for _qh in range(nh // nkv):
+            for qlen, kvlen in requests:
+                for q in range(qlen):
+                    for k in range(kvlen):
+                        if not causal or k <= kvlen - qlen + q:
+                            count += 1
+    return count
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_attention_brute_elementwise_blocks(orc, seed):
+    """With BQ = BKV = 1 every task is one score row; tensor ops must equal
+    4*hd*(scores) and XU ops 2*(scores) (one exp2 + one rescale per 1-wide KV
+    block, R13) -- exact element counts (SPEC S:145-146 exactness)."""
+    rng = np.random.default_rng(100 + seed)
+    nkv = int(rng.choice([1, 2]))
+    g = int(rng.choice([1, 2, 3]))
+    hd = int(rng.choice([1, 2, 4]))
+    bs = int(rng.integers(1, 4))
+    causal = int(rng.integers(0, 2))
+    reqs = []
+    for _ in range(bs):
+        q = int(rng.integers(1, 6))
+        reqs.append((q, q + int(rng.integers(0, 5))))
+    cfg = dict(BS=bs, NH=nkv * g, NKV=nkv, HD=hd, BQ=1, BKV=1, KV_CHUNK=0, CAUSAL=causal,
+               WARPS=1, REGS=32, SMEM=0, DTYPE=0)
+    ints, _, st = feats(orc, one(gen.ATTENTION, cfg, reqs), A100)
+    assert st == 0
+    scores = brute_attention_scores(reqs, nkv * g, nkv, causal)
+    assert ints["tot_T"] == 4 * hd * scores
+    assert ints["tot_X"] == 2 * scores
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_attention_padded_bounds_exact(orc, seed):
+    """Block-granular padding only ever adds work, by less than one block
+    row/column per task (SPEC S:646 'block-rounding slack'):
+    exact <= clamped <= padded."""
+    rng = np.random.default_rng(200 + seed)
+    nkv, g = int(rng.choice([1, 2])), int(rng.choice([1, 2, 4]))
+    hd, bq, bkv = 2, int(rng.choice([2, 4, 8])), int(rng.choice([2, 4, 8]))
+    reqs = [(int(q), int(q + rng.integers(0, 9))) for q in rng.integers(1, 12, int(rng.integers(1, 4)))]
+    cfg = dict(BS=len(reqs), NH=nkv * g, NKV=nkv, HD=hd, BQ=bq, BKV=bkv, KV_CHUNK=0, CAUSAL=1,
+               WARPS=1, REGS=32, SMEM=0, DTYPE=0)
+    b = one(gen.ATTENTION, cfg, reqs)
+    exact = 4 * hd * brute_attention_scores(reqs, nkv * g, nkv, True)
+    clamped = feats(orc, b, A100, flags=orc.CLAMPED)[0]["tot_T"]
+    padded = feats(orc, b, A100)[0]["tot_T"]
+    n_tasks = feats(orc, b, A100)[0]["n_tasks"]
+    assert exact <= clamped <= padded
+    assert padded - exact < n_tasks * 4 * hd * (bq * bkv + bq * 20 + bkv * 20)
+
+
+def test_causal_kv_extent_monotone(orc):
+    """within a sequence, kv extent is non-decreasing in q-block."""
+    cfg = dict(BS=1, NH=4, NKV=1, HD=64, BQ=64, BKV=32, KV_CHUNK=0, CAUSAL=1, WARPS=4, REGS=128,
+               SMEM=0, DTYPE=0)
+    tl = orc.task_list(one(gen.ATTENTION, cfg, [(777, 1500)]))
+    assert (np.diff(tl[:, 0]) >= 0).all() and tl[0, 0] < tl[-1, 0]
+
+
+# ------------------------------------------------------------ closed forms
+
+def _random_batches(n=200, seed=7):
+    return [gen.gen_gemm(n, seed), gen.gen_attention(n // 2, n // 2, seed + 1, max_bs=4,
+                                                     qlen_max=3000, kvlen_max=4000),
+            gen.gen_moe(n, seed + 2), gen.gen_rowwise(gen.RMSNORM, n, seed + 3),
+            gen.gen_rowwise(gen.SILU_MUL, n, seed + 4)]
+
+
+@pytest.fixture(scope="module")
+def rand_feats(orc):
+    sp = specs.paper_gpu_specs()
+    out = []
+    for b in _random_batches():
+        out.append((b, orc.featurize(b, sp)))
+    return sp, out
+
+
+PIPES = {gen.GEMM: [0], gen.FUSED_MOE: [0], gen.ATTENTION: [0, 2], gen.RMSNORM: [1, 2],
+         gen.SILU_MUL: [1, 2]}
+
+
+def test_waves_closed_form(orc, rand_feats):
+    """north_star: waves = ceil(CTAs / (SMs * occupancy))."""
+    sp, out = rand_feats
+    for b, f in out:
+        c, g = orc.cross_pairs(b.n_configs, (0, len(sp)))
+        ok = f.status == 0
+        T, occ, waves = f.ints[0][ok], f.ints[1][ok], f.ints[2][ok]
+        nsm = sp["num_sms"][g[ok]].astype(np.int64)
+        assert (waves == -(-T // (nsm * occ))).all()
+        assert (occ >= 1).all()
+
+
+def test_eq5_identity_and_max_ge_mean(orc, rand_feats):
+    """Eq.5: C^GPU * N_SM * Th = N^GPU; C^SM = N^maxSM / Th; max >= mean."""
+    sp, out = rand_feats
+    for b, f in out:
+        c, g = orc.cross_pairs(b.n_configs, (0, len(sp)))
+        ok = f.status == 0
+        nsm = sp["num_sms"][g].astype(np.float64)
+        th = [sp["th_tensor_bf16"][g], sp["th_fma"][g], sp["th_xu"][g]]
+        for p in PIPES[b.family]:
+            tot, mx = f.ints[3 + p][ok], f.ints[6 + p][ok]
+            cg, cs = f.flts[p][ok], f.flts[3 + p][ok]
+            np.testing.assert_allclose(cg * nsm[ok] * th[p][ok], tot, rtol=1e-12)
+            np.testing.assert_allclose(cs * th[p][ok], mx, rtol=1e-12)
+            assert (cs >= cg * (1 - 1e-12)).all()
+            assert (mx * nsm[ok] >= tot).all()
+
+
+def test_roofline_closed_form_physical_units(orc, rand_feats):
+    """north_star roofline: t_theory = max(ops/peak, bytes/BW) in seconds, with
+    peak = N_SM * Th * f ops/s and BW in bytes/s -- an expression in physical
+    units, not the oracle's cycle route."""
+    sp, out = rand_feats
+    for b, f in out:
+        c, g = orc.cross_pairs(b.n_configs, (0, len(sp)))
+        ok = f.status == 0
+        s = sp[g[ok]]
+        hz = s["sm_clock_mhz"] * 1e6
+        th = {0: s["th_tensor_bf16"], 1: s["th_fma"], 2: s["th_xu"]}
+        t = np.maximum(f.ints[9][ok] / (s["bw_global_gbps"] * 1e9), f.ints[9][ok] / (s["bw_l2_gbps"] * 1e9))
+        for p in PIPES[b.family]:
+            t = np.maximum(t, f.ints[3 + p][ok] / (s["num_sms"] * th[p] * hz))
+        np.testing.assert_allclose(f.flts[11][ok], t * 1e6, rtol=1e-12)
+
+
+def test_uniform_families_max_sm_closed_form(orc, rand_feats):
+    """Uniform tasks under round robin: the busiest SM holds ceil(T/N) tasks
+    (SPEC S:212 'counts differ by at most 1'), so max-SM = ceil(T/N) * per-task."""
+    sp, out = rand_feats
+    for b, f in out:
+        if b.family == gen.ATTENTION:
+            continue
+        c, g = orc.cross_pairs(b.n_configs, (0, len(sp)))
+        ok = f.status == 0
+        T = f.ints[0][ok]
+        per_sm = -(-T // sp["num_sms"][g[ok]].astype(np.int64))
+        for p in PIPES[b.family]:
+            assert (f.ints[6 + p][ok] * T == per_sm * f.ints[3 + p][ok]).all()
+        assert (f.ints[10][ok] * T == per_sm * f.ints[9][ok]).all()
+
+
+def test_partition_and_conservation(orc):
+    """Eq.2: the per-SM sets partition T (union = T, disjoint); counts
+    differ by <= 1; per-SM sums add up to the GPU totals."""
+    b = gen.gen_attention(6, 6, 31, max_bs=3, qlen_max=500, kvlen_max=900)
+    sp = specs.paper_gpu_specs()
+    f = orc.featurize(b, sp)
+    for c in range(b.n_configs):
+        tl = orc.task_list(b, c)
+        for gi in range(len(sp)):
+            n = int(sp["num_sms"][gi])
+            sm_of = orc.schedule_rr(len(tl), n)
+            members = [np.nonzero(sm_of == j)[0] for j in range(n)]
+            allm = np.concatenate(members)
+            assert np.array_equal(np.sort(allm), np.arange(len(tl)))
+            counts = np.array([len(m) for m in members])
+            assert counts.max() - counts.min() <= 1
+            per_sm = np.array([tl[m].sum(0) if len(m) else np.zeros(4, np.int64) for m in members])
+            p = gi * b.n_configs + c
+            assert per_sm.sum(0)[0] == f.ints[3, p] and per_sm.sum(0)[3] == f.ints[9, p]
+            assert per_sm[:, 0].max() == f.ints[6, p]
+            assert per_sm[:, 2].max() == f.ints[8, p]
+            assert per_sm[:, 3].max() == f.ints[10, p]
+            assert tl[:, 0].sum() == f.ints[3, p]
+
+
+def test_schedule_independence_of_totals(orc):
+    """GPU totals do not depend on the partition (vary N_SM)."""
+    b = gen.gen_attention(20, 20, 5, max_bs=4, qlen_max=2000, kvlen_max=3000)
+    tots = []
+    for n in (1, 7, 32, 108, 1000):
+        f = orc.featurize(b, spec_with(num_sms=n))
+        tots.append(f.ints[[0, 3, 4, 5, 9]])
+    for t in tots[1:]:
+        assert np.array_equal(t, tots[0])
+
+
+def test_scaling_doubling_k(orc):
+    """doubling K (a multiple of BK) doubles Tensor ops and bytes."""
+    b = gen.gen_gemm(200, 3)
+    k = b.field("K") - b.field("K") % 64 + 64
+    b.fields[gen.FIELDS[gen.GEMM].index("K")] = k
+    b2 = gen.ConfigBatch(b.family, b.fields.copy())
+    b2.fields[gen.FIELDS[gen.GEMM].index("K")] = 2 * k
+    f1, f2 = orc.featurize(b, A100), orc.featurize(b2, A100)
+    for slot in (3, 6, 9, 10):
+        assert np.array_equal(2 * f1.ints[slot], f2.ints[slot])
+
+
+@pytest.mark.parametrize("fam,field", [(gen.GEMM, "M"), (gen.GEMM, "N"), (gen.GEMM, "K"),
+                                       (gen.RMSNORM, "SEQ"), (gen.RMSNORM, "DIM"),
+                                       (gen.SILU_MUL, "DIM"), (gen.FUSED_MOE, "M")])
+def test_monotone_in_problem_size(orc, fam, field):
+    """Totals are non-decreasing in every problem dimension (north_star)."""
+    b = {gen.GEMM: gen.gen_gemm, gen.FUSED_MOE: gen.gen_moe}.get(fam)
+    b = b(100, 11) if b else gen.gen_rowwise(fam, 100, 11)
+    b2 = gen.ConfigBatch(b.family, b.fields.copy(), b.ragged, None if b.ragged_off is None else
+                         np.full(b.n_configs, -1, np.int64))
+    b = gen.ConfigBatch(b.family, b.fields, b.ragged, b2.ragged_off)
+    i = gen.FIELDS[fam].index(field)
+    b2.fields[i] = b.fields[i] + np.maximum(1, b.fields[i] // 3)
+    f1, f2 = orc.featurize(b, A100), orc.featurize(b2, A100)
+    for slot in (0, 3, 4, 5, 9):
+        assert (f2.ints[slot] >= f1.ints[slot]).all()
+
+
+def test_attention_monotone_in_lengths(orc):
+    b = gen.gen_attention(50, 50, 13, max_bs=4, qlen_max=3000, kvlen_max=4000)
+    b2 = gen.ConfigBatch(b.family, b.fields, b.ragged.copy(), b.ragged_off)
+    b2.ragged[1::2] += 100  # longer KV cache
+    b3 = gen.ConfigBatch(b.family, b.fields, b2.ragged.copy(), b.ragged_off)
+    b3.ragged[0::2] += 50  # 50 more query tokens appended to each sequence: under the
+    b3.ragged[1::2] += 50  # causal mask they also extend the KV cache they attend to
+    f1, f2, f3 = (orc.featurize(x, A100) for x in (b, b2, b3))
+    for slot in (0, 3, 5, 9):
+        assert (f2.ints[slot] >= f1.ints[slot]).all()
+        assert (f3.ints[slot] >= f2.ints[slot]).all()
+
+
+def test_moe_balanced_equals_explicit_histogram(orc):
+    """The balanced split (R16: q + [e < r]) equals passing that histogram."""
+    b = gen.gen_moe(100, 21)
+    bal = np.nonzero(b.ragged_off < 0)[0]
+    sub = b.subset(bal)
+    rows, offs = [], []
+    pos = 0
+    for c in range(sub.n_configs):
+        M, E, k = (int(sub.field(n)[c]) for n in ("M", "E", "TOPK"))
+        q, r = divmod(M * k, E)
+        rows += [q + (e < r) for e in range(E)]
+        offs.append(pos)
+        pos += E
+    hist = gen.ConfigBatch(sub.family, sub.fields, np.array(rows, np.int32), np.array(offs, np.int64))
+    f1, f2 = orc.featurize(sub, A100), orc.featurize(hist, A100)
+    assert np.array_equal(f1.ints, f2.ints)
+
+
+def test_domain_errors(orc):
+    cfg = dict(BS=1, NH=6, NKV=4, HD=64, BQ=64, BKV=32, KV_CHUNK=0, CAUSAL=1, WARPS=4, REGS=64,
+               SMEM=0, DTYPE=0)
+    assert feats(orc, one(gen.ATTENTION, cfg, [(10, 10)]), A100)[2] == 3  # nh % nkv
+    cfg["NH"] = 8
+    assert feats(orc, one(gen.ATTENTION, cfg, [(10, 5)]), A100)[2] == 5  # causal kv < q
+    g = dict(M=0, N=8, K=8, TM=8, TN=8, BK=8, STAGES=1, WARPS=1, REGS=32, SMEM=0, DTYPE=0)
+    ints, flts, st = feats(orc, one(gen.GEMM, g), A100)
+    assert st == 1 and ints["n_tasks"] == -1 and math.isnan(flts["t_theory_us"])
+    m = dict(M=4, E=2, TOPK=2, H=64, N=64, BM=16, BN=16, BK=16, GROUP_M=1, STAGES=2, WARPS=4,
+             REGS=64, SMEM=0, DTYPE=0)
+    assert feats(orc, one(gen.FUSED_MOE, m, hist=[3, 4]), A100)[2] == 4  # sum != M*topk
+    assert feats(orc, one(gen.FUSED_MOE, m, hist=[8, 0]), A100)[2] == 0  # zero-token expert ok
+    g.update(M=8, DTYPE=3)
+    assert feats(orc, one(gen.GEMM, g), A100)[2] == 7  # fp8: NEXT-4
+
+
+# -------------------------------------------------------------------- MLP
+
+def test_zero_output_layer_gives_twice_t_theory(orc):
+    """zero final layer -> sigmoid(0) = 0.5 -> latency = 2 t_theory."""
+    for b in _random_batches(40, 3):
+        f = orc.featurize(b, specs.paper_gpu_specs())
+        m = models.zero_output_mlp(b.family, 1)
+        lat, eff, z = orc.predict(m, f)
+        ok = f.status == 0
+        assert (eff[ok] == 0.5).all()
+        assert np.array_equal(lat[ok], 2.0 * f.flts[11][ok])
+
+
+def test_identity_bn_matches_torch_mlp(orc):
+    """With identity BatchNorm the estimator is a plain Linear/ReLU MLP with a
+    sigmoid head; compare against torch.nn in fp64 (library routine)."""
+    import torch
+
+    b = gen.gen_attention(30, 30, 9, max_bs=4, qlen_max=2000, kvlen_max=3000)
+    f = orc.featurize(b, specs.paper_gpu_specs())
+    m = models.identity_bn_mlp(b.family, 4)
+    lat, eff, z = orc.predict(m, f)
+    net = torch.nn.Sequential(
+        torch.nn.Linear(m["n_in"], 256), torch.nn.ReLU(), torch.nn.Linear(256, 128),
+        torch.nn.ReLU(), torch.nn.Linear(128, 64), torch.nn.ReLU(), torch.nn.Linear(64, 1)).double()
+    with torch.no_grad():
+        for li, lin in zip((1, 2, 3), (net[0], net[2], net[4])):
+            lin.weight.copy_(torch.from_numpy(m[f"w{li}"].astype(np.float64)))
+            lin.bias.copy_(torch.from_numpy(m[f"b{li}"].astype(np.float64)))
+        net[6].weight.copy_(torch.from_numpy(m["w4"].astype(np.float64))[None])
+        net[6].bias.fill_(float(m["b4"]))
+    ok = np.nonzero(f.status == 0)[0][:200]
+    X = np.stack([orc.mlp_input(m, f.ints[:, p], f.flts[:, p]) for p in ok])
+    # the normalisation itself, against numpy's log1p (R17)
+    p0 = ok[0]
+    v0 = [f.ints[3, p0], f.flts[0, p0], f.ints[6, p0], f.flts[3, p0], f.ints[5, p0],
+          f.flts[2, p0], f.ints[8, p0], f.flts[5, p0], f.ints[9, p0], f.flts[6, p0],
+          f.flts[7, p0], f.ints[10, p0], f.flts[8, p0], f.flts[9, p0], f.flts[10, p0]]
+    np.testing.assert_allclose(X[0], (np.log1p(np.array(v0, np.float64)) - m["mu"]) / m["sigma"],
+                               rtol=1e-12, atol=1e-12)
+    with torch.no_grad():
+        zt = net(torch.from_numpy(X)).numpy()[:, 0]
+    # BN is identity up to sqrt((1-eps)+eps) rounding in fp32 storage: ~1e-8 rel
+    np.testing.assert_allclose(z[ok], zt, rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(eff[ok], torch.sigmoid(torch.from_numpy(zt)).numpy(), rtol=1e-6)
+    np.testing.assert_allclose(lat[ok], f.flts[11][ok] / eff[ok], rtol=1e-12)
+
+
+def test_predict_exceeds_roof_and_is_deterministic(orc):
+    """latency > t_theory (sigmoid < 1); S:147 determinism."""
+    b = gen.gen_gemm(300, 17)
+    f = orc.featurize(b, specs.paper_gpu_specs())
+    m = models.random_mlp(gen.GEMM, 2)
+    lat, eff, _ = orc.predict(m, f)
+    lat2, _, _ = orc.predict(m, orc.featurize(b, specs.paper_gpu_specs()))
+    ok = f.status == 0
+    assert (lat[ok] > f.flts[11][ok]).all() and ((eff[ok] > 0) & (eff[ok] < 1)).all()
+    assert np.array_equal(lat, lat2, equal_nan=True)
