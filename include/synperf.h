@@ -1,0 +1,301 @@
+/*
+ * synperf.h -- C-ABI of libsynperf.so, the B200-native batched SynPerf predictor.
+ *
+ * SynPerf (arXiv 2601.14910) predicts a kernel's latency on a GPU in two
+ * stages (§IV):
+ *   1. an analytical feature stage -- Kernel Decomposer F (Eq.1),
+ *      Scheduling Simulator M (Eq.2) and Feature Analyzer (Eq.3-5,
+ *      P:334-357) -- producing the Table IV feature vector;
+ *   2. a per-kernel-category MLP mapping the features to an
+ *      execution efficiency e in (0,1); latency = t_theory / e.
+ * This library evaluates both stages for every (kernel config x GPU spec)
+ * pair of a batch, on the GPU, in hand-written sm_100a kernels.
+ *
+ * Conventions
+ *  - Plain C types only.  Pointers documented DEVICE must be CUDA device
+ *    memory of the context's device (e.g. torch tensors' data_ptr()); HOST
+ *    pointers are ordinary host memory and are only read during the call.
+ *  - `stream` arguments are cudaStream_t passed as void* (NULL = legacy
+ *    default stream).  sp_featurize / sp_predict are asynchronous on that
+ *    stream: no allocation, no host synchronisation inside.
+ *  - No exception crosses the ABI and the library never aborts.  Every call
+ *    returns an sp_status; sp_last_error() describes the last failure (or
+ *    the last warning) of a context.  There is no CPU fallback: without a
+ *    usable sm_100 device, sp_create fails.
+ *  - Readings of passages where the paper is silent or ambiguous are listed
+ *    as R1..R22 in DESIGN.md §3 and cited below as such.
+ */
+#ifndef SYNPERF_H_
+#define SYNPERF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+
+typedef enum sp_status {
+  SP_OK = 0,
+  SP_E_ARG = 1,         /* bad argument: NULL, size, family mismatch (SPEC S:604 exit 1) */
+  SP_E_DATA = 2,        /* invalid data: spec or model values (SPEC S:604 exit 2) */
+  SP_E_INTERNAL = 3,    /* CUDA error or launch failure (SPEC S:604 exit 3) */
+  SP_E_UNSUPPORTED = 4  /* valid but not implemented (e.g. FP8 Scaled MM, NEXT-4) */
+} sp_status;
+
+/* Per-pair status written by sp_featurize (one byte per pair).  A pair with a
+ * nonzero status has all int slots = -1 and all float slots = NaN; the batch
+ * still succeeds.  Domain rules: SPEC S:103 (nh divisible by nkv, histogram
+ * sums to M*topk), S:121 (dimensions >= 1), causal requires kvlen >= qlen;
+ * exact-integer range R22. */
+typedef enum sp_pair_status {
+  SP_PAIR_OK = 0,
+  SP_PAIR_E_DIM = 1,     /* a problem dimension < 1 (or attention config without requests) */
+  SP_PAIR_E_TILE = 2,    /* a tile / block / stage field < 1 (kv_chunk < 0) */
+  SP_PAIR_E_HEADS = 3,   /* nh % nkv != 0 */
+  SP_PAIR_E_HIST = 4,    /* MoE histogram: negative count or sum != M*topk */
+  SP_PAIR_E_CAUSAL = 5,  /* causal attention request with kvlen < qlen */
+  SP_PAIR_E_RES = 6,     /* warps < 1, regs < 1 or smem < 0 */
+  SP_PAIR_E_DTYPE = 7,   /* dtype not supported by the family, or spec lacks that tensor rate */
+  SP_PAIR_E_RANGE = 8,   /* outside the exact range: T >= 2^31, a total >= 2^63, per-kv-head
+                            sum kv_eff/BKV >= 2^32, M*topk >= 2^31 or qlen*g >= 2^31 (R22) */
+  SP_PAIR_E_INDEX = 9    /* SP_PAIRS_LIST entry with a config or spec index out of range */
+} sp_pair_status;
+
+/* ---------------------------------------------------------------- families */
+
+/* Kernel categories of Table V.  Scaled MM (FP8) is NEXT-4. */
+typedef enum sp_family {
+  SP_GEMM = 0,       /* cuBLAS GEMM, Tensor pipe */
+  SP_ATTENTION = 1,  /* FlashInfer FA2 prefill/decode, Tensor + XU */
+  SP_FUSED_MOE = 2,  /* SGLang fused MoE (Triton), Tensor */
+  SP_RMSNORM = 3,    /* FlashInfer RMSNorm, FMA + XU */
+  SP_SILU_MUL = 4    /* FlashInfer SiLU&Mul, FMA + XU */
+} sp_family;
+
+typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_dtype;
+
+/*
+ * Config fields, int32, one row per field (structure of arrays), in this
+ * order per family.  The generator workloads/gen.py FIELDS uses the same order.
+ *
+ * SP_GEMM (11):      M, N, K, TM, TN, BK, STAGES, WARPS, REGS, SMEM, DTYPE
+ * SP_ATTENTION (12): BS, NH, NKV, HD, BQ, BKV, KV_CHUNK, CAUSAL, WARPS, REGS, SMEM, DTYPE
+ *                    ragged: 2*BS int32 per config, (qlen, kvlen) interleaved
+ * SP_FUSED_MOE (14): M, E, TOPK, H, N, BM, BN, BK, GROUP_M, STAGES, WARPS, REGS, SMEM, DTYPE
+ *                    ragged: E int32 per-expert token counts; ragged_off = -1 means
+ *                    the balanced split q + [e < r], q = M*TOPK / E, r = M*TOPK % E (R16)
+ * SP_RMSNORM (6):    SEQ, DIM, WARPS, REGS, SMEM, DTYPE
+ * SP_SILU_MUL (6):   SEQ, DIM, WARPS, REGS, SMEM, DTYPE   (DIM = output width, R15)
+ *
+ * SMEM = per-task shared memory bytes, 0 = default footprint.
+ * GROUP_M does not change any feature under cyclic dealing (it only permutes
+ * uniform tiles); it is accepted for completeness of the Triton knob set.
+ */
+enum {
+  SP_NFIELDS_GEMM = 11, SP_NFIELDS_ATTENTION = 12, SP_NFIELDS_FUSED_MOE = 14,
+  SP_NFIELDS_RMSNORM = 6, SP_NFIELDS_SILU_MUL = 6
+};
+
+/* -------------------------------------------------------------- hardware S */
+
+/*
+ * Hardware specification S: the Table II parameter vector of one
+ * GPU.  Values for the paper's 11 GPUs are in Table VI plus the
+ * fills of R19.  112 bytes, natural alignment (workloads/specs.py SPEC_DTYPE).
+ */
+typedef struct sp_gpu_spec {
+  char name[32];
+  int32_t cc_major, cc_minor;       /* compute capability, 8.0 - 12.0 */
+  int32_t num_sms;                  /* N_SM, 78 - 188 */
+  int32_t th_tensor_bf16;           /* Tensor pipe, ops/clk/SM, 512 - 4096 */
+  int32_t th_tensor_fp16;
+  int32_t th_tensor_fp8;            /* 0 = absent */
+  int32_t th_fma;                   /* FMA pipe, ops/clk/SM, 64 - 128 */
+  int32_t th_xu;                    /* XU pipe, ops/clk/SM, 16 */
+  int32_t smem_bw_bytes_per_clk;    /* shared memory bandwidth per SM, 128 */
+  int32_t smem_per_sm_bytes;        /* 100 - 228 KB */
+  int32_t regfile_per_sm_bytes;     /* 256 KB */
+  int32_t max_warps_per_sm;         /* occupancy limit (not in Table II) */
+  int32_t max_ctas_per_sm;          /* occupancy limit */
+  int32_t reserved_;
+  double sm_clock_mhz;              /* f, 1410 - 2520 MHz */
+  double bw_global_gbps;            /* BW_glob, 696 - 4916 GB/s (GB = 1e9 B) */
+  double bw_l2_gbps;                /* BW_L2, 2430 - 10400 GB/s */
+} sp_gpu_spec;
+
+/* ----------------------------------------------------------------- batches */
+
+typedef struct sp_config_batch {
+  int32_t family;             /* sp_family */
+  int32_t n_fields;           /* must equal SP_NFIELDS_<family> */
+  int64_t n_configs;          /* C >= 0 */
+  int64_t field_ld;           /* elements between field rows, >= n_configs */
+  const int32_t *fields;      /* DEVICE int32 [n_fields][field_ld] */
+  const int32_t *ragged;      /* DEVICE int32 [n_ragged]; NULL if the family has none */
+  const int64_t *ragged_off;  /* DEVICE int64 [n_configs]; offset into ragged, or -1 */
+  int64_t n_ragged;
+} sp_config_batch;
+
+typedef enum sp_pairing_kind {
+  SP_PAIRS_CROSS = 0,  /* specs [spec_begin, spec_end) x all configs, spec-major:
+                          pair p = (g - spec_begin) * n_configs + c */
+  SP_PAIRS_LIST = 1    /* explicit list: pair p = (cfg_idx[p], spec_idx[p]) */
+} sp_pairing_kind;
+
+typedef struct sp_pairing {
+  int32_t kind;          /* sp_pairing_kind */
+  int32_t spec_begin;    /* CROSS */
+  int32_t spec_end;      /* CROSS */
+  int32_t reserved_;
+  int64_t n_pairs;       /* LIST: number of pairs */
+  const int64_t *cfg_idx;   /* LIST: DEVICE int64 [n_pairs] */
+  const int32_t *spec_idx;  /* LIST: DEVICE int32 [n_pairs] */
+} sp_pairing;
+
+/*
+ * Feature record per pair (SURVEY §8 uniform record; Table IV),
+ * structure of arrays with leading dimension ld (>= n_pairs):
+ *   ints[k*ld + p], k = 0..10 (int64):
+ *     0 n_tasks T            1 occupancy            2 waves = ceil(T/(N_SM*occ))
+ *     3..5 total ops N^GPU_p for p = Tensor, FMA, XU (Eq.5 numerator)
+ *     6..8 max-SM ops max_j N^SM_j_p (R7)
+ *     9 total load bytes B^GPU    10 max-SM load bytes max_j B^SM_j
+ *   flts[k*ld + p], k = 0..11 (fp32):
+ *     0..2 C^GPU_p = N^GPU_p / (N_SM Th_p) (Eq.5)   3..5 C^SM_p = max-SM ops / Th_p (Eq.4)
+ *     6 C_glob^GPU  7 C_L2^GPU  (B^GPU / BW, cycles at f)
+ *     8 C_glob^SM   9 C_L2^SM   (max-SM bytes / (BW/N_SM), R8)   10 C_smem^SM
+ *     11 t_theory_us = max(GPU-level roofs of the family) / f (R9)
+ *   status[p]: sp_pair_status.
+ * Pipes absent from a family (Table V) hold 0.
+ */
+typedef struct sp_features {
+  int32_t family;        /* sp_family of the batch that produced it */
+  int32_t reserved_;
+  int64_t n_pairs;
+  int64_t ld;
+  int64_t *ints;         /* DEVICE int64 [11][ld] */
+  float *flts;           /* DEVICE fp32 [12][ld] */
+  uint8_t *status;       /* DEVICE uint8 [n_pairs] */
+} sp_features;
+
+/* ---------------------------------------------------------------- MLP model */
+
+typedef enum sp_precision {
+  SP_MLP_FP32 = 0,  /* CUDA-core fp32 path: parity within 1e-5 relative of the fp64 oracle */
+  SP_MLP_BF16 = 1   /* tcgen05/TMEM bf16 path (fp32 accumulate): parity within 1e-2 */
+} sp_precision;
+
+/*
+ * Per-kernel-category estimator: 3 hidden layers of 256, 128, 64
+ * units, each Linear -> ReLU -> BatchNorm(eval) -> Dropout(identity at eval),
+ * then Linear(64 -> 1) -> sigmoid = efficiency (R18).  Inputs are the
+ * family's Table IV vector in frozen order (per pipe present, Tensor, FMA, XU:
+ * [total ops, C^GPU, max-SM ops, C^SM], then [B^GPU, C_glob^GPU, C_L2^GPU,
+ * max-SM B, C_glob^SM, C_L2^SM, C_smem^SM]; 11 or 15 values), normalised as
+ * (ln(1+v) - mu) / max(sigma, 1e-8) (R17).  All pointers are HOST fp32,
+ * row-major [out][in]; the library copies what it needs.
+ */
+typedef struct sp_mlp_desc {
+  int32_t family;      /* sp_family the model was trained for */
+  int32_t n_in;        /* 4 * (#pipes) + 7: 11 (GEMM, MoE) or 15 */
+  int32_t precision;   /* sp_precision */
+  int32_t reserved_;
+  const float *mu, *sigma;              /* [n_in] */
+  const float *w1, *b1;                 /* [256][n_in], [256] */
+  const float *g1, *be1, *m1, *v1;      /* BN1 gamma, beta, running mean, running var [256] */
+  const float *w2, *b2;                 /* [128][256], [128] */
+  const float *g2, *be2, *m2, *v2;      /* [128] */
+  const float *w3, *b3;                 /* [64][128], [64] */
+  const float *g3, *be3, *m3, *v3;      /* [64] */
+  const float *w4;                      /* [64] */
+  float b4;
+  float bn_eps;                         /* BatchNorm epsilon, > 0 (default 1e-5) */
+} sp_mlp_desc;
+
+/* ------------------------------------------------------------------ handles */
+
+typedef struct sp_ctx sp_ctx;
+typedef struct sp_specs sp_specs;
+typedef struct sp_model sp_model;
+
+/* Flags of sp_load_gpu_specs */
+#define SP_STRICT 1u  /* reject values outside Table II's ranges; default: warn */
+
+/* ---------------------------------------------------------------------- API */
+
+/* Creates a context on CUDA device `device` (must be sm_100).  Library-owned;
+ * one per device.  SP_E_ARG on a bad device, SP_E_UNSUPPORTED if it is not
+ * sm_100, SP_E_INTERNAL if CUDA is unusable. */
+sp_status sp_create(int device, sp_ctx **out);
+void sp_destroy(sp_ctx *ctx);
+
+/* Message of the context's last error or warning ("" if none).  Valid until
+ * the next call on that context.  sp_last_error(NULL) reports failures of
+ * calls that had no context (sp_create). */
+const char *sp_last_error(const sp_ctx *ctx);
+
+/* Version string and the number of SMs of the context's device. */
+const char *sp_version(void);
+int32_t sp_device_sms(const sp_ctx *ctx);
+
+/*
+ * a1 spec staging (Table II).  Copies n HOST records, validates them
+ * (SP_E_DATA on num_sms < 1 "invalid SM count", non-positive clock,
+ * bandwidth, FMA/XU throughput, smem bandwidth, register file, warps or CTAs
+ * (S:39); with SP_STRICT also values outside Table II's ranges --
+ * otherwise those set a warning readable through sp_last_error), derives the
+ * per-spec constants used by Eq.4-5 and C_mem = B/BW and uploads
+ * them.  The handle is immutable and may be shared across streams.
+ */
+sp_status sp_load_gpu_specs(sp_ctx *ctx, const sp_gpu_spec *host_specs, int32_t n,
+                            uint32_t flags, sp_specs **out);
+void sp_free_specs(sp_specs *specs);
+int32_t sp_specs_count(const sp_specs *specs);
+
+/*
+ * Estimator load.  Copies the HOST description, checks
+ * n_in == 4*pipes(family)+7 and that every value is finite and sigma, var,
+ * bn_eps are sane (SP_E_DATA otherwise), and builds device layouts:
+ * SP_MLP_FP32 keeps fp32 weights with BN as a per-unit affine; SP_MLP_BF16
+ * folds each BN affine into the next layer (algebraically exact, R18) and
+ * packs bf16 weights in the tcgen05 UMMA shared-memory layout.
+ */
+sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *desc, sp_model **out);
+void sp_free_model(sp_model *model);
+
+/*
+ * Feature stage, steps a2..a9: for every pair, decompose the kernel into tasks
+ * (Eq.1), deal them round-robin onto the spec's SMs (Eq.2, R5), accumulate
+ * per-SM and GPU demands (Eq.3), and derive cycles and t_theory
+ * (Eq.4-5, R9).  Writes out->ints/flts/status for out->n_pairs pairs.
+ *   cfg:   configs of one family (DEVICE arrays).
+ *   specs: from sp_load_gpu_specs.
+ *   pairs: CROSS (n_pairs = (spec_end-spec_begin)*n_configs) or LIST.
+ *   out:   caller-owned DEVICE SoA; out->family must equal cfg->family and
+ *          out->n_pairs the pairing's pair count.
+ * Integer slots are exact (bit-identical to the fp64 oracle); float slots are
+ * computed in fp64 from the exact integers and rounded once to fp32 (R20).
+ * Synchronous errors: SP_E_ARG (NULL, sizes, family/field-count mismatch,
+ * spec index range), SP_E_UNSUPPORTED (attention on a spec with > 4096 SMs),
+ * SP_E_INTERNAL (launch failure).  Per-pair domain errors go to status[p].
+ */
+sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs,
+                       const sp_pairing *pairs, const sp_features *out, void *stream);
+
+/*
+ * Predictor stage, steps a10..a12: for each pair p < in->n_pairs,
+ * x = normalised Table IV vector of in (O8-O9), e = sigmoid(MLP(x)),
+ * latency_us[p] = t_theory_us[p] / e.  efficiency may be NULL.  Pairs with
+ * status != 0 yield NaN.  latency_us / efficiency: DEVICE fp32 [n_pairs].
+ * SP_E_ARG if in->family != the model's family.
+ */
+sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_features *in, float *latency_us,
+                     float *efficiency, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SYNPERF_H_ */

@@ -29,7 +29,7 @@ FLT_NAMES = ["cg_T", "cg_F", "cg_X", "cs_T", "cs_F", "cs_X", "glob_gpu", "l2_gpu
 def build(force: bool = False) -> str:
     """Compile the oracle (gcc, -O2, no fast-math, OpenMP)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-shared", "-fPIC",
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fopenmp", "-shared", "-fPIC",
                                "-o", LIB, SRC, "-lm"])
     return LIB
 
@@ -44,8 +44,9 @@ def lib():
         L = C.CDLL(LIB)
         L.orc_featurize.restype = C.c_int
         L.orc_featurize.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
-                                    C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
-                                    C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+                                    C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                    C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_int]
         L.orc_predict.restype = C.c_int
         L.orc_predict.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
@@ -97,7 +98,7 @@ def featurize(batch, specs: np.ndarray, cfg_idx=None, spec_idx=None, flags: int 
     flts = np.zeros((N_FLTS, n), np.float64)
     status = np.zeros(n, np.uint8)
     rc = lib().orc_featurize(batch.family, batch.n_configs, _ptr(fields), fields.shape[1],
-                             _ptr(ragged), _ptr(roff), _ptr(specs), n, _ptr(cfg_idx),
+                             _ptr(ragged), _ptr(roff), _ptr(specs), len(specs), n, _ptr(cfg_idx),
                              _ptr(spec_idx), flags, _ptr(ints), _ptr(flts), _ptr(status),
                              nthreads)
     if rc != 0:

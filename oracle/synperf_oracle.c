@@ -53,7 +53,7 @@ enum { DT_BF16 = 0, DT_FP16 = 1, DT_FP32 = 2, DT_FP8 = 3 };
 /* per-pair status codes (include/synperf.h sp_pair_status) */
 enum {
   ST_OK = 0, ST_DIM = 1, ST_TILE = 2, ST_HEADS = 3, ST_HIST = 4,
-  ST_CAUSAL = 5, ST_RES = 6, ST_DTYPE = 7, ST_RANGE = 8
+  ST_CAUSAL = 5, ST_RES = 6, ST_DTYPE = 7, ST_RANGE = 8, ST_INDEX = 9
 };
 
 /* field order of each family (workloads/gen.py FIELDS) */
@@ -83,10 +83,15 @@ enum { F_CG_T, F_CG_F, F_CG_X, F_CS_T, F_CS_F, F_CS_X, F_GLOB_G, F_L2_G, F_GLOB_
 
 #define INT32_LIM 2147483647LL
 #define UINT32_LIM 4294967295LL
+#define INT64_LIM 9223372036854775807LL
+
+/* Demands are accumulated in 128-bit integers so that the exact-range rule
+ * (status 8 when a count does not fit in int64, R22) is decided exactly. */
+typedef __int128 i128;
+#define SAT128 ((i128)1 << 100)
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
-static int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
 
 static int bytes_per_elem(int dtype) {
   switch (dtype) {
@@ -102,18 +107,19 @@ static int bytes_per_elem(int dtype) {
 typedef struct {
   int64_t n_sm;
   int64_t t;          /* tasks enumerated so far (= next task index) */
-  int64_t *sm_sum;    /* [n_sm][4] explicit per-SM sums  S_j(X) */
+  i128 *sm_sum;       /* [n_sm][4] explicit per-SM sums  S_j(X) */
   int64_t *sm_count;  /* [n_sm] tasks per SM */
-  int64_t total[4];   /* sum over the task list */
+  i128 total[4];      /* sum over the task list */
 } orc_sched;
 
 /* One task tau_t with demands d[4]: Eq.2 cyclic dealing (R5) + O4 totals. */
-static void emit_task(orc_sched *s, int64_t ops_t, int64_t ops_f, int64_t ops_x, int64_t bytes) {
-  int64_t d[4] = {ops_t, ops_f, ops_x, bytes};
+static void emit_task(orc_sched *s, i128 ops_t, i128 ops_f, i128 ops_x, i128 bytes) {
+  i128 d[4] = {ops_t, ops_f, ops_x, bytes};
   int64_t j = s->t % s->n_sm; /* M: task t -> SM (t mod N_SM) */
   for (int q = 0; q < 4; ++q) {
-    s->sm_sum[j * 4 + q] += d[q];
-    s->total[q] += d[q];
+    /* saturate far above int64 (only the > INT64_MAX decision matters there) */
+    if (s->sm_sum[j * 4 + q] < SAT128) s->sm_sum[j * 4 + q] += d[q];
+    if (s->total[q] < SAT128) s->total[q] += d[q];
   }
   s->sm_count[j] += 1;
   s->t += 1;
@@ -133,9 +139,9 @@ static void decompose_gemm(const int64_t *x, int flags, orc_sched *s) {
     for (int64_t j = 0; j < cdiv(N, tn); ++j) {
       if (flags & ORC_CLAMPED) {
         int64_t ma = imin(tm, M - i * tm), na = imin(tn, N - j * tn);
-        emit_task(s, 2 * ma * na * K, 0, 0, (ma + na) * K * bpe);
+        emit_task(s, (i128)2 * ma * na * K, 0, 0, (i128)(ma + na) * K * bpe);
       } else {
-        emit_task(s, 2 * tm * tn * kpad, 0, 0, (tm + tn) * kpad * bpe);
+        emit_task(s, (i128)2 * tm * tn * kpad, 0, 0, (i128)(tm + tn) * kpad * bpe);
       }
     }
   }
@@ -157,9 +163,9 @@ static void decompose_moe(const int64_t *x, const int32_t *hist, int flags, orc_
       for (int64_t nb = 0; nb < cdiv(N, bn); ++nb) {
         if (flags & ORC_CLAMPED) {
           int64_t ma = imin(bm, te - mb * bm), na = imin(bn, N - nb * bn);
-          emit_task(s, 2 * ma * na * H, 0, 0, (ma + na) * H * bpe);
+          emit_task(s, (i128)2 * ma * na * H, 0, 0, (i128)(ma + na) * H * bpe);
         } else {
-          emit_task(s, 2 * bm * bn * hpad, 0, 0, (bm + bn) * hpad * bpe);
+          emit_task(s, (i128)2 * bm * bn * hpad, 0, 0, (i128)(bm + bn) * hpad * bpe);
         }
       }
     }
@@ -171,7 +177,7 @@ static void decompose_moe(const int64_t *x, const int32_t *hist, int flags, orc_
  * Table III), loads = input row + weight vector = 2*dim elements. */
 static void decompose_rmsnorm(const int64_t *x, orc_sched *s) {
   int64_t seq = x[R_SEQ], dim = x[R_DIM], bpe = bytes_per_elem((int)x[R_DTYPE]);
-  for (int64_t row = 0; row < seq; ++row) emit_task(s, 0, 3 * dim, 1, 2 * dim * bpe);
+  for (int64_t row = 0; row < seq; ++row) emit_task(s, 0, (i128)3 * dim, 1, (i128)2 * dim * bpe);
 }
 
 /* SiLU&Mul (Table V, FMA+XU; R15): one task per row; dim = output
@@ -179,7 +185,7 @@ static void decompose_rmsnorm(const int64_t *x, orc_sched *s) {
  * up halves = 2*dim elements. */
 static void decompose_silu(const int64_t *x, orc_sched *s) {
   int64_t seq = x[R_SEQ], dim = x[R_DIM], bpe = bytes_per_elem((int)x[R_DTYPE]);
-  for (int64_t row = 0; row < seq; ++row) emit_task(s, 0, 4 * dim, 2 * dim, 2 * dim * bpe);
+  for (int64_t row = 0; row < seq; ++row) emit_task(s, 0, (i128)4 * dim, (i128)2 * dim, (i128)2 * dim * bpe);
 }
 
 /* Attention, FlashInfer FA2 (Table V; Eq.3 alpha = 4; P:262
@@ -210,12 +216,12 @@ static void decompose_attention(const int64_t *x, const int32_t *req, int flags,
           int64_t len = chunk > 0 ? imin(chunk, kv_need - c * chunk) : kv_need;
           if (flags & ORC_CLAMPED) {
             int64_t qr = imin(bq, rows - i * bq);
-            emit_task(s, 4 * qr * len * hd, 0, qr * len + qr * cdiv(len, bkv),
-                      (qr * hd + 2 * len * hd) * bpe);
+            emit_task(s, (i128)4 * qr * len * hd, 0, (i128)qr * len + (i128)qr * cdiv(len, bkv),
+                      ((i128)qr * hd + (i128)2 * len * hd) * bpe);
           } else {
             int64_t kv_eff = cdiv(len, bkv) * bkv;
-            emit_task(s, 4 * bq * kv_eff * hd, 0, bq * kv_eff + bq * (kv_eff / bkv),
-                      (bq * hd + 2 * kv_eff * hd) * bpe);
+            emit_task(s, (i128)4 * bq * kv_eff * hd, 0, (i128)bq * kv_eff + (i128)bq * (kv_eff / bkv),
+                      ((i128)bq * hd + (i128)2 * kv_eff * hd) * bpe);
           }
         }
       }
@@ -250,7 +256,7 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
       if (x[E_DTYPE] != DT_BF16 && x[E_DTYPE] != DT_FP16) return ST_DTYPE;
       int64_t mt = x[E_M] * x[E_TOPK];
       if (mt > INT32_LIM) return ST_RANGE;
-      int64_t T = 0;
+      i128 T = 0;
       if (rag) {
         int64_t sum = 0;
         for (int64_t e = 0; e < x[E_E]; ++e) {
@@ -261,11 +267,11 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
         for (int64_t e = 0; e < x[E_E]; ++e) T += cdiv(rag[e], x[E_BM]);
       } else {
         int64_t q = mt / x[E_E], r = mt % x[E_E];
-        T = r * cdiv(q + 1, x[E_BM]) + (x[E_E] - r) * cdiv(q, x[E_BM]);
+        T = (i128)r * cdiv(q + 1, x[E_BM]) + (i128)(x[E_E] - r) * cdiv(q, x[E_BM]);
       }
       T *= cdiv(x[E_N], x[E_BN]);
       if (T > INT32_LIM) return ST_RANGE;
-      *T_out = T;
+      *T_out = (int64_t)T;
       return ST_OK;
     }
     case FAM_RMSNORM: case FAM_SILU: {
@@ -315,33 +321,39 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
 
 /* O2: per-task resource footprint and occupancy, R6 register units. */
 static int64_t occupancy(int fam, const int64_t *x, const orc_spec *sp) {
-  int64_t smem = 0, warps = 0, regs = 0;
+  i128 smem = 0;
+  int64_t warps = 0, regs = 0;
   switch (fam) {
     case FAM_GEMM:
       warps = x[G_WARPS]; regs = x[G_REGS];
-      smem = x[G_SMEM] > 0 ? x[G_SMEM]
-                           : x[G_STAGES] * (x[G_TM] + x[G_TN]) * x[G_BK] * bytes_per_elem((int)x[G_DTYPE]);
+      smem = x[G_SMEM] > 0 ? (i128)x[G_SMEM]
+                           : (i128)x[G_STAGES] * (x[G_TM] + x[G_TN]) * x[G_BK] * bytes_per_elem((int)x[G_DTYPE]);
       break;
     case FAM_MOE:
       warps = x[E_WARPS]; regs = x[E_REGS];
-      smem = x[E_SMEM] > 0 ? x[E_SMEM]
-                           : x[E_STAGES] * (x[E_BM] + x[E_BN]) * x[E_BK] * bytes_per_elem((int)x[E_DTYPE]);
+      smem = x[E_SMEM] > 0 ? (i128)x[E_SMEM]
+                           : (i128)x[E_STAGES] * (x[E_BM] + x[E_BN]) * x[E_BK] * bytes_per_elem((int)x[E_DTYPE]);
       break;
     case FAM_ATTENTION:
       warps = x[A_WARPS]; regs = x[A_REGS];
-      smem = x[A_SMEM] > 0 ? x[A_SMEM]
-                           : (x[A_BQ] + 2 * x[A_BKV]) * x[A_HD] * bytes_per_elem((int)x[A_DTYPE]);
+      smem = x[A_SMEM] > 0 ? (i128)x[A_SMEM]
+                           : (i128)(x[A_BQ] + 2 * x[A_BKV]) * x[A_HD] * bytes_per_elem((int)x[A_DTYPE]);
       break;
     default:
       warps = x[R_WARPS]; regs = x[R_REGS];
-      smem = x[R_SMEM] > 0 ? x[R_SMEM] : warps * 4;
+      smem = x[R_SMEM] > 0 ? (i128)x[R_SMEM] : (i128)warps * 4;
       break;
   }
-  int64_t occ = sp->max_ctas_per_sm;
-  if (smem > 0) occ = imin(occ, sp->smem_per_sm_bytes / smem);
-  occ = imin(occ, (sp->regfile_per_sm_bytes / 4) / (regs * 32 * warps));
-  occ = imin(occ, sp->max_warps_per_sm / warps);
-  return imax(1, occ);
+  i128 occ = sp->max_ctas_per_sm;
+  if (smem > 0) {
+    i128 q = (i128)sp->smem_per_sm_bytes / smem;
+    if (q < occ) occ = q;
+  }
+  i128 rq = (i128)(sp->regfile_per_sm_bytes / 4) / ((i128)regs * 32 * warps);
+  if (rq < occ) occ = rq;
+  i128 wq = (i128)sp->max_warps_per_sm / warps;
+  if (wq < occ) occ = wq;
+  return occ < 1 ? 1 : (int64_t)occ;
 }
 
 /* Pipes present per family (Table V): bit 0 Tensor, 1 FMA, 2 XU */
@@ -377,7 +389,7 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
   orc_sched s;
   memset(&s, 0, sizeof s);
   s.n_sm = sp->num_sms;
-  s.sm_sum = (int64_t *)calloc((size_t)s.n_sm * 4, sizeof(int64_t));
+  s.sm_sum = (i128 *)calloc((size_t)s.n_sm * 4, sizeof(i128));
   s.sm_count = (int64_t *)calloc((size_t)s.n_sm, sizeof(int64_t));
 
   switch (fam) { /* O1 + O3 + O4 */
@@ -389,22 +401,39 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
   }
 
   /* O5: per-quantity max over SMs (R7) */
-  int64_t mx[4] = {0, 0, 0, 0};
+  i128 mx128[4] = {0, 0, 0, 0};
   for (int64_t j = 0; j < s.n_sm; ++j)
-    for (int q = 0; q < 4; ++q) mx[q] = imax(mx[q], s.sm_sum[j * 4 + q]);
+    for (int q = 0; q < 4; ++q)
+      if (s.sm_sum[j * 4 + q] > mx128[q]) mx128[q] = s.sm_sum[j * 4 + q];
+
+  /* exact-range rule (R22): every count must fit in int64; max <= total */
+  int range_ok = 1;
+  for (int q = 0; q < 4; ++q)
+    if (s.total[q] > (i128)INT64_LIM) range_ok = 0;
+  free(s.sm_sum);
+  free(s.sm_count);
+  if (!range_ok) {
+    set_error(ints, flts);
+    return ST_RANGE;
+  }
+  int64_t mx[4], tot[4];
+  for (int q = 0; q < 4; ++q) {
+    mx[q] = (int64_t)mx128[q];
+    tot[q] = (int64_t)s.total[q];
+  }
 
   /* O2 */
   int64_t occ = occupancy(fam, x, sp);
   ints[I_NTASKS] = s.t;
   ints[I_OCC] = occ;
   ints[I_WAVES] = cdiv(s.t, (int64_t)sp->num_sms * occ);
-  ints[I_TOT_T] = s.total[0];
-  ints[I_TOT_F] = s.total[1];
-  ints[I_TOT_X] = s.total[2];
+  ints[I_TOT_T] = tot[0];
+  ints[I_TOT_F] = tot[1];
+  ints[I_TOT_X] = tot[2];
   ints[I_MAX_T] = mx[0];
   ints[I_MAX_F] = mx[1];
   ints[I_MAX_X] = mx[2];
-  ints[I_BYTES] = s.total[3];
+  ints[I_BYTES] = tot[3];
   ints[I_BYTES_MAX] = mx[3];
 
   /* O6: Eq.4 C_p = N_ops,p / Th_p ; Eq.5 C_p^GPU = N^GPU / (N_SM Th_p) */
@@ -413,7 +442,7 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
   int pipes = pipes_of(fam);
   for (int p = 0; p < 3; ++p) {
     if (pipes & (1 << p)) {
-      flts[F_CG_T + p] = (double)s.total[p] / (nsm * th[p]);
+      flts[F_CG_T + p] = (double)tot[p] / (nsm * th[p]);
       flts[F_CS_T + p] = (double)mx[p] / th[p];
     } else {
       flts[F_CG_T + p] = 0.0;
@@ -421,7 +450,7 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
     }
   }
   /* C_mem = B / BW in SM-clock cycles: B bytes / (BW GB/s * 1e3 B/us) * f cycles/us (R8) */
-  double B = (double)s.total[3], Bm = (double)mx[3];
+  double B = (double)tot[3], Bm = (double)mx[3];
   flts[F_GLOB_G] = B / (sp->bw_global_gbps * 1e3) * f;
   flts[F_L2_G] = B / (sp->bw_l2_gbps * 1e3) * f;
   flts[F_GLOB_S] = Bm / (sp->bw_global_gbps * 1e3 / nsm) * f;
@@ -433,9 +462,6 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
   for (int p = 0; p < 3; ++p)
     if (pipes & (1 << p)) roof = fmax(roof, flts[F_CG_T + p]);
   flts[F_TTHEORY] = roof / f;
-
-  free(s.sm_sum);
-  free(s.sm_count);
   return ST_OK;
 }
 
@@ -460,10 +486,9 @@ static int n_fields_of(int fam) {
  */
 int orc_featurize(int fam, int64_t n_configs, const int32_t *fields, int64_t field_ld,
                   const int32_t *ragged, const int64_t *ragged_off, const orc_spec *specs,
-                  int64_t n_pairs, const int64_t *cfg_idx, const int64_t *spec_idx, int flags,
+                  int64_t n_specs, int64_t n_pairs, const int64_t *cfg_idx, const int64_t *spec_idx, int flags,
                   int64_t *ints, double *flts, uint8_t *status, int nthreads) {
   if (fam < 0 || fam > 4) return -1;
-  (void)n_configs;
   int nf = n_fields_of(fam);
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -473,6 +498,13 @@ int orc_featurize(int fam, int64_t n_configs, const int32_t *fields, int64_t fie
     int64_t x[16], pi[N_I];
     double pf[N_F];
     int64_t c = cfg_idx[p];
+    if (c < 0 || c >= n_configs || spec_idx[p] < 0 || spec_idx[p] >= n_specs) {
+      set_error(pi, pf);
+      status[p] = ST_INDEX;
+      for (int k = 0; k < N_I; ++k) ints[(int64_t)k * n_pairs + p] = pi[k];
+      for (int k = 0; k < N_F; ++k) flts[(int64_t)k * n_pairs + p] = pf[k];
+      continue;
+    }
     load_config(fields, field_ld, c, nf, x);
     const int32_t *rag = NULL;
     if (ragged_off && ragged_off[c] >= 0) rag = ragged + ragged_off[c];
@@ -509,7 +541,7 @@ int64_t orc_task_list(int fam, const int32_t *fields, int64_t field_ld, int64_t 
   s.n_sm = T > 0 ? T : 1;
   if (s.n_sm > cap) return -(int64_t)100;
   (void)n_sm;
-  s.sm_sum = (int64_t *)calloc((size_t)s.n_sm * 4, sizeof(int64_t));
+  s.sm_sum = (i128 *)calloc((size_t)s.n_sm * 4, sizeof(i128));
   s.sm_count = (int64_t *)calloc((size_t)s.n_sm, sizeof(int64_t));
   switch (fam) {
     case FAM_GEMM: decompose_gemm(x, flags, &s); break;
@@ -518,7 +550,7 @@ int64_t orc_task_list(int fam, const int32_t *fields, int64_t field_ld, int64_t 
     case FAM_SILU: decompose_silu(x, &s); break;
     case FAM_ATTENTION: decompose_attention(x, rag, flags, &s); break;
   }
-  memcpy(out, s.sm_sum, (size_t)s.t * 4 * sizeof(int64_t));
+  for (int64_t k = 0; k < s.t * 4; ++k) out[k] = (int64_t)s.sm_sum[k];
   int64_t n = s.t;
   free(s.sm_sum);
   free(s.sm_count);

@@ -1,0 +1,106 @@
+"""ctypes mirror of include/synperf.h (argument marshalling only).
+
+Loads the in-tree libsynperf.so.  There is no fallback: if the library is
+missing or cannot be loaded, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsynperf.so")
+
+# sp_status
+SP_OK, SP_E_ARG, SP_E_DATA, SP_E_INTERNAL, SP_E_UNSUPPORTED = 0, 1, 2, 3, 4
+STATUS_NAMES = {0: "SP_OK", 1: "SP_E_ARG", 2: "SP_E_DATA", 3: "SP_E_INTERNAL", 4: "SP_E_UNSUPPORTED"}
+# sp_family
+SP_GEMM, SP_ATTENTION, SP_FUSED_MOE, SP_RMSNORM, SP_SILU_MUL = 0, 1, 2, 3, 4
+NFIELDS = {SP_GEMM: 11, SP_ATTENTION: 12, SP_FUSED_MOE: 14, SP_RMSNORM: 6, SP_SILU_MUL: 6}
+# sp_pairing_kind
+SP_PAIRS_CROSS, SP_PAIRS_LIST = 0, 1
+# sp_precision
+SP_MLP_FP32, SP_MLP_BF16 = 0, 1
+SP_STRICT = 1
+
+
+class sp_gpu_spec(C.Structure):
+    _fields_ = [
+        ("name", C.c_char * 32),
+        ("cc_major", C.c_int32), ("cc_minor", C.c_int32), ("num_sms", C.c_int32),
+        ("th_tensor_bf16", C.c_int32), ("th_tensor_fp16", C.c_int32), ("th_tensor_fp8", C.c_int32),
+        ("th_fma", C.c_int32), ("th_xu", C.c_int32), ("smem_bw_bytes_per_clk", C.c_int32),
+        ("smem_per_sm_bytes", C.c_int32), ("regfile_per_sm_bytes", C.c_int32),
+        ("max_warps_per_sm", C.c_int32), ("max_ctas_per_sm", C.c_int32), ("reserved_", C.c_int32),
+        ("sm_clock_mhz", C.c_double), ("bw_global_gbps", C.c_double), ("bw_l2_gbps", C.c_double),
+    ]
+
+
+assert C.sizeof(sp_gpu_spec) == 112
+
+
+class sp_config_batch(C.Structure):
+    _fields_ = [
+        ("family", C.c_int32), ("n_fields", C.c_int32), ("n_configs", C.c_int64),
+        ("field_ld", C.c_int64), ("fields", C.c_void_p), ("ragged", C.c_void_p),
+        ("ragged_off", C.c_void_p), ("n_ragged", C.c_int64),
+    ]
+
+
+class sp_pairing(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("spec_begin", C.c_int32), ("spec_end", C.c_int32),
+        ("reserved_", C.c_int32), ("n_pairs", C.c_int64), ("cfg_idx", C.c_void_p),
+        ("spec_idx", C.c_void_p),
+    ]
+
+
+class sp_features(C.Structure):
+    _fields_ = [
+        ("family", C.c_int32), ("reserved_", C.c_int32), ("n_pairs", C.c_int64), ("ld", C.c_int64),
+        ("ints", C.c_void_p), ("flts", C.c_void_p), ("status", C.c_void_p),
+    ]
+
+
+MLP_ARRAYS = ["mu", "sigma", "w1", "b1", "g1", "be1", "m1", "v1", "w2", "b2", "g2", "be2", "m2",
+              "v2", "w3", "b3", "g3", "be3", "m3", "v3", "w4"]
+
+
+class sp_mlp_desc(C.Structure):
+    _fields_ = [("family", C.c_int32), ("n_in", C.c_int32), ("precision", C.c_int32),
+                ("reserved_", C.c_int32)] + [(k, C.c_void_p) for k in MLP_ARRAYS] + [
+        ("b4", C.c_float), ("bn_eps", C.c_float)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libsynperf.so not found at {LIB_PATH}; build it with "
+            "`python -m paper_2601_14910_b200.build` (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
+    sig = {
+        "sp_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "sp_destroy": (None, [vp]),
+        "sp_last_error": (C.c_char_p, [vp]),
+        "sp_version": (C.c_char_p, []),
+        "sp_device_sms": (i32, [vp]),
+        "sp_load_gpu_specs": (C.c_int, [vp, vp, i32, u32, C.POINTER(vp)]),
+        "sp_free_specs": (None, [vp]),
+        "sp_specs_count": (i32, [vp]),
+        "sp_load_model": (C.c_int, [vp, vp, C.POINTER(vp)]),
+        "sp_free_model": (None, [vp]),
+        "sp_featurize": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+        "sp_predict": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+lib = _load()
+
+EXPORTED = ["sp_create", "sp_destroy", "sp_last_error", "sp_version", "sp_device_sms",
+            "sp_load_gpu_specs", "sp_free_specs", "sp_specs_count", "sp_load_model",
+            "sp_free_model", "sp_featurize", "sp_predict"]

@@ -1,0 +1,260 @@
+"""Thin Python binding over the C-ABI (include/synperf.h).
+
+Argument marshalling only: torch supplies device memory and streams; every
+step of the prediction path runs in libsynperf.so's CUDA kernels.  Names
+follow the C entry points (sp_featurize -> Context.featurize, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import lib
+
+N_INTS, N_FLTS = 11, 12
+INT_NAMES = ["n_tasks", "occupancy", "waves", "tot_T", "tot_F", "tot_X", "max_T", "max_F",
+             "max_X", "bytes", "bytes_max"]
+FLT_NAMES = ["cg_T", "cg_F", "cg_X", "cs_T", "cs_F", "cs_X", "glob_gpu", "l2_gpu", "glob_sm",
+             "l2_sm", "smem_sm", "t_theory_us"]
+
+
+class SynPerfError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_abi.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) or None
+
+
+@dataclass
+class DeviceBatch:
+    """Device-resident configs of one family (the C sp_config_batch)."""
+
+    family: int
+    fields: torch.Tensor  # int32 [n_fields, n_configs]
+    ragged: torch.Tensor | None
+    ragged_off: torch.Tensor | None
+
+    @property
+    def n_configs(self) -> int:
+        return int(self.fields.shape[1])
+
+    @staticmethod
+    def from_host(batch, device, non_blocking: bool = False) -> "DeviceBatch":
+        """From any object with .family, .fields (int32 [F, C]), .ragged, .ragged_off."""
+        dev = torch.device(device)
+
+        def up(a, dt):
+            if a is None:
+                return None
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+            return t.to(device=dev, dtype=dt, non_blocking=non_blocking).contiguous()
+
+        return DeviceBatch(int(batch.family), up(batch.fields, torch.int32),
+                           up(batch.ragged, torch.int32), up(batch.ragged_off, torch.int64))
+
+    def c_struct(self) -> _abi.sp_config_batch:
+        s = _abi.sp_config_batch()
+        s.family = self.family
+        s.n_fields = int(self.fields.shape[0])
+        s.n_configs = self.n_configs
+        s.field_ld = int(self.fields.stride(0)) if self.n_configs > 0 else 0
+        s.fields = self.fields.data_ptr() if self.n_configs > 0 else None
+        if self.ragged is not None and self.ragged.numel() > 0:
+            s.ragged = self.ragged.data_ptr()
+            s.n_ragged = self.ragged.numel()
+        if self.ragged_off is not None and self.ragged_off.numel() > 0:
+            s.ragged_off = self.ragged_off.data_ptr()
+        return s
+
+
+@dataclass
+class Features:
+    """Caller-owned device feature record (the C sp_features), SoA."""
+
+    family: int
+    ints: torch.Tensor  # int64 [11, ld]
+    flts: torch.Tensor  # fp32 [12, ld]
+    status: torch.Tensor  # uint8 [n_pairs]
+    n_pairs: int
+
+    @staticmethod
+    def empty(family: int, n_pairs: int, device) -> "Features":
+        dev = torch.device(device)
+        return Features(family, torch.empty((N_INTS, max(n_pairs, 1)), dtype=torch.int64, device=dev),
+                        torch.empty((N_FLTS, max(n_pairs, 1)), dtype=torch.float32, device=dev),
+                        torch.empty(max(n_pairs, 1), dtype=torch.uint8, device=dev), n_pairs)
+
+    def view(self, start: int, n: int) -> "Features":
+        """Sub-range [start, start+n) sharing storage (the C struct uses ld = full width)."""
+        return Features(self.family, self.ints[:, start:], self.flts[:, start:],
+                        self.status[start:], n)
+
+    def c_struct(self) -> _abi.sp_features:
+        s = _abi.sp_features()
+        s.family = self.family
+        s.n_pairs = self.n_pairs
+        s.ld = int(self.ints.stride(0))
+        assert int(self.flts.stride(0)) == s.ld, "ints and flts must share a leading dimension"
+        s.ints = self.ints.data_ptr()
+        s.flts = self.flts.data_ptr()
+        s.status = self.status.data_ptr()
+        return s
+
+
+def cross(spec_begin: int, spec_end: int) -> _abi.sp_pairing:
+    p = _abi.sp_pairing()
+    p.kind = _abi.SP_PAIRS_CROSS
+    p.spec_begin, p.spec_end = int(spec_begin), int(spec_end)
+    return p
+
+
+def pair_list(cfg_idx: torch.Tensor, spec_idx: torch.Tensor) -> _abi.sp_pairing:
+    assert cfg_idx.dtype == torch.int64 and spec_idx.dtype == torch.int32
+    assert cfg_idx.is_contiguous() and spec_idx.is_contiguous()
+    p = _abi.sp_pairing()
+    p.kind = _abi.SP_PAIRS_LIST
+    p.n_pairs = int(cfg_idx.numel())
+    p.cfg_idx = cfg_idx.data_ptr() if p.n_pairs else None
+    p.spec_idx = spec_idx.data_ptr() if p.n_pairs else None
+    return p
+
+
+class Specs:
+    def __init__(self, ctx: "Context", handle: int, n: int):
+        self._ctx, self._h, self.n = ctx, handle, n
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __len__(self):
+        return self.n
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.sp_free_specs(self._h)
+            self._h = None
+
+
+class Model:
+    def __init__(self, ctx: "Context", handle: int, family: int, precision: int):
+        self._ctx, self._h, self.family, self.precision = ctx, handle, family, precision
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.sp_free_model(self._h)
+            self._h = None
+
+
+class Context:
+    """sp_ctx on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        st = lib.sp_create(int(device), C.byref(h))
+        if st != _abi.SP_OK:
+            raise SynPerfError(st, lib.sp_last_error(None).decode())
+        self._h = h.value
+        self.device = int(device)
+        self.torch_device = torch.device("cuda", self.device)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.sp_destroy(self._h)
+            self._h = None
+
+    @property
+    def num_sms(self) -> int:
+        return int(lib.sp_device_sms(self._h))
+
+    def last_error(self) -> str:
+        return lib.sp_last_error(self._h).decode()
+
+    def _check(self, st):
+        if st != _abi.SP_OK:
+            raise SynPerfError(st, self.last_error())
+
+    # -- a1
+    def load_gpu_specs(self, specs: np.ndarray, strict: bool = False) -> Specs:
+        arr = np.ascontiguousarray(specs)
+        assert arr.dtype.itemsize == C.sizeof(_abi.sp_gpu_spec)
+        h = C.c_void_p()
+        self._check(lib.sp_load_gpu_specs(self._h, arr.ctypes.data, len(arr),
+                                          _abi.SP_STRICT if strict else 0, C.byref(h)))
+        return Specs(self, h.value, len(arr))
+
+    # -- estimator
+    def load_model(self, model: dict, precision: str = "bf16") -> Model:
+        d = _abi.sp_mlp_desc()
+        d.family = int(model["family"])
+        d.n_in = int(model["n_in"])
+        d.precision = _abi.SP_MLP_BF16 if precision == "bf16" else _abi.SP_MLP_FP32
+        keep = []
+        for k in _abi.MLP_ARRAYS:
+            a = np.ascontiguousarray(model[k], dtype=np.float32)
+            keep.append(a)
+            setattr(d, k, a.ctypes.data)
+        d.b4 = float(model["b4"])
+        d.bn_eps = float(model.get("bn_eps", 1e-5))
+        h = C.c_void_p()
+        self._check(lib.sp_load_model(self._h, C.byref(d), C.byref(h)))
+        del keep
+        return Model(self, h.value, d.family, d.precision)
+
+    # -- feature stage (a2..a9)
+    def featurize(self, batch: DeviceBatch, specs: Specs, out: Features, pairs=None,
+                  stream=None) -> Features:
+        if pairs is None:
+            pairs = cross(0, len(specs))
+        cb = batch.c_struct()
+        fs = out.c_struct()
+        self._check(lib.sp_featurize(self._h, C.byref(cb), specs.handle, C.byref(pairs),
+                                     C.byref(fs), _stream_ptr(stream)))
+        return out
+
+    # -- predictor stage (a10..a12)
+    def predict(self, model: Model, feats: Features, latency: torch.Tensor,
+                efficiency: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        assert latency.dtype == torch.float32 and latency.is_contiguous()
+        assert latency.numel() >= feats.n_pairs
+        fs = feats.c_struct()
+        self._check(lib.sp_predict(self._h, model.handle, C.byref(fs), latency.data_ptr(),
+                                   efficiency.data_ptr() if efficiency is not None else None,
+                                   _stream_ptr(stream)))
+        return latency
+
+    # -- end-to-end convenience: host configs in, host latencies out
+    def predict_host(self, batch, specs: Specs, model: Model, spec_range=None,
+                     out: np.ndarray | None = None, stream=None) -> np.ndarray:
+        """The user-facing call: host (pinned or pageable) config arrays ->
+        H2D -> featurize -> predict -> D2H of fp32 latencies (spec-major)."""
+        g0, g1 = spec_range if spec_range is not None else (0, len(specs))
+        db = DeviceBatch.from_host(batch, self.torch_device, non_blocking=True)
+        n = (g1 - g0) * db.n_configs
+        feats = Features.empty(db.family, n, self.torch_device)
+        lat = torch.empty(max(n, 1), dtype=torch.float32, device=self.torch_device)
+        self.featurize(db, specs, feats, cross(g0, g1), stream)
+        self.predict(model, feats, lat, None, stream)
+        host = lat[:n].to("cpu", non_blocking=False)
+        if out is not None:
+            out[:n] = host.numpy()
+            return out
+        return host.numpy()
+
+
+def features_to_host(f: Features) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    n = f.n_pairs
+    return (f.ints[:, :n].cpu().numpy(), f.flts[:, :n].cpu().numpy(), f.status[:n].cpu().numpy())

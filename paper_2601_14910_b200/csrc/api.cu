@@ -1,0 +1,501 @@
+// Host side of the C-ABI (include/synperf.h): argument validation, spec
+// staging (step a1), model layout, per-range attention plans and kernel
+// dispatch.  No exception crosses the ABI; every entry point returns an
+// sp_status and records a message for sp_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sp_internal.h"
+#include "synperf.h"
+
+using namespace sp;
+
+struct sp_ctx {
+  int device = 0;
+  int num_sms = 0;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_noctx_err;
+
+struct DevBuf {
+  void *p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc_copy(const void *host, size_t bytes) {
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+    if (e != cudaSuccess) { p = nullptr; return e; }
+    if (bytes) e = cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice);
+    return e;
+  }
+};
+
+sp_status fail(sp_ctx *ctx, sp_status st, const std::string &msg) {
+  if (ctx) ctx->err = msg;
+  else g_noctx_err = msg;
+  return st;
+}
+
+sp_status cuda_fail(sp_ctx *ctx, int e, const char *what) {
+  return fail(ctx, SP_E_INTERNAL, std::string(what) + ": " + cudaGetErrorString((cudaError_t)e));
+}
+
+int nfields_of(int fam) {
+  switch (fam) {
+    case SP_GEMM: return SP_NFIELDS_GEMM;
+    case SP_ATTENTION: return SP_NFIELDS_ATTENTION;
+    case SP_FUSED_MOE: return SP_NFIELDS_FUSED_MOE;
+    case SP_RMSNORM: return SP_NFIELDS_RMSNORM;
+    case SP_SILU_MUL: return SP_NFIELDS_SILU_MUL;
+    default: return -1;
+  }
+}
+
+int pipes_count(int fam) {
+  int p = family_pipes(fam), n = 0;
+  for (int k = 0; k < 3; ++k) n += (p >> k) & 1;
+  return n;
+}
+
+constexpr int kAttnMaxSms = 4096;
+constexpr int kAttnWordBudget = 2048;
+constexpr int kAttnMaxDistinct = 16;
+
+// Device copy of one attention spec-group plan (see featurize_attention.cu).
+struct AttnPlanDev {
+  DevBuf groups, group_specs, spec_dist, distinct_n, distinct_off;
+  AttnPlan view{};
+};
+
+}  // namespace
+
+struct sp_specs {
+  sp_ctx *ctx = nullptr;
+  std::vector<sp_gpu_spec> host;
+  DevBuf dev;  // DevSpec[n]
+  int32_t n = 0;
+  int32_t max_sms = 0;
+  std::mutex mu;
+  std::map<std::pair<int, int>, std::unique_ptr<AttnPlanDev>> plans;
+};
+
+struct sp_model {
+  int family = 0, n_in = 0, precision = 0;
+  DevBuf fp32;   // fp32 path buffers (one allocation)
+  MlpFp32 m32{};
+  DevBuf bf16w;  // bf16 path: packed weights
+  DevBuf bf16v;  // bf16 path: fp32 vectors
+  MlpBf16 m16{};
+};
+
+// ------------------------------------------------------------------ context
+
+extern "C" const char *sp_version(void) { return "synperf-b200 0.1 (sm_100a)"; }
+
+extern "C" sp_status sp_create(int device, sp_ctx **out) {
+  if (!out) return fail(nullptr, SP_E_ARG, "sp_create: out is NULL");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "sp_create: cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(nullptr, SP_E_ARG, "sp_create: bad device index");
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "sp_create: cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(nullptr, SP_E_UNSUPPORTED,
+                "sp_create: libsynperf is built for sm_100a (B200); device is sm_" +
+                    std::to_string(prop.major) + std::to_string(prop.minor));
+  sp_ctx *c = new (std::nothrow) sp_ctx;
+  if (!c) return fail(nullptr, SP_E_INTERNAL, "sp_create: out of host memory");
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  *out = c;
+  return SP_OK;
+}
+
+extern "C" void sp_destroy(sp_ctx *ctx) { delete ctx; }
+
+extern "C" const char *sp_last_error(const sp_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : g_noctx_err.c_str();
+}
+
+extern "C" int32_t sp_device_sms(const sp_ctx *ctx) { return ctx ? ctx->num_sms : 0; }
+
+// ------------------------------------------------------------ a1 spec staging
+
+extern "C" sp_status sp_load_gpu_specs(sp_ctx *ctx, const sp_gpu_spec *host_specs, int32_t n,
+                                       uint32_t flags, sp_specs **out) {
+  if (!ctx || !out || (!host_specs && n > 0) || n < 0)
+    return fail(ctx, SP_E_ARG, "sp_load_gpu_specs: NULL argument or negative count");
+  *out = nullptr;
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  std::vector<DevSpec> dev(n);
+  std::string warn;
+  int32_t max_sms = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const sp_gpu_spec &s = host_specs[i];
+    const std::string who = "spec " + std::to_string(i) + " (" + std::string(s.name, strnlen(s.name, 32)) + ")";
+    // positivity invariants
+    if (s.num_sms < 1) return fail(ctx, SP_E_DATA, who + ": invalid SM count");
+    if (!(s.sm_clock_mhz > 0) || !std::isfinite(s.sm_clock_mhz))
+      return fail(ctx, SP_E_DATA, who + ": non-positive SM clock");
+    if (!(s.bw_global_gbps > 0) || !std::isfinite(s.bw_global_gbps) || !(s.bw_l2_gbps > 0) ||
+        !std::isfinite(s.bw_l2_gbps))
+      return fail(ctx, SP_E_DATA, who + ": non-positive memory bandwidth");
+    if (s.th_fma < 1 || s.th_xu < 1 || s.smem_bw_bytes_per_clk < 1)
+      return fail(ctx, SP_E_DATA, who + ": non-positive pipe throughput");
+    if (s.th_tensor_bf16 < 0 || s.th_tensor_fp16 < 0 || s.th_tensor_fp8 < 0)
+      return fail(ctx, SP_E_DATA, who + ": negative tensor throughput");
+    if (s.smem_per_sm_bytes < 0 || s.regfile_per_sm_bytes < 4 || s.max_warps_per_sm < 1 ||
+        s.max_ctas_per_sm < 1)
+      return fail(ctx, SP_E_DATA, who + ": invalid occupancy limits");
+    // Table II ranges: warnings unless SP_STRICT
+    std::string out_of_range;
+    const double cc = s.cc_major + s.cc_minor / 10.0;
+    if (cc < 8.0 || cc > 12.0) out_of_range += " compute capability";
+    if (s.num_sms < 78 || s.num_sms > 188) out_of_range += " SMs";
+    if (s.sm_clock_mhz < 1410 || s.sm_clock_mhz > 2520) out_of_range += " clock";
+    if (s.th_tensor_bf16 < 512 || s.th_tensor_bf16 > 4096) out_of_range += " tensor";
+    if (s.th_fma < 64 || s.th_fma > 128) out_of_range += " FMA";
+    if (s.th_xu != 16) out_of_range += " XU";
+    if (s.bw_global_gbps < 696 || s.bw_global_gbps > 4916) out_of_range += " global-BW";
+    if (s.bw_l2_gbps < 2430 || s.bw_l2_gbps > 10400) out_of_range += " L2-BW";
+    if (s.smem_bw_bytes_per_clk != 128) out_of_range += " smem-BW";
+    if (s.smem_per_sm_bytes < 100 * 1024 || s.smem_per_sm_bytes > 228 * 1024) out_of_range += " smem";
+    if (s.regfile_per_sm_bytes != 256 * 1024) out_of_range += " RF";
+    if (!out_of_range.empty()) {
+      if (flags & SP_STRICT) return fail(ctx, SP_E_DATA, who + ": outside Table II ranges:" + out_of_range);
+      if (warn.empty()) warn = "warning: " + who + " outside Table II ranges:" + out_of_range;
+    }
+    // derived constants in fp64 (Eq.4-5; C_mem = B/BW; R8)
+    DevSpec d{};
+    const double N = s.num_sms, f = s.sm_clock_mhz;
+    d.num_sms = s.num_sms;
+    d.smem_per_sm = s.smem_per_sm_bytes;
+    d.regs_per_sm = s.regfile_per_sm_bytes / 4;
+    d.max_warps = s.max_warps_per_sm;
+    d.max_ctas = s.max_ctas_per_sm;
+    const int32_t th_t[2] = {s.th_tensor_bf16, s.th_tensor_fp16};
+    for (int k = 0; k < 2; ++k) {
+      d.tensor_ok[k] = th_t[k] > 0;
+      d.cg_tensor[k] = th_t[k] > 0 ? 1.0 / (N * th_t[k]) : 0.0;
+      d.cs_tensor[k] = th_t[k] > 0 ? 1.0 / th_t[k] : 0.0;
+    }
+    d.cg_fma = 1.0 / (N * s.th_fma);
+    d.cs_fma = 1.0 / s.th_fma;
+    d.cg_xu = 1.0 / (N * s.th_xu);
+    d.cs_xu = 1.0 / s.th_xu;
+    d.glob_g = f / (s.bw_global_gbps * 1e3);
+    d.l2_g = f / (s.bw_l2_gbps * 1e3);
+    d.glob_s = f / (s.bw_global_gbps * 1e3 / N);
+    d.l2_s = f / (s.bw_l2_gbps * 1e3 / N);
+    d.smem_s = 1.0 / s.smem_bw_bytes_per_clk;
+    d.inv_f = 1.0 / f;
+    dev[i] = d;
+    max_sms = std::max(max_sms, s.num_sms);
+  }
+  sp_specs *h = new (std::nothrow) sp_specs;
+  if (!h) return fail(ctx, SP_E_INTERNAL, "sp_load_gpu_specs: out of host memory");
+  h->ctx = ctx;
+  h->host.assign(host_specs, host_specs + n);
+  h->n = n;
+  h->max_sms = max_sms;
+  cudaError_t e = h->dev.alloc_copy(dev.data(), dev.size() * sizeof(DevSpec));
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_fail(ctx, e, "sp_load_gpu_specs: upload");
+  }
+  *out = h;
+  ctx->err = warn;
+  return SP_OK;
+}
+
+extern "C" void sp_free_specs(sp_specs *specs) { delete specs; }
+extern "C" int32_t sp_specs_count(const sp_specs *specs) { return specs ? specs->n : 0; }
+
+// Attention plan for specs [b, e): distinct SM counts grouped so a warp's
+// accumulators fit its shared-memory budget.  Built once per range, cached.
+static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPlan **out) {
+  std::lock_guard<std::mutex> lock(sp->mu);
+  auto key = std::make_pair(b, e);
+  auto it = sp->plans.find(key);
+  if (it != sp->plans.end()) { *out = &it->second->view; return SP_OK; }
+  std::vector<int32_t> Ns;
+  for (int g = b; g < e; ++g) Ns.push_back(sp->host[g].num_sms);
+  std::sort(Ns.begin(), Ns.end());
+  Ns.erase(std::unique(Ns.begin(), Ns.end()), Ns.end());
+  if (!Ns.empty() && Ns.back() > kAttnMaxSms)
+    return fail(ctx, SP_E_UNSUPPORTED, "attention featurization supports at most 4096 SMs per spec");
+  const int budget = std::max(kAttnWordBudget, Ns.empty() ? 0 : ((Ns.back() + 3) & ~3));
+  std::vector<AttnGroup> groups;
+  std::vector<int32_t> gspecs, sdist, dn, doff;
+  size_t i = 0;
+  int words_max = 0;
+  while (i < Ns.size()) {
+    AttnGroup gr{};
+    gr.distinct_first = (int32_t)dn.size();
+    int words = 0;
+    while (i < Ns.size() && gr.n_distinct < kAttnMaxDistinct && words + Ns[i] <= budget) {
+      dn.push_back(Ns[i]);
+      doff.push_back(words);
+      words += Ns[i];
+      ++gr.n_distinct;
+      ++i;
+    }
+    words_max = std::max(words_max, (words + 3) & ~3);
+    gr.spec_first = (int32_t)gspecs.size();
+    for (int g = b; g < e; ++g) {
+      const int32_t n = sp->host[g].num_sms;
+      for (int d = 0; d < gr.n_distinct; ++d) {
+        if (dn[gr.distinct_first + d] == n) {
+          gspecs.push_back(g);
+          sdist.push_back(gr.distinct_first + d);
+          ++gr.n_specs;
+        }
+      }
+    }
+    groups.push_back(gr);
+  }
+  std::unique_ptr<AttnPlanDev> pd(new (std::nothrow) AttnPlanDev);
+  if (!pd) return fail(ctx, SP_E_INTERNAL, "attention plan: out of host memory");
+  cudaError_t err;
+  if ((err = pd->groups.alloc_copy(groups.data(), groups.size() * sizeof(AttnGroup))) != cudaSuccess ||
+      (err = pd->group_specs.alloc_copy(gspecs.data(), gspecs.size() * 4)) != cudaSuccess ||
+      (err = pd->spec_dist.alloc_copy(sdist.data(), sdist.size() * 4)) != cudaSuccess ||
+      (err = pd->distinct_n.alloc_copy(dn.data(), dn.size() * 4)) != cudaSuccess ||
+      (err = pd->distinct_off.alloc_copy(doff.data(), doff.size() * 4)) != cudaSuccess)
+    return cuda_fail(ctx, err, "attention plan upload");
+  pd->view.groups = (const AttnGroup *)pd->groups.p;
+  pd->view.group_specs = (const int32_t *)pd->group_specs.p;
+  pd->view.spec_dist = (const int32_t *)pd->spec_dist.p;
+  pd->view.distinct_n = (const int32_t *)pd->distinct_n.p;
+  pd->view.distinct_off = (const int32_t *)pd->distinct_off.p;
+  pd->view.n_groups = (int32_t)groups.size();
+  pd->view.words_per_warp = words_max;
+  *out = &pd->view;
+  sp->plans.emplace(key, std::move(pd));
+  return SP_OK;
+}
+
+// --------------------------------------------------------------- featurize
+
+extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs_c,
+                                  const sp_pairing *pairs, const sp_features *out, void *stream) {
+  if (!ctx) return fail(nullptr, SP_E_ARG, "sp_featurize: ctx is NULL");
+  if (!cfg || !specs_c || !pairs || !out) return fail(ctx, SP_E_ARG, "sp_featurize: NULL argument");
+  sp_specs *specs = const_cast<sp_specs *>(specs_c);
+  const int fam = cfg->family;
+  if (nfields_of(fam) < 0) return fail(ctx, SP_E_ARG, "sp_featurize: unknown family");
+  if (cfg->n_fields != nfields_of(fam))
+    return fail(ctx, SP_E_ARG, "sp_featurize: n_fields does not match the family's field count");
+  if (cfg->n_configs < 0 || cfg->field_ld < cfg->n_configs)
+    return fail(ctx, SP_E_ARG, "sp_featurize: bad n_configs / field_ld");
+  if (cfg->n_configs > 0 && !cfg->fields) return fail(ctx, SP_E_ARG, "sp_featurize: fields is NULL");
+  if (fam == SP_ATTENTION && cfg->n_configs > 0 && (!cfg->ragged || !cfg->ragged_off))
+    return fail(ctx, SP_E_ARG, "sp_featurize: attention needs ragged (qlen, kvlen) data");
+  if (fam == SP_FUSED_MOE && cfg->ragged_off && !cfg->ragged)
+    return fail(ctx, SP_E_ARG, "sp_featurize: MoE ragged_off without ragged");
+  if (out->family != fam) return fail(ctx, SP_E_ARG, "sp_featurize: out->family != cfg->family");
+  int64_t n_pairs;
+  if (pairs->kind == SP_PAIRS_CROSS) {
+    if (pairs->spec_begin < 0 || pairs->spec_end > specs->n || pairs->spec_begin > pairs->spec_end)
+      return fail(ctx, SP_E_ARG, "sp_featurize: spec range out of bounds");
+    n_pairs = (int64_t)(pairs->spec_end - pairs->spec_begin) * cfg->n_configs;
+  } else if (pairs->kind == SP_PAIRS_LIST) {
+    n_pairs = pairs->n_pairs;
+    if (n_pairs < 0 || (n_pairs > 0 && (!pairs->cfg_idx || !pairs->spec_idx)))
+      return fail(ctx, SP_E_ARG, "sp_featurize: bad pair list");
+  } else {
+    return fail(ctx, SP_E_ARG, "sp_featurize: unknown pairing kind");
+  }
+  if (out->n_pairs != n_pairs || out->ld < n_pairs)
+    return fail(ctx, SP_E_ARG, "sp_featurize: out->n_pairs / ld do not match the pairing");
+  if (n_pairs > 0 && (!out->ints || !out->flts || !out->status))
+    return fail(ctx, SP_E_ARG, "sp_featurize: output buffers are NULL");
+  if (n_pairs == 0) return SP_OK;
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+
+  ConfigView cv{cfg->fields, cfg->ragged, cfg->ragged_off, cfg->n_configs, cfg->field_ld};
+  FeatOut fo{out->ints, out->flts, out->status, out->ld};
+  const DevSpec *ds = (const DevSpec *)specs->dev.p;
+  int e;
+  if (fam == SP_ATTENTION) {
+    if (pairs->kind == SP_PAIRS_CROSS) {
+      const AttnPlan *plan = nullptr;
+      sp_status st = attn_plan(ctx, specs, pairs->spec_begin, pairs->spec_end, &plan);
+      if (st != SP_OK) return st;
+      e = launch_featurize_attention(cv, ds, pairs->spec_begin, specs->n, *plan, n_pairs, nullptr, nullptr,
+                                     specs->max_sms, fo, ctx->num_sms, stream);
+    } else {
+      if (specs->max_sms > kAttnMaxSms)
+        return fail(ctx, SP_E_UNSUPPORTED, "attention featurization supports at most 4096 SMs per spec");
+      AttnPlan none{};
+      e = launch_featurize_attention(cv, ds, 0, specs->n, none, n_pairs, pairs->cfg_idx, pairs->spec_idx,
+                                     specs->max_sms, fo, ctx->num_sms, stream);
+    }
+  } else if (pairs->kind == SP_PAIRS_CROSS) {
+    e = launch_featurize_uniform(fam, cv, ds, pairs->spec_begin, pairs->spec_end, n_pairs, nullptr, nullptr,
+                                 fo, stream);
+  } else {
+    e = launch_featurize_uniform(fam, cv, ds, 0, specs->n, n_pairs, pairs->cfg_idx, pairs->spec_idx, fo,
+                                 stream);
+  }
+  if (e) return cuda_fail(ctx, e, "sp_featurize: launch");
+  return SP_OK;
+}
+
+// -------------------------------------------------------------------- model
+
+static bool all_finite(const float *p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+extern "C" sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *d, sp_model **out) {
+  if (!ctx || !d || !out) return fail(ctx, SP_E_ARG, "sp_load_model: NULL argument");
+  *out = nullptr;
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  if (nfields_of(d->family) < 0) return fail(ctx, SP_E_ARG, "sp_load_model: unknown family");
+  const int n_in = d->n_in;
+  if (n_in != 4 * pipes_count(d->family) + 7)
+    return fail(ctx, SP_E_DATA, "sp_load_model: n_in does not match the family's Table IV layout");
+  if (d->precision != SP_MLP_FP32 && d->precision != SP_MLP_BF16)
+    return fail(ctx, SP_E_ARG, "sp_load_model: unknown precision");
+  const float *arrs[] = {d->mu, d->sigma, d->w1, d->b1, d->g1, d->be1, d->m1, d->v1, d->w2, d->b2, d->g2,
+                         d->be2, d->m2, d->v2, d->w3, d->b3, d->g3, d->be3, d->m3, d->v3, d->w4};
+  const size_t lens[] = {(size_t)n_in, (size_t)n_in, 256u * n_in, 256, 256, 256, 256, 256, 128 * 256, 128,
+                         128, 128, 128, 128, 64 * 128, 64, 64, 64, 64, 64, 64};
+  for (int k = 0; k < 21; ++k) {
+    if (!arrs[k]) return fail(ctx, SP_E_ARG, "sp_load_model: NULL weight pointer");
+    if (!all_finite(arrs[k], lens[k])) return fail(ctx, SP_E_DATA, "sp_load_model: non-finite value");
+  }
+  if (!std::isfinite(d->b4) || !(d->bn_eps > 0) || !std::isfinite(d->bn_eps))
+    return fail(ctx, SP_E_DATA, "sp_load_model: bad b4 or bn_eps");
+  const float *vs[3] = {d->v1, d->v2, d->v3};
+  const int W[3] = {256, 128, 64};
+  for (int l = 0; l < 3; ++l)
+    for (int i = 0; i < W[l]; ++i)
+      if (!((double)vs[l][i] + (double)d->bn_eps > 0))
+        return fail(ctx, SP_E_DATA, "sp_load_model: BatchNorm variance + eps must be > 0");
+
+  // BN(eval) after ReLU as a per-unit affine: s = gamma / sqrt(var + eps),
+  // t = beta - s * mean (R18), computed in fp64.
+  std::vector<double> s[3], t[3];
+  const float *gs[3] = {d->g1, d->g2, d->g3}, *bes[3] = {d->be1, d->be2, d->be3},
+              *ms[3] = {d->m1, d->m2, d->m3};
+  for (int l = 0; l < 3; ++l) {
+    s[l].resize(W[l]);
+    t[l].resize(W[l]);
+    for (int i = 0; i < W[l]; ++i) {
+      s[l][i] = (double)gs[l][i] / std::sqrt((double)vs[l][i] + (double)d->bn_eps);
+      t[l][i] = (double)bes[l][i] - s[l][i] * (double)ms[l][i];
+    }
+  }
+  std::unique_ptr<sp_model> m(new (std::nothrow) sp_model);
+  if (!m) return fail(ctx, SP_E_INTERNAL, "sp_load_model: out of host memory");
+  m->family = d->family;
+  m->n_in = n_in;
+  m->precision = d->precision;
+
+  // fp32 layout (always built: it is also the reference layout of the bf16 pack)
+  {
+    std::vector<float> buf;
+    auto push = [&](size_t n) { size_t o = buf.size(); buf.resize(o + ((n + 3) & ~size_t(3)), 0.f); return o; };
+    const size_t o_w1t = push(256u * n_in), o_w2t = push(256 * 128), o_w3t = push(128 * 64);
+    const size_t o_v[9] = {push(256), push(256), push(256), push(128), push(128), push(128), push(64), push(64), push(64)};
+    const size_t o_w4 = push(64), o_mu = push(16), o_is = push(16);
+    for (int k = 0; k < n_in; ++k)
+      for (int n = 0; n < 256; ++n) buf[o_w1t + k * 256 + n] = d->w1[n * n_in + k];
+    for (int k = 0; k < 256; ++k)
+      for (int n = 0; n < 128; ++n) buf[o_w2t + k * 128 + n] = d->w2[n * 256 + k];
+    for (int k = 0; k < 128; ++k)
+      for (int n = 0; n < 64; ++n) buf[o_w3t + k * 64 + n] = d->w3[n * 128 + k];
+    const float *bs[3] = {d->b1, d->b2, d->b3};
+    for (int l = 0; l < 3; ++l)
+      for (int i = 0; i < W[l]; ++i) {
+        buf[o_v[3 * l] + i] = bs[l][i];
+        buf[o_v[3 * l + 1] + i] = (float)s[l][i];
+        buf[o_v[3 * l + 2] + i] = (float)t[l][i];
+      }
+    for (int i = 0; i < 64; ++i) buf[o_w4 + i] = d->w4[i];
+    for (int i = 0; i < n_in; ++i) {
+      buf[o_mu + i] = d->mu[i];
+      buf[o_is + i] = (float)(1.0 / std::max((double)d->sigma[i], 1e-8));
+    }
+    cudaError_t e = m->fp32.alloc_copy(buf.data(), buf.size() * 4);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "sp_load_model: upload");
+    const float *base = (const float *)m->fp32.p;
+    MlpFp32 &q = m->m32;
+    q.w1t = base + o_w1t; q.w2t = base + o_w2t; q.w3t = base + o_w3t;
+    q.b1 = base + o_v[0]; q.s1 = base + o_v[1]; q.t1 = base + o_v[2];
+    q.b2 = base + o_v[3]; q.s2 = base + o_v[4]; q.t2 = base + o_v[5];
+    q.b3 = base + o_v[6]; q.s3 = base + o_v[7]; q.t3 = base + o_v[8];
+    q.w4 = base + o_w4; q.mu = base + o_mu; q.inv_sigma = base + o_is;
+    q.b4 = d->b4;
+    q.n_in = n_in;
+    q.family = d->family;
+  }
+  if (d->precision == SP_MLP_BF16) {
+    std::vector<uint16_t> wpack;
+    std::vector<float> vecs;
+    float b4 = 0.f;
+    if (!pack_bf16_model(*d, s, t, wpack, vecs, b4))
+      return fail(ctx, SP_E_UNSUPPORTED, "sp_load_model: bf16 tcgen05 path unavailable in this build");
+    cudaError_t e = m->bf16w.alloc_copy(wpack.data(), wpack.size() * 2);
+    if (e == cudaSuccess) e = m->bf16v.alloc_copy(vecs.data(), vecs.size() * 4);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "sp_load_model: bf16 upload");
+    m->m16.wpack = m->bf16w.p;
+    m->m16.vecs = (const float *)m->bf16v.p;
+    m->m16.b4 = b4;
+    m->m16.n_in = n_in;
+    m->m16.family = d->family;
+  }
+  *out = m.release();
+  return SP_OK;
+}
+
+extern "C" void sp_free_model(sp_model *model) { delete model; }
+
+// ------------------------------------------------------------------ predict
+
+extern "C" sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_features *in, float *latency_us,
+                                float *efficiency, void *stream) {
+  if (!ctx) return fail(nullptr, SP_E_ARG, "sp_predict: ctx is NULL");
+  if (!model || !in) return fail(ctx, SP_E_ARG, "sp_predict: NULL argument");
+  if (in->family != model->family) return fail(ctx, SP_E_ARG, "sp_predict: features/model family mismatch");
+  if (in->n_pairs < 0 || in->ld < in->n_pairs) return fail(ctx, SP_E_ARG, "sp_predict: bad n_pairs / ld");
+  if (in->n_pairs == 0) return SP_OK;
+  if (!latency_us || !in->ints || !in->flts || !in->status)
+    return fail(ctx, SP_E_ARG, "sp_predict: NULL buffer");
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  int e;
+  if (model->precision == SP_MLP_BF16)
+    e = launch_predict_tcgen05(model->m16, *in, latency_us, efficiency, ctx->num_sms, stream);
+  else
+    e = launch_predict_simt(model->m32, *in, latency_us, efficiency, ctx->num_sms, stream);
+  if (e) return cuda_fail(ctx, e, "sp_predict: launch");
+  return SP_OK;
+}

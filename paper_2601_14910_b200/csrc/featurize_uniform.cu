@@ -1,0 +1,233 @@
+// Feature stage for the uniform-task families: GEMM (Table V), fused MoE
+// (P:419), RMSNorm, SiLU&Mul.
+//
+// Every task of these kernels has the same demands (padded tiles R2, one task
+// per row for the row-wise kernels), so the round-robin schedule (Eq.2, R5)
+// has a closed form: SM j holds ceil((T - j)/N) tasks and the busiest SM holds
+// ceil(T/N).  Per pair the work is O(1): no task list, no loop.
+//
+// Layout: one thread per config, looping over a tile of specs staged in shared
+// memory; for each spec the thread writes pair p = (g - g0)*C + c, so a warp's
+// stores to every SoA row are 32 consecutive elements (coalesced).  Config
+// invariants (T, per-task demands, footprint, status) are computed once per
+// config and reused across the spec tile.  The kernel is bound by the
+// 137 B/pair record written to HBM.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace sp {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kSpecTile = 16;
+constexpr int64_t kI32Max = 2147483647LL;
+constexpr unsigned __int128 kI64Max = 9223372036854775807ULL;
+
+struct UniformCfg {
+  int status;       // config-level status (validation order of the oracle)
+  int range_bad;    // totals do not fit in int64 (checked after the spec dtype check)
+  int tdt;          // tensor dtype index: 0 bf16, 1 fp16, -1 none
+  int64_t T;
+  int64_t task[4];  // per-task Tensor, FMA, XU ops, load bytes
+  int64_t tot[4];
+  Footprint fp;
+};
+
+__device__ __forceinline__ int32_t fld(const ConfigView &v, int k, int64_t c) {
+  return __ldg(v.fields + (int64_t)k * v.ld + c);
+}
+
+__device__ __forceinline__ int64_t sat40(unsigned __int128 x) {
+  const unsigned __int128 lim = (unsigned __int128)1 << 40;
+  return (int64_t)(x > lim ? lim : x);
+}
+
+// Task demands and totals with the exact-range rule (R22): uniform tasks, so
+// tot = T * task; all in 128-bit before narrowing.
+__device__ __forceinline__ void finish_totals(UniformCfg &u, const unsigned __int128 task[4]) {
+  u.range_bad = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    unsigned __int128 t = task[q] * (unsigned __int128)u.T;
+    if (task[q] > kI64Max || t > kI64Max) u.range_bad = 1;
+    u.task[q] = (int64_t)task[q];
+    u.tot[q] = (int64_t)t;
+  }
+}
+
+// GEMM: T = ceil(M/tm) * ceil(N/tn); task = 2*tm*tn*K_pad Tensor ops, (tm+tn)*K_pad*bpe bytes
+// (Eq.3 alpha = 2; R1, R2); smem default stages*(tm+tn)*BK*bpe.
+__device__ UniformCfg gemm_cfg(const ConfigView &v, int64_t c) {
+  UniformCfg u{};
+  const int64_t M = fld(v, 0, c), N = fld(v, 1, c), K = fld(v, 2, c), tm = fld(v, 3, c),
+                tn = fld(v, 4, c), bk = fld(v, 5, c), stages = fld(v, 6, c), warps = fld(v, 7, c),
+                regs = fld(v, 8, c), smem = fld(v, 9, c), dt = fld(v, 10, c);
+  if (M < 1 || N < 1 || K < 1) { u.status = SP_PAIR_E_DIM; return u; }
+  if (tm < 1 || tn < 1 || bk < 1 || stages < 1) { u.status = SP_PAIR_E_TILE; return u; }
+  if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return u; }
+  if (dt != SP_BF16 && dt != SP_FP16) { u.status = SP_PAIR_E_DTYPE; return u; }
+  const int64_t T = cdiv64(M, tm) * cdiv64(N, tn);
+  if (T > kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
+  u.T = T;
+  u.tdt = (int)dt;
+  const int64_t kpad = cdiv64(K, bk) * bk;
+  unsigned __int128 task[4] = {(unsigned __int128)(2 * tm * tn) * kpad, 0, 0,
+                               (unsigned __int128)(tm + tn) * kpad * 2};
+  finish_totals(u, task);
+  u.fp.smem = smem > 0 ? smem : sat40((unsigned __int128)stages * (tm + tn) * bk * 2);
+  u.fp.warps = warps;
+  u.fp.regs = regs;
+  return u;
+}
+
+// Fused MoE (R16): t_e from the histogram or the balanced split; tasks are
+// padded BM x BN x H_pad tiles: T = sum_e ceil(t_e/BM) * ceil(N/BN).
+__device__ UniformCfg moe_cfg(const ConfigView &v, int64_t c) {
+  UniformCfg u{};
+  const int64_t M = fld(v, 0, c), E = fld(v, 1, c), topk = fld(v, 2, c), H = fld(v, 3, c),
+                N = fld(v, 4, c), bm = fld(v, 5, c), bn = fld(v, 6, c), bk = fld(v, 7, c),
+                stages = fld(v, 9, c), warps = fld(v, 10, c), regs = fld(v, 11, c),
+                smem = fld(v, 12, c), dt = fld(v, 13, c);
+  if (M < 1 || E < 1 || topk < 1 || H < 1 || N < 1) { u.status = SP_PAIR_E_DIM; return u; }
+  if (bm < 1 || bn < 1 || bk < 1 || stages < 1) { u.status = SP_PAIR_E_TILE; return u; }
+  if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return u; }
+  if (dt != SP_BF16 && dt != SP_FP16) { u.status = SP_PAIR_E_DTYPE; return u; }
+  const int64_t mt = M * topk;
+  if (mt > kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
+  const int64_t off = v.ragged_off ? __ldg(v.ragged_off + c) : -1;
+  unsigned __int128 mblocks = 0;
+  if (off >= 0) {
+    const int32_t *h = v.ragged + off;
+    int64_t sum = 0;
+    for (int64_t e = 0; e < E; ++e) {
+      const int64_t te = __ldg(h + e);
+      if (te < 0) { u.status = SP_PAIR_E_HIST; return u; }
+      sum += te;
+    }
+    if (sum != mt) { u.status = SP_PAIR_E_HIST; return u; }
+    for (int64_t e = 0; e < E; ++e) mblocks += cdiv64(__ldg(h + e), bm);
+  } else {
+    const int64_t q = mt / E, r = mt % E;
+    mblocks = (unsigned __int128)r * cdiv64(q + 1, bm) + (unsigned __int128)(E - r) * cdiv64(q, bm);
+  }
+  const unsigned __int128 T = mblocks * (unsigned __int128)cdiv64(N, bn);
+  if (T > (unsigned __int128)kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
+  u.T = (int64_t)T;
+  u.tdt = (int)dt;
+  const int64_t hpad = cdiv64(H, bk) * bk;
+  unsigned __int128 task[4] = {(unsigned __int128)(2 * bm * bn) * hpad, 0, 0,
+                               (unsigned __int128)(bm + bn) * hpad * 2};
+  finish_totals(u, task);
+  u.fp.smem = smem > 0 ? smem : sat40((unsigned __int128)stages * (bm + bn) * bk * 2);
+  u.fp.warps = warps;
+  u.fp.regs = regs;
+  return u;
+}
+
+// RMSNorm (R14): per row FMA 3*dim, XU 1, bytes 2*dim*bpe.
+// SiLU&Mul (R15): per row FMA 4*dim, XU 2*dim, bytes 2*dim*bpe.  One task per row.
+__device__ UniformCfg rowwise_cfg(const ConfigView &v, int64_t c, bool silu) {
+  UniformCfg u{};
+  const int64_t seq = fld(v, 0, c), dim = fld(v, 1, c), warps = fld(v, 2, c), regs = fld(v, 3, c),
+                smem = fld(v, 4, c), dt = fld(v, 5, c);
+  if (seq < 1 || dim < 1) { u.status = SP_PAIR_E_DIM; return u; }
+  if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return u; }
+  const int bpe = bytes_per_elem((int)dt);
+  if (bpe == 0) { u.status = SP_PAIR_E_DTYPE; return u; }
+  u.T = seq;
+  u.tdt = -1;
+  unsigned __int128 task[4] = {0, (unsigned __int128)(silu ? 4 : 3) * dim,
+                               silu ? (unsigned __int128)2 * dim : (unsigned __int128)1,
+                               (unsigned __int128)2 * dim * bpe};
+  finish_totals(u, task);
+  u.fp.smem = smem > 0 ? smem : warps * 4;
+  u.fp.warps = warps;
+  u.fp.regs = regs;
+  return u;
+}
+
+__device__ __forceinline__ UniformCfg config_of(int fam, const ConfigView &v, int64_t c) {
+  switch (fam) {
+    case SP_GEMM: return gemm_cfg(v, c);
+    case SP_FUSED_MOE: return moe_cfg(v, c);
+    case SP_RMSNORM: return rowwise_cfg(v, c, false);
+    default: return rowwise_cfg(v, c, true);
+  }
+}
+
+// One pair: spec-dependent checks in the oracle's order, then the closed-form
+// schedule (busiest SM = ceil(T/N) tasks) and the record.
+__device__ __forceinline__ void uniform_pair(const FeatOut &out, int64_t p, const UniformCfg &u,
+                                             const DevSpec &s, int pipes) {
+  if (u.status != 0) { emit_error(out, p, u.status); return; }
+  if (u.tdt >= 0 && !s.tensor_ok[u.tdt]) { emit_error(out, p, SP_PAIR_E_DTYPE); return; }
+  if (u.range_bad) { emit_error(out, p, SP_PAIR_E_RANGE); return; }
+  PairDemand d;
+  d.T = u.T;
+  const int64_t per_sm = (int64_t)(((uint32_t)u.T + (uint32_t)s.num_sms - 1u) / (uint32_t)s.num_sms);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    d.tot[q] = u.tot[q];
+    d.mx[q] = per_sm * u.task[q];
+  }
+  emit_pair(out, p, d, u.fp, s, pipes, u.tdt < 0 ? 0 : u.tdt);
+}
+
+__global__ void __launch_bounds__(kThreads) featurize_uniform_cross(int fam, ConfigView cfg,
+                                                                    const DevSpec *__restrict__ specs,
+                                                                    int g0, int g1, FeatOut out) {
+  __shared__ DevSpec s_spec[kSpecTile];
+  const int gt0 = g0 + blockIdx.y * kSpecTile;
+  const int gt1 = min(g1, gt0 + kSpecTile);
+  {
+    const int n_words = (gt1 - gt0) * (int)(sizeof(DevSpec) / 16);
+    const int4 *src = reinterpret_cast<const int4 *>(specs + gt0);
+    int4 *dst = reinterpret_cast<int4 *>(s_spec);
+    for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (c >= cfg.n_configs) return;
+  const UniformCfg u = config_of(fam, cfg, c);
+  const int pipes = family_pipes(fam);
+  const int64_t C = cfg.n_configs;
+  for (int g = gt0; g < gt1; ++g) uniform_pair(out, (int64_t)(g - g0) * C + c, u, s_spec[g - gt0], pipes);
+}
+
+__global__ void __launch_bounds__(kThreads) featurize_uniform_list(int fam, ConfigView cfg,
+                                                                   const DevSpec *__restrict__ specs,
+                                                                   int n_specs, int64_t n_pairs,
+                                                                   const int64_t *__restrict__ cfg_idx,
+                                                                   const int32_t *__restrict__ spec_idx,
+                                                                   FeatOut out) {
+  const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (p >= n_pairs) return;
+  const int64_t c = __ldg(cfg_idx + p);
+  const int32_t g = __ldg(spec_idx + p);
+  if (c < 0 || c >= cfg.n_configs || g < 0 || g >= n_specs) { emit_error(out, p, SP_PAIR_E_INDEX); return; }
+  const UniformCfg u = config_of(fam, cfg, c);
+  uniform_pair(out, p, u, specs[g], family_pipes(fam));
+}
+
+}  // namespace
+
+int launch_featurize_uniform(int family, const ConfigView &cfg, const DevSpec *specs, int spec_begin,
+                             int spec_end, int64_t n_pairs, const int64_t *cfg_idx,
+                             const int32_t *spec_idx, const FeatOut &out, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cfg_idx == nullptr) {  // CROSS
+    if (cfg.n_configs == 0 || spec_end <= spec_begin) return 0;
+    dim3 grid((unsigned)((cfg.n_configs + kThreads - 1) / kThreads),
+              (unsigned)((spec_end - spec_begin + kSpecTile - 1) / kSpecTile));
+    featurize_uniform_cross<<<grid, kThreads, 0, st>>>(family, cfg, specs, spec_begin, spec_end, out);
+  } else {
+    if (n_pairs == 0) return 0;
+    unsigned blocks = (unsigned)((n_pairs + kThreads - 1) / kThreads);
+    featurize_uniform_list<<<blocks, kThreads, 0, st>>>(family, cfg, specs, spec_end, n_pairs, cfg_idx,
+                                                         spec_idx, out);
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sp

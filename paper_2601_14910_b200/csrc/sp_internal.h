@@ -1,0 +1,126 @@
+// Internal declarations shared by the host API (api.cu) and the kernels.
+// Not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "synperf.h"
+
+namespace sp {
+
+constexpr int kNumInts = 11;
+constexpr int kNumFlts = 12;
+
+// Slot indices of the uniform feature record (include/synperf.h sp_features).
+enum IntSlot { I_NTASKS, I_OCC, I_WAVES, I_TOT_T, I_TOT_F, I_TOT_X, I_MAX_T, I_MAX_F, I_MAX_X,
+               I_BYTES, I_BYTES_MAX };
+enum FltSlot { F_CG_T, F_CG_F, F_CG_X, F_CS_T, F_CS_F, F_CS_X, F_GLOB_G, F_L2_G, F_GLOB_S,
+               F_L2_S, F_SMEM_S, F_TTHEORY };
+
+// Pipes per family (Table V): bit 0 Tensor, bit 1 FMA, bit 2 XU.
+__host__ __device__ inline int family_pipes(int fam) {
+  return (fam == SP_GEMM || fam == SP_FUSED_MOE) ? 1 : (fam == SP_ATTENTION ? 5 : 6);
+}
+
+// Step a1: per-spec constants derived once on the host in fp64 (Eq.4-5).
+// 128-byte aligned so a warp reads one spec in a single pass.
+struct alignas(16) DevSpec {
+  int32_t num_sms;       // N_SM
+  int32_t smem_per_sm;   // bytes
+  int32_t regs_per_sm;   // 32-bit registers (R6)
+  int32_t max_warps;
+  int32_t max_ctas;
+  int32_t tensor_ok[2];  // tensor rate present for {bf16, fp16}
+  int32_t pad_;
+  double cg_tensor[2];   // 1 / (N_SM * Th_tensor)   (Eq.5)
+  double cs_tensor[2];   // 1 / Th_tensor           (Eq.4)
+  double cg_fma, cs_fma, cg_xu, cs_xu;
+  double glob_g;         // f / (BW_glob * 1e3): bytes -> cycles at GPU level (R8)
+  double l2_g;
+  double glob_s;         // f * N_SM / (BW_glob * 1e3): per-SM share BW/N_SM (R8)
+  double l2_s;
+  double smem_s;         // 1 / smem bytes per clk
+  double inv_f;          // 1 / f (cycles -> us)
+};
+static_assert(sizeof(DevSpec) == 144, "DevSpec layout");
+
+// Device feature-record view.
+struct FeatOut {
+  int64_t *ints;
+  float *flts;
+  uint8_t *status;
+  int64_t ld;
+};
+
+struct ConfigView {
+  const int32_t *fields;
+  const int32_t *ragged;
+  const int64_t *ragged_off;
+  int64_t n_configs;
+  int64_t ld;
+};
+
+// -------------------------------------------------------------- launchers
+// All return cudaError_t cast to int (0 = success).
+
+// Uniform families (GEMM, fused MoE, RMSNorm, SiLU&Mul): closed-form schedule.
+int launch_featurize_uniform(int family, const ConfigView &cfg, const DevSpec *specs,
+                             int spec_begin, int spec_end, int64_t n_pairs, const int64_t *cfg_idx,
+                             const int32_t *spec_idx, const FeatOut &out, void *stream);
+
+// Attention: per-task loop with per-SM shared-memory accumulators.
+// Host-built spec groups for CROSS mode (see featurize_attention.cu).
+struct AttnGroup {
+  int32_t spec_first;    // index into group_specs
+  int32_t n_specs;
+  int32_t distinct_first;  // index into distinct_n / distinct_off
+  int32_t n_distinct;
+};
+struct AttnPlan {
+  const AttnGroup *groups;     // DEVICE [n_groups]
+  const int32_t *group_specs;  // DEVICE spec index (absolute)
+  const int32_t *spec_dist;    // DEVICE, per group_specs entry: distinct slot (absolute)
+  const int32_t *distinct_n;   // DEVICE N_SM of each distinct slot
+  const int32_t *distinct_off; // DEVICE word offset of the slot in the warp's smem region
+  int32_t n_groups;
+  int32_t words_per_warp;      // u32 accumulator words per warp
+};
+int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin,
+                               int n_specs, const AttnPlan &plan, int64_t n_pairs, const int64_t *cfg_idx,
+                               const int32_t *spec_idx, int32_t max_sms, const FeatOut &out,
+                               int num_device_sms, void *stream);
+
+// MLP predictor.
+struct MlpFp32 {        // DEVICE pointers, fp32
+  const float *w1t;     // [n_in][256]  (transposed: k-major)
+  const float *w2t;     // [256][128]
+  const float *w3t;     // [128][64]
+  const float *b1, *s1, *t1;  // bias, BN scale gamma/sqrt(var+eps), BN shift beta - scale*mean
+  const float *b2, *s2, *t2;
+  const float *b3, *s3, *t3;
+  const float *w4;      // [64]
+  const float *mu, *inv_sigma;  // [n_in]
+  float b4;
+  int32_t n_in;
+  int32_t family;
+};
+int launch_predict_simt(const MlpFp32 &m, const sp_features &in, float *latency, float *eff,
+                        int num_device_sms, void *stream);
+
+struct MlpBf16 {
+  const void *wpack;    // DEVICE packed bf16 weights in UMMA canonical layout (see predict_tcgen05.cu)
+  const float *vecs;    // DEVICE fp32 per-unit vectors: b1[256], b2'[128], b3'[64], w4'[64], mu[16], inv_sigma[16]
+  float b4;
+  int32_t n_in;
+  int32_t family;
+};
+// Host: BN-folded bf16 weights in the kernel's shared-memory image, plus fp32
+// vectors.  s[l], t[l]: BN(eval) affine of hidden layer l (fp64).  Returns
+// false if the tcgen05 path is not available.
+bool pack_bf16_model(const sp_mlp_desc &d, const std::vector<double> *s, const std::vector<double> *t,
+                     std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4);
+int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *latency, float *eff,
+                           int num_device_sms, void *stream);
+
+}  // namespace sp

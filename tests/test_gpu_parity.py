@@ -1,0 +1,247 @@
+"""GPU (CUDA path, through the C-ABI) vs the fp64 CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): every integer slot and status bit-exact;
+fp32 float features within 1e-5 relative of the fp64 oracle; latency within
+1e-5 relative for the fp32 MLP and 1e-2 for the bf16 tcgen05 MLP.
+"""
+import numpy as np
+import pytest
+import torch
+
+from workloads import gen, models, specs
+
+pytestmark = pytest.mark.gpu
+
+FEAT_RTOL = 1e-5
+LAT_RTOL_FP32 = 1e-5
+LAT_RTOL_BF16 = 1e-2
+
+
+@pytest.fixture(scope="module")
+def sp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_14910_b200 as sp
+
+    return sp
+
+
+@pytest.fixture(scope="module")
+def ctx(sp):
+    return sp.Context(0)
+
+
+def gpu_features(sp, ctx, batch, spec_arr, pairs=None, specs_handle=None):
+    sh = specs_handle or ctx.load_gpu_specs(spec_arr)
+    db = sp.DeviceBatch.from_host(batch, ctx.torch_device)
+    if pairs is None:
+        n = len(spec_arr) * batch.n_configs
+        pr = sp.cross(0, len(spec_arr))
+    else:
+        ci, si = pairs
+        n = len(ci)
+        pr = sp.pair_list(torch.from_numpy(np.asarray(ci, np.int64)).cuda(),
+                          torch.from_numpy(np.asarray(si, np.int32)).cuda())
+    f = sp.Features.empty(batch.family, n, ctx.torch_device)
+    ctx.featurize(db, sh, f, pr)
+    torch.cuda.synchronize()
+    return f, sp.features_to_host(f)
+
+
+def assert_feature_parity(g, o, where=""):
+    gi, gf, gs = g
+    assert np.array_equal(gs, o.status), f"status mismatch {where}: {np.nonzero(gs != o.status)[0][:10]}"
+    bad = np.nonzero((gi != o.ints).any(0))[0]
+    assert bad.size == 0, f"int mismatch {where} at pairs {bad[:10]}: gpu {gi[:, bad[0]]} oracle {o.ints[:, bad[0]]}"
+    of = o.flts
+    nan_g, nan_o = np.isnan(gf), np.isnan(of)
+    assert np.array_equal(nan_g, nan_o), f"NaN pattern mismatch {where}"
+    ok = ~nan_o
+    np.testing.assert_allclose(gf[ok].astype(np.float64), of[ok], rtol=FEAT_RTOL, atol=0,
+                               err_msg=f"float features {where}")
+
+
+FAMILY_BATCHES = {
+    "gemm": lambda: gen.gen_gemm(700, 1001),
+    "attention": lambda: gen.gen_attention(150, 150, 1002, max_bs=6, qlen_max=4000, kvlen_max=6000),
+    "moe": lambda: gen.gen_moe(600, 1003),
+    "rmsnorm": lambda: gen.gen_rowwise(gen.RMSNORM, 500, 1004),
+    "silu": lambda: gen.gen_rowwise(gen.SILU_MUL, 500, 1005),
+}
+
+
+@pytest.mark.parametrize("fam", list(FAMILY_BATCHES))
+def test_featurize_cross_parity(sp, ctx, orc, fam):
+    b = FAMILY_BATCHES[fam]()
+    sa = specs.paper_gpu_specs()
+    _, g = gpu_features(sp, ctx, b, sa)
+    o = orc.featurize(b, sa)
+    assert (o.status == 0).all()
+    assert_feature_parity(g, o, fam)
+
+
+@pytest.mark.parametrize("fam", list(FAMILY_BATCHES))
+def test_featurize_list_parity(sp, ctx, orc, fam):
+    b = FAMILY_BATCHES[fam]()
+    sa = specs.paper_gpu_specs()
+    rng = np.random.default_rng(7)
+    n = 900
+    ci = rng.integers(0, b.n_configs, n)
+    si = rng.integers(0, len(sa), n)
+    ci[:3] = [-1, b.n_configs, 0]   # out-of-range indices -> SP_PAIR_E_INDEX
+    si[2] = len(sa)
+    _, g = gpu_features(sp, ctx, b, sa, pairs=(ci, si))
+    o = orc.featurize(b, sa, cfg_idx=ci, spec_idx=si)
+    assert (o.status[:3] == 9).all()
+    assert_feature_parity(g, o, fam + " list")
+
+
+def odd_specs():
+    """SM counts below, at and around the warp width, and a large one."""
+    base = specs.paper_gpu_specs()
+    out = np.concatenate([base[:4]] * 2)
+    for i, n in enumerate([1, 7, 31, 32, 33, 64, 97, 1000]):
+        out[i]["num_sms"] = n
+    return out
+
+
+@pytest.mark.parametrize("fam", list(FAMILY_BATCHES))
+def test_featurize_odd_sm_counts(sp, ctx, orc, fam):
+    b = FAMILY_BATCHES[fam]().subset(np.arange(60))
+    sa = odd_specs()
+    _, g = gpu_features(sp, ctx, b, sa)
+    assert_feature_parity(g, orc.featurize(b, sa), fam + " odd SMs")
+
+
+def test_attention_edge_cases(sp, ctx, orc):
+    """qlen = 1, kvlen < BKV, nkv = nh, causal + split-KV, T < N, T multiple of N,
+    long single requests, domain errors."""
+    cols = {k: [] for k in gen.FIELDS[gen.ATTENTION]}
+    rag, off = [], []
+
+    def add(bs_reqs, **kw):
+        d = dict(NH=8, NKV=2, HD=128, BQ=64, BKV=64, KV_CHUNK=0, CAUSAL=1, WARPS=4, REGS=128, SMEM=0,
+                 DTYPE=0)
+        d.update(kw)
+        d["BS"] = len(bs_reqs) if "BS" not in kw else kw["BS"]
+        for k in cols:
+            cols[k].append(d[k])
+        off.append(len(rag))
+        for q, kv in bs_reqs:
+            rag.extend([q, kv])
+
+    add([(1, 3)])                              # qlen 1, kvlen < BKV
+    add([(1, 1)], NH=4, NKV=4)                 # nkv = nh (group 1)
+    add([(300, 5000), (2000, 2000)], KV_CHUNK=512)   # causal + split-KV (generic path)
+    add([(77, 77)] * 5, KV_CHUNK=64, BQ=16)    # many small chunks
+    add([(1, 20481)] * 16, NH=128, NKV=8, BQ=16, KV_CHUNK=2048, CAUSAL=0)  # decode, split
+    add([(20097, 20481)], NH=32, NKV=8, BQ=128, BKV=32)   # long prefill
+    add([(108 * 64, 108 * 64)], NH=1, NKV=1, CAUSAL=0)    # T = 108 q-blocks (multiple of N=108)
+    add([(5, 9)], NH=6, NKV=4)                 # nh % nkv != 0 -> status 3
+    add([(9, 5)])                              # causal kv < q -> status 5
+    add([(0, 5)])                              # qlen 0 -> status 1
+    add([(5, 5)], BQ=0)                        # tile 0 -> status 2
+    add([(5, 5)], DTYPE=3)                     # fp8 -> status 7
+    add([(5, 5)], WARPS=0)                     # resources -> status 6
+    b = gen.make_batch(gen.ATTENTION, cols, rag, off)
+    sa = np.concatenate([specs.paper_gpu_specs(), odd_specs()])
+    _, g = gpu_features(sp, ctx, b, sa)
+    o = orc.featurize(b, sa)
+    assert set(np.unique(o.status)) >= {0, 1, 2, 3, 5, 6, 7}
+    assert_feature_parity(g, o, "attention edges")
+
+
+def test_uniform_edge_cases(sp, ctx, orc):
+    g_cols = dict(M=[1, 4096, 131072, 7, 0, 5, 5], N=[1, 4096, 152064, 9, 5, 5, 5],
+                  K=[1, 4096, 53248, 3, 5, 5, 5], TM=[128, 128, 256, 1, 8, 0, 8],
+                  TN=[128, 128, 128, 1, 8, 8, 8], BK=[64, 64, 64, 1, 8, 8, 8],
+                  STAGES=[3, 3, 5, 1, 1, 1, 1], WARPS=[8, 8, 8, 1, 1, 1, 1],
+                  REGS=[232, 232, 232, 1, 1, 1, 1], SMEM=[0, 0, 0, 300000, 0, 0, 0],
+                  DTYPE=[0, 1, 0, 1, 0, 0, 3])
+    b = gen.make_batch(gen.GEMM, g_cols)
+    sa = np.concatenate([specs.paper_gpu_specs(), odd_specs()])
+    sa[3]["th_tensor_fp16"] = 0  # missing fp16 rate -> status 7 for fp16 configs
+    _, g = gpu_features(sp, ctx, b, sa)
+    assert_feature_parity(g, orc.featurize(b, sa), "gemm edges")
+    m_cols = dict(M=[4, 4, 8192, 3], E=[2, 2, 128, 8], TOPK=[2, 2, 8, 2], H=[64, 64, 4096, 100],
+                  N=[64, 64, 3072, 100], BM=[16, 16, 16, 16], BN=[16, 16, 32, 16],
+                  BK=[16, 16, 32, 16], GROUP_M=[1, 1, 1, 1], STAGES=[2, 2, 5, 2],
+                  WARPS=[4, 4, 8, 4], REGS=[64, 64, 255, 64], SMEM=[0, 0, 0, 0], DTYPE=[0, 0, 0, 0])
+    hist = [8, 0, 3, 4]
+    m = gen.make_batch(gen.FUSED_MOE, m_cols, hist, [0, 2, -1, -1])
+    _, g = gpu_features(sp, ctx, m, sa)
+    o = orc.featurize(m, sa)
+    assert o.status[1] == 4 and o.status[0] == 0
+    assert_feature_parity(g, o, "moe edges")
+
+
+def test_full_size_sampled_cfg2(sp, ctx, orc):
+    """BASELINE config 2 at full size (1e6 configs x 11 specs), in the launch
+    configuration bench.py times; 3000 sampled pairs checked one by one."""
+    b = gen.gen_attention(500_000, 500_000, 1002)
+    b, _ = gen.shuffle(b, 7)
+    sa = specs.paper_gpu_specs()
+    f, _ = gpu_features(sp, ctx, b, sa)
+    rng = np.random.default_rng(3)
+    p = rng.integers(0, f.n_pairs, 3000)
+    ci, si = p % b.n_configs, p // b.n_configs
+    o = orc.featurize(b, sa, cfg_idx=ci, spec_idx=si)
+    pt = torch.from_numpy(p).cuda()
+    g = (f.ints[:, pt].cpu().numpy(), f.flts[:, pt].cpu().numpy(), f.status[pt].cpu().numpy())
+    assert_feature_parity(g, o, "cfg2 full-size sample")
+
+
+def _predict_both(sp, ctx, orc, batch, sa, precision, seed=5):
+    model = models.random_mlp(batch.family, seed)
+    f, _ = gpu_features(sp, ctx, batch, sa)
+    mh = ctx.load_model(model, precision)
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    eff = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    ctx.predict(mh, f, lat, eff)
+    torch.cuda.synchronize()
+    o = orc.featurize(batch, sa)
+    olat, oeff, _ = orc.predict(model, o)
+    return lat.cpu().numpy(), eff.cpu().numpy(), olat, oeff
+
+
+@pytest.mark.parametrize("fam", list(FAMILY_BATCHES))
+def test_predict_fp32_parity(sp, ctx, orc, fam):
+    b = FAMILY_BATCHES[fam]().subset(np.arange(300))
+    sa = specs.paper_gpu_specs()
+    lat, eff, olat, oeff = _predict_both(sp, ctx, orc, b, sa, "fp32")
+    ok = ~np.isnan(olat)
+    assert np.array_equal(np.isnan(lat), ~ok)
+    np.testing.assert_allclose(lat[ok], olat[ok], rtol=LAT_RTOL_FP32)
+    np.testing.assert_allclose(eff[ok], oeff[ok], rtol=LAT_RTOL_FP32)
+
+
+@pytest.mark.parametrize("fam", list(FAMILY_BATCHES))
+def test_predict_bf16_parity(sp, ctx, orc, fam):
+    b = FAMILY_BATCHES[fam]().subset(np.arange(300))
+    sa = specs.paper_gpu_specs()
+    lat, eff, olat, oeff = _predict_both(sp, ctx, orc, b, sa, "bf16")
+    ok = ~np.isnan(olat)
+    assert np.array_equal(np.isnan(lat), ~ok)
+    np.testing.assert_allclose(lat[ok], olat[ok], rtol=LAT_RTOL_BF16)
+
+
+def test_predict_zero_output_layer_exact(sp, ctx, orc):
+    """Zero final layer: e = 0.5 exactly, latency = 2 t_theory, both paths."""
+    b = gen.gen_gemm(200, 9)
+    sa = specs.paper_gpu_specs()
+    f, (gi, gf, gs) = gpu_features(sp, ctx, b, sa)
+    for prec in ("fp32", "bf16"):
+        mh = ctx.load_model(models.zero_output_mlp(gen.GEMM, 1), prec)
+        lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+        ctx.predict(mh, f, lat)
+        torch.cuda.synchronize()
+        assert np.array_equal(lat.cpu().numpy(), 2.0 * gf[11]), prec
+
+
+def test_featurize_deterministic(sp, ctx):
+    b = FAMILY_BATCHES["attention"]()
+    sa = specs.paper_gpu_specs()
+    _, a = gpu_features(sp, ctx, b, sa)
+    _, c = gpu_features(sp, ctx, b, sa)
+    for x, y in zip(a, c):
+        assert np.array_equal(x, y, equal_nan=True)
