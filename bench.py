@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SynPerf hot path: predictions/sec over (kernel config x
+GPU spec) pairs.  One step = feature stage (sp_featurize) + predictor stage
+(sp_predict) over one batch of synthetic pairs [+ the NCCL all-gather of
+predictions when N > 1], through the C-ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...   # the fp64 CPU oracle arm
+
+Rank 0 prints ONE JSON line (contract in the task statement / DESIGN.md §7).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import gen, models, specs  # noqa: E402
+
+BASELINE_METRIC = "predictions/sec (kernel-config×GPU pairs) at 1/2/4/8 B200; % HBM / tensor peak"
+UNIT = "pairs/s"
+MLP_FLOP_PER_PAIR = {11: 87_680, 15: 89_728}  # 2*(n_in*256 + 256*128 + 128*64 + 64), SURVEY §8(a) a11
+RECORD_BYTES = 11 * 8 + 12 * 4 + 1  # a9: 137 B/pair written
+
+
+# ----------------------------------------------------------------- workloads
+
+WORKLOADS = {
+    "cfg1": "1,000 GEMM configs x 1 GPU spec (A100, Table VI)",
+    "cfg2": "FlashAttention prefill/decode sweep, 1e6 configs x the paper's 11 GPU specs",
+    "cfg3": "fused MoE Triton config space, 1e6 configs x 11 GPU specs",
+    "cfg5": "1,000 serving GEMMs x 100,000 hypothetical GPU specs (1e8 pairs), sharded by spec",
+}
+
+
+def build_workload(name: str, rank: int, world: int, scale: float = 1.0):
+    """Returns (batch, spec_array, (g0, g1), scaling) for this rank."""
+    if name == "cfg1":
+        return gen.gen_gemm(1000, 1001), specs.spec_by_name("A100"), (0, 1), "weak"
+    if name == "cfg2":
+        n = int(500_000 * scale)
+        b = gen.gen_attention(n, n, 1002 + 7919 * rank)
+        b, _ = gen.shuffle(b, 7 + rank)  # mix prefill/decode cost for balance
+        sa = specs.paper_gpu_specs()
+        return b, sa, (0, len(sa)), "weak"
+    if name == "cfg3":
+        b = gen.gen_moe(int(1_000_000 * scale), 1003 + 7919 * rank)
+        sa = specs.paper_gpu_specs()
+        return b, sa, (0, len(sa)), "weak"
+    if name == "cfg5":
+        b = gen.gen_serving_gemms(1000, 1005)
+        sa = specs.hypothetical_sweep_specs(int(100_000 * scale))
+        G = len(sa)
+        return b, sa, (rank * G // world, (rank + 1) * G // world), "strong"
+    raise SystemExit(f"unknown workload {name}")
+
+
+# -------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Polls NVML during the timed region: SM clock, max clock, throttle reasons."""
+
+    REASONS = {
+        "hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+        "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+        "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+        "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+        "hw_power_brake_slowdown": "nvmlClocksEventReasonHwPowerBrakeSlowdown",
+    }
+
+    def __init__(self, index: int, period: float = 0.01):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            self.nv = pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # no NVML: report nulls
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS.items():
+                    if r & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------- reference (oracle)
+
+def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int = 0):
+    """Times the fp64 oracle (as it stands) on a bounded random sample of the
+    workload's pairs: featurize + predict.  Returns (pairs/s, n_sample, secs, threads)."""
+    from oracle import oracle as O
+
+    O.build()
+    rng = np.random.default_rng(seed)
+    g0, g1 = spec_range
+    total = (g1 - g0) * batch.n_configs
+
+    def run(n):
+        p = rng.integers(0, total, n)
+        ci, si = p % batch.n_configs, g0 + p // batch.n_configs
+        t = time.perf_counter()
+        f = O.featurize(batch, spec_arr, cfg_idx=ci, spec_idx=si)
+        O.predict(model, f)
+        return time.perf_counter() - t
+
+    n = 256
+    dt = run(n)
+    while dt < 0.5 and n < 10_000_000:
+        n *= 4
+        dt = run(n)
+    n = max(256, int(n * target_s / max(dt, 1e-6)))
+    dt = run(n)
+    return n / dt, n, dt, O.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    b, sa, rng_, _ = build_workload(args.workload, 0, 1, args.scale)
+    model = models.random_mlp(b.family, 42)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    per_step = min(10.0, budget)
+    from oracle import oracle as O
+
+    O.build()
+    # size one step's sample from a calibration run
+    _, n_cal, dt_cal, threads = oracle_rate(b, sa, rng_, model, target_s=min(2.0, per_step), seed=1)
+    n_step = max(256, int(n_cal * per_step / max(dt_cal, 1e-6)))
+    rng = np.random.default_rng(11)
+    g0, g1 = rng_
+    total = (g1 - g0) * b.n_configs
+    times = []
+    for s in range(args.warmup + args.steps):
+        p = rng.integers(0, total, n_step)
+        ci, si = p % b.n_configs, g0 + p // b.n_configs
+        t = time.perf_counter()
+        f = O.featurize(b, sa, cfg_idx=ci, spec_idx=si)
+        O.predict(model, f)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t)
+    tot = float(np.sum(times))
+    value = n_step * args.steps / tot
+    sample = (f"{n_step} random pairs per step of workload {args.workload} "
+              f"({total} pairs), featurize + predict, fp64")
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
+                   "pairs_per_step": n_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+
+    import paper_2601_14910_b200 as sp
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = sp.Context(local_rank)
+    b, sa, (g0, g1), scaling = build_workload(args.workload, rank, world, args.scale)
+    specs_h = ctx.load_gpu_specs(sa)
+    model_d = models.random_mlp(b.family, 42)
+    precision = args.precision
+    try:
+        model = ctx.load_model(model_d, precision)
+    except sp.SynPerfError as e:
+        if precision == "bf16" and e.status == 4 and not args.strict_precision:
+            precision = "fp32"
+            model = ctx.load_model(model_d, precision)
+        else:
+            raise
+    n_in = int(model_d["n_in"])
+    db = sp.DeviceBatch.from_host(b, dev)
+    n_pairs = (g1 - g0) * b.n_configs
+    feats = sp.Features.empty(b.family, n_pairs, dev)
+    lat = torch.empty(max(n_pairs, 1), dtype=torch.float32, device=dev)
+    pairs = sp.cross(g0, g1)
+    stream = torch.cuda.current_stream()
+    gathered = None
+    if dist is not None and not args.no_gather:
+        gathered = torch.empty(world * n_pairs, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        ctx.featurize(db, specs_h, feats, pairs, stream)
+        if ev is not None:
+            ev[1].record(stream)
+        ctx.predict(model, feats, lat, None, stream)
+        if ev is not None:
+            ev[2].record(stream)
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered, lat[:n_pairs])
+        if ev is not None:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for s in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps, outside the events
+            step(evs[s])
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t_feat = np.array([e[0].elapsed_time(e[1]) for e in evs])
+    t_pred = np.array([e[1].elapsed_time(e[2]) for e in evs])
+    t_step = np.array([e[0].elapsed_time(e[3]) for e in evs])
+    tot_ms = float(t_step.sum())
+    if dist is not None:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    pairs_all = n_pairs * (world if scaling == "weak" else 1)
+    if scaling == "strong":
+        pairs_all = len(sa) * b.n_configs
+    value = pairs_all * args.steps / (tot_ms * 1e-3)
+
+    # ---- parity spot-check of this run's output (sampled, oracle) is done in tests;
+    # here only sanity: no NaN outside error pairs.
+    st = feats.status[:n_pairs]
+    bad = int(((st == 0) & torch.isnan(lat[:n_pairs])).sum().item())
+    if bad:
+        raise SystemExit(f"{bad} valid pairs produced NaN latency")
+
+    # ---- e2e through the public API with host buffers (rank-local)
+    e2e = run_e2e(args, ctx, specs_h, model, b, (g0, g1), dev, dist, world, scaling, len(sa))
+
+    # ---- roofline of the dominant kernel
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json")) or {}
+    feat_ms, pred_ms = float(t_feat.mean()), float(t_pred.mean())
+    roof = roofline(args, b, n_pairs, n_in, precision, feat_ms, pred_ms, peaks, prof, tot_ms)
+
+    line = {
+        "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "bf16" if precision == "bf16" else "f32",
+        "data": "synthetic (seeded generators, workloads/; seeded random MLP weights)",
+        "config": {
+            "workload": args.workload, "description": WORKLOADS[args.workload],
+            "pairs_per_gpu": n_pairs, "configs_per_gpu": b.n_configs, "specs": g1 - g0,
+            "family": gen.FAMILY_NAMES[b.family], "mlp_precision": precision,
+            "parallelism": f"dp{world}" + ("+allgather" if gathered is not None else ""),
+            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+        },
+        "stage_ms": {"featurize": feat_ms, "predict": pred_ms,
+                     "allgather": float((t_step - t_feat - t_pred).mean())},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, dt, thr = oracle_rate(b, sa, (g0, g1), model_d, target_s=args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+            "sample": f"{n} random pairs of this workload, fp64 oracle featurize+predict, {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling, n_specs):
+    """Same metric through Context.predict_host with pinned host buffers: every
+    step copies the configs H2D and the fp32 latencies D2H."""
+    import torch
+
+    fields = torch.from_numpy(b.fields).pin_memory()
+    ragged = torch.from_numpy(b.ragged).pin_memory() if b.ragged is not None else None
+    roff = torch.from_numpy(b.ragged_off).pin_memory() if b.ragged_off is not None else None
+
+    class HostBatch:
+        family = b.family
+
+    hb = HostBatch()
+    hb.fields, hb.ragged, hb.ragged_off = fields, ragged, roff
+    g0, g1 = spec_range
+    n_pairs = (g1 - g0) * b.n_configs
+    out = torch.empty(n_pairs, dtype=torch.float32).pin_memory().numpy()
+    h2d = fields.numel() * 4 + (ragged.numel() * 4 if ragged is not None else 0) + \
+        (roff.numel() * 8 if roff is not None else 0)
+    d2h = n_pairs * 4
+    for _ in range(max(1, min(args.warmup, 2))):
+        ctx.predict_host(hb, specs_h, model, spec_range, out=out)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(steps):
+        ctx.predict_host(hb, specs_h, model, spec_range, out=out)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t
+    if dist is not None:
+        tt = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    pairs_all = n_pairs * world if scaling == "weak" else n_specs * b.n_configs
+    return {"value": pairs_all * steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "api": "Context.predict_host (pinned host configs -> H2D -> sp_featurize -> "
+                   "sp_predict -> D2H latencies)"}
+
+
+def roofline(args, b, n_pairs, n_in, precision, feat_ms, pred_ms, peaks, prof, tot_ms):
+    """Roofline object for the dominant kernel of the step."""
+    hbm = peaks.get("hbm_gbs")
+    long_region = tot_ms > 1000.0
+    bf16_peak = peaks.get("bf16_tflops_sustained" if long_region else "bf16_tflops")
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if pred_ms >= feat_ms:
+        kernel = "predict_tcgen05_bf16" if precision == "bf16" else "predict_simt_fp32"
+        flop = MLP_FLOP_PER_PAIR[n_in] * n_pairs
+        achieved = flop / (pred_ms * 1e-3) / 1e12
+        if precision == "bf16":
+            peak, bound, src = bf16_peak, "tensor", ("MEASURED_PEAKS.json " +
+                                                     ("bf16_tflops_sustained" if long_region else "bf16_tflops"))
+        else:
+            # fp32 FFMA peak from unit counts: 148 SMs x 128 lanes x 2 FLOP x max SM clock
+            peak, bound, src = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "alu", \
+                "148 SMs x 128 FP32 lanes x 2 FLOP x sm_max_mhz (DESIGN.md §6)"
+        unit, ms, per_unit = "TFLOP/s", pred_ms, f"{MLP_FLOP_PER_PAIR[n_in]} FLOP/pair"
+    else:
+        if b.family == gen.ATTENTION:
+            kernel = "featurize_attention_cross"
+            # issue-rate roofline: warp instructions per launch from the committed ncu capture
+            instr = (prof.get(args.workload, {}) or {}).get("featurize_inst_executed")
+            achieved = None if instr is None else instr / (feat_ms * 1e-3) / 1e9
+            peak = 4 * 148 * sm_mhz * 1e6 / 1e9
+            bound, unit, src = "alu", "Ginstr/s", "4 warp-instr/clk/SM x 148 x sm_max_mhz (DESIGN.md §6)"
+            per_unit = "warp instructions per launch (ncu sm__inst_executed.sum)"
+        else:
+            kernel = "featurize_uniform_cross"
+            nbytes = n_pairs * RECORD_BYTES + b.fields.nbytes + \
+                (b.ragged.nbytes if b.ragged is not None else 0)
+            achieved = nbytes / (feat_ms * 1e-3) / 1e9
+            peak, bound, unit, src = hbm, "hbm", "GB/s", "MEASURED_PEAKS.json hbm_gbs"
+            per_unit = f"{RECORD_BYTES} B/pair written + config bytes read"
+        ms = feat_ms
+    traffic = (prof.get(args.workload, {}) or {}).get(kernel + "_dram_bytes")
+    return {"kernel": kernel, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": (achieved / peak) if (achieved is not None and peak) else None,
+            "traffic": traffic, "avg_launch_ms": ms, "per_unit": per_unit, "peak_source": src}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--scale", type=float, default=1.0, help="workload size multiplier (testing)")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--strict-precision", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_gpu(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -76,11 +76,13 @@ int pipes_count(int fam) {
 
 constexpr int kAttnMaxSms = 4096;
 constexpr int kAttnWordBudget = 2048;
-constexpr int kAttnMaxDistinct = 16;
+constexpr int kAttnMaxDistinct = 8;  // featurize_attention.cu kMaxDistinct
 
 // Device copy of one attention spec-group plan (see featurize_attention.cu).
 struct AttnPlanDev {
   DevBuf groups, group_specs, spec_dist, distinct_n, distinct_off;
+  std::vector<int32_t> nd;   // host copies for the launcher
+  std::vector<uint8_t> small;
   AttnPlan view{};
 };
 
@@ -291,6 +293,12 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
   pd->view.distinct_off = (const int32_t *)pd->distinct_off.p;
   pd->view.n_groups = (int32_t)groups.size();
   pd->view.words_per_warp = words_max;
+  for (const AttnGroup &gr : groups) {
+    pd->nd.push_back(gr.n_distinct);
+    pd->small.push_back(dn[gr.distinct_first] < 32);  // Ns ascending: first is the smallest
+  }
+  pd->view.host_nd = pd->nd.data();
+  pd->view.host_small = pd->small.data();
   *out = &pd->view;
   sp->plans.emplace(key, std::move(pd));
   return SP_OK;

@@ -4,20 +4,22 @@
 // Tasks: kv-head h outermost, then request b, q-block i, kv-chunk c (R4).  A
 // task's demands are affine in its kv units u = kv_eff/BKV:
 //   Tensor = 4*BQ*hd*BKV*u, XU = BQ*(BKV+1)*u, bytes = bpe*hd*(BQ + 2*BKV*u),
-// so per SM only two numbers matter: the task count n_j (closed form under
-// cyclic dealing) and the unit sum S_j.  All nkv kv-heads repeat the same
+// so per SM only two numbers matter: its task count n_j (closed form under
+// cyclic dealing, R5) and its unit sum S_j.  All nkv kv-heads repeat the same
 // task sequence of length L, so with A[r] = sum of u over head-0 tasks k with
 // k mod N = r, the per-SM sums are the rotations S_j = sum_h A[(j - h*L) mod N]
-// (exact identity of t -> t mod N with t = h*L + k).
+// (exact: task t = h*L + k goes to SM t mod N).
 //
 // Layout: one warp per config.  Lanes take 32 consecutive head-0 tasks per
-// step; the 32 SM residues are then distinct (N >= 32), so each lane updates
-// its own shared-memory accumulator with a plain load/add/store.  The task
+// step; with N >= 32 the 32 residues are distinct, so each lane updates its
+// own shared-memory accumulator with a plain load/add/store.  The task
 // sequence does not depend on the spec, so in SP_PAIRS_CROSS mode a warp
 // accumulates once per *distinct SM count* of the spec range (the 11 GPUs of
-// Table VI have 7 distinct counts) and then emits every spec of the group.
-// This kernel is ALU/issue bound (a handful of integer ops per task), not HBM
-// bound.
+// Table VI have 7) and then emits every spec of its group; the distinct set
+// is a template parameter so residues and offsets live in registers.  Configs
+// with T <= min N (every SM holds at most one task: most decode batches) skip
+// the accumulators: max_j S_j is the largest task's u.
+// The kernel is bound by integer issue, not by HBM.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -26,22 +28,16 @@ namespace sp {
 namespace {
 
 constexpr int kWarps = 8;           // warps per block
-constexpr int kMaxDistinct = 16;    // distinct SM counts per group
+constexpr int kMaxDistinct = 8;     // distinct SM counts per group (api.cu plans accordingly)
 constexpr int64_t kI32Max = 2147483647LL;
 constexpr int64_t kU32Max = 4294967295LL;
 constexpr unsigned __int128 kI64Max = 9223372036854775807ULL;
+typedef unsigned __int128 u128;
 
 // Field indices (include/synperf.h, SP_ATTENTION)
 enum { BS, NH, NKV, HD, BQ, BKV, CHUNK, CAUSAL, WARPS, REGS, SMEM, DTYPE };
 
-struct DistinctSet {
-  int nd;
-  const int32_t *N;     // [nd] SM counts
-  const int32_t *off;   // [nd] word offsets in the warp's accumulator region
-  const FastDiv *fd;    // [nd] divisors N
-};
-
-__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -56,6 +52,16 @@ __device__ __forceinline__ int64_t warp_min64(int64_t v) {
   for (int o = 16; o > 0; o >>= 1) v = min(v, (int64_t)__shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
+
+// Cheap FastDiv setup: powers of two need no division.
+__device__ __forceinline__ FastDiv make_fd(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.s = d <= 1 ? 0 : 32 - __clz(d - 1);
+  f.m = (d & (d - 1)) ? (uint32_t)((((1ull << f.s) - d) << 32) / d + 1) : 1u;
+  return f;
+}
 
 // Per-config scalars shared by all lanes.
 struct AttnCfg {
@@ -67,7 +73,7 @@ struct AttnCfg {
 
 __device__ __forceinline__ AttnCfg load_cfg(const ConfigView &v, int64_t c, int lane) {
   AttnCfg a{};
-  int32_t f = lane < 12 ? __ldg(v.fields + (int64_t)lane * v.ld + c) : 0;
+  const int32_t f = lane < 12 ? __ldg(v.fields + (int64_t)lane * v.ld + c) : 0;
   a.bs = __shfl_sync(0xffffffffu, f, BS);
   a.nh = __shfl_sync(0xffffffffu, f, NH);
   a.nkv = __shfl_sync(0xffffffffu, f, NKV);
@@ -108,117 +114,149 @@ __device__ __forceinline__ AttnCfg load_cfg(const ConfigView &v, int64_t c, int 
   return a;
 }
 
-// Advance a residue by 32 modulo N.
-__device__ __forceinline__ uint32_t step32(uint32_t r, uint32_t N, const FastDiv &fd) {
-  r += 32u;
-  if (r >= N) r -= N;
-  if (r >= N) r = fd.mod(r);
-  return r;
+// kv extent of q-block i of a request (R10-R11): q_last = floor((min((i+1)BQ, rows)-1)/g),
+// kv_need = min(kvlen, kvlen - qlen + q_last + 1) if causal, else kvlen.
+__device__ __forceinline__ uint32_t kv_need(uint64_t i, uint64_t bq, uint64_t rows, uint32_t qlen,
+                                            uint32_t kvlen, bool causal, const FastDiv &fg) {
+  if (!causal) return kvlen;
+  const uint64_t e = min((i + 1) * bq, rows) - 1;
+  const uint32_t q_last = fg.div((uint32_t)e);
+  return min(kvlen, kvlen - qlen + q_last + 1);
 }
 
-// Accumulate unit value u of head-0 task position `pos` (residues r[d]) into
-// every distinct slot.  Lanes of one call hold distinct positions; when
-// N >= 32 their residues are distinct so a plain RMW is race-free.
-__device__ __forceinline__ void accumulate(uint32_t *acc, const DistinctSet &ds, const uint32_t *r,
-                                           uint32_t u, bool active) {
-#pragma unroll
-  for (int d = 0; d < kMaxDistinct; ++d) {
-    if (d < ds.nd && active) {
-      uint32_t *a = acc + ds.off[d] + r[d];
-      if (ds.N[d] >= 32) *a += u;
-      else atomicAdd(a, u);
+__device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b) {
+  const uint64_t lim = 1ull << 40;
+  const uint64_t s = a + b;
+  return s > lim ? lim : s;
+}
+
+// Pre-pass: per-head task count L (lanes over requests; causal split-KV walks
+// the request's q-blocks).  Saturates at 2^40 (anything above 2^31 is RANGE).
+__device__ int64_t count_tasks(const AttnCfg &a, int lane, const FastDiv &fg) {
+  uint64_t part = 0;
+  for (int64_t b = lane; b < a.bs; b += 32) {
+    const uint32_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
+    const uint64_t rows = (uint64_t)q * a.g, nqb = (rows + a.bq - 1) / a.bq;
+    if (a.chunk == 0) {
+      part = sat_add(part, nqb);
+    } else if (!a.causal) {
+      part = sat_add(part, nqb * ((kv + a.chunk - 1) / a.chunk));
+    } else {
+      for (uint64_t i = 0; i < nqb && part < (1ull << 40); ++i)
+        part = sat_add(part, (kv_need(i, a.bq, rows, q, kv, true, fg) + a.chunk - 1) / a.chunk);
     }
   }
+  return (int64_t)min(warp_sum_u64(part), (uint64_t)(1ull << 40));
 }
 
-// Results per distinct SM count: max_j S_j and max_j (BQ*n_j + 2*BKV*S_j).
+// Sparse path (T <= min N): every SM holds at most one task, so only the unit
+// sum U and the largest unit umax are needed.  Lanes over requests.
+__device__ void sparse_units(const AttnCfg &a, int lane, const FastDiv &fg, uint64_t &U, uint32_t &umax) {
+  uint64_t us = 0;
+  uint32_t um = 0;
+  for (int64_t b = lane; b < a.bs; b += 32) {
+    const uint32_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
+    const uint64_t rows = (uint64_t)q * a.g, nqb = (rows + a.bq - 1) / a.bq;
+    for (uint64_t i = 0; i < nqb; ++i) {
+      const uint32_t need = kv_need(i, a.bq, rows, q, kv, a.causal, fg);
+      if (a.chunk == 0) {
+        const uint32_t u = (uint32_t)((need + a.bkv - 1) / a.bkv);
+        us += u;
+        um = max(um, u);
+      } else {
+        for (uint64_t c0 = 0; c0 < need; c0 += a.chunk) {
+          const uint32_t u = (uint32_t)((min((uint64_t)a.chunk, need - c0) + a.bkv - 1) / a.bkv);
+          us += u;
+          um = max(um, u);
+        }
+      }
+    }
+  }
+  U = warp_sum_u64(us);
+  umax = warp_max_u32(um);
+}
+
 struct DistinctMax {
-  int64_t maxS, maxB;
+  int64_t maxS, maxB;  // max_j S_j and max_j (BQ*n_j + 2*BKV*S_j)
 };
 
-// Runs the task loop of one config for every distinct SM count; returns the
-// per-head task count L and unit sum U (or a RANGE status), and fills res[d].
-__device__ int attn_accumulate(const AttnCfg &a, uint32_t *acc, int words, const DistinctSet &ds,
-                               int lane, int64_t &L_out, int64_t &U_out, DistinctMax *res) {
+// General path: per-SM accumulators in the warp's shared-memory region.
+// N[d], off[d]: distinct SM counts of the group and their word offsets.
+template <int ND, bool SMALL>
+__device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, const int32_t (&N)[ND],
+                               const int32_t (&off)[ND], const FastDiv *fdN, int lane, const FastDiv &fg) {
   for (int w = lane * 4; w < words; w += 128) *reinterpret_cast<uint4 *>(acc + w) = make_uint4(0, 0, 0, 0);
   __syncwarp();
-  FastDiv fg, fbkv;
-  fg.init((uint32_t)a.g);
-  fbkv.init((uint32_t)a.bkv);
-  int64_t base = 0;     // head-0 task index of the current request's first task
-  int64_t usum = 0;     // per-lane partial of U
-  int status = 0;
-  uint32_t r[kMaxDistinct];
-  for (int64_t b = 0; b < a.bs && status == 0; ++b) {
-    const int64_t qlen = __ldg(a.req + 2 * b), kvlen = __ldg(a.req + 2 * b + 1);
-    const int64_t rows = qlen * a.g;
-    const int64_t nqb = cdiv64(rows, a.bq);
-    const bool split = a.chunk > 0;
-    if (!split || !a.causal) {
+  const FastDiv fbkv = make_fd((uint32_t)a.bkv);
+  uint32_t base = 0;  // head-0 index of the request's first task (< 2^31, checked by the pre-pass)
+  uint64_t usum = 0;
+  for (int64_t b = 0; b < a.bs; ++b) {
+    const uint32_t qlen = __ldg(a.req + 2 * b), kvlen = __ldg(a.req + 2 * b + 1);
+    const uint64_t rows = (uint64_t)qlen * a.g;
+    const uint64_t nqb = (rows + a.bq - 1) / a.bq;
+    if (a.chunk == 0 || !a.causal) {
       // every q-block has the same chunk count (unsplit, or non-causal kv_need = kvlen)
-      const int64_t n_ch = split ? cdiv64(kvlen, a.chunk) : 1;
-      const int64_t tasks = nqb * n_ch;
-      if (base + tasks > kI32Max) { status = SP_PAIR_E_RANGE; break; }
-      FastDiv fch;
-      fch.init((uint32_t)n_ch);
-      const uint32_t u_full = split ? (uint32_t)cdiv64(min(a.chunk, kvlen), a.bkv) : 0;
-      const uint32_t u_last = split ? (uint32_t)cdiv64(kvlen - (n_ch - 1) * a.chunk, a.bkv) : 0;
+      const bool split = a.chunk > 0;
+      const uint32_t n_ch = split ? (uint32_t)((kvlen + a.chunk - 1) / a.chunk) : 1u;
+      const uint32_t tasks = (uint32_t)(nqb * n_ch);
+      const FastDiv fch = make_fd(n_ch);
+      const uint32_t u_full = split ? (uint32_t)((min((uint64_t)a.chunk, (uint64_t)kvlen) + a.bkv - 1) / a.bkv) : 0;
+      const uint32_t u_last = split ? (uint32_t)((kvlen - (uint64_t)(n_ch - 1) * a.chunk + a.bkv - 1) / a.bkv) : 0;
+      int32_t p[ND];
 #pragma unroll
-      for (int d = 0; d < kMaxDistinct; ++d)
-        if (d < ds.nd) r[d] = ds.fd[d].mod((uint32_t)(base + lane));
-      for (int64_t k0 = 0; k0 < tasks; k0 += 32) {
-        const int64_t k = k0 + lane;
+      for (int d = 0; d < ND; ++d) p[d] = off[d] + (int32_t)fdN[d].mod(base + lane);
+      for (uint32_t k0 = 0; k0 < tasks; k0 += 32) {
+        const uint32_t k = k0 + lane;
         const bool active = k < tasks;
         uint32_t u = 0;
         if (active) {
-          if (split) {  // non-causal: kv_need = kvlen for every q-block
-            const uint32_t ch = fch.mod((uint32_t)k);
-            u = ch == (uint32_t)(n_ch - 1) ? u_last : u_full;
+          if (split) {
+            u = fch.mod(k) == n_ch - 1 ? u_last : u_full;
           } else {
-            // q_last = floor((min((i+1)BQ, rows) - 1) / g); kv_need (causal) = min(kvlen, kvlen - qlen + q_last + 1)
-            const int64_t end = min((k + 1) * a.bq, rows) - 1;
-            const int64_t q_last = fg.div((uint32_t)end);
-            const int64_t need = a.causal ? min(kvlen, kvlen - qlen + q_last + 1) : kvlen;
-            u = fbkv.div((uint32_t)(need + a.bkv - 1));
+            const uint32_t need = kv_need(k, a.bq, rows, qlen, kvlen, a.causal, fg);
+            u = fbkv.div(need + (uint32_t)a.bkv - 1);
           }
         }
-        accumulate(acc, ds, r, u, active);
         usum += u;
-        __syncwarp();
+        if (SMALL) {
 #pragma unroll
-        for (int d = 0; d < kMaxDistinct; ++d)
-          if (d < ds.nd) r[d] = step32(r[d], (uint32_t)ds.N[d], ds.fd[d]);
+          for (int d = 0; d < ND; ++d)
+            if (active) atomicAdd(acc + off[d] + fdN[d].mod(base + k), u);
+        } else {
+#pragma unroll
+          for (int d = 0; d < ND; ++d) {
+            if (active) acc[p[d]] += u;
+            p[d] += 32;
+            if (p[d] >= off[d] + N[d]) p[d] -= N[d];
+          }
+        }
+        __syncwarp();
       }
       base += tasks;
     } else {
       // causal + split-KV: each q-block has its own chunk count.  Lanes take
       // 32 q-blocks, scan their chunk counts, then walk their own chunks
-      // (positions are no longer lane-consecutive: atomic adds).
-      for (int64_t i0 = 0; i0 < nqb && status == 0; i0 += 32) {
-        const int64_t i = i0 + lane;
-        int64_t need = 0, n_ch = 0;
+      // (positions no longer lane-consecutive: atomic adds).
+      for (uint64_t i0 = 0; i0 < nqb; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        uint32_t need = 0, n_ch = 0;
         if (i < nqb) {
-          const int64_t end = min((i + 1) * a.bq, rows) - 1;
-          const int64_t q_last = fg.div((uint32_t)end);
-          need = min(kvlen, kvlen - qlen + q_last + 1);
-          n_ch = cdiv64(need, a.chunk);
+          need = kv_need(i, a.bq, rows, qlen, kvlen, true, fg);
+          n_ch = (uint32_t)((need + a.chunk - 1) / a.chunk);
         }
-        int64_t incl = n_ch;
+        uint32_t incl = n_ch;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += t;
         }
-        const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (base + total > kI32Max) { status = SP_PAIR_E_RANGE; break; }
-        const int64_t start = base + incl - n_ch;
-        for (int64_t ch = 0; ch < n_ch; ++ch) {
-          const int64_t len = min(a.chunk, need - ch * a.chunk);
-          const uint32_t u = (uint32_t)cdiv64(len, a.bkv);
-          const uint32_t pos = (uint32_t)(start + ch);
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t start = base + incl - n_ch;
+        for (uint32_t ch = 0; ch < n_ch; ++ch) {
+          const uint64_t len = min((uint64_t)a.chunk, (uint64_t)need - (uint64_t)ch * a.chunk);
+          const uint32_t u = (uint32_t)((len + a.bkv - 1) / a.bkv);
 #pragma unroll
-          for (int d = 0; d < kMaxDistinct; ++d)
-            if (d < ds.nd) atomicAdd(acc + ds.off[d] + ds.fd[d].mod(pos), u);
+          for (int d = 0; d < ND; ++d) atomicAdd(acc + off[d] + fdN[d].mod(start + ch), u);
           usum += u;
         }
         base += total;
@@ -226,47 +264,34 @@ __device__ int attn_accumulate(const AttnCfg &a, uint32_t *acc, int words, const
       }
     }
   }
-  const int64_t U = warp_sum64(usum);
-  const int64_t L = base;
-  if (status == 0 && (U > kU32Max || L * a.nkv > kI32Max)) status = SP_PAIR_E_RANGE;
-  L_out = L;
-  U_out = U;
-  if (status) return status;
   __syncwarp();
-  // fold the nkv rotations and take the per-quantity maxima per distinct N
-  const int64_t T = L * a.nkv;
-  for (int d = 0; d < ds.nd; ++d) {
-    const int64_t N = ds.N[d];
-    const uint32_t Lm = ds.fd[d].mod((uint32_t)L);
-    const uint32_t *A = acc + ds.off[d];
-    int64_t mS = 0, mB = 0;
-    for (int64_t s = lane; s < N; s += 32) {
-      int64_t S = 0;
-      int64_t o = 0;  // (h * L) mod N
-      for (int64_t h = 0; h < a.nkv; ++h) {
-        int64_t idx = s - o;
-        if (idx < 0) idx += N;
-        S += A[idx];
-        o += Lm;
-        if (o >= N) o -= N;
-      }
-      const int64_t n_s = s < T ? (T - s - 1) / N + 1 : 0;
-      mS = max(mS, S);
-      mB = max(mB, a.bq * n_s + 2 * a.bkv * S);
-    }
-    mS = warp_max64(mS);
-    mB = warp_max64(mB);
-    if (lane == 0) res[d] = DistinctMax{mS, mB};
-  }
-  __syncwarp();
-  return 0;
+  return warp_sum_u64(usum);
 }
 
-typedef unsigned __int128 u128;
+// Fold the nkv rotations of one distinct N and take the per-quantity maxima.
+__device__ DistinctMax fold(const AttnCfg &a, const uint32_t *A, int32_t N, const FastDiv &fdN, uint32_t L,
+                            uint32_t T, int lane) {
+  const uint32_t Lm = fdN.mod(L);
+  const uint32_t qn = fdN.div(T), rn = T - qn * (uint32_t)N;  // SM j holds qn + (j < rn) tasks
+  int64_t mS = 0, mB = 0;
+  for (int32_t s = lane; s < N; s += 32) {
+    uint64_t S = 0;
+    int32_t o = 0;  // (h * L) mod N
+    for (int64_t h = 0; h < a.nkv; ++h) {
+      int32_t idx = s - o;
+      idx += idx < 0 ? N : 0;
+      S += A[idx];
+      o += (int32_t)Lm;
+      o -= o >= N ? N : 0;
+    }
+    const int64_t n_s = (int64_t)qn + ((uint32_t)s < rn ? 1 : 0);
+    mS = max(mS, (int64_t)S);
+    mB = max(mB, a.bq * n_s + 2 * a.bkv * (int64_t)S);
+  }
+  return DistinctMax{warp_max64(mS), warp_max64(mB)};
+}
 
-// a*b, flagging (bad = true) a product above INT64_MAX without overflowing:
-// operands are each < 2^96 here, so either one exceeds 2^63 (and the other is
-// nonzero) or the product is < 2^126.
+// a*b with a "> INT64_MAX" flag, without 128-bit overflow (operands < 2^96).
 __device__ __forceinline__ u128 mul_le_i64(u128 a, u128 b, bool &bad) {
   if (a == 0 || b == 0) return 0;
   if (a > kI64Max || b > kI64Max) { bad = true; return 0; }
@@ -275,7 +300,7 @@ __device__ __forceinline__ u128 mul_le_i64(u128 a, u128 b, bool &bad) {
 
 // One (config, spec) record from the accumulated per-distinct maxima.
 __device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const AttnCfg &a, int cfg_status,
-                                          int64_t L, int64_t U, const DistinctMax &m, const DevSpec &s) {
+                                          int64_t L, uint64_t U, const DistinctMax &m, const DevSpec &s) {
   if (cfg_status) { emit_error(out, p, cfg_status); return; }
   const int tdt = (int)a.dt;
   if (!s.tensor_ok[tdt]) { emit_error(out, p, SP_PAIR_E_DTYPE); return; }
@@ -299,54 +324,81 @@ __device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const A
   emit_pair(out, p, d, a.fp, s, 5, tdt);
 }
 
-__global__ void __launch_bounds__(kWarps * 32) featurize_attention_cross(ConfigView cfg,
-                                                                         const DevSpec *__restrict__ specs,
-                                                                         int g0, AttnPlan plan, FeatOut out) {
-  extern __shared__ uint32_t smem[];
-  __shared__ int32_t s_N[kMaxDistinct], s_off[kMaxDistinct];
-  __shared__ FastDiv s_fd[kMaxDistinct];
-  __shared__ DistinctMax s_res[kWarps][kMaxDistinct];
-  const AttnGroup grp = plan.groups[blockIdx.y];
-  if (threadIdx.x < grp.n_distinct) {
-    const int n = plan.distinct_n[grp.distinct_first + threadIdx.x];
-    s_N[threadIdx.x] = n;
-    s_off[threadIdx.x] = plan.distinct_off[grp.distinct_first + threadIdx.x];
-    s_fd[threadIdx.x].init((uint32_t)n);
+// Whole per-config pipeline for one distinct set; results in res[0..ND).
+template <int ND, bool SMALL>
+__device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, const int32_t (&N)[ND],
+                           const int32_t (&off)[ND], const FastDiv *fdN, int32_t minN, int lane, int64_t &L,
+                           uint64_t &U, DistinctMax *res) {
+  const FastDiv fg = make_fd((uint32_t)a.g);
+  L = count_tasks(a, lane, fg);
+  if (L > kI32Max || L * a.nkv > kI32Max) return SP_PAIR_E_RANGE;
+  const int64_t T = L * a.nkv;
+  if (T <= minN) {
+    uint32_t umax;
+    sparse_units(a, lane, fg, U, umax);
+    if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) res[d] = DistinctMax{(int64_t)umax, a.bq + 2 * a.bkv * (int64_t)umax};
+    return 0;
   }
+  U = accumulate<ND, SMALL>(a, acc, words, N, off, fdN, lane, fg);
+  if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) res[d] = fold(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
+  return 0;
+}
+
+template <int ND, bool SMALL>
+__global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_cross(ConfigView cfg,
+                                                                            const DevSpec *__restrict__ specs,
+                                                                            int g0, AttnPlan plan, FeatOut out) {
+  extern __shared__ uint32_t smem[];
+  __shared__ FastDiv s_fd[kMaxDistinct];
+  const AttnGroup grp = plan.groups[blockIdx.y];
+  int32_t N[ND], off[ND];
+  int32_t minN = INT32_MAX, words = 0;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    N[d] = __ldg(plan.distinct_n + grp.distinct_first + d);
+    off[d] = __ldg(plan.distinct_off + grp.distinct_first + d);
+    minN = min(minN, N[d]);
+    words = max(words, off[d] + N[d]);
+  }
+  words = (words + 3) & ~3;
+  if (threadIdx.x < ND) s_fd[threadIdx.x] = make_fd((uint32_t)N[threadIdx.x]);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *acc = smem + (size_t)warp * plan.words_per_warp;
-  const DistinctSet ds{grp.n_distinct, s_N, s_off, s_fd};
-  int words = 0;
-  for (int d = 0; d < grp.n_distinct; ++d) words = max(words, s_off[d] + s_N[d]);
-  words = (words + 3) & ~3;
   const int64_t C = cfg.n_configs;
   for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < C; c += (int64_t)gridDim.x * kWarps) {
     const AttnCfg a = load_cfg(cfg, c, lane);
     int st = a.status;
-    int64_t L = 0, U = 0;
-    if (st == 0) st = attn_accumulate(a, acc, words, ds, lane, L, U, s_res[warp]);
+    int64_t L = 0;
+    uint64_t U = 0;
+    DistinctMax res[ND];
+    if (st == 0) st = attn_config<ND, SMALL>(a, acc, words, N, off, s_fd, minN, lane, L, U, res);
     for (int j = lane; j < grp.n_specs; j += 32) {
-      const int g = plan.group_specs[grp.spec_first + j];
-      const int d = plan.spec_dist[grp.spec_first + j] - grp.distinct_first;
-      const int64_t p = (int64_t)(g - g0) * C + c;
-      attn_emit(out, p, a, st, L, U, s_res[warp][d], specs[g]);
+      const int g = __ldg(plan.group_specs + grp.spec_first + j);
+      const int dsel = __ldg(plan.spec_dist + grp.spec_first + j) - grp.distinct_first;
+      DistinctMax m = res[0];
+#pragma unroll
+      for (int d = 1; d < ND; ++d)
+        if (dsel == d) m = res[d];
+      attn_emit(out, (int64_t)(g - g0) * C + c, a, st, L, U, m, specs[g]);
     }
     __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) featurize_attention_list(ConfigView cfg,
-                                                                        const DevSpec *__restrict__ specs,
-                                                                        int n_specs, int words_per_warp,
-                                                                        int64_t n_pairs,
-                                                                        const int64_t *__restrict__ cfg_idx,
-                                                                        const int32_t *__restrict__ spec_idx,
-                                                                        FeatOut out) {
+__global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(ConfigView cfg,
+                                                                           const DevSpec *__restrict__ specs,
+                                                                           int n_specs, int words_per_warp,
+                                                                           int64_t n_pairs,
+                                                                           const int64_t *__restrict__ cfg_idx,
+                                                                           const int32_t *__restrict__ spec_idx,
+                                                                           FeatOut out) {
   extern __shared__ uint32_t smem[];
-  __shared__ int32_t s_N[kWarps], s_off[kWarps];
   __shared__ FastDiv s_fd[kWarps];
-  __shared__ DistinctMax s_res[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *acc = smem + (size_t)warp * words_per_warp;
   for (int64_t p = (int64_t)blockIdx.x * kWarps + warp; p < n_pairs; p += (int64_t)gridDim.x * kWarps) {
@@ -356,52 +408,87 @@ __global__ void __launch_bounds__(kWarps * 32) featurize_attention_list(ConfigVi
       if (lane == 0) emit_error(out, p, SP_PAIR_E_INDEX);
       continue;
     }
-    const int N = specs[g].num_sms;
-    if (lane == 0) {
-      s_N[warp] = N;
-      s_off[warp] = 0;
-      s_fd[warp].init((uint32_t)N);
-    }
+    const int32_t N[1] = {specs[g].num_sms}, off[1] = {0};
+    if (lane == 0) s_fd[warp] = make_fd((uint32_t)N[0]);
     __syncwarp();
-    const DistinctSet ds{1, s_N + warp, s_off + warp, s_fd + warp};
     const AttnCfg a = load_cfg(cfg, c, lane);
     int st = a.status;
-    int64_t L = 0, U = 0;
-    if (st == 0) st = attn_accumulate(a, acc, (N + 3) & ~3, ds, lane, L, U, s_res + warp);
-    if (lane == 0) attn_emit(out, p, a, st, L, U, s_res[warp], specs[g]);
+    int64_t L = 0;
+    uint64_t U = 0;
+    DistinctMax res[1];
+    const int words = (N[0] + 3) & ~3;
+    if (st == 0) {
+      if (N[0] >= 32) st = attn_config<1, false>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, res);
+      else st = attn_config<1, true>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, res);
+    }
+    if (lane == 0) attn_emit(out, p, a, st, L, U, res[0], specs[g]);
     __syncwarp();
+  }
+}
+
+template <int ND, bool SMALL>
+int launch_cross(const ConfigView &cfg, const DevSpec *specs, int g0, const AttnPlan &plan, const FeatOut &out,
+                 int num_device_sms, cudaStream_t st, int group_y0, int n_groups) {
+  const size_t smem = (size_t)kWarps * plan.words_per_warp * 4;
+  cudaError_t e = cudaFuncSetAttribute(featurize_attention_cross<ND, SMALL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  int64_t want = (cfg.n_configs + kWarps - 1) / kWarps;
+  int64_t cap = (int64_t)num_device_sms * 8;
+  AttnPlan sub = plan;
+  sub.groups = plan.groups + group_y0;
+  dim3 grid((unsigned)(want < cap ? want : cap), (unsigned)n_groups);
+  featurize_attention_cross<ND, SMALL><<<grid, kWarps * 32, smem, st>>>(cfg, specs, g0, sub, out);
+  return (int)cudaGetLastError();
+}
+
+template <bool SMALL>
+int launch_nd(int nd, const ConfigView &cfg, const DevSpec *specs, int g0, const AttnPlan &plan,
+              const FeatOut &out, int sms, cudaStream_t st, int y0, int ny) {
+  switch (nd) {
+    case 1: return launch_cross<1, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    case 2: return launch_cross<2, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    case 3: return launch_cross<3, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    case 4: return launch_cross<4, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    case 5: return launch_cross<5, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    case 6: return launch_cross<6, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    case 7: return launch_cross<7, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    default: return launch_cross<8, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
   }
 }
 
 }  // namespace
 
-int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin,
-                               int n_specs, const AttnPlan &plan, int64_t n_pairs, const int64_t *cfg_idx,
+int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
+                               const AttnPlan &plan, int64_t n_pairs, const int64_t *cfg_idx,
                                const int32_t *spec_idx, int32_t max_sms, const FeatOut &out,
                                int num_device_sms, void *stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (cfg_idx == nullptr) {
     if (cfg.n_configs == 0 || plan.n_groups == 0) return 0;
-    const size_t smem = (size_t)kWarps * plan.words_per_warp * 4;
-    cudaError_t e = cudaFuncSetAttribute(featurize_attention_cross,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    int64_t want = (cfg.n_configs + kWarps - 1) / kWarps;
-    int64_t cap = (int64_t)num_device_sms * 16;
-    dim3 grid((unsigned)(want < cap ? want : cap), (unsigned)plan.n_groups);
-    featurize_attention_cross<<<grid, kWarps * 32, smem, st>>>(cfg, specs, spec_begin, plan, out);
-  } else {
-    if (n_pairs == 0) return 0;
-    const int words = (max_sms + 3) & ~3;
-    const size_t smem = (size_t)kWarps * words * 4;
-    cudaError_t e = cudaFuncSetAttribute(featurize_attention_list,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    int64_t want = (n_pairs + kWarps - 1) / kWarps;
-    int64_t cap = (int64_t)num_device_sms * 16;
-    featurize_attention_list<<<(unsigned)(want < cap ? want : cap), kWarps * 32, smem, st>>>(
-        cfg, specs, n_specs, words, n_pairs, cfg_idx, spec_idx, out);
+    // one launch per run of groups with the same (distinct count, small-N) shape
+    for (int y = 0; y < plan.n_groups;) {
+      const int nd = plan.host_nd[y];
+      const bool small = plan.host_small[y];
+      int y1 = y + 1;
+      while (y1 < plan.n_groups && plan.host_nd[y1] == nd && plan.host_small[y1] == small) ++y1;
+      int e = small ? launch_nd<true>(nd, cfg, specs, spec_begin, plan, out, num_device_sms, st, y, y1 - y)
+                    : launch_nd<false>(nd, cfg, specs, spec_begin, plan, out, num_device_sms, st, y, y1 - y);
+      if (e) return e;
+      y = y1;
+    }
+    return 0;
   }
+  if (n_pairs == 0) return 0;
+  const int words = (max_sms + 3) & ~3;
+  const size_t smem = (size_t)kWarps * words * 4;
+  cudaError_t e = cudaFuncSetAttribute(featurize_attention_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  int64_t want = (n_pairs + kWarps - 1) / kWarps;
+  int64_t cap = (int64_t)num_device_sms * 8;
+  featurize_attention_list<<<(unsigned)(want < cap ? want : cap), kWarps * 32, smem, st>>>(
+      cfg, specs, n_specs, words, n_pairs, cfg_idx, spec_idx, out);
   return (int)cudaGetLastError();
 }
 

@@ -85,6 +85,8 @@ struct AttnPlan {
   const int32_t *distinct_off; // DEVICE word offset of the slot in the warp's smem region
   int32_t n_groups;
   int32_t words_per_warp;      // u32 accumulator words per warp
+  const int32_t *host_nd;      // HOST [n_groups]: distinct count per group (kernel template)
+  const uint8_t *host_small;   // HOST [n_groups]: group holds an SM count < 32 (atomic path)
 };
 int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin,
                                int n_specs, const AttnPlan &plan, int64_t n_pairs, const int64_t *cfg_idx,
