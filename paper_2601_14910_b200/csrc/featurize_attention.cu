@@ -66,7 +66,7 @@ __device__ __forceinline__ FastDiv make_fd(uint32_t d) {
 // Per-config scalars shared by all lanes.
 struct AttnCfg {
   int status;
-  int64_t bs, nh, nkv, hd, bq, bkv, chunk, causal, dt, g;
+  int32_t bs, nh, nkv, hd, bq, bkv, chunk, causal, dt, g;  // input fields are int32
   const int32_t *req;
   Footprint fp;
 };
@@ -108,7 +108,7 @@ __device__ __forceinline__ AttnCfg load_cfg(const ConfigView &v, int64_t c, int 
   }
   first = warp_min64(first);
   if (first != INT64_MAX) { a.status = (int)(first % 16); return a; }
-  a.fp.smem = smem > 0 ? smem : (a.bq + 2 * a.bkv) * a.hd * 2;
+  a.fp.smem = smem > 0 ? smem : ((int64_t)a.bq + 2 * (int64_t)a.bkv) * a.hd * 2;
   a.fp.warps = warps;
   a.fp.regs = regs;
   return a;
@@ -188,35 +188,35 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, const
   for (int w = lane * 4; w < words; w += 128) *reinterpret_cast<uint4 *>(acc + w) = make_uint4(0, 0, 0, 0);
   __syncwarp();
   const FastDiv fbkv = make_fd((uint32_t)a.bkv);
+  const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);  // shared-window byte address
   uint32_t base = 0;  // head-0 index of the request's first task (< 2^31, checked by the pre-pass)
   uint64_t usum = 0;
   for (int64_t b = 0; b < a.bs; ++b) {
     const uint32_t qlen = __ldg(a.req + 2 * b), kvlen = __ldg(a.req + 2 * b + 1);
-    const uint64_t rows = (uint64_t)qlen * a.g;
-    const uint64_t nqb = (rows + a.bq - 1) / a.bq;
+    const uint32_t rows = qlen * (uint32_t)a.g;  // < 2^31 (validated)
+    const uint32_t nqb = (rows + (uint32_t)a.bq - 1u) / (uint32_t)a.bq;
     if (a.chunk == 0 || !a.causal) {
       // every q-block has the same chunk count (unsplit, or non-causal kv_need = kvlen)
       const bool split = a.chunk > 0;
       const uint32_t n_ch = split ? (uint32_t)((kvlen + a.chunk - 1) / a.chunk) : 1u;
-      const uint32_t tasks = (uint32_t)(nqb * n_ch);
-      const FastDiv fch = make_fd(n_ch);
+      const uint32_t tasks = nqb * n_ch;  // <= L < 2^31 (pre-pass)
+      const FastDiv fch = split ? make_fd(n_ch) : FastDiv{1u, 1u, 0u};
       const uint32_t u_full = split ? (uint32_t)((min((uint64_t)a.chunk, (uint64_t)kvlen) + a.bkv - 1) / a.bkv) : 0;
       const uint32_t u_last = split ? (uint32_t)((kvlen - (uint64_t)(n_ch - 1) * a.chunk + a.bkv - 1) / a.bkv) : 0;
-      int32_t p[ND];
+      uint32_t p[ND];  // byte address of this lane's accumulator for each distinct N
 #pragma unroll
-      for (int d = 0; d < ND; ++d) p[d] = off[d] + (int32_t)fdN[d].mod(base + lane);
+      for (int d = 0; d < ND; ++d) p[d] = acc_s + 4u * (uint32_t)(off[d] + (int32_t)fdN[d].mod(base + lane));
       for (uint32_t k0 = 0; k0 < tasks; k0 += 32) {
         const uint32_t k = k0 + lane;
         const bool active = k < tasks;
-        uint32_t u = 0;
-        if (active) {
-          if (split) {
-            u = fch.mod(k) == n_ch - 1 ? u_last : u_full;
-          } else {
-            const uint32_t need = kv_need(k, a.bq, rows, qlen, kvlen, a.causal, fg);
-            u = fbkv.div(need + (uint32_t)a.bkv - 1);
-          }
+        uint32_t u;
+        if (split) {
+          u = fch.mod(k) == n_ch - 1 ? u_last : u_full;
+        } else {
+          const uint32_t need = kv_need(k, a.bq, rows, qlen, kvlen, a.causal, fg);
+          u = fbkv.div(need + (uint32_t)a.bkv - 1);
         }
+        u = active ? u : 0u;  // idle lanes add 0 to their own (distinct) residue
         usum += u;
         if (SMALL) {
 #pragma unroll
@@ -225,9 +225,12 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, const
         } else {
 #pragma unroll
           for (int d = 0; d < ND; ++d) {
-            if (active) acc[p[d]] += u;
-            p[d] += 32;
-            if (p[d] >= off[d] + N[d]) p[d] -= N[d];
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(p[d]));
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(p[d]), "r"(v + u) : "memory");
+            p[d] += 128u;
+            const uint32_t hi = acc_s + 4u * (uint32_t)(off[d] + N[d]);
+            p[d] = p[d] >= hi ? p[d] - 4u * (uint32_t)N[d] : p[d];
           }
         }
         __syncwarp();
@@ -286,7 +289,7 @@ __device__ DistinctMax fold(const AttnCfg &a, const uint32_t *A, int32_t N, cons
     }
     const int64_t n_s = (int64_t)qn + ((uint32_t)s < rn ? 1 : 0);
     mS = max(mS, (int64_t)S);
-    mB = max(mB, a.bq * n_s + 2 * a.bkv * (int64_t)S);
+    mB = max(mB, (int64_t)a.bq * n_s + 2 * (int64_t)a.bkv * (int64_t)S);
   }
   return DistinctMax{warp_max64(mS), warp_max64(mB)};
 }
@@ -307,9 +310,9 @@ __device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const A
   const int64_t T = L * a.nkv;
   const u128 Ua = (u128)U * (u128)a.nkv;  // < 2^63 (U < 2^32, nkv < 2^31)
   bool bad = false;
-  const u128 totT = mul_le_i64((u128)(4 * a.bq) * (u128)a.hd * (u128)a.bkv, Ua, bad);
-  const u128 totX = mul_le_i64((u128)a.bq * (u128)(a.bkv + 1), Ua, bad);
-  const u128 totB = mul_le_i64((u128)(2 * a.hd), (u128)a.bq * (u128)T + (u128)(2 * a.bkv) * Ua, bad);
+  const u128 totT = mul_le_i64((u128)4 * (u128)a.bq * (u128)a.hd * (u128)a.bkv, Ua, bad);
+  const u128 totX = mul_le_i64((u128)a.bq * ((u128)a.bkv + 1), Ua, bad);
+  const u128 totB = mul_le_i64((u128)2 * (u128)a.hd, (u128)a.bq * (u128)T + (u128)2 * (u128)a.bkv * Ua, bad);
   if (bad || totT > kI64Max || totX > kI64Max || totB > kI64Max) { emit_error(out, p, SP_PAIR_E_RANGE); return; }
   PairDemand d;
   d.T = T;
@@ -317,14 +320,15 @@ __device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const A
   d.tot[1] = 0;
   d.tot[2] = (int64_t)totX;
   d.tot[3] = (int64_t)totB;
-  d.mx[0] = 4 * a.bq * a.hd * a.bkv * m.maxS;
+  d.mx[0] = (int64_t)4 * a.bq * a.hd * a.bkv * m.maxS;  // <= totT (maxS <= U*nkv)
   d.mx[1] = 0;
-  d.mx[2] = a.bq * (a.bkv + 1) * m.maxS;
-  d.mx[3] = 2 * a.hd * m.maxB;
+  d.mx[2] = (int64_t)a.bq * ((int64_t)a.bkv + 1) * m.maxS;
+  d.mx[3] = (int64_t)2 * a.hd * m.maxB;
   emit_pair(out, p, d, a.fp, s, 5, tdt);
 }
 
-// Whole per-config pipeline for one distinct set; results in res[0..ND).
+// Whole per-config pipeline for one distinct set; results in res[0..ND)
+// (the warp's shared-memory slots, written by lane 0).
 template <int ND, bool SMALL>
 __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, const int32_t (&N)[ND],
                            const int32_t (&off)[ND], const FastDiv *fdN, int32_t minN, int lane, int64_t &L,
@@ -337,23 +341,29 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, const int
     uint32_t umax;
     sparse_units(a, lane, fg, U, umax);
     if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
-#pragma unroll
-    for (int d = 0; d < ND; ++d) res[d] = DistinctMax{(int64_t)umax, a.bq + 2 * a.bkv * (int64_t)umax};
+    if (lane == 0)
+      for (int d = 0; d < ND; ++d) res[d] = DistinctMax{(int64_t)umax, (int64_t)a.bq + 2 * (int64_t)a.bkv * umax};
+    __syncwarp();
     return 0;
   }
   U = accumulate<ND, SMALL>(a, acc, words, N, off, fdN, lane, fg);
   if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
-#pragma unroll
-  for (int d = 0; d < ND; ++d) res[d] = fold(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
+#pragma unroll 1
+  for (int d = 0; d < ND; ++d) {
+    const DistinctMax m = fold(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
+    if (lane == 0) res[d] = m;
+  }
+  __syncwarp();
   return 0;
 }
 
 template <int ND, bool SMALL>
-__global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_cross(ConfigView cfg,
+__global__ void __launch_bounds__(kWarps * 32, 3) featurize_attention_cross(ConfigView cfg,
                                                                             const DevSpec *__restrict__ specs,
                                                                             int g0, AttnPlan plan, FeatOut out) {
   extern __shared__ uint32_t smem[];
   __shared__ FastDiv s_fd[kMaxDistinct];
+  __shared__ DistinctMax s_res[kWarps][kMaxDistinct];
   const AttnGroup grp = plan.groups[blockIdx.y];
   int32_t N[ND], off[ND];
   int32_t minN = INT32_MAX, words = 0;
@@ -375,16 +385,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_cross(Conf
     int st = a.status;
     int64_t L = 0;
     uint64_t U = 0;
-    DistinctMax res[ND];
-    if (st == 0) st = attn_config<ND, SMALL>(a, acc, words, N, off, s_fd, minN, lane, L, U, res);
+    if (st == 0) st = attn_config<ND, SMALL>(a, acc, words, N, off, s_fd, minN, lane, L, U, s_res[warp]);
     for (int j = lane; j < grp.n_specs; j += 32) {
       const int g = __ldg(plan.group_specs + grp.spec_first + j);
       const int dsel = __ldg(plan.spec_dist + grp.spec_first + j) - grp.distinct_first;
-      DistinctMax m = res[0];
-#pragma unroll
-      for (int d = 1; d < ND; ++d)
-        if (dsel == d) m = res[d];
-      attn_emit(out, (int64_t)(g - g0) * C + c, a, st, L, U, m, specs[g]);
+      attn_emit(out, (int64_t)(g - g0) * C + c, a, st, L, U, s_res[warp][dsel], specs[g]);
     }
     __syncwarp();
   }
@@ -399,6 +404,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
                                                                            FeatOut out) {
   extern __shared__ uint32_t smem[];
   __shared__ FastDiv s_fd[kWarps];
+  __shared__ DistinctMax s_res[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *acc = smem + (size_t)warp * words_per_warp;
   for (int64_t p = (int64_t)blockIdx.x * kWarps + warp; p < n_pairs; p += (int64_t)gridDim.x * kWarps) {
@@ -415,13 +421,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
     int st = a.status;
     int64_t L = 0;
     uint64_t U = 0;
-    DistinctMax res[1];
     const int words = (N[0] + 3) & ~3;
     if (st == 0) {
-      if (N[0] >= 32) st = attn_config<1, false>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, res);
-      else st = attn_config<1, true>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, res);
+      if (N[0] >= 32) st = attn_config<1, false>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, s_res + warp);
+      else st = attn_config<1, true>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, s_res + warp);
     }
-    if (lane == 0) attn_emit(out, p, a, st, L, U, res[0], specs[g]);
+    if (lane == 0) attn_emit(out, p, a, st, L, U, s_res[warp], specs[g]);
     __syncwarp();
   }
 }
