@@ -224,14 +224,7 @@ def run_gpu(args, rank, world, local_rank):
     specs_h = ctx.load_gpu_specs(sa)
     model_d = models.random_mlp(b.family, 42)
     precision = args.precision
-    try:
-        model = ctx.load_model(model_d, precision)
-    except sp.SynPerfError as e:
-        if precision == "bf16" and e.status == 4 and not args.strict_precision:
-            precision = "fp32"
-            model = ctx.load_model(model_d, precision)
-        else:
-            raise
+    model = ctx.load_model(model_d, precision)
     n_in = int(model_d["n_in"])
     db = sp.DeviceBatch.from_host(b, dev)
     n_pairs = (g1 - g0) * b.n_configs
@@ -306,7 +299,7 @@ def run_gpu(args, rank, world, local_rank):
         "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-        "dtype": "bf16" if precision == "bf16" else "f32",
+        "dtype": {"bf16": "bf16", "fp16": "f16", "fp32": "f32"}[precision],
         "data": "synthetic (seeded generators, workloads/; seeded random MLP weights)",
         "config": {
             "workload": args.workload, "description": WORKLOADS[args.workload],
@@ -382,10 +375,10 @@ def roofline(args, b, n_pairs, n_in, precision, feat_ms, pred_ms, peaks, prof, t
     bf16_peak = peaks.get("bf16_tflops_sustained" if long_region else "bf16_tflops")
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if pred_ms >= feat_ms:
-        kernel = "predict_tcgen05_bf16" if precision == "bf16" else "predict_simt_fp32"
+        kernel = f"predict_tcgen05_{precision}" if precision != "fp32" else "predict_simt_fp32"
         flop = MLP_FLOP_PER_PAIR[n_in] * n_pairs
         achieved = flop / (pred_ms * 1e-3) / 1e12
-        if precision == "bf16":
+        if precision != "fp32":  # fp16 and bf16 share the dense tensor rate (guide: ratio 1)
             peak, bound, src = bf16_peak, "tensor", ("MEASURED_PEAKS.json " +
                                                      ("bf16_tflops_sustained" if long_region else "bf16_tflops"))
         else:
@@ -424,8 +417,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--scale", type=float, default=1.0, help="workload size multiplier (testing)")
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--strict-precision", action="store_true")
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"])
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -19,7 +19,8 @@ NFIELDS = {SP_GEMM: 11, SP_ATTENTION: 12, SP_FUSED_MOE: 14, SP_RMSNORM: 6, SP_SI
 # sp_pairing_kind
 SP_PAIRS_CROSS, SP_PAIRS_LIST = 0, 1
 # sp_precision
-SP_MLP_FP32, SP_MLP_BF16 = 0, 1
+SP_MLP_FP32, SP_MLP_BF16, SP_MLP_FP16 = 0, 1, 2
+PRECISIONS = {"fp32": SP_MLP_FP32, "bf16": SP_MLP_BF16, "fp16": SP_MLP_FP16}
 SP_STRICT = 1
 
 

@@ -197,11 +197,12 @@ class Context:
         return Specs(self, h.value, len(arr))
 
     # -- estimator
-    def load_model(self, model: dict, precision: str = "bf16") -> Model:
+    def load_model(self, model: dict, precision: str = "fp16") -> Model:
+        """precision: "fp16" / "bf16" (tcgen05 tensor-core path) or "fp32" (CUDA cores)."""
         d = _abi.sp_mlp_desc()
         d.family = int(model["family"])
         d.n_in = int(model["n_in"])
-        d.precision = _abi.SP_MLP_BF16 if precision == "bf16" else _abi.SP_MLP_FP32
+        d.precision = _abi.PRECISIONS[precision]
         keep = []
         for k in _abi.MLP_ARRAYS:
             a = np.ascontiguousarray(model[k], dtype=np.float32)

@@ -389,7 +389,7 @@ extern "C" sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *d, sp_model *
   const int n_in = d->n_in;
   if (n_in != 4 * pipes_count(d->family) + 7)
     return fail(ctx, SP_E_DATA, "sp_load_model: n_in does not match the family's Table IV layout");
-  if (d->precision != SP_MLP_FP32 && d->precision != SP_MLP_BF16)
+  if (d->precision != SP_MLP_FP32 && d->precision != SP_MLP_BF16 && d->precision != SP_MLP_FP16)
     return fail(ctx, SP_E_ARG, "sp_load_model: unknown precision");
   const float *arrs[] = {d->mu, d->sigma, d->w1, d->b1, d->g1, d->be1, d->m1, d->v1, d->w2, d->b2, d->g2,
                          d->be2, d->m2, d->v2, d->w3, d->b3, d->g3, d->be3, d->m3, d->v3, d->w4};
@@ -465,11 +465,13 @@ extern "C" sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *d, sp_model *
     q.n_in = n_in;
     q.family = d->family;
   }
-  if (d->precision == SP_MLP_BF16) {
+  if (d->precision == SP_MLP_BF16 || d->precision == SP_MLP_FP16) {
     std::vector<uint16_t> wpack;
     std::vector<float> vecs;
     float b4 = 0.f;
-    if (!pack_bf16_model(*d, s, t, wpack, vecs, b4))
+    const bool bf16 = d->precision == SP_MLP_BF16;
+    m->m16.bf16 = bf16 ? 1 : 0;
+    if (!pack_mlp_16bit(*d, s, t, bf16, wpack, vecs, b4))
       return fail(ctx, SP_E_UNSUPPORTED, "sp_load_model: bf16 tcgen05 path unavailable in this build");
     cudaError_t e = m->bf16w.alloc_copy(wpack.data(), wpack.size() * 2);
     if (e == cudaSuccess) e = m->bf16v.alloc_copy(vecs.data(), vecs.size() * 4);
@@ -500,7 +502,7 @@ extern "C" sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_fea
   ctx->err.clear();
   cudaSetDevice(ctx->device);
   int e;
-  if (model->precision == SP_MLP_BF16)
+  if (model->precision == SP_MLP_BF16 || model->precision == SP_MLP_FP16)
     e = launch_predict_tcgen05(model->m16, *in, latency_us, efficiency, ctx->num_sms, stream);
   else
     e = launch_predict_simt(model->m32, *in, latency_us, efficiency, ctx->num_sms, stream);

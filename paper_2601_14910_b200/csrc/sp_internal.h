@@ -110,7 +110,8 @@ struct MlpFp32 {        // DEVICE pointers, fp32
 int launch_predict_simt(const MlpFp32 &m, const sp_features &in, float *latency, float *eff,
                         int num_device_sms, void *stream);
 
-struct MlpBf16 {
+struct MlpBf16 {  // tcgen05 path, 16-bit operands (bf16 or fp16)
+  int32_t bf16;         // 1: bf16 operands, 0: fp16 operands
   const void *wpack;    // DEVICE packed bf16 weights in UMMA canonical layout (see predict_tcgen05.cu)
   const float *vecs;    // DEVICE fp32 per-unit vectors: b1[256], b2'[128], b3'[64], w4'[64], mu[16], inv_sigma[16]
   float b4;
@@ -120,8 +121,8 @@ struct MlpBf16 {
 // Host: BN-folded bf16 weights in the kernel's shared-memory image, plus fp32
 // vectors.  s[l], t[l]: BN(eval) affine of hidden layer l (fp64).  Returns
 // false if the tcgen05 path is not available.
-bool pack_bf16_model(const sp_mlp_desc &d, const std::vector<double> *s, const std::vector<double> *t,
-                     std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4);
+bool pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const std::vector<double> *t, bool bf16,
+                    std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4);
 int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *latency, float *eff,
                            int num_device_sms, void *stream);
 
