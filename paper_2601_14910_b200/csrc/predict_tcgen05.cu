@@ -60,19 +60,19 @@ __host__ __device__ constexpr uint32_t op_off(uint32_t r, uint32_t k, uint32_t K
   return (r / 8) * (16 * K) + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2;
 }
 
-// Table IV order (O8); see predict_simt.cu.  slot | 256 for float slots.
-__device__ __forceinline__ int feature_slot(int pipes, int k) {
+// Table IV order (O8): per pipe present (Tensor, FMA, XU) [total ops, C^GPU,
+// max-SM ops, C^SM], then the 7 MIO features.  Record slot, +16 for a float slot.
+static int feature_slot_host(int pipes, int k) {
   int n = 0;
   for (int p = 0; p < 3; ++p) {
     if (!(pipes & (1 << p))) continue;
     if (k == n) return I_TOT_T + p;
-    if (k == n + 1) return (F_CG_T + p) | 256;
+    if (k == n + 1) return 16 + F_CG_T + p;
     if (k == n + 2) return I_MAX_T + p;
-    if (k == n + 3) return (F_CS_T + p) | 256;
+    if (k == n + 3) return 16 + F_CS_T + p;
     n += 4;
   }
-  const int mio[7] = {I_BYTES, F_GLOB_G | 256, F_L2_G | 256, I_BYTES_MAX, F_GLOB_S | 256,
-                      F_L2_S | 256, F_SMEM_S | 256};
+  const int mio[7] = {I_BYTES, 16 + F_GLOB_G, 16 + F_L2_G, I_BYTES_MAX, 16 + F_GLOB_S, 16 + F_L2_S, 16 + F_SMEM_S};
   return mio[k - n];
 }
 
@@ -82,7 +82,33 @@ struct Params {
   float *latency;
   float *eff;
   int64_t n_tiles;
+  int32_t n_in;
+  int32_t slot[kK1];  // Table IV order (O8): feature j -> record slot; +16 marks a float slot
 };
+
+// One row's raw MLP inputs (features as fp32), validity and t_theory.
+struct TileIn {
+  float v[kK1];
+  float t_theory;
+  bool valid;
+};
+
+__device__ __forceinline__ TileIn load_tile_in(const Params &P, int64_t t, uint32_t row) {
+  TileIn r;
+  const int64_t p = t * kTile + row;
+  r.valid = t < P.n_tiles && p < P.in.n_pairs && P.in.status[p] == 0;
+  const int64_t ld = P.in.ld;
+#pragma unroll
+  for (int j = 0; j < kK1; ++j) {
+    r.v[j] = 0.f;
+    if (r.valid && j < P.n_in) {
+      const int sl = P.slot[j];
+      r.v[j] = sl >= 16 ? __ldg(P.in.flts + (int64_t)(sl - 16) * ld + p) : (float)__ldg(P.in.ints + (int64_t)sl * ld + p);
+    }
+  }
+  r.t_theory = r.valid ? __ldg(P.in.flts + (int64_t)F_TTHEORY * ld + p) : 0.f;
+  return r;
+}
 
 // Epilogue of one hidden layer: rows of D (TMEM columns [col0, col0+ncols))
 // + bias, ReLU, 16-bit -> next operand (K = ncols) in shared memory.
@@ -183,29 +209,25 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
     const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * 256);
     const uint32_t slot = sbase + kOffSlot0 + s * kSlotBytes;
     const uint32_t xbuf = slot, hbuf = slot + kXBytes;
-    const int pipes = family_pipes(P.m.family);
-    const int n_in = P.m.n_in;
-    const float *b1 = vec, *b2 = vec + 256, *b3 = vec + 384, *w4 = vec + 448, *mu = vec + 512,
-                *isg = vec + 528;
-    const int64_t n_pairs = P.in.n_pairs, ld = P.in.ld;
+    const float *b1 = vec, *b2 = vec + 256, *b3 = vec + 384, *w4 = vec + 448, *na = vec + 512,
+                *nc = vec + 528;
+    const int64_t n_pairs = P.in.n_pairs;
     uint32_t pd = 0;
+    // Inputs of this slot's next tile are loaded one tile ahead, so their HBM
+    // latency hides behind the current tile's epilogues.
+    TileIn cur = load_tile_in(P, blockIdx.x + (int64_t)s * G, row);
     for (int64_t k = s;; k += 2) {
       const int64_t t = blockIdx.x + k * G;
       if (t >= P.n_tiles) break;
       const int64_t p = t * kTile + row;
-      const bool valid = p < n_pairs && P.in.status[p] == 0;
-      // a10: x = (ln(1+v) - mu) / sigma, bf16, K padded to 16
+      const bool valid = cur.valid;
+      const float t_theory = cur.t_theory;
+      // a10: x = (ln(1+v) - mu) / sigma = log2(1+v) * (ln2/sigma) - mu/sigma, K padded to 16
       float x[kK1];
 #pragma unroll
-      for (int j = 0; j < kK1; ++j) {
-        x[j] = 0.f;
-        if (valid && j < n_in) {
-          const int slot_id = feature_slot(pipes, j);
-          const float v = (slot_id & 256) ? P.in.flts[(int64_t)(slot_id & 255) * ld + p]
-                                          : (float)P.in.ints[(int64_t)slot_id * ld + p];
-          x[j] = (log1pf(v) - mu[j]) * isg[j];
-        }
-      }
+      for (int j = 0; j < kK1; ++j)
+        x[j] = (valid && j < P.n_in) ? fmaf(__log2f(1.f + cur.v[j]), na[j], nc[j]) : 0.f;
+      cur = load_tile_in(P, t + 2 * G, row);  // prefetch
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         uint32_t w[4];
@@ -242,7 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
         tc::tmem_ld32(tmem_row + 128 + c0, v);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z = fmaf(w4[c0 + j], fmaxf(__uint_as_float(v[j]) + b3[c0 + j], 0.f), z);
+        for (int j = 0; j < 32; j += 4) {
+          const float4 w = *reinterpret_cast<const float4 *>(w4 + c0 + j);
+          const float4 bb = *reinterpret_cast<const float4 *>(b3 + c0 + j);
+          z = fmaf(w.x, fmaxf(__uint_as_float(v[j + 0]) + bb.x, 0.f), z);
+          z = fmaf(w.y, fmaxf(__uint_as_float(v[j + 1]) + bb.y, 0.f), z);
+          z = fmaf(w.z, fmaxf(__uint_as_float(v[j + 2]) + bb.z, 0.f), z);
+          z = fmaf(w.w, fmaxf(__uint_as_float(v[j + 3]) + bb.w, 0.f), z);
+        }
       }
       tc::fence_before();
       if (p < n_pairs) {
@@ -252,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
         } else {
           const float ez = __expf(-z);
           e = 1.f / (1.f + ez);
-          lat = P.in.flts[(int64_t)F_TTHEORY * ld + p] * (1.f + ez);
+          lat = t_theory * (1.f + ez);
         }
         P.latency[p] = lat;
         if (P.eff) P.eff[p] = e;
@@ -318,9 +347,11 @@ bool pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const st
     vecs[448 + k] = (float)((double)d.w4[k] * s[2][k]);
     bb += (double)d.w4[k] * t[2][k];
   }
+  // x_k = (ln(1+v) - mu_k) / sigma_k = log2(1+v) * (ln2 / sigma_k) - mu_k / sigma_k  (R17)
   for (int k = 0; k < n_in; ++k) {
-    vecs[512 + k] = d.mu[k];
-    vecs[528 + k] = (float)(1.0 / std::fmax((double)d.sigma[k], 1e-8));
+    const double sg = std::fmax((double)d.sigma[k], 1e-8);
+    vecs[512 + k] = (float)(0.69314718055994530942 / sg);
+    vecs[528 + k] = (float)(-(double)d.mu[k] / sg);
   }
   b4 = (float)bb;
   return true;
@@ -338,6 +369,8 @@ int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *laten
   P.latency = latency;
   P.eff = eff;
   P.n_tiles = (in.n_pairs + kTile - 1) / kTile;
+  P.n_in = m.n_in;
+  for (int j = 0; j < kK1; ++j) P.slot[j] = j < m.n_in ? feature_slot_host(family_pipes(m.family), j) : 0;
   const int64_t grid = P.n_tiles < num_device_sms ? P.n_tiles : num_device_sms;
   kern<<<(unsigned)grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(P);
   return (int)cudaGetLastError();
