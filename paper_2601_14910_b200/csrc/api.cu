@@ -292,7 +292,7 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
   pd->view.distinct_n = (const int32_t *)pd->distinct_n.p;
   pd->view.distinct_off = (const int32_t *)pd->distinct_off.p;
   pd->view.n_groups = (int32_t)groups.size();
-  pd->view.words_per_warp = words_max;
+  pd->view.words_per_warp = words_max + kAttnScratchWords;  // accumulators + request scratch
   for (const AttnGroup &gr : groups) {
     pd->nd.push_back(gr.n_distinct);
     pd->small.push_back(dn[gr.distinct_first] < 32);  // Ns ascending: first is the smallest

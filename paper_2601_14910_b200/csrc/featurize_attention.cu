@@ -180,118 +180,204 @@ struct DistinctMax {
   int64_t maxS, maxB;  // max_j S_j and max_j (BQ*n_j + 2*BKV*S_j)
 };
 
-// General path: per-SM accumulators in the warp's shared-memory region.
-// N[d], off[d]: distinct SM counts of the group and their word offsets.
+// Per-warp scratch (words) after the accumulators: per-request parameters of
+// a chunk of 32 requests, 7 arrays of 32.
+constexpr int kScratchWords = kAttnScratchWords;
+
+__device__ __forceinline__ uint32_t lanemask_le() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
+}
+
+// Causal + split-KV (rare): each q-block has its own chunk count.  Lanes take
+// 32 q-blocks of one request, scan their chunk counts, then walk their own
+// chunks (positions are not lane-consecutive: atomic adds).
+template <int ND>
+__device__ uint64_t accumulate_causal_split(const AttnCfg &a, uint32_t *acc, const int32_t (&off)[ND],
+                                            const FastDiv *fdN, int lane, const FastDiv &fg, const FastDiv &fbkv) {
+  uint32_t base = 0;
+  uint64_t usum = 0;
+  for (int64_t b = 0; b < a.bs; ++b) {
+    const uint32_t qlen = __ldg(a.req + 2 * b), kvlen = __ldg(a.req + 2 * b + 1);
+    const uint32_t rows = qlen * (uint32_t)a.g;
+    const uint32_t nqb = (rows + (uint32_t)a.bq - 1u) / (uint32_t)a.bq;
+    for (uint32_t i0 = 0; i0 < nqb; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      uint32_t need = 0, n_ch = 0;
+      if (i < nqb) {
+        need = kv_need(i, a.bq, rows, qlen, kvlen, true, fg);
+        n_ch = (uint32_t)((need + (uint64_t)a.chunk - 1) / a.chunk);
+      }
+      uint32_t incl = n_ch;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t start = base + incl - n_ch;
+      for (uint32_t ch = 0; ch < n_ch; ++ch) {
+        const uint32_t len = min((uint32_t)a.chunk, need - ch * (uint32_t)a.chunk);
+        const uint32_t u = fbkv.div(len + (uint32_t)a.bkv - 1);
+#pragma unroll
+        for (int d = 0; d < ND; ++d) atomicAdd(acc + off[d] + fdN[d].mod(start + ch), u);
+        usum += u;
+      }
+      base += total;
+      __syncwarp();
+    }
+  }
+  return usum;
+}
+
+// General path: per-SM accumulators in the warp's shared-memory region, one
+// region per distinct SM count (N[d] words at off[d]).  The head-0 task stream
+// is walked flat across request boundaries: requests are taken 32 at a time
+// (lane = request: its task count, start and per-request constants go to the
+// warp's scratch), then each step gives lane l the task k0 + l and finds its
+// request from a boundary bitmask (one warp OR-reduction per step).
 template <int ND, bool SMALL>
-__device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, const int32_t (&N)[ND],
+__device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint32_t *scr, const int32_t (&N)[ND],
                                const int32_t (&off)[ND], const FastDiv *fdN, int lane, const FastDiv &fg) {
   for (int w = lane * 4; w < words; w += 128) *reinterpret_cast<uint4 *>(acc + w) = make_uint4(0, 0, 0, 0);
   __syncwarp();
   const FastDiv fbkv = make_fd((uint32_t)a.bkv);
+  const bool split = a.chunk > 0;
+  if (split && a.causal) {
+    const uint64_t us = accumulate_causal_split<ND>(a, acc, off, fdN, lane, fg, fbkv);
+    __syncwarp();
+    return warp_sum_u64(us);
+  }
+  const FastDiv fbq = make_fd((uint32_t)a.bq);
+  const FastDiv fchunk = split ? make_fd((uint32_t)a.chunk) : FastDiv{1u, 1u, 0u};
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);  // shared-window byte address
-  uint32_t base = 0;  // head-0 index of the request's first task (< 2^31, checked by the pre-pass)
+  const uint32_t lm_le = lanemask_le();
+  uint32_t *s_start = scr, *s_a1 = scr + 32, *s_a2 = scr + 64, *s_a3 = scr + 96, *s_uf = scr + 128,
+           *s_ul = scr + 160;
+  uint32_t base = 0;  // head-0 index of the chunk's first task (< 2^31, checked by the pre-pass)
   uint64_t usum = 0;
-  for (int64_t b = 0; b < a.bs; ++b) {
-    const uint32_t qlen = __ldg(a.req + 2 * b), kvlen = __ldg(a.req + 2 * b + 1);
-    const uint32_t rows = qlen * (uint32_t)a.g;  // < 2^31 (validated)
-    const uint32_t nqb = (rows + (uint32_t)a.bq - 1u) / (uint32_t)a.bq;
-    if (a.chunk == 0 || !a.causal) {
-      // every q-block has the same chunk count (unsplit, or non-causal kv_need = kvlen)
-      const bool split = a.chunk > 0;
-      const uint32_t n_ch = split ? (uint32_t)((kvlen + a.chunk - 1) / a.chunk) : 1u;
-      const uint32_t tasks = nqb * n_ch;  // <= L < 2^31 (pre-pass)
-      const FastDiv fch = split ? make_fd(n_ch) : FastDiv{1u, 1u, 0u};
-      const uint32_t u_full = split ? (uint32_t)((min((uint64_t)a.chunk, (uint64_t)kvlen) + a.bkv - 1) / a.bkv) : 0;
-      const uint32_t u_last = split ? (uint32_t)((kvlen - (uint64_t)(n_ch - 1) * a.chunk + a.bkv - 1) / a.bkv) : 0;
-      uint32_t p[ND];  // byte address of this lane's accumulator for each distinct N
-#pragma unroll
-      for (int d = 0; d < ND; ++d) p[d] = acc_s + 4u * (uint32_t)(off[d] + (int32_t)fdN[d].mod(base + lane));
-      for (uint32_t k0 = 0; k0 < tasks; k0 += 32) {
-        const uint32_t k = k0 + lane;
-        const bool active = k < tasks;
-        uint32_t u;
-        if (split) {
-          u = fch.mod(k) == n_ch - 1 ? u_last : u_full;
+  for (int64_t b0 = 0; b0 < a.bs; b0 += 32) {
+    // ---- lane = request b0 + lane: task count and per-request constants
+    const bool has = b0 + lane < a.bs;
+    uint32_t tasks = 0, a1 = 0, a2 = 0, a3 = 0, uf = 0, ul = 0;
+    if (has) {
+      const uint32_t q = __ldg(a.req + 2 * (b0 + lane)), kv = __ldg(a.req + 2 * (b0 + lane) + 1);
+      const uint32_t rows = q * (uint32_t)a.g;  // < 2^31 (validated)
+      const uint32_t nqb = fbq.div(rows + (uint32_t)a.bq - 1u);
+      if (!split) {
+        tasks = nqb;
+        if (a.causal) {
+          a1 = rows;
+          a2 = q;
+          a3 = kv;
         } else {
-          const uint32_t need = kv_need(k, a.bq, rows, qlen, kvlen, a.causal, fg);
-          u = fbkv.div(need + (uint32_t)a.bkv - 1);
+          uf = ul = fbkv.div(kv + (uint32_t)a.bkv - 1u);  // kv_need = kvlen for every q-block
         }
-        u = active ? u : 0u;  // idle lanes add 0 to their own (distinct) residue
-        usum += u;
-        if (SMALL) {
-#pragma unroll
-          for (int d = 0; d < ND; ++d)
-            if (active) atomicAdd(acc + off[d] + fdN[d].mod(base + k), u);
-        } else {
-#pragma unroll
-          for (int d = 0; d < ND; ++d) {
-            uint32_t v;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(p[d]));
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(p[d]), "r"(v + u) : "memory");
-            p[d] += 128u;
-            const uint32_t hi = acc_s + 4u * (uint32_t)(off[d] + N[d]);
-            p[d] = p[d] >= hi ? p[d] - 4u * (uint32_t)N[d] : p[d];
-          }
-        }
-        __syncwarp();
-      }
-      base += tasks;
-    } else {
-      // causal + split-KV: each q-block has its own chunk count.  Lanes take
-      // 32 q-blocks, scan their chunk counts, then walk their own chunks
-      // (positions no longer lane-consecutive: atomic adds).
-      for (uint64_t i0 = 0; i0 < nqb; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        uint32_t need = 0, n_ch = 0;
-        if (i < nqb) {
-          need = kv_need(i, a.bq, rows, qlen, kvlen, true, fg);
-          n_ch = (uint32_t)((need + a.chunk - 1) / a.chunk);
-        }
-        uint32_t incl = n_ch;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t start = base + incl - n_ch;
-        for (uint32_t ch = 0; ch < n_ch; ++ch) {
-          const uint64_t len = min((uint64_t)a.chunk, (uint64_t)need - (uint64_t)ch * a.chunk);
-          const uint32_t u = (uint32_t)((len + a.bkv - 1) / a.bkv);
-#pragma unroll
-          for (int d = 0; d < ND; ++d) atomicAdd(acc + off[d] + fdN[d].mod(start + ch), u);
-          usum += u;
-        }
-        base += total;
-        __syncwarp();
+      } else {  // non-causal split-KV: chunks of one q-block share kv_need = kvlen
+        const uint32_t n_ch = fchunk.div(kv + (uint32_t)a.chunk - 1u);
+        tasks = nqb * n_ch;
+        const FastDiv f = make_fd(n_ch);
+        a1 = n_ch;
+        a2 = f.m;
+        a3 = f.s;
+        uf = fbkv.div(min((uint32_t)a.chunk, kv) + (uint32_t)a.bkv - 1u);
+        ul = fbkv.div(kv - (n_ch - 1u) * (uint32_t)a.chunk + (uint32_t)a.bkv - 1u);
       }
     }
+    uint32_t incl = tasks;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t start = incl - tasks, total = __shfl_sync(0xffffffffu, incl, 31);
+    s_start[lane] = start;
+    s_a1[lane] = a1;
+    s_a2[lane] = a2;
+    s_a3[lane] = a3;
+    s_uf[lane] = uf;
+    s_ul[lane] = ul;
+    __syncwarp();
+    const uint32_t nreq = (uint32_t)min((int64_t)32, a.bs - b0);
+    uint32_t p[ND];  // byte address of this lane's accumulator for each distinct N
+#pragma unroll
+    for (int d = 0; d < ND; ++d) p[d] = acc_s + 4u * (uint32_t)(off[d] + (int32_t)fdN[d].mod(base + lane));
+    uint32_t bcur = 0;  // chunk-local request holding task k0
+    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const bool active = k < total;
+      const uint32_t bit = (has && start > k0 && start < k0 + 32) ? (1u << (start - k0)) : 0u;
+      const uint32_t M = __reduce_or_sync(0xffffffffu, bit);
+      const uint32_t bl = min(bcur + __popc(M & lm_le), nreq - 1);
+      const uint32_t kl = k - s_start[bl];  // task index within its request
+      uint32_t u;
+      if (!split) {
+        if (a.causal) {  // q-block kl: q_last = floor((min((kl+1)BQ, rows)-1)/g), kv_need, kv_eff
+          const uint32_t rows = s_a1[bl], q = s_a2[bl], kv = s_a3[bl];
+          const uint32_t e = (uint32_t)min((uint64_t)(kl + 1) * (uint64_t)a.bq, (uint64_t)rows) - 1u;
+          const uint32_t need = min(kv, kv - q + fg.div(e) + 1u);
+          u = fbkv.div(need + (uint32_t)a.bkv - 1u);
+        } else {
+          u = s_uf[bl];
+        }
+      } else {  // chunk index kl mod n_ch: full chunks, then the last one
+        const FastDiv f{s_a1[bl], s_a2[bl], s_a3[bl]};
+        u = f.mod(kl) == f.d - 1u ? s_ul[bl] : s_uf[bl];
+      }
+      u = active ? u : 0u;  // idle lanes add 0 to their own (distinct) residue
+      usum += u;
+      if (SMALL) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d)
+          if (active) atomicAdd(acc + off[d] + fdN[d].mod(base + k), u);
+      } else {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          uint32_t v;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(p[d]));
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(p[d]), "r"(v + u) : "memory");
+          p[d] += 128u;
+          const uint32_t hi = acc_s + 4u * (uint32_t)(off[d] + N[d]);
+          p[d] = p[d] >= hi ? p[d] - 4u * (uint32_t)N[d] : p[d];
+        }
+      }
+      __syncwarp();
+      bcur += __popc(M) + (__any_sync(0xffffffffu, has && start == k0 + 32) ? 1u : 0u);
+    }
+    base += total;
+    __syncwarp();
   }
-  __syncwarp();
   return warp_sum_u64(usum);
 }
 
 // Fold the nkv rotations of one distinct N and take the per-quantity maxima.
+// SM j holds qn + (j < rn) tasks; max_j (BQ n_j + 2 BKV S_j) is taken over the
+// two task-count classes separately.  S_j fits 32 bits when nkv * U < 2^32.
+template <typename SumT>
 __device__ DistinctMax fold(const AttnCfg &a, const uint32_t *A, int32_t N, const FastDiv &fdN, uint32_t L,
                             uint32_t T, int lane) {
   const uint32_t Lm = fdN.mod(L);
-  const uint32_t qn = fdN.div(T), rn = T - qn * (uint32_t)N;  // SM j holds qn + (j < rn) tasks
-  int64_t mS = 0, mB = 0;
+  const uint32_t qn = fdN.div(T), rn = T - qn * (uint32_t)N;
+  SumT m_lo = 0, m_hi = 0;
   for (int32_t s = lane; s < N; s += 32) {
-    uint64_t S = 0;
+    SumT S = 0;
     int32_t o = 0;  // (h * L) mod N
-    for (int64_t h = 0; h < a.nkv; ++h) {
+    for (int32_t h = 0; h < a.nkv; ++h) {
       int32_t idx = s - o;
       idx += idx < 0 ? N : 0;
       S += A[idx];
       o += (int32_t)Lm;
       o -= o >= N ? N : 0;
     }
-    const int64_t n_s = (int64_t)qn + ((uint32_t)s < rn ? 1 : 0);
-    mS = max(mS, (int64_t)S);
-    mB = max(mB, (int64_t)a.bq * n_s + 2 * (int64_t)a.bkv * (int64_t)S);
+    if ((uint32_t)s < rn) m_lo = max(m_lo, S);
+    else m_hi = max(m_hi, S);
   }
-  return DistinctMax{warp_max64(mS), warp_max64(mB)};
+  const int64_t lo = warp_max64((int64_t)m_lo), hi = warp_max64((int64_t)m_hi);
+  int64_t mB = 0;
+  if (rn > 0) mB = (int64_t)a.bq * (qn + 1) + 2 * (int64_t)a.bkv * lo;
+  if (rn < (uint32_t)N) mB = max(mB, (int64_t)a.bq * qn + 2 * (int64_t)a.bkv * hi);
+  return DistinctMax{max(lo, hi), mB};
 }
 
 // a*b with a "> INT64_MAX" flag, without 128-bit overflow (operands < 2^96).
@@ -346,11 +432,13 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, const int
     __syncwarp();
     return 0;
   }
-  U = accumulate<ND, SMALL>(a, acc, words, N, off, fdN, lane, fg);
+  U = accumulate<ND, SMALL>(a, acc, words, acc + words, N, off, fdN, lane, fg);
   if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
+  const bool s32 = U * (uint64_t)a.nkv < (1ull << 32);
 #pragma unroll 1
   for (int d = 0; d < ND; ++d) {
-    const DistinctMax m = fold(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
+    const DistinctMax m = s32 ? fold<uint32_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane)
+                              : fold<uint64_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
     if (lane == 0) res[d] = m;
   }
   __syncwarp();
@@ -485,7 +573,7 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
     return 0;
   }
   if (n_pairs == 0) return 0;
-  const int words = (max_sms + 3) & ~3;
+  const int words = ((max_sms + 3) & ~3) + kScratchWords;  // accumulators + request scratch
   const size_t smem = (size_t)kWarps * words * 4;
   cudaError_t e = cudaFuncSetAttribute(featurize_attention_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

@@ -77,6 +77,7 @@ struct AttnGroup {
   int32_t distinct_first;  // index into distinct_n / distinct_off
   int32_t n_distinct;
 };
+constexpr int kAttnScratchWords = 224;  // per-warp request scratch (7 x 32 words)
 struct AttnPlan {
   const AttnGroup *groups;     // DEVICE [n_groups]
   const int32_t *group_specs;  // DEVICE spec index (absolute)
