@@ -8,7 +8,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsynperf.so")
+# SYNPERF_LIB: an alternative in-tree build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("SYNPERF_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsynperf.so")
 
 # sp_status
 SP_OK, SP_E_ARG, SP_E_DATA, SP_E_INTERNAL, SP_E_UNSUPPORTED = 0, 1, 2, 3, 4

@@ -27,6 +27,10 @@
 namespace sp {
 namespace {
 
+#ifndef SP_ATTN_MINB
+#define SP_ATTN_MINB 3
+#endif
+
 constexpr int kWarps = 8;           // warps per block
 constexpr int kMaxDistinct = 8;     // distinct SM counts per group (api.cu plans accordingly)
 constexpr int64_t kI32Max = 2147483647LL;
@@ -303,29 +307,23 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
     uint32_t p[ND];  // byte address of this lane's accumulator for each distinct N
 #pragma unroll
     for (int d = 0; d < ND; ++d) p[d] = acc_s + 4u * (uint32_t)(off[d] + (int32_t)fdN[d].mod(base + lane));
-    uint32_t bcur = 0;  // chunk-local request holding task k0
-    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
-      const uint32_t k = k0 + lane;
-      const bool active = k < total;
-      const uint32_t bit = (has && start > k0 && start < k0 + 32) ? (1u << (start - k0)) : 0u;
-      const uint32_t M = __reduce_or_sync(0xffffffffu, bit);
-      const uint32_t bl = min(bcur + __popc(M & lm_le), nreq - 1);
-      const uint32_t kl = k - s_start[bl];  // task index within its request
-      uint32_t u;
+    uint32_t hi[ND];  // end of each region (byte address): residue wrap point
+#pragma unroll
+    for (int d = 0; d < ND; ++d) hi[d] = acc_s + 4u * (uint32_t)(off[d] + N[d]);
+    // kv units of task kl of a request described by (a1, a2, a3, uf, ul)
+    auto unit = [&](uint32_t kl, uint32_t r1, uint32_t r2, uint32_t r3, uint32_t ruf, uint32_t rul) -> uint32_t {
       if (!split) {
-        if (a.causal) {  // q-block kl: q_last = floor((min((kl+1)BQ, rows)-1)/g), kv_need, kv_eff
-          const uint32_t rows = s_a1[bl], q = s_a2[bl], kv = s_a3[bl];
-          const uint32_t e = (uint32_t)min((uint64_t)(kl + 1) * (uint64_t)a.bq, (uint64_t)rows) - 1u;
-          const uint32_t need = min(kv, kv - q + fg.div(e) + 1u);
-          u = fbkv.div(need + (uint32_t)a.bkv - 1u);
-        } else {
-          u = s_uf[bl];
-        }
-      } else {  // chunk index kl mod n_ch: full chunks, then the last one
-        const FastDiv f{s_a1[bl], s_a2[bl], s_a3[bl]};
-        u = f.mod(kl) == f.d - 1u ? s_ul[bl] : s_uf[bl];
+        if (!a.causal) return ruf;
+        // q-block kl: q_last = floor((min((kl+1)BQ, rows)-1)/g), kv_need, kv_eff = ceil(need/BKV)*BKV
+        const uint32_t e = (uint32_t)min((uint64_t)(kl + 1) * (uint64_t)a.bq, (uint64_t)r1) - 1u;
+        const uint32_t need = min(r3, r3 - r2 + fg.div(e) + 1u);
+        return fbkv.div(need + (uint32_t)a.bkv - 1u);
       }
-      u = active ? u : 0u;  // idle lanes add 0 to their own (distinct) residue
+      const FastDiv f{r1, r2, r3};  // chunk index kl mod n_ch: full chunks, then the last one
+      return f.mod(kl) == f.d - 1u ? rul : ruf;
+    };
+    // one step: lane task base + k0 + lane gets u (0 for idle lanes)
+    auto add = [&](uint32_t k, uint32_t u, bool active) {
       usum += u;
       if (SMALL) {
 #pragma unroll
@@ -338,12 +336,37 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
           asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(p[d]));
           asm volatile("st.shared.u32 [%0], %1;" ::"r"(p[d]), "r"(v + u) : "memory");
           p[d] += 128u;
-          const uint32_t hi = acc_s + 4u * (uint32_t)(off[d] + N[d]);
-          p[d] = p[d] >= hi ? p[d] - 4u * (uint32_t)N[d] : p[d];
+          p[d] = p[d] >= hi[d] ? p[d] - 4u * (uint32_t)N[d] : p[d];
         }
       }
       __syncwarp();
+    };
+    uint32_t bcur = 0;  // chunk-local request holding task k0
+    uint32_t k0 = 0;
+    while (k0 < total) {
+      // steps wholly inside request bcur: its constants are warp-uniform
+      const uint32_t st = s_start[bcur];
+      const uint32_t nxt = bcur + 1 < nreq ? s_start[bcur + 1] : total;
+      if (k0 + 32 <= nxt) {
+        const uint32_t r1 = s_a1[bcur], r2 = s_a2[bcur], r3 = s_a3[bcur], ruf = s_uf[bcur], rul = s_ul[bcur];
+        for (; k0 + 32 <= nxt; k0 += 32) {
+          const uint32_t k = k0 + lane;
+          add(k, unit(k - st, r1, r2, r3, ruf, rul), true);
+        }
+        if (k0 >= total) break;
+        if (k0 == nxt) { ++bcur; continue; }
+      }
+      // a step crossing request boundaries: each lane finds its request from
+      // the bitmask of request starts inside (k0, k0 + 32)
+      const uint32_t k = k0 + lane;
+      const bool active = k < total;
+      const uint32_t bit = (has && start > k0 && start < k0 + 32) ? (1u << (start - k0)) : 0u;
+      const uint32_t M = __reduce_or_sync(0xffffffffu, bit);
+      const uint32_t bl = min(bcur + __popc(M & lm_le), nreq - 1);
+      const uint32_t u = unit(k - s_start[bl], s_a1[bl], s_a2[bl], s_a3[bl], s_uf[bl], s_ul[bl]);
+      add(k, active ? u : 0u, active);
       bcur += __popc(M) + (__any_sync(0xffffffffu, has && start == k0 + 32) ? 1u : 0u);
+      k0 += 32;
     }
     base += total;
     __syncwarp();
@@ -360,18 +383,20 @@ __device__ DistinctMax fold(const AttnCfg &a, const uint32_t *A, int32_t N, cons
   const uint32_t Lm = fdN.mod(L);
   const uint32_t qn = fdN.div(T), rn = T - qn * (uint32_t)N;
   SumT m_lo = 0, m_hi = 0;
-  for (int32_t s = lane; s < N; s += 32) {
-    SumT S = 0;
-    int32_t o = 0;  // (h * L) mod N
-    for (int32_t h = 0; h < a.nkv; ++h) {
-      int32_t idx = s - o;
-      idx += idx < 0 ? N : 0;
-      S += A[idx];
-      o += (int32_t)Lm;
-      o -= o >= N ? N : 0;
+  {
+    for (int32_t s = lane; s < N; s += 32) {
+      SumT S = 0;
+      int32_t o = 0;
+      for (int32_t h = 0; h < a.nkv; ++h) {
+        int32_t idx = s - o;
+        idx += idx < 0 ? N : 0;
+        S += A[idx];
+        o += (int32_t)Lm;
+        o -= o >= N ? N : 0;
+      }
+      if ((uint32_t)s < rn) m_lo = max(m_lo, S);
+      else m_hi = max(m_hi, S);
     }
-    if ((uint32_t)s < rn) m_lo = max(m_lo, S);
-    else m_hi = max(m_hi, S);
   }
   const int64_t lo = warp_max64((int64_t)m_lo), hi = warp_max64((int64_t)m_hi);
   int64_t mB = 0;
@@ -446,7 +471,7 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, const int
 }
 
 template <int ND, bool SMALL>
-__global__ void __launch_bounds__(kWarps * 32, 3) featurize_attention_cross(ConfigView cfg,
+__global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) featurize_attention_cross(ConfigView cfg,
                                                                             const DevSpec *__restrict__ specs,
                                                                             int g0, AttnPlan plan, FeatOut out) {
   extern __shared__ uint32_t smem[];

@@ -77,7 +77,8 @@ struct AttnGroup {
   int32_t distinct_first;  // index into distinct_n / distinct_off
   int32_t n_distinct;
 };
-constexpr int kAttnScratchWords = 224;  // per-warp request scratch (7 x 32 words)
+// per-warp scratch after the accumulators: request parameters (7 x 32 words)
+constexpr int kAttnScratchWords = 224;
 struct AttnPlan {
   const AttnGroup *groups;     // DEVICE [n_groups]
   const int32_t *group_specs;  // DEVICE spec index (absolute)
@@ -113,8 +114,8 @@ int launch_predict_simt(const MlpFp32 &m, const sp_features &in, float *latency,
 
 struct MlpBf16 {  // tcgen05 path, 16-bit operands (bf16 or fp16)
   int32_t bf16;         // 1: bf16 operands, 0: fp16 operands
-  const void *wpack;    // DEVICE packed bf16 weights in UMMA canonical layout (see predict_tcgen05.cu)
-  const float *vecs;    // DEVICE fp32 per-unit vectors: b1[256], b2'[128], b3'[64], w4'[64], mu[16], inv_sigma[16]
+  const void *wpack;    // DEVICE packed 16-bit weights in the UMMA canonical layout (predict_tcgen05.cu)
+  const float *vecs;    // DEVICE fp32 vectors: b2'[128], b3'[64], w4'[64], ln2/sigma[16], -mu/sigma[16]
   float b4;
   int32_t n_in;
   int32_t family;
