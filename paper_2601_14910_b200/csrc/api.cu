@@ -24,7 +24,11 @@ using namespace sp;
 struct sp_ctx {
   int device = 0;
   int num_sms = 0;
+  int *counters = nullptr;  // DEVICE work counters of the attention kernel (kAttnMaxGroups)
   std::string err;
+  ~sp_ctx() {
+    if (counters) cudaFree(counters);
+  }
 };
 
 namespace {
@@ -129,6 +133,13 @@ extern "C" sp_status sp_create(int device, sp_ctx **out) {
   if (!c) return fail(nullptr, SP_E_INTERNAL, "sp_create: out of host memory");
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  cudaSetDevice(device);
+  e = cudaMalloc(&c->counters, kAttnMaxGroups * sizeof(int));
+  if (e != cudaSuccess) {
+    c->counters = nullptr;
+    delete c;
+    return cuda_fail(nullptr, e, "sp_create: scratch allocation");
+  }
   *out = c;
   return SP_OK;
 }
@@ -352,7 +363,11 @@ extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const
       const AttnPlan *plan = nullptr;
       sp_status st = attn_plan(ctx, specs, pairs->spec_begin, pairs->spec_end, &plan);
       if (st != SP_OK) return st;
-      e = launch_featurize_attention(cv, ds, pairs->spec_begin, specs->n, *plan, n_pairs, nullptr, nullptr,
+      if (plan->n_groups > kAttnMaxGroups)
+        return fail(ctx, SP_E_UNSUPPORTED, "attention featurization: too many distinct SM-count groups");
+      AttnPlan run = *plan;
+      run.counters = ctx->counters;
+      e = launch_featurize_attention(cv, ds, pairs->spec_begin, specs->n, run, n_pairs, nullptr, nullptr,
                                      specs->max_sms, fo, ctx->num_sms, stream);
     } else {
       if (specs->max_sms > kAttnMaxSms)

@@ -184,9 +184,8 @@ struct DistinctMax {
   int64_t maxS, maxB;  // max_j S_j and max_j (BQ*n_j + 2*BKV*S_j)
 };
 
-// Per-warp scratch (words) after the accumulators: per-request parameters of
-// a chunk of 32 requests, 7 arrays of 32.
-constexpr int kScratchWords = kAttnScratchWords;
+// Request scratch (accumulate): per-request parameters of a chunk of 32
+// requests, 7 arrays of 32 words.
 
 __device__ __forceinline__ uint32_t lanemask_le() {
   uint32_t m;
@@ -438,12 +437,12 @@ __device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const A
   emit_pair(out, p, d, a.fp, s, 5, tdt);
 }
 
-// Whole per-config pipeline for one distinct set; results in res[0..ND)
-// (the warp's shared-memory slots, written by lane 0).
+// Whole per-config pipeline for one distinct set; per-distinct maxima go to
+// mS[d], mB[d] (the warp's shared-memory stash, written by lane 0).
 template <int ND, bool SMALL>
-__device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, const int32_t (&N)[ND],
+__device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, uint32_t *scr, const int32_t (&N)[ND],
                            const int32_t (&off)[ND], const FastDiv *fdN, int32_t minN, int lane, int64_t &L,
-                           uint64_t &U, DistinctMax *res) {
+                           uint64_t &U, int64_t *mS, int64_t *mB) {
   const FastDiv fg = make_fd((uint32_t)a.g);
   L = count_tasks(a, lane, fg);
   if (L > kI32Max || L * a.nkv > kI32Max) return SP_PAIR_E_RANGE;
@@ -453,30 +452,60 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, const int
     sparse_units(a, lane, fg, U, umax);
     if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
     if (lane == 0)
-      for (int d = 0; d < ND; ++d) res[d] = DistinctMax{(int64_t)umax, (int64_t)a.bq + 2 * (int64_t)a.bkv * umax};
+      for (int d = 0; d < ND; ++d) {
+        mS[d] = (int64_t)umax;
+        mB[d] = (int64_t)a.bq + 2 * (int64_t)a.bkv * umax;
+      }
     __syncwarp();
     return 0;
   }
-  U = accumulate<ND, SMALL>(a, acc, words, acc + words, N, off, fdN, lane, fg);
+  U = accumulate<ND, SMALL>(a, acc, words, scr, N, off, fdN, lane, fg);
   if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
   const bool s32 = U * (uint64_t)a.nkv < (1ull << 32);
 #pragma unroll 1
   for (int d = 0; d < ND; ++d) {
     const DistinctMax m = s32 ? fold<uint32_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane)
                               : fold<uint64_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
-    if (lane == 0) res[d] = m;
+    if (lane == 0) {
+      mS[d] = m.maxS;
+      mB[d] = m.maxB;
+    }
   }
   __syncwarp();
   return 0;
 }
 
+// Fields the record needs, read by the lane that owns config c (no validation:
+// only used for configs whose stashed status is 0).
+__device__ __forceinline__ AttnCfg load_cfg_lane(const ConfigView &v, int64_t c) {
+  AttnCfg a{};
+  a.nkv = __ldg(v.fields + (int64_t)NKV * v.ld + c);
+  a.hd = __ldg(v.fields + (int64_t)HD * v.ld + c);
+  a.bq = __ldg(v.fields + (int64_t)BQ * v.ld + c);
+  a.bkv = __ldg(v.fields + (int64_t)BKV * v.ld + c);
+  a.dt = __ldg(v.fields + (int64_t)DTYPE * v.ld + c);
+  const int64_t smem = __ldg(v.fields + (int64_t)SMEM * v.ld + c);
+  a.fp.smem = smem > 0 ? smem : ((int64_t)a.bq + 2 * (int64_t)a.bkv) * a.hd * 2;
+  a.fp.warps = __ldg(v.fields + (int64_t)WARPS * v.ld + c);
+  a.fp.regs = __ldg(v.fields + (int64_t)REGS * v.ld + c);
+  return a;
+}
+
+// Per-warp shared-memory region: [stash of 32 configs | request scratch | accumulators].
+constexpr int kStashWords = 32 + 64 + 64 + 32 * kMaxDistinct * 2 * 2;  // status, L, U, maxS[8], maxB[8]
+static_assert(kStashWords + 224 == kAttnScratchWords, "api.cu sizes the warp region with kAttnScratchWords");
+
+// CROSS mode.  Warps take chunks of 32 consecutive configs from a per-group
+// work counter (dynamic: per-config cost is heavy-tailed), run every config of
+// the chunk, stash its per-distinct results, then write the chunk's records
+// with lane j owning config c0 + j, so each SoA row store of a spec is 32
+// consecutive elements (full sectors, no partial-write read-modify-write).
 template <int ND, bool SMALL>
 __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) featurize_attention_cross(ConfigView cfg,
                                                                             const DevSpec *__restrict__ specs,
                                                                             int g0, AttnPlan plan, FeatOut out) {
   extern __shared__ uint32_t smem[];
   __shared__ FastDiv s_fd[kMaxDistinct];
-  __shared__ DistinctMax s_res[kWarps][kMaxDistinct];
   const AttnGroup grp = plan.groups[blockIdx.y];
   int32_t N[ND], off[ND];
   int32_t minN = INT32_MAX, words = 0;
@@ -491,18 +520,49 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) featurize_attention
   if (threadIdx.x < ND) s_fd[threadIdx.x] = make_fd((uint32_t)N[threadIdx.x]);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t *acc = smem + (size_t)warp * plan.words_per_warp;
+  uint32_t *region = smem + (size_t)warp * plan.words_per_warp;
+  uint32_t *s_st = region;
+  int64_t *s_L = reinterpret_cast<int64_t *>(region + 32);
+  uint64_t *s_U = reinterpret_cast<uint64_t *>(region + 96);
+  int64_t *s_mS = reinterpret_cast<int64_t *>(region + 160);
+  int64_t *s_mB = s_mS + 32 * kMaxDistinct;
+  uint32_t *scr = region + kStashWords;
+  uint32_t *acc = region + kAttnScratchWords;
   const int64_t C = cfg.n_configs;
-  for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < C; c += (int64_t)gridDim.x * kWarps) {
-    const AttnCfg a = load_cfg(cfg, c, lane);
-    int st = a.status;
-    int64_t L = 0;
-    uint64_t U = 0;
-    if (st == 0) st = attn_config<ND, SMALL>(a, acc, words, N, off, s_fd, minN, lane, L, U, s_res[warp]);
-    for (int j = lane; j < grp.n_specs; j += 32) {
-      const int g = __ldg(plan.group_specs + grp.spec_first + j);
-      const int dsel = __ldg(plan.spec_dist + grp.spec_first + j) - grp.distinct_first;
-      attn_emit(out, (int64_t)(g - g0) * C + c, a, st, L, U, s_res[warp][dsel], specs[g]);
+  const int64_t n_chunks = (C + 31) / 32;
+  int *counter = plan.counters + blockIdx.y;
+  for (;;) {
+    int64_t chunk = 0;
+    if (lane == 0) chunk = atomicAdd(counter, 1);
+    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    if (chunk >= n_chunks) break;
+    const int64_t c0 = chunk * 32;
+    const int nc = (int)min((int64_t)32, C - c0);
+    for (int j = 0; j < nc; ++j) {
+      const AttnCfg a = load_cfg(cfg, c0 + j, lane);
+      int st = a.status;
+      int64_t L = 0;
+      uint64_t U = 0;
+      if (st == 0)
+        st = attn_config<ND, SMALL>(a, acc, words, scr, N, off, s_fd, minN, lane, L, U, s_mS + j * kMaxDistinct,
+                                    s_mB + j * kMaxDistinct);
+      if (lane == 0) {
+        s_st[j] = (uint32_t)st;
+        s_L[j] = L;
+        s_U[j] = U;
+      }
+    }
+    __syncwarp();
+    if (lane < nc) {
+      const int64_t c = c0 + lane;
+      const AttnCfg al = load_cfg_lane(cfg, c);
+      const int st = (int)s_st[lane];
+      for (int j = 0; j < grp.n_specs; ++j) {
+        const int g = __ldg(plan.group_specs + grp.spec_first + j);
+        const int dsel = __ldg(plan.spec_dist + grp.spec_first + j) - grp.distinct_first;
+        const DistinctMax m{s_mS[lane * kMaxDistinct + dsel], s_mB[lane * kMaxDistinct + dsel]};
+        attn_emit(out, (int64_t)(g - g0) * C + c, al, st, s_L[lane], s_U[lane], m, specs[g]);
+      }
     }
     __syncwarp();
   }
@@ -517,9 +577,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
                                                                            FeatOut out) {
   extern __shared__ uint32_t smem[];
   __shared__ FastDiv s_fd[kWarps];
-  __shared__ DistinctMax s_res[kWarps];
+  __shared__ int64_t s_m[kWarps][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t *acc = smem + (size_t)warp * words_per_warp;
+  uint32_t *region = smem + (size_t)warp * words_per_warp;
+  uint32_t *scr = region + kStashWords, *acc = region + kAttnScratchWords;
   for (int64_t p = (int64_t)blockIdx.x * kWarps + warp; p < n_pairs; p += (int64_t)gridDim.x * kWarps) {
     const int64_t c = __ldg(cfg_idx + p);
     const int32_t g = __ldg(spec_idx + p);
@@ -536,10 +597,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
     uint64_t U = 0;
     const int words = (N[0] + 3) & ~3;
     if (st == 0) {
-      if (N[0] >= 32) st = attn_config<1, false>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, s_res + warp);
-      else st = attn_config<1, true>(a, acc, words, N, off, s_fd + warp, N[0], lane, L, U, s_res + warp);
+      if (N[0] >= 32)
+        st = attn_config<1, false>(a, acc, words, scr, N, off, s_fd + warp, N[0], lane, L, U, &s_m[warp][0],
+                                   &s_m[warp][1]);
+      else
+        st = attn_config<1, true>(a, acc, words, scr, N, off, s_fd + warp, N[0], lane, L, U, &s_m[warp][0],
+                                  &s_m[warp][1]);
     }
-    if (lane == 0) attn_emit(out, p, a, st, L, U, s_res[warp], specs[g]);
+    if (lane == 0) attn_emit(out, p, a, st, L, U, DistinctMax{s_m[warp][0], s_m[warp][1]}, specs[g]);
     __syncwarp();
   }
 }
@@ -551,10 +616,17 @@ int launch_cross(const ConfigView &cfg, const DevSpec *specs, int g0, const Attn
   cudaError_t e = cudaFuncSetAttribute(featurize_attention_cross<ND, SMALL>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  int64_t want = (cfg.n_configs + kWarps - 1) / kWarps;
-  int64_t cap = (int64_t)num_device_sms * 8;
+  // chunks of 32 configs are handed out dynamically: launch about as many
+  // warps as can be resident, never more than there are chunks
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, featurize_attention_cross<ND, SMALL>, kWarps * 32, smem);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t chunks = (cfg.n_configs + 31) / 32;
+  int64_t want = (chunks + kWarps - 1) / kWarps;
+  int64_t cap = (int64_t)num_device_sms * (per_sm > 0 ? per_sm : 1);
   AttnPlan sub = plan;
   sub.groups = plan.groups + group_y0;
+  sub.counters = plan.counters + group_y0;
   dim3 grid((unsigned)(want < cap ? want : cap), (unsigned)n_groups);
   featurize_attention_cross<ND, SMALL><<<grid, kWarps * 32, smem, st>>>(cfg, specs, g0, sub, out);
   return (int)cudaGetLastError();
@@ -585,6 +657,8 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
   if (cfg_idx == nullptr) {
     if (cfg.n_configs == 0 || plan.n_groups == 0) return 0;
     // one launch per run of groups with the same (distinct count, small-N) shape
+    cudaError_t me = cudaMemsetAsync(plan.counters, 0, (size_t)plan.n_groups * sizeof(int), st);
+    if (me != cudaSuccess) return (int)me;
     for (int y = 0; y < plan.n_groups;) {
       const int nd = plan.host_nd[y];
       const bool small = plan.host_small[y];
@@ -598,7 +672,7 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
     return 0;
   }
   if (n_pairs == 0) return 0;
-  const int words = ((max_sms + 3) & ~3) + kScratchWords;  // accumulators + request scratch
+  const int words = ((max_sms + 3) & ~3) + kAttnScratchWords;  // stash + request scratch + accumulators
   const size_t smem = (size_t)kWarps * words * 4;
   cudaError_t e = cudaFuncSetAttribute(featurize_attention_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

@@ -77,8 +77,10 @@ struct AttnGroup {
   int32_t distinct_first;  // index into distinct_n / distinct_off
   int32_t n_distinct;
 };
-// per-warp scratch after the accumulators: request parameters (7 x 32 words)
-constexpr int kAttnScratchWords = 224;
+// per-warp shared memory before the accumulators: the stash of 32 configs'
+// results (32 + 64 + 64 + 32*8*4 words) and the request scratch (7 x 32 words)
+constexpr int kAttnScratchWords = 1184 + 224;
+constexpr int kAttnMaxGroups = 4096;  // work counters per launch (sp_ctx scratch)
 struct AttnPlan {
   const AttnGroup *groups;     // DEVICE [n_groups]
   const int32_t *group_specs;  // DEVICE spec index (absolute)
@@ -89,6 +91,7 @@ struct AttnPlan {
   int32_t words_per_warp;      // u32 accumulator words per warp
   const int32_t *host_nd;      // HOST [n_groups]: distinct count per group (kernel template)
   const uint8_t *host_small;   // HOST [n_groups]: group holds an SM count < 32 (atomic path)
+  int *counters;               // DEVICE [n_groups] work counters (context scratch, zeroed per launch)
 };
 int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin,
                                int n_specs, const AttnPlan &plan, int64_t n_pairs, const int64_t *cfg_idx,

@@ -1,0 +1,21 @@
+#!/usr/bin/env bash
+# Collects the ncu evidence for one round (run under gpurun, 1 GPU):
+#   1. launch list with device times (--metrics gpu__time_duration.sum, cold-cache, serialised)
+#   2. one `ncu --set full` capture each of the feature kernel and the tcgen05 predictor
+# at the exact bench.py workload, then summarises them into profiles/ (tools/ncu_summary.py).
+# Usage: tools/profile_round.sh r01 [workload]
+set -euo pipefail
+R=${1:-r01}
+W=${2:-cfg2}
+OUT=gpurun_out/prof_$R
+mkdir -p "$OUT"
+BENCH="python bench.py --workload $W --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" $BENCH \
+  > "$OUT/launches_bench.log" 2>&1 || true
+FEAT=featurize_attention_cross
+[ "$W" != "cfg2" ] && FEAT=featurize_uniform_cross
+ncu --set full --clock-control none --import-source on -k regex:$FEAT -s 3 -c 1 -o "$OUT/featurize" $BENCH \
+  > "$OUT/featurize.log" 2>&1 || true
+ncu --set full --clock-control none --import-source on -k regex:predict_tcgen05 -s 3 -c 1 -o "$OUT/predict" $BENCH \
+  > "$OUT/predict.log" 2>&1 || true
+ls -la "$OUT"
