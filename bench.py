@@ -229,12 +229,19 @@ def run_gpu(args, rank, world, local_rank):
     db = sp.DeviceBatch.from_host(b, dev)
     n_pairs = (g1 - g0) * b.n_configs
     feats = sp.Features.empty(b.family, n_pairs, dev)
-    lat = torch.empty(max(n_pairs, 1), dtype=torch.float32, device=dev)
+    # predictions padded to the all-gather's equal per-rank count (dist.Sharder)
+    from paper_2601_14910_b200.dist import Sharder
+
+    if scaling == "strong":
+        padded = Sharder(b.n_configs, len(sa), world, rank, "spec").padded_pairs
+    else:
+        padded = n_pairs  # weak scaling: every rank has a same-sized workload of its own
+    lat = torch.full((max(padded, 1),), float("nan"), dtype=torch.float32, device=dev)
     pairs = sp.cross(g0, g1)
     stream = torch.cuda.current_stream()
     gathered = None
     if dist is not None and not args.no_gather:
-        gathered = torch.empty(world * n_pairs, dtype=torch.float32, device=dev)
+        gathered = torch.empty(world * padded, dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(ev=None):
@@ -246,8 +253,8 @@ def run_gpu(args, rank, world, local_rank):
         ctx.predict(model, feats, lat, None, stream)
         if ev is not None:
             ev[2].record(stream)
-        if gathered is not None:
-            dist.all_gather_into_tensor(gathered, lat[:n_pairs])
+        if gathered is not None:  # the single exchange: ncclAllGather of fp32 predictions
+            dist.all_gather_into_tensor(gathered, lat[:padded])
         if ev is not None:
             ev[3].record(stream)
 
