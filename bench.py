@@ -349,7 +349,7 @@ def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling,
     hb.fields, hb.ragged, hb.ragged_off = fields, ragged, roff
     g0, g1 = spec_range
     n_pairs = (g1 - g0) * b.n_configs
-    out = torch.empty(n_pairs, dtype=torch.float32).pin_memory().numpy()
+    out = torch.empty(n_pairs, dtype=torch.float32).pin_memory()
     h2d = fields.numel() * 4 + (ragged.numel() * 4 if ragged is not None else 0) + \
         (roff.numel() * 8 if roff is not None else 0)
     d2h = n_pairs * 4

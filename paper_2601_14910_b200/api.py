@@ -237,23 +237,100 @@ class Context:
                                    _stream_ptr(stream)))
         return latency
 
-    # -- end-to-end convenience: host configs in, host latencies out
+    # -- end-to-end: host configs in, host latencies out
     def predict_host(self, batch, specs: Specs, model: Model, spec_range=None,
-                     out: np.ndarray | None = None, stream=None) -> np.ndarray:
-        """The user-facing call: host (pinned or pageable) config arrays ->
-        H2D -> featurize -> predict -> D2H of fp32 latencies (spec-major)."""
+                     out: np.ndarray | torch.Tensor | None = None, chunks: int = 4,
+                     stream=None) -> np.ndarray:
+        """The user-facing call.  Host config arrays (numpy or torch; pinned
+        memory gives asynchronous copies) -> H2D -> sp_featurize -> sp_predict
+        -> D2H of fp32 latencies in spec-major order [spec][config].
+
+        The configs are split into `chunks` slices pipelined over three
+        streams: the H2D of slice i+1 and the D2H of slice i-1 overlap the
+        kernels of slice i.  Device buffers are cached across calls."""
         g0, g1 = spec_range if spec_range is not None else (0, len(specs))
-        db = DeviceBatch.from_host(batch, self.torch_device, non_blocking=True)
-        n = (g1 - g0) * db.n_configs
-        feats = Features.empty(db.family, n, self.torch_device)
-        lat = torch.empty(max(n, 1), dtype=torch.float32, device=self.torch_device)
-        self.featurize(db, specs, feats, cross(g0, g1), stream)
-        self.predict(model, feats, lat, None, stream)
-        host = lat[:n].to("cpu", non_blocking=False)
-        if out is not None:
-            out[:n] = host.numpy()
-            return out
-        return host.numpy()
+        G = g1 - g0
+        fam = int(batch.family)
+
+        def host_t(a, dt):
+            if a is None:
+                return None
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+            return t if t.dtype == dt else t.to(dt)
+
+        fh = host_t(batch.fields, torch.int32)
+        rh = host_t(batch.ragged, torch.int32)
+        oh = host_t(batch.ragged_off, torch.int64)
+        nf, C = int(fh.shape[0]), int(fh.shape[1])
+        n = G * C
+        if out is None:
+            out_t = torch.empty(max(n, 1), dtype=torch.float32, pin_memory=True)
+        else:
+            out_t = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+        if n == 0:
+            return out_t[:0].numpy()
+        chunks = max(1, min(chunks, C))
+        bounds = [C * i // chunks for i in range(chunks + 1)]
+        cmax = max(b1 - b0 for b0, b1 in zip(bounds, bounds[1:]))
+        dev = self.torch_device
+        key = (fam, nf, C, G, cmax, 0 if rh is None else rh.numel())
+        cache = getattr(self, "_host_cache", None)
+        if cache is None or cache["key"] != key:
+            cache = {
+                "key": key,
+                "fields": torch.empty((nf, C), dtype=torch.int32, device=dev),
+                "ragged": None if rh is None else torch.empty(max(rh.numel(), 1), dtype=torch.int32, device=dev),
+                "roff": None if oh is None else torch.empty(C, dtype=torch.int64, device=dev),
+                "feats": Features.empty(fam, G * cmax, dev),
+                "lat": [torch.empty(G * cmax, dtype=torch.float32, device=dev) for _ in range(2)],
+                "h2d": torch.cuda.Stream(dev),
+                "d2h": torch.cuda.Stream(dev),
+            }
+            self._host_cache = cache
+        comp = stream or torch.cuda.current_stream(dev)
+        s_h2d, s_d2h = cache["h2d"], cache["d2h"]
+        s_h2d.wait_stream(comp)
+        out2d = out_t[:n].view(G, C)
+        if rh is not None and oh is not None:
+            o = oh.numpy()
+            lens = (2 * fh[0].numpy().astype(np.int64) if fam == _abi.SP_ATTENTION
+                    else fh[1].numpy().astype(np.int64))  # attention: 2*bs; MoE: E
+        d2h_done = []
+        for i, (c0, c1) in enumerate(zip(bounds, bounds[1:])):
+            nc = c1 - c0
+            with torch.cuda.stream(s_h2d):
+                cache["fields"][:, c0:c1].copy_(fh[:, c0:c1], non_blocking=True)
+                if cache["roff"] is not None:
+                    cache["roff"][c0:c1].copy_(oh[c0:c1], non_blocking=True)
+                    valid = o[c0:c1] >= 0
+                    if valid.any():
+                        r0 = int(o[c0:c1][valid].min())
+                        r1 = int((o[c0:c1][valid] + lens[c0:c1][valid]).max())
+                        cache["ragged"][r0:r1].copy_(rh[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_h2d)
+            comp.wait_event(ev)
+            db = DeviceBatch(fam, cache["fields"][:, c0:c1], cache["ragged"],
+                             None if cache["roff"] is None else cache["roff"][c0:c1])
+            feats = cache["feats"]
+            feats.n_pairs = G * nc
+            lat = cache["lat"][i % 2]
+            if i >= 2:  # the D2H that read this buffer two slices ago must be done
+                comp.wait_event(d2h_done[i - 2])
+            self.featurize(db, specs, feats, cross(g0, g1), comp)
+            self.predict(model, feats, lat, None, comp)
+            ev2 = torch.cuda.Event()
+            ev2.record(comp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev2)
+                for g in range(G):  # contiguous row pieces: async DMA into pinned memory
+                    out2d[g, c0:c1].copy_(lat[g * nc:(g + 1) * nc], non_blocking=True)
+                ev3 = torch.cuda.Event()
+                ev3.record(s_d2h)
+                d2h_done.append(ev3)
+        s_d2h.synchronize()
+        comp.wait_stream(s_d2h)
+        return out_t[:n].numpy()
 
 
 def features_to_host(f: Features) -> tuple[np.ndarray, np.ndarray, np.ndarray]:

@@ -248,6 +248,31 @@ def test_predict_zero_output_layer_exact(sp, ctx, orc):
         assert np.array_equal(lat.cpu().numpy(), 2.0 * gf[11]), prec
 
 
+@pytest.mark.parametrize("fam", ["attention", "moe", "gemm"])
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_predict_host_equals_device_path(sp, ctx, fam, chunks):
+    """The public host-buffer call (pipelined H2D / kernels / D2H) returns
+    exactly what the device-resident featurize + predict returns."""
+    b = FAMILY_BATCHES[fam]()
+    sa = specs.paper_gpu_specs()
+    sh = ctx.load_gpu_specs(sa)
+    m = ctx.load_model(models.random_mlp(b.family, 5), "fp16")
+    f, _ = gpu_features(sp, ctx, b, sa, specs_handle=sh)
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    ctx.predict(m, f, lat)
+    torch.cuda.synchronize()
+
+    class Host:
+        family = b.family
+
+    h = Host()
+    h.fields = torch.from_numpy(b.fields).pin_memory()
+    h.ragged = None if b.ragged is None else torch.from_numpy(b.ragged).pin_memory()
+    h.ragged_off = None if b.ragged_off is None else torch.from_numpy(b.ragged_off).pin_memory()
+    got = ctx.predict_host(h, sh, m, chunks=chunks)
+    assert np.array_equal(got, lat.cpu().numpy(), equal_nan=True)
+
+
 def test_featurize_deterministic(sp, ctx):
     b = FAMILY_BATCHES["attention"]()
     sa = specs.paper_gpu_specs()
