@@ -5,21 +5,37 @@
 //   D1[128x256] = X [128x16]  . W1^T   (x in cols 0..n_in-1, col 15 = 1 carries b1)
 //   D2[128x128] = H1[128x256] . W2'^T  (W2' = W2 diag(s1): BN1 folded, R18)
 //   D3[128x64]  = H2[128x128] . W3'^T  (W3' = W3 diag(s2))
-// issued by one thread as tcgen05.mma (M = 128, 16-bit in, fp32 accumulate in
-// TMEM).  The folded BatchNorm shifts become biases (b2' = b2 + W2 t1, ...)
-// that the epilogue writes into the D2/D3 accumulators (tcgen05.st) before the
-// MMAs accumulate onto them, and the last BN goes into the output layer
-// (w4' = w4 s3, b4' = b4 + w4.t3).  Each hidden epilogue is therefore only
-// TMEM load -> cvt.rn.relu.{f16,bf16}x2 -> 16-byte st.shared, and the final
-// 64 -> 1 layer is 64 FMAs per row on CUDA cores.
+// issued by one thread as tcgen05.mma (M = 128, 16-bit in, fp32 accumulate).
+// The folded BatchNorm shifts become biases (b2' = b2 + W2 t1, ...) that the
+// epilogue presets into the D2/D3 accumulators (tcgen05.st) before the MMAs
+// accumulate onto them; the last BN goes into the output layer (w4' = w4 s3,
+// b4' = b4 + w4.t3).  The activations H1, H2 never touch shared memory: each
+// epilogue reads D from TMEM, applies ReLU + 16-bit packing (one
+// cvt.rn.relu.f16x2 per two values) and writes the packed rows back into TMEM,
+// where the next layer reads them as its A operand ("TS" MMA); only the
+// weights (B) stream from shared memory.  The final 64 -> 1 layer is 64 FMAs
+// per row.
 //
-// CTA = 16 epilogue warps (4 warpgroups: 2 tile slots x 2 column halves) + 1
-// MMA warp, persistent over tiles.  Weights (88 KB, UMMA no-swizzle K-major
-// layout prepacked on the host) stay resident in shared memory; each slot owns
-// 256 TMEM columns (D1, then D2/D3 reusing them) and 68 KB of activation
-// buffers (X, then H1, with H2 aliasing H1).  The two slots interleave so the
-// tensor pipe works on one tile while the other tile's epilogue runs.  The
-// feature loads of a slot's next tile are issued one tile ahead.
+// Warp roles (persistent CTA, one per SM, 21 warps):
+//   producers (4 warps): stream the feature columns of the CTA's tiles into
+//     shared memory with cp.async (kNR tiles ahead), normalise them (a10:
+//     log1p + z-score) and write the 16-bit X tile into a kNX-deep ring;
+//   MMA issuer (1 thread): a small scheduler that issues whichever layer of
+//     either TMEM slot is ready (X tile present + slot free, or activations
+//     written back), so the tensor pipe never idles behind one slot;
+//   epilogue (16 warps = 2 TMEM slots x 2 column halves x 4 lane quadrants).
+// Keeping the feature decode off the epilogue warps takes it off the
+// layer-to-layer critical path.  TMEM columns of slot s (base B = 256 s):
+//   D1 [B, B+256)        -> H1 K 0..127 packed in [B, B+64) (half 0),
+//                           H1 K 128..255 packed in [B+192, B+256) (half 1)
+//   D2 [B+64, B+192)     (N = 128 in one MMA per K step: a TS MMA reads its
+//                         4 KB A slice from TMEM at ~64 B/clk, so N = 64 would
+//                         halve the tensor rate; N = 128 matches it)
+//   H2 [B, B+64)         (half h: K 64h..64h+63 in [B+32h, B+32h+32))
+//   D3 [B+192, B+256)
+// Each half writes only columns it has itself read (half 1 packs its D1
+// columns back to front), or columns whose readers the MMA barrier already
+// retired, so the halves need no barrier between them.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -36,8 +52,12 @@ namespace {
 
 constexpr int kTile = 128;
 constexpr int kEpiWarps = 16;
-constexpr int kThreads = (kEpiWarps + 1) * 32;
+constexpr int kProdWarps = 4;
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;
+constexpr int kThreads = (kMmaWarp + 1) * 32;
 constexpr int kK1 = 16;  // n_in padded; column 15 is the constant-1 bias column
+constexpr int kNX = 4;   // X ring depth (tiles)
+constexpr int kNR = 3;   // raw feature staging depth (tiles in flight per producer thread)
 
 // Shared-memory image, bytes.  Operand layout (K-major, no swizzle):
 //   off(r, k) = (r / 8) * SBO + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2,  SBO = 16 * K
@@ -45,18 +65,21 @@ constexpr uint32_t kW1Bytes = 256 * kK1 * 2;   //  8 KB
 constexpr uint32_t kW2Bytes = 128 * 256 * 2;   // 64 KB
 constexpr uint32_t kW3Bytes = 64 * 128 * 2;    // 16 KB
 constexpr uint32_t kWBytes = kW1Bytes + kW2Bytes + kW3Bytes;
-constexpr uint32_t kXBytes = kTile * kK1 * 2;  //  4 KB
-constexpr uint32_t kHBytes = kTile * 256 * 2;  // 64 KB (H1; H2 = 32 KB aliases it)
-constexpr uint32_t kSlotBytes = kXBytes + kHBytes;
+constexpr uint32_t kXBytes = kTile * kK1 * 2;  //  4 KB per X stage
+constexpr uint32_t kRawBytes = 16 * kTile * 8; // 16 KB per raw stage: [feature][row] u64
 // fp32 vectors: b2'[128] b3'[64] w4'[64] na[16] nc[16]  (x = log2(1+v) * na + nc)
 constexpr int kVB2 = 0, kVB3 = 128, kVW4 = 192, kVNA = 256, kVNC = 272, kVecFloats = 288;
 constexpr uint32_t kVecBytes = kVecFloats * 4;
 constexpr uint32_t kOffW1 = 0, kOffW2 = kW1Bytes, kOffW3 = kW1Bytes + kW2Bytes;
-constexpr uint32_t kOffSlot0 = kWBytes;
-constexpr uint32_t kOffVec = kWBytes + 2 * kSlotBytes;
+constexpr uint32_t kOffX = kWBytes;
+constexpr uint32_t kOffRaw = kOffX + kNX * kXBytes;
+constexpr uint32_t kOffVec = kOffRaw + kNR * kRawBytes;
 constexpr uint32_t kOffZx = kOffVec + kVecBytes;  // [2][128] fp32 partial logits
 constexpr uint32_t kOffBar = kOffZx + 2 * kTile * 4;
-constexpr uint32_t kSmemBytes = kOffBar + 64;
+// barriers: x_full[kNX] x_empty[kNX] d_full[2] a_ready[2] slot_free[2], then the TMEM base
+constexpr int kBarXFull = 0, kBarXEmpty = kNX, kBarDFull = 2 * kNX, kBarAReady = 2 * kNX + 2,
+              kBarSlotFree = 2 * kNX + 4, kNumBars = 2 * kNX + 6;
+constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 __host__ __device__ constexpr uint32_t op_off(uint32_t r, uint32_t k, uint32_t K) {
@@ -81,6 +104,24 @@ __host__ __device__ constexpr int in_slot(int fam, int k) {
 }
 __host__ __device__ constexpr int n_in_of(int fam) { return (fam == SP_GEMM || fam == SP_FUSED_MOE) ? 11 : 15; }
 
+#ifdef SP_PRED_TRACE
+// Debug build only: clock64 stamps of CTA 0 (role r: 0 = slot-0 epilogue, 1 =
+// slot-1 epilogue, 2 = MMA issuer) for the first 64 iterations.
+__device__ long long g_pred_trace[3][64][16];
+__device__ long long g_pred_wtrace[16][64][16];  // every epilogue warp (lane 0)
+#define PTRACE(role, it, idx) \
+  if (blockIdx.x == 0 && (it) < 64) g_pred_trace[role][it][idx] = clock64()
+#define EPT(idx)                                                                   \
+  do {                                                                             \
+    const long long c_ = clock64();                                                \
+    if (blockIdx.x == 0 && it < 64 && lane == 0) g_pred_wtrace[warp][it][idx] = c_; \
+    if (tr) PTRACE(s, it, idx);                                                    \
+  } while (0)
+#else
+#define EPT(idx)
+#define PTRACE(role, it, idx)
+#endif
+
 struct Params {
   MlpBf16 m;
   sp_features in;
@@ -89,69 +130,36 @@ struct Params {
   int64_t n_tiles;
 };
 
-// Half a row's raw MLP inputs (features 8h..8h+7), loaded unconditionally
-// (row index clamped) so the loads never wait on each other; int64 slots as
-// raw bits, float slots in the low word.  Decoded at use time.
-struct TileIn {
-  uint64_t raw[8];
-  float t_theory;
-  uint32_t status;
-  bool in_range;
-};
-
-template <int FAM>
-__device__ __forceinline__ TileIn load_tile_in(const Params &P, int64_t t, uint32_t row, int h) {
-  TileIn r;
-  int64_t p = t * kTile + row;
-  r.in_range = t < P.n_tiles && p < P.in.n_pairs;
-  p = r.in_range ? p : 0;
-  const int64_t ld = P.in.ld;
-  const unsigned long long *ints = reinterpret_cast<const unsigned long long *>(P.in.ints);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    r.raw[i] = 0;
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {  // h is warp-uniform; both variants are compile-time slots
-      const int sl = in_slot(FAM, 8 * hh + i);
-      if (hh == h && 8 * hh + i < n_in_of(FAM))
-        r.raw[i] = sl >= 16 ? (uint64_t)__float_as_uint(__ldg(P.in.flts + (int64_t)(sl - 16) * ld + p))
-                            : (uint64_t)__ldg(ints + (int64_t)sl * ld + p);
-    }
-  }
-  r.t_theory = h == 0 ? __ldg(P.in.flts + (int64_t)F_TTHEORY * ld + p) : 0.f;
-  r.status = __ldg(P.in.status + p);
-  return r;
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
-template <int FAM>
-__device__ __forceinline__ float decode_in(const TileIn &r, int i, int h) {
-  const int sl0 = in_slot(FAM, i), sl1 = in_slot(FAM, 8 + i);
-  const bool is_f = h == 0 ? sl0 >= 16 : sl1 >= 16;
-  return is_f ? __uint_as_float((uint32_t)r.raw[i]) : (float)(int64_t)r.raw[i];
-}
-
-// Hidden epilogue: TMEM columns [c_begin, c_begin + NC) of this lane's row ->
-// ReLU -> 16-bit -> next operand (K = KN) columns [c_begin, ...) in shared memory.
-template <int NC, int KN, bool BF16>
-__device__ __forceinline__ void epi_hidden(uint32_t tmem_row, uint32_t c_begin, uint32_t dst, uint32_t row) {
+// Hidden epilogue in TMEM: fp32 columns [src, src + NC) of this lane's row ->
+// ReLU -> packed 16-bit pairs -> columns [dst, dst + NC/2).  Every 64-column
+// read completes before its 32 packed columns are written, and the chunk
+// order keeps the output off unread input (dst <= src forward, or
+// dst >= src + NC/2 back to front).
+// With REV the 64-column chunks go back to front, for dst > src.
+template <int NC, bool BF16, bool REV = false>
+__device__ __forceinline__ void epi_hidden_tmem(uint32_t tmem_row, uint32_t src, uint32_t dst) {
 #pragma unroll 1
-  for (int c00 = 0; c00 < NC; c00 += 64) {
-    uint32_t vv[2][32];  // two TMEM loads in flight per wait
-    tc::tmem_ld32(tmem_row + c_begin + c00, vv[0]);
-    tc::tmem_ld32(tmem_row + c_begin + c00 + 32, vv[1]);
+  for (int i = 0; i < NC / 64; ++i) {
+    const int c = REV ? NC - 64 * (i + 1) : 64 * i;
+    uint32_t v[64];
+    tc::tmem_ld32(tmem_row + src + c, *reinterpret_cast<uint32_t(*)[32]>(v));
+    tc::tmem_ld32(tmem_row + src + c + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
     tc::tmem_wait_ld();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // 4 chunks of 8 columns = 16 bytes
-        const uint32_t *v = vv[h] + q * 8;
-        tc::st_shared_v4(dst + op_off(row, c_begin + c00 + 32 * h + q * 8, KN),
-                         tc::relu_x2<BF16>(__uint_as_float(v[0]), __uint_as_float(v[1])),
-                         tc::relu_x2<BF16>(__uint_as_float(v[2]), __uint_as_float(v[3])),
-                         tc::relu_x2<BF16>(__uint_as_float(v[4]), __uint_as_float(v[5])),
-                         tc::relu_x2<BF16>(__uint_as_float(v[6]), __uint_as_float(v[7])));
-      }
-    }
+    for (int j = 0; j < 32; ++j) v[j] = tc::relu_x2<BF16>(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+    tc::tmem_st32(tmem_row + dst + c / 2, *reinterpret_cast<uint32_t(*)[32]>(v));
   }
 }
 
@@ -173,6 +181,27 @@ __device__ __forceinline__ void bias_to_tmem(uint32_t tmem_row, uint32_t c, cons
   }
 }
 
+// ---- producer: features of CTA tile j -> raw stage j % kNR (cp.async; each
+// thread copies, and later reads, only its own row: no barrier needed).
+template <int FAM>
+__device__ __forceinline__ void produce_issue(const Params &P, int64_t j, int64_t n_local, uint32_t row,
+                                              uint32_t raw_base) {
+  if (j < n_local) {
+    const int64_t t = blockIdx.x + j * (int64_t)gridDim.x;
+    int64_t p = t * kTile + row;
+    if (p >= P.in.n_pairs) p = 0;  // tail rows: harmless copy, output never stored
+    const int64_t ld = P.in.ld;
+    const uint32_t dst = raw_base + (uint32_t)(j % kNR) * kRawBytes + row * 8;
+#pragma unroll
+    for (int f = 0; f < n_in_of(FAM); ++f) {
+      const int sl = in_slot(FAM, f);
+      if (sl >= 16) cp_async4(dst + f * kTile * 8, P.in.flts + (int64_t)(sl - 16) * ld + p);
+      else cp_async8(dst + f * kTile * 8, P.in.ints + (int64_t)sl * ld + p);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per tile
+}
+
 template <bool BF16, int FAM>
 __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -180,10 +209,9 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
   const uint32_t sbase = tc::smem_u32(smem);
   float *vec = reinterpret_cast<float *>(smem + kOffVec);
   float *zx = reinterpret_cast<float *>(smem + kOffZx);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kOffBar);  // a_full[2], d_full[2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kOffBar + 32);
-  const uint32_t bar_a[2] = {tc::smem_u32(bars + 0), tc::smem_u32(bars + 1)};
-  const uint32_t bar_d[2] = {tc::smem_u32(bars + 2), tc::smem_u32(bars + 3)};
+  const uint32_t bar0 = sbase + kOffBar;
+  auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kOffBar + kNumBars * 8);
 
   // ---- one-time setup: weights + vectors to smem, barriers, TMEM
   {
@@ -193,13 +221,18 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
     for (int i = threadIdx.x; i < kVecFloats; i += kThreads) vec[i] = __ldg(P.m.vecs + i);
   }
   if (threadIdx.x == 0) {
-    tc::mbar_init(bar_a[0], 256);
-    tc::mbar_init(bar_a[1], 256);
-    tc::mbar_init(bar_d[0], 1);
-    tc::mbar_init(bar_d[1], 1);
+    for (int i = 0; i < kNX; ++i) {
+      tc::mbar_init(bar(kBarXFull + i), kProdWarps * 32);
+      tc::mbar_init(bar(kBarXEmpty + i), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(bar(kBarDFull + s), 1);
+      tc::mbar_init(bar(kBarAReady + s), 256);
+      tc::mbar_init(bar(kBarSlotFree + s), 256);
+    }
     tc::mbar_init_fence();
   }
-  if (warp == kEpiWarps) tc::tmem_alloc<512>(tc::smem_u32(tmem_slot));
+  if (warp == kMmaWarp) tc::tmem_alloc<512>(tc::smem_u32(tmem_slot));
   tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
@@ -207,121 +240,182 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
   const uint32_t tmem = *tmem_slot;
 
   const int64_t G = gridDim.x;
-  if (warp == kEpiWarps) {
+  const int64_t n_local = P.n_tiles > (int64_t)blockIdx.x ? (P.n_tiles - blockIdx.x + G - 1) / G : 0;
+  if (warp == kMmaWarp) {
     // ================= MMA issuer (one thread) =================
+    // Per TMEM slot s (CTA tiles j = s, s+2, ...): layer 0 needs the X tile
+    // (x_full) and the slot's previous tile fully read (slot_free); layers 1, 2
+    // need the epilogue's activations (a_ready).  Issue whatever is ready.
     if (lane == 0) {
-      const uint32_t i1 = tc::idesc_f16kind_f32(128, 256, BF16), i2 = tc::idesc_f16kind_f32(128, 128, BF16),
-                     i3 = tc::idesc_f16kind_f32(128, 64, BF16);
-      uint32_t pa[2] = {0, 0};
-      for (int64_t k = 0;; k += 2) {
-        const int64_t t0 = blockIdx.x + k * G;
-        if (t0 >= P.n_tiles) break;
-        const int nslots = (t0 + G < P.n_tiles) ? 2 : 1;
-        for (int layer = 0; layer < 3; ++layer) {
-          for (int s = 0; s < nslots; ++s) {
-            const uint32_t slot = sbase + kOffSlot0 + s * kSlotBytes;
-            const uint32_t dcol = tmem + (uint32_t)(s * 256);
-            tc::mbar_wait(bar_a[s], pa[s]);
+      const uint32_t i1 = tc::idesc_f16kind_f32(128, 256, BF16), i128 = tc::idesc_f16kind_f32(128, 128, BF16),
+                     i64 = tc::idesc_f16kind_f32(128, 64, BF16);
+      int64_t js[2] = {0, 1};
+      int layer[2] = {0, 0};
+      uint32_t pa[2] = {0, 0}, pf[2] = {0, 0};
+      while (js[0] < n_local || js[1] < n_local) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int64_t j = js[s];
+          if (j >= n_local) continue;
+          const uint32_t B = tmem + (uint32_t)(s * 256);
+          if (layer[s] == 0) {
+            const int xi = (int)(j % kNX);
+            if (!tc::mbar_test(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u)) continue;
+            if (j >= 2 && !tc::mbar_test(bar(kBarSlotFree + s), pf[s])) continue;
+            if (j >= 2) pf[s] ^= 1;
+            tc::fence_after();
+            // X from smem; b1 rides on X's constant-1 column
+            tc::mma_f16kind(B, tc::smem_desc(sbase + kOffX + xi * kXBytes, 128, 16 * kK1),
+                            tc::smem_desc(sbase + kOffW1, 128, 16 * kK1), i1, 0);
+            tc::commit(bar(kBarXEmpty + xi));
+          } else {
+            if (!tc::mbar_test(bar(kBarAReady + s), pa[s])) continue;
             pa[s] ^= 1;
             tc::fence_after();
-            if (layer == 0) {  // bias b1 rides on X's constant-1 column: no accumulate
-              tc::mma_f16kind(dcol, tc::smem_desc(slot, 128, 16 * kK1), tc::smem_desc(sbase + kOffW1, 128, 16 * kK1),
-                              i1, 0);
-            } else if (layer == 1) {  // D2 was preset to b2' by the epilogue: accumulate onto it
+            if (layer[s] == 1) {  // H1 from TMEM; D2 preset to b2'
 #pragma unroll
-              for (int ks = 0; ks < 256 / 16; ++ks)
-                tc::mma_f16kind(dcol, tc::smem_desc(slot + kXBytes + ks * 256, 128, 16 * 256),
-                                tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i2, 1);
-            } else {
+              for (int ks = 0; ks < 16; ++ks) {
+                const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
+                tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
+              }
+            } else {  // H2 from TMEM; D3 preset to b3'
 #pragma unroll
-              for (int ks = 0; ks < 128 / 16; ++ks)
-                tc::mma_f16kind(dcol + 128, tc::smem_desc(slot + kXBytes + ks * 256, 128, 16 * 128),
-                                tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i3, 1);
+              for (int ks = 0; ks < 8; ++ks)
+                tc::mma_f16kind_ts(B + 192, B + 8 * ks, tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64,
+                                   1);
             }
-            tc::commit(bar_d[s]);
+          }
+          PTRACE(2, (int)(j >> 1), 1 + layer[s] * 2 + s);
+          tc::commit(bar(kBarDFull + s));
+          if (++layer[s] == 3) {
+            layer[s] = 0;
+            js[s] += 2;
           }
         }
       }
     }
+  } else if (warp >= kEpiWarps) {
+    // ================= producers =================
+    const uint32_t row = (uint32_t)(warp - kEpiWarps) * 32 + lane;
+    const uint32_t raw_base = sbase + kOffRaw;
+    const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + kOffRaw);
+    float na[15], nc[15];
+#pragma unroll
+    for (int f = 0; f < 15; ++f) {
+      na[f] = vec[kVNA + f];
+      nc[f] = vec[kVNC + f];
+    }
+#pragma unroll
+    for (int j = 0; j < kNR - 1; ++j) produce_issue<FAM>(P, j, n_local, row, raw_base);
+    for (int64_t j = 0; j < n_local; ++j) {
+      produce_issue<FAM>(P, j + kNR - 1, n_local, row, raw_base);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kNR - 1) : "memory");  // tile j's copies landed
+      // a10: x = (ln(1+v) - mu) / sigma = log2(1+v) * (ln2/sigma) - mu/sigma; x[15] = 1 (bias b1)
+      const uint64_t *rj = raw + (size_t)(j % kNR) * (kRawBytes / 8) + row;
+      uint32_t xp[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float x2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int f = 2 * q + e;
+          if (f == 15) {
+            x2[e] = 1.f;
+          } else if (f < n_in_of(FAM)) {
+            const uint64_t u = rj[f * kTile];
+            const float v = in_slot(FAM, f) >= 16 ? __uint_as_float((uint32_t)u) : (float)(int64_t)u;
+            x2[e] = fmaf(lg2_ftz(1.f + v), na[f], nc[f]);
+          } else {
+            x2[e] = 0.f;
+          }
+        }
+        xp[q] = tc::pack_x2<BF16>(x2[0], x2[1]);
+      }
+      const int xi = (int)(j % kNX);
+      if (j >= kNX) tc::mbar_wait_sleep(bar(kBarXEmpty + xi), (uint32_t)((j / kNX) - 1) & 1u);
+      const uint32_t xb = sbase + kOffX + (uint32_t)xi * kXBytes;
+      tc::st_shared_v4(xb + op_off(row, 0, kK1), xp[0], xp[1], xp[2], xp[3]);
+      tc::st_shared_v4(xb + op_off(row, 8, kK1), xp[4], xp[5], xp[6], xp[7]);
+      tc::fence_proxy_async();
+      tc::mbar_arrive(bar(kBarXFull + xi));
+      if (warp == kEpiWarps && lane == 0) PTRACE(2, (int)(j >> 1), 8 + (int)(j & 1));
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
     // ================= epilogue warpgroups =================
     const int grp = warp >> 2;                    // 0..3
     const int s = grp >> 1, h = grp & 1;          // tile slot, column half
     const uint32_t row = (warp & 3) * 32 + lane;  // TMEM lane == tile row
     const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * 256);
-    const uint32_t xbuf = sbase + kOffSlot0 + s * kSlotBytes, hbuf = xbuf + kXBytes;
-    const float *na = vec + kVNA, *nc = vec + kVNC, *w4 = vec + kVW4;
+    const float *w4 = vec + kVW4;
     const int64_t n_pairs = P.in.n_pairs;
+    const uint32_t bar_d = bar(kBarDFull + s), bar_a = bar(kBarAReady + s), bar_f = bar(kBarSlotFree + s);
     uint32_t pd = 0;
-    TileIn cur = load_tile_in<FAM>(P, blockIdx.x + (int64_t)s * G, row, h);
-    for (int64_t k = s;; k += 2) {
-      const int64_t t = blockIdx.x + k * G;
-      if (t >= P.n_tiles) break;
-      const int64_t p = t * kTile + row;
-      const bool valid = cur.in_range && cur.status == 0;
-      const float t_theory = cur.t_theory;
-      // a10: x = (ln(1+v) - mu) / sigma = log2(1+v) * (ln2/sigma) - mu/sigma;
-      // this half writes X columns 8h..8h+7 (column 15 = 1 for the bias b1).
-      float x[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int j = 8 * h + i;
-        x[i] = j == 15 ? 1.f
-                       : ((valid && j < n_in_of(FAM)) ? fmaf(__log2f(1.f + decode_in<FAM>(cur, i, h)), na[j], nc[j]) : 0.f);
+    const bool tr = (warp & 7) == 0 && lane == 0;  // half-0 warp 0 of each slot
+    (void)tr;
+    for (int64_t j = s; j < n_local; j += 2) {
+      const int64_t p = (blockIdx.x + j * G) * kTile + row;
+      const int it = (int)(j >> 1);
+      (void)it;
+      EPT(0);
+      // output-side inputs, loaded now and used after layer 3
+      float t_theory = 0.f;
+      uint32_t stbyte = 1;
+      if (h == 0 && p < n_pairs) {
+        t_theory = __ldg(P.in.flts + (int64_t)F_TTHEORY * P.in.ld + p);
+        stbyte = __ldg(P.in.status + p);
       }
-      cur = load_tile_in<FAM>(P, t + 2 * G, row, h);  // prefetch this slot's next tile
-      tc::st_shared_v4(xbuf + op_off(row, 8 * h, kK1), tc::pack_x2<BF16>(x[0], x[1]), tc::pack_x2<BF16>(x[2], x[3]),
-                       tc::pack_x2<BF16>(x[4], x[5]), tc::pack_x2<BF16>(x[6], x[7]));
-      tc::fence_proxy_async();
-      tc::mbar_arrive(bar_a[s]);
-      // layer 1: D1 cols [128h, 128h+128) -> H1; then preset the next accumulators:
-      // half 0 read D1[0,128) and presets D2 = b2' there; half 1 read D1[128,256)
-      // and presets D3 = b3' in [128,192).
-      tc::mbar_wait(bar_d[s], pd);
+      // layer 1: D1 half h -> H1 (half 0 -> [0, 64), half 1 -> [192, 256));
+      // preset D2 columns 64h..64h+63 (TMEM [64+64h, 128+64h), read by this half) = b2'[64h..]
+      tc::mbar_wait_sleep(bar_d, pd);
+      EPT(2);
       pd ^= 1;
       tc::fence_after();
-      epi_hidden<128, 256, BF16>(tmem_row, 128 * h, hbuf, row);
-      if (h == 0) bias_to_tmem<128>(tmem_row, 0, vec + kVB2);
-      else bias_to_tmem<64>(tmem_row, 128, vec + kVB3);
+      if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
+      else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
+      bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
       tc::tmem_wait_st();
       tc::fence_before();
-      tc::fence_proxy_async();
-      tc::mbar_arrive(bar_a[s]);
-      // layer 2: D2 cols [64h, 64h+64) -> H2 (aliases H1)
-      tc::mbar_wait(bar_d[s], pd);
+      tc::mbar_arrive(bar_a);
+      EPT(3);
+      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 packed in [32h, 32h+32) (H1 is retired);
+      // preset D3 columns 32h.. [192+32h, 224+32h) = b3'[32h..]
+      tc::mbar_wait_sleep(bar_d, pd);
+      EPT(4);
       pd ^= 1;
       tc::fence_after();
-      epi_hidden<64, 128, BF16>(tmem_row, 64 * h, hbuf, row);
+      epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
+      bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
+      tc::tmem_wait_st();
       tc::fence_before();
-      tc::fence_proxy_async();
-      tc::mbar_arrive(bar_a[s]);
+      tc::mbar_arrive(bar_a);
+      EPT(5);
       // layer 3 + output layer: z = b4' + sum_j w4'_j relu(D3_j); this half sums 32 columns
-      tc::mbar_wait(bar_d[s], pd);
+      tc::mbar_wait_sleep(bar_d, pd);
+      EPT(6);
       pd ^= 1;
       tc::fence_after();
-      float zp;
-      {
-        uint32_t v[32];
-        tc::tmem_ld32(tmem_row + 128 + 32 * h, v);
-        tc::tmem_wait_ld();
-        float zz[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const float4 w = *reinterpret_cast<const float4 *>(w4 + 32 * h + j);
-          zz[0] = fmaf(w.x, fmaxf(__uint_as_float(v[j + 0]), 0.f), zz[0]);
-          zz[1] = fmaf(w.y, fmaxf(__uint_as_float(v[j + 1]), 0.f), zz[1]);
-          zz[2] = fmaf(w.z, fmaxf(__uint_as_float(v[j + 2]), 0.f), zz[2]);
-          zz[3] = fmaf(w.w, fmaxf(__uint_as_float(v[j + 3]), 0.f), zz[3]);
-        }
-        zp = (zz[0] + zz[1]) + (zz[2] + zz[3]);
-      }
+      uint32_t v[32];
+      tc::tmem_ld32(tmem_row + 192 + 32 * h, v);
+      tc::tmem_wait_ld();
       tc::fence_before();
+      tc::mbar_arrive(bar_f);  // the slot's TMEM may take the next tile
+      float zz[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < 32; q += 4) {
+        const float4 w = *reinterpret_cast<const float4 *>(w4 + 32 * h + q);
+        zz[0] = fmaf(w.x, fmaxf(__uint_as_float(v[q + 0]), 0.f), zz[0]);
+        zz[1] = fmaf(w.y, fmaxf(__uint_as_float(v[q + 1]), 0.f), zz[1]);
+        zz[2] = fmaf(w.z, fmaxf(__uint_as_float(v[q + 2]), 0.f), zz[2]);
+        zz[3] = fmaf(w.w, fmaxf(__uint_as_float(v[q + 3]), 0.f), zz[3]);
+      }
+      const float zp = (zz[0] + zz[1]) + (zz[2] + zz[3]);
       if (h == 1) zx[s * kTile + row] = zp;
       asm volatile("bar.sync %0, 256;" ::"r"(1 + s) : "memory");  // the slot's two halves
       if (h == 0 && p < n_pairs) {
         const float z = P.m.b4 + zp + zx[s * kTile + row];
         float lat, e;
-        if (!valid) {
+        if (stbyte != 0) {
           lat = e = __int_as_float(0x7fc00000);
         } else {
           const float ez = __expf(-z);
@@ -331,11 +425,12 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
         P.latency[p] = lat;
         if (P.eff) P.eff[p] = e;
       }
+      EPT(7);
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == kEpiWarps) {
+  if (warp == kMmaWarp) {
     tc::fence_after();
     tc::tmem_dealloc<512>(tmem);
   }
@@ -416,6 +511,15 @@ static cudaError_t launch_fam(int fam, const Params &P, unsigned grid, cudaStrea
   kern<<<grid, kThreads, kSmemBytes, st>>>(P);
   return cudaGetLastError();
 }
+
+#ifdef SP_PRED_TRACE
+extern "C" int sp_debug_pred_trace(long long *host_out) {
+  cudaError_t e = cudaMemcpyFromSymbol(host_out, g_pred_trace, sizeof(g_pred_trace));
+  if (e == cudaSuccess)
+    e = cudaMemcpyFromSymbol(host_out + sizeof(g_pred_trace) / 8, g_pred_wtrace, sizeof(g_pred_wtrace));
+  return (int)e;
+}
+#endif
 
 int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *latency, float *eff,
                            int num_device_sms, void *stream) {
