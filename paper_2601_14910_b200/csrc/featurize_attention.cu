@@ -12,7 +12,8 @@
 //
 // Layout: one warp per config.  Lanes take 32 consecutive head-0 tasks per
 // step; with N >= 32 the 32 residues are distinct, so each lane updates its
-// own shared-memory accumulator with a plain load/add/store.  The task
+// own shared-memory accumulator with one shared reduction (red.shared.add,
+// one issue slot instead of load + add + store).  The task
 // sequence does not depend on the spec, so in SP_PAIRS_CROSS mode a warp
 // accumulates once per *distinct SM count* of the spec range (the 11 GPUs of
 // Table VI have 7) and then emits every spec of its group; the distinct set
@@ -331,9 +332,8 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       } else {
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
-          uint32_t v;
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(p[d]));
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(p[d]), "r"(v + u) : "memory");
+          // one ATOMS.ADD instead of load + add + store: the kernel is issue bound
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(p[d]), "r"(u) : "memory");
           p[d] += 128u;
           p[d] = p[d] >= hi[d] ? p[d] - 4u * (uint32_t)N[d] : p[d];
         }
@@ -376,13 +376,63 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
 // Fold the nkv rotations of one distinct N and take the per-quantity maxima.
 // SM j holds qn + (j < rn) tasks; max_j (BQ n_j + 2 BKV S_j) is taken over the
 // two task-count classes separately.  S_j fits 32 bits when nkv * U < 2^32.
+//
+// Fast form (N <= kFoldDupMax): A is first duplicated into A[N, 2N), so the
+// rotated index j - h*L mod N becomes the plain offset j + N - (h*L mod N);
+// each lane keeps the sums of its R = ceil(N/32) residues in registers and a
+// head costs R shared loads + R adds.  Reads reach index 2N + 31 (the caller
+// guarantees that much readable space; lanes past N are discarded).  32-bit
+// sums only, and few instantiations: the kernel is instruction-cache bound
+// once its code grows (ncu: stalled_no_instructions).
+#ifndef SP_FOLD_DUP_MAX
+#define SP_FOLD_DUP_MAX 192
+#endif
+constexpr int kFoldDupMax = SP_FOLD_DUP_MAX;
+
+template <typename SumT, int R>
+__device__ __forceinline__ void fold_rows(const uint32_t *A, int32_t N, uint32_t Lm, int32_t nkv, uint32_t rn,
+                                          int lane, SumT &m_lo, SumT &m_hi) {
+  SumT S[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) S[i] = 0;
+  const uint32_t *b0 = A + N + lane;
+  uint32_t o = 0;  // h * L mod N
+#pragma unroll 1  // code size: the kernel is instruction-cache sensitive
+  for (int32_t h = 0; h < nkv; ++h) {
+    const uint32_t *b = b0 - o;
+#pragma unroll
+    for (int i = 0; i < R; ++i) S[i] += b[32 * i];
+    o += Lm;
+    o = o >= (uint32_t)N ? o - (uint32_t)N : o;
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const uint32_t sj = (uint32_t)(lane + 32 * i);
+    if (sj < (uint32_t)N) {
+      if (sj < rn) m_lo = max(m_lo, S[i]);
+      else m_hi = max(m_hi, S[i]);
+    }
+  }
+}
+
 template <typename SumT>
-__device__ DistinctMax fold(const AttnCfg &a, const uint32_t *A, int32_t N, const FastDiv &fdN, uint32_t L,
-                            uint32_t T, int lane) {
+__device__ DistinctMax fold(const AttnCfg &a, uint32_t *A, int32_t N, const FastDiv &fdN, uint32_t L, uint32_t T,
+                            int lane) {
   const uint32_t Lm = fdN.mod(L);
   const uint32_t qn = fdN.div(T), rn = T - qn * (uint32_t)N;
   SumT m_lo = 0, m_hi = 0;
-  {
+  if (sizeof(SumT) == 4 && N <= kFoldDupMax) {
+    for (int32_t x = lane; x < N; x += 32) A[N + x] = A[x];
+    __syncwarp();
+    switch ((N + 31) >> 5) {
+      case 1: fold_rows<SumT, 1>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
+      case 2: fold_rows<SumT, 2>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
+      case 3: fold_rows<SumT, 3>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
+      case 4: fold_rows<SumT, 4>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
+      case 5: fold_rows<SumT, 5>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
+      default: fold_rows<SumT, 6>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
+    }
+  } else {
     for (int32_t s = lane; s < N; s += 32) {
       SumT S = 0;
       int32_t o = 0;
@@ -462,8 +512,10 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, uint32_t 
   U = accumulate<ND, SMALL>(a, acc, words, scr, N, off, fdN, lane, fg);
   if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
   const bool s32 = U * (uint64_t)a.nkv < (1ull << 32);
+  // last region first: fold() duplicates region d into [off_d + N_d, off_d + 2 N_d),
+  // over regions already folded and the (dead) request scratch that follows them
 #pragma unroll 1
-  for (int d = 0; d < ND; ++d) {
+  for (int d = ND - 1; d >= 0; --d) {
     const DistinctMax m = s32 ? fold<uint32_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane)
                               : fold<uint64_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
     if (lane == 0) {
@@ -494,6 +546,8 @@ __device__ __forceinline__ AttnCfg load_cfg_lane(const ConfigView &v, int64_t c)
 // Per-warp shared-memory region: [stash of 32 configs | request scratch | accumulators].
 constexpr int kStashWords = 32 + 64 + 64 + 32 * kMaxDistinct * 2 * 2;  // status, L, U, maxS[8], maxB[8]
 static_assert(kStashWords + 224 == kAttnScratchWords, "api.cu sizes the warp region with kAttnScratchWords");
+// fold()'s duplicate of the last region (N <= kFoldDupMax, reads to 2N + 31) must fit in the request scratch
+static_assert(224 >= kFoldDupMax + 32, "fold duplicate overruns the warp region");
 
 // CROSS mode.  Warps take chunks of 32 consecutive configs from a per-group
 // work counter (dynamic: per-config cost is heavy-tailed), run every config of
@@ -526,8 +580,9 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) featurize_attention
   uint64_t *s_U = reinterpret_cast<uint64_t *>(region + 96);
   int64_t *s_mS = reinterpret_cast<int64_t *>(region + 160);
   int64_t *s_mB = s_mS + 32 * kMaxDistinct;
-  uint32_t *scr = region + kStashWords;
-  uint32_t *acc = region + kAttnScratchWords;
+  // warp region: [stash][accumulators: words_per_warp - kAttnScratchWords][request scratch]
+  uint32_t *acc = region + kStashWords;
+  uint32_t *scr = acc + (plan.words_per_warp - kAttnScratchWords);
   const int64_t C = cfg.n_configs;
   const int64_t n_chunks = (C + 31) / 32;
   int *counter = plan.counters + blockIdx.y;
@@ -580,7 +635,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
   __shared__ int64_t s_m[kWarps][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *region = smem + (size_t)warp * words_per_warp;
-  uint32_t *scr = region + kStashWords, *acc = region + kAttnScratchWords;
+  uint32_t *acc = region + kStashWords, *scr = acc + (words_per_warp - kAttnScratchWords);
   for (int64_t p = (int64_t)blockIdx.x * kWarps + warp; p < n_pairs; p += (int64_t)gridDim.x * kWarps) {
     const int64_t c = __ldg(cfg_idx + p);
     const int32_t g = __ldg(spec_idx + p);

@@ -122,6 +122,18 @@ __device__ long long g_pred_wtrace[16][64][16];  // every epilogue warp (lane 0)
 #define PTRACE(role, it, idx)
 #endif
 
+#ifdef SP_EPI_SPIN
+#define EPI_WAIT(b, ph) tc::mbar_wait(b, ph)
+#else
+#define EPI_WAIT(b, ph) tc::mbar_wait_sleep(b, ph)
+#endif
+
+#ifdef SP_EXP_NOMMA
+constexpr bool kNoMma = true;
+#else
+constexpr bool kNoMma = false;
+#endif
+
 struct Params {
   MlpBf16 m;
   sp_features in;
@@ -265,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
             if (j >= 2) pf[s] ^= 1;
             tc::fence_after();
             // X from smem; b1 rides on X's constant-1 column
-            tc::mma_f16kind(B, tc::smem_desc(sbase + kOffX + xi * kXBytes, 128, 16 * kK1),
+            if (!kNoMma) tc::mma_f16kind(B, tc::smem_desc(sbase + kOffX + xi * kXBytes, 128, 16 * kK1),
                             tc::smem_desc(sbase + kOffW1, 128, 16 * kK1), i1, 0);
             tc::commit(bar(kBarXEmpty + xi));
           } else {
@@ -276,12 +288,13 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
 #pragma unroll
               for (int ks = 0; ks < 16; ++ks) {
                 const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
-                tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
+                if (!kNoMma)
+                  tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
             } else {  // H2 from TMEM; D3 preset to b3'
 #pragma unroll
               for (int ks = 0; ks < 8; ++ks)
-                tc::mma_f16kind_ts(B + 192, B + 8 * ks, tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64,
+                if (!kNoMma) tc::mma_f16kind_ts(B + 192, B + 8 * ks, tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64,
                                    1);
             }
           }
@@ -367,31 +380,39 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       }
       // layer 1: D1 half h -> H1 (half 0 -> [0, 64), half 1 -> [192, 256));
       // preset D2 columns 64h..64h+63 (TMEM [64+64h, 128+64h), read by this half) = b2'[64h..]
-      tc::mbar_wait_sleep(bar_d, pd);
+      EPI_WAIT(bar_d, pd);
       EPT(2);
       pd ^= 1;
       tc::fence_after();
+#ifndef SP_EXP_NOEPI
       if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
       else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
+#endif
+#ifndef SP_EXP_NOBIAS
       bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
+#endif
       tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
       // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 packed in [32h, 32h+32) (H1 is retired);
       // preset D3 columns 32h.. [192+32h, 224+32h) = b3'[32h..]
-      tc::mbar_wait_sleep(bar_d, pd);
+      EPI_WAIT(bar_d, pd);
       EPT(4);
       pd ^= 1;
       tc::fence_after();
+#ifndef SP_EXP_NOEPI
       epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
+#endif
+#ifndef SP_EXP_NOBIAS
       bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
+#endif
       tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(5);
       // layer 3 + output layer: z = b4' + sum_j w4'_j relu(D3_j); this half sums 32 columns
-      tc::mbar_wait_sleep(bar_d, pd);
+      EPI_WAIT(bar_d, pd);
       EPT(6);
       pd ^= 1;
       tc::fence_after();

@@ -40,23 +40,24 @@ wbuf = allbuf[3 * 64 * 16:].reshape(16, 64, 16)
 names = ["start", "-", "D1 ready", "A2 arrived", "D2 ready", "A3 arrived", "D3 ready", "end"]
 t = buf[2, 2:60, 1].astype(np.float64)
 print("period (L1s0 issue to next):", np.median(np.diff(t)))
-# one iteration's events of all roles on a common clock
-it = 10
+# a window of iterations, all roles on a common clock
 ev = []
-for role, nm in ((0, "s0"), (1, "s1")):
-    for i, name in enumerate(names):
-        if name != "-":
-            ev.append((buf[role, it, i], f"{nm} {name}"))
-mma = ["iter", "L1s0 issued", "L1s1 issued", "L2s0 issued", "L2s1 issued", "L3s0 issued", "L3s1 issued", "-", "X(s0) full", "X(s1) full"]
-for i, name in enumerate(mma):
-    if buf[2, it, i] and name != "-":
-        ev.append((buf[2, it, i], f"MMA {name}"))
+for it in (9, 10, 11):
+    for role, nm in ((0, "s0"), (1, "s1")):
+        for i, name in enumerate(names):
+            if name != "-":
+                ev.append((buf[role, it, i], f"{nm} {name} [{it}]"))
+    mma = ["iter", "L1s0 issued", "L1s1 issued", "L2s0 issued", "L2s1 issued", "L3s0 issued", "L3s1 issued", "-",
+           "X(s0) full", "X(s1) full"]
+    for i, name in enumerate(mma):
+        if buf[2, it, i] and name != "-" and "full" not in name:
+            ev.append((buf[2, it, i], f"    MMA {name} [{it}]"))
 ev.sort()
 t0 = ev[0][0]
-print("iteration", it, "timeline (cycles):")
+it = 10
+print("timeline (cycles):")
 for t, name in ev:
     print(f"  {t - t0:7d}  {name}")
-
 print("per-warp (rows: warp = slot*8 + half*4 + quadrant), cycles from t0:")
 print("      " + " ".join(f"{n[:10]:>10}" for n in names))
 for w in range(16):
