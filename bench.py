@@ -266,11 +266,15 @@ def run_gpu(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
+    ctx.profile_read(reset=True)
+    ctx.set_profiling(True)  # per-kernel CUDA events on the launch stream (sp_set_profiling)
     with ClockSampler(local_rank) as clk:
         for s in range(args.steps):
             flush.zero_()  # L2 flush between timed steps, outside the events
             step(evs[s])
         torch.cuda.synchronize()
+    ctx.set_profiling(False)
+    kst = ctx.profile_read(reset=True)  # {kernel: (launches, device ms)} of the timed region
     if dist is not None:
         dist.barrier()
     t_feat = np.array([e[0].elapsed_time(e[1]) for e in evs])
@@ -300,7 +304,7 @@ def run_gpu(args, rank, world, local_rank):
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json")) or {}
     feat_ms, pred_ms = float(t_feat.mean()), float(t_pred.mean())
-    roof = roofline(args, b, n_pairs, n_in, precision, feat_ms, pred_ms, peaks, prof, tot_ms)
+    roof = roofline(args, b, n_pairs, n_in, precision, kst, peaks, prof, tot_ms)
 
     line = {
         "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -318,8 +322,9 @@ def run_gpu(args, rank, world, local_rank):
         "stage_ms": {"featurize": feat_ms, "predict": pred_ms,
                      "allgather": float((t_step - t_feat - t_pred).mean())},
         "roofline": roof,
+        "kernels": {k: {"launches": n, "avg_ms": t / max(n, 1)} for k, (n, t) in sorted(kst.items())},
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": int(sum(n for n, _ in kst.values())),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -375,16 +380,21 @@ def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling,
                    "sp_predict -> D2H latencies)"}
 
 
-def roofline(args, b, n_pairs, n_in, precision, feat_ms, pred_ms, peaks, prof, tot_ms):
-    """Roofline object for the dominant kernel of the step."""
+def roofline(args, b, n_pairs, n_in, precision, kst, peaks, prof, tot_ms):
+    """Roofline object for the dominant kernel of the step: the kernel with
+    the largest device time in the timed region (per-kernel CUDA events, sp_set_profiling);
+    achieved = its algorithmic work per launch / its measured average launch time."""
     hbm = peaks.get("hbm_gbs")
     long_region = tot_ms > 1000.0
     bf16_peak = peaks.get("bf16_tflops_sustained" if long_region else "bf16_tflops")
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    if pred_ms >= feat_ms:
-        kernel = f"predict_tcgen05_{precision}" if precision != "fp32" else "predict_simt_fp32"
-        flop = MLP_FLOP_PER_PAIR[n_in] * n_pairs
-        achieved = flop / (pred_ms * 1e-3) / 1e12
+    kernel, (launches, total) = max(kst.items(), key=lambda kv: kv[1][1])
+    ms = total / max(launches, 1)
+    per_launch_pairs = n_pairs  # one launch covers the step's pairs (featurize / predict)
+    wp = prof.get(args.workload, {}) or {}
+    if kernel.startswith("predict"):
+        flop = MLP_FLOP_PER_PAIR[n_in] * per_launch_pairs
+        achieved = flop / (ms * 1e-3) / 1e12
         if precision != "fp32":  # fp16 and bf16 share the dense tensor rate (guide: ratio 1)
             peak, bound, src = bf16_peak, "tensor", ("MEASURED_PEAKS.json " +
                                                      ("bf16_tflops_sustained" if long_region else "bf16_tflops"))
@@ -392,28 +402,27 @@ def roofline(args, b, n_pairs, n_in, precision, feat_ms, pred_ms, peaks, prof, t
             # fp32 FFMA peak from unit counts: 148 SMs x 128 lanes x 2 FLOP x max SM clock
             peak, bound, src = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "alu", \
                 "148 SMs x 128 FP32 lanes x 2 FLOP x sm_max_mhz (DESIGN.md §6)"
-        unit, ms, per_unit = "TFLOP/s", pred_ms, f"{MLP_FLOP_PER_PAIR[n_in]} FLOP/pair"
-    else:
-        if b.family == gen.ATTENTION:
-            kernel = "featurize_attention_cross"
-            # issue-rate roofline: warp instructions per launch from the committed ncu capture
-            instr = (prof.get(args.workload, {}) or {}).get("featurize_inst_executed")
-            achieved = None if instr is None else instr / (feat_ms * 1e-3) / 1e9
-            peak = 4 * 148 * sm_mhz * 1e6 / 1e9
-            bound, unit, src = "alu", "Ginstr/s", "4 warp-instr/clk/SM x 148 x sm_max_mhz (DESIGN.md §6)"
-            per_unit = "warp instructions per launch (ncu sm__inst_executed.sum)"
-        else:
-            kernel = "featurize_uniform_cross"
-            nbytes = n_pairs * RECORD_BYTES + b.fields.nbytes + \
-                (b.ragged.nbytes if b.ragged is not None else 0)
-            achieved = nbytes / (feat_ms * 1e-3) / 1e9
-            peak, bound, unit, src = hbm, "hbm", "GB/s", "MEASURED_PEAKS.json hbm_gbs"
-            per_unit = f"{RECORD_BYTES} B/pair written + config bytes read"
-        ms = feat_ms
-    traffic = (prof.get(args.workload, {}) or {}).get(kernel + "_dram_bytes")
+        unit, per_unit = "TFLOP/s", f"{MLP_FLOP_PER_PAIR[n_in]} FLOP/pair x {per_launch_pairs} pairs"
+        traffic = wp.get(f"predict_tcgen05_{precision}_dram_bytes")
+    elif kernel == "attn_schedule_cross":
+        # integer-issue roofline: warp instructions per launch (ncu capture of this workload)
+        instr = wp.get("attn_schedule_cross_inst_executed")
+        achieved = None if instr is None else instr / (ms * 1e-3) / 1e9
+        peak = 4 * 148 * sm_mhz * 1e6 / 1e9
+        bound, unit, src = "alu", "Ginstr/s", "4 warp-instr/clk/SM x 148 x sm_max_mhz (DESIGN.md §6)"
+        per_unit = "warp instructions per launch (ncu smsp__inst_executed.sum, profiles/ncu_traffic.json)"
+        traffic = wp.get("attn_schedule_cross_dram_bytes")
+    else:  # record-writing kernels: HBM
+        nbytes = n_pairs * RECORD_BYTES + b.fields.nbytes + \
+            (b.ragged.nbytes if b.ragged is not None else 0)
+        achieved = nbytes / (ms * 1e-3) / 1e9
+        peak, bound, unit, src = hbm, "hbm", "GB/s", "MEASURED_PEAKS.json hbm_gbs"
+        per_unit = f"{RECORD_BYTES} B/pair written + config bytes read"
+        traffic = wp.get(f"{kernel}_dram_bytes")
     return {"kernel": kernel, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": (achieved / peak) if (achieved is not None and peak) else None,
-            "traffic": traffic, "avg_launch_ms": ms, "per_unit": per_unit, "peak_source": src}
+            "traffic": traffic, "avg_launch_ms": ms, "launches": launches, "per_unit": per_unit,
+            "peak_source": src}
 
 
 def main():

@@ -296,6 +296,27 @@ sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *
 sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_features *in, float *latency_us,
                      float *efficiency, void *stream);
 
+/*
+ * Kernel accounting, for measurement (bench.py's roofline and launch count,
+ * DESIGN.md section 6).  Every kernel launched by sp_featurize / sp_predict is
+ * counted per kernel name.  With profiling enabled (off by default) each such
+ * launch is also bracketed by two CUDA events recorded on the caller's stream,
+ * so the per-kernel device time is measured in place, inside the caller's
+ * timed region.  sp_profile_read waits for the pending events, writes up to
+ * `max` entries (kernel name: static library-owned string; launches; summed
+ * device milliseconds, 0 for launches made while profiling was off) and
+ * returns the number of kernels seen; reset != 0 clears the totals.  Returns
+ * -1 on a NULL context or a CUDA error (message in sp_last_error).
+ */
+typedef struct sp_kernel_stat {
+  const char *kernel;
+  int64_t launches;
+  double total_ms;
+} sp_kernel_stat;
+
+sp_status sp_set_profiling(sp_ctx *ctx, int32_t enable);
+int32_t sp_profile_read(sp_ctx *ctx, sp_kernel_stat *out, int32_t max, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,10 @@ class sp_features(C.Structure):
     ]
 
 
+class sp_kernel_stat(C.Structure):
+    _fields_ = [("kernel", C.c_char_p), ("launches", C.c_int64), ("total_ms", C.c_double)]
+
+
 MLP_ARRAYS = ["mu", "sigma", "w1", "b1", "g1", "be1", "m1", "v1", "w2", "b2", "g2", "be2", "m2",
               "v2", "w3", "b3", "g3", "be3", "m3", "v3", "w4"]
 
@@ -93,6 +97,8 @@ def _load():
         "sp_free_model": (None, [vp]),
         "sp_featurize": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "sp_predict": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+        "sp_set_profiling": (C.c_int, [vp, i32]),
+        "sp_profile_read": (i32, [vp, C.POINTER(sp_kernel_stat), i32, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -105,4 +111,4 @@ lib = _load()
 
 EXPORTED = ["sp_create", "sp_destroy", "sp_last_error", "sp_version", "sp_device_sms",
             "sp_load_gpu_specs", "sp_free_specs", "sp_specs_count", "sp_load_model",
-            "sp_free_model", "sp_featurize", "sp_predict"]
+            "sp_free_model", "sp_featurize", "sp_predict", "sp_set_profiling", "sp_profile_read"]

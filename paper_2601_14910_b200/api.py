@@ -187,6 +187,19 @@ class Context:
         if st != _abi.SP_OK:
             raise SynPerfError(st, self.last_error())
 
+    # -- kernel accounting (measurement)
+    def set_profiling(self, enable: bool) -> None:
+        """Bracket every kernel launch of this context with CUDA events (sp_set_profiling)."""
+        self._check(lib.sp_set_profiling(self._h, 1 if enable else 0))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        """{kernel: (launches, device ms summed)} since the last reset (sp_profile_read)."""
+        buf = (_abi.sp_kernel_stat * 32)()
+        n = lib.sp_profile_read(self._h, buf, 32, 1 if reset else 0)
+        if n < 0:
+            raise SynPerfError(_abi.SP_E_INTERNAL, self.last_error())
+        return {buf[i].kernel.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(min(n, 32))}
+
     # -- a1
     def load_gpu_specs(self, specs: np.ndarray, strict: bool = False) -> Specs:
         arr = np.ascontiguousarray(specs)

@@ -25,10 +25,66 @@ struct sp_ctx {
   int device = 0;
   int num_sms = 0;
   int *counters = nullptr;  // DEVICE work counters of the attention kernel (kAttnMaxGroups)
+  void *attn_res = nullptr;  // DEVICE per-config attention results (AttnResults), grow-only
+  size_t attn_res_bytes = 0;
   std::string err;
+  // kernel accounting (sp_set_profiling / sp_profile_read)
+  struct KStat {
+    int64_t launches = 0;
+    double ms = 0;
+  };
+  struct Pending {
+    const char *kernel;
+    cudaEvent_t a, b;
+  };
+  bool prof = false;
+  std::mutex prof_mu;
+  std::map<std::string, KStat> kstats;
+  std::map<std::string, const char *> knames;  // stable name strings
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  const char *open_kernel = nullptr;
+  cudaEvent_t open_ev = nullptr;
   ~sp_ctx() {
     if (counters) cudaFree(counters);
+    if (attn_res) cudaFree(attn_res);
+    for (auto &p : pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto &kv : knames) free(const_cast<char *>(kv.second));
   }
+  cudaEvent_t event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+  }
+  static void hook_begin(void *self, const char *kernel, void *stream) {
+    sp_ctx *c = static_cast<sp_ctx *>(self);
+    std::lock_guard<std::mutex> lk(c->prof_mu);
+    ++c->kstats[kernel].launches;
+    c->open_kernel = kernel;
+    c->open_ev = nullptr;
+    if (c->prof && (c->open_ev = c->event()) != nullptr)
+      cudaEventRecord(c->open_ev, reinterpret_cast<cudaStream_t>(stream));
+  }
+  static void hook_end(void *self, void *stream) {
+    sp_ctx *c = static_cast<sp_ctx *>(self);
+    std::lock_guard<std::mutex> lk(c->prof_mu);
+    if (!c->open_ev) return;
+    cudaEvent_t b = c->event();
+    if (!b) return;
+    cudaEventRecord(b, reinterpret_cast<cudaStream_t>(stream));
+    c->pending.push_back({c->open_kernel, c->open_ev, b});
+    c->open_ev = nullptr;
+  }
+  LaunchHook hook() { return LaunchHook{&hook_begin, &hook_end, this}; }
 };
 
 namespace {
@@ -84,7 +140,7 @@ constexpr int kAttnMaxDistinct = 8;  // featurize_attention.cu kMaxDistinct
 
 // Device copy of one attention spec-group plan (see featurize_attention.cu).
 struct AttnPlanDev {
-  DevBuf groups, group_specs, spec_dist, distinct_n, distinct_off;
+  DevBuf groups, group_specs, spec_dist, distinct_n, distinct_off, spec_slot;
   std::vector<int32_t> nd;   // host copies for the launcher
   std::vector<uint8_t> small;
   AttnPlan view{};
@@ -288,6 +344,10 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
     }
     groups.push_back(gr);
   }
+  std::vector<int32_t> slot(e - b, -1);  // per spec of the range: its distinct slot
+  for (int g = b; g < e; ++g)
+    for (size_t d = 0; d < dn.size(); ++d)
+      if (dn[d] == sp->host[g].num_sms) slot[g - b] = (int32_t)d;
   std::unique_ptr<AttnPlanDev> pd(new (std::nothrow) AttnPlanDev);
   if (!pd) return fail(ctx, SP_E_INTERNAL, "attention plan: out of host memory");
   cudaError_t err;
@@ -295,13 +355,16 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
       (err = pd->group_specs.alloc_copy(gspecs.data(), gspecs.size() * 4)) != cudaSuccess ||
       (err = pd->spec_dist.alloc_copy(sdist.data(), sdist.size() * 4)) != cudaSuccess ||
       (err = pd->distinct_n.alloc_copy(dn.data(), dn.size() * 4)) != cudaSuccess ||
-      (err = pd->distinct_off.alloc_copy(doff.data(), doff.size() * 4)) != cudaSuccess)
+      (err = pd->distinct_off.alloc_copy(doff.data(), doff.size() * 4)) != cudaSuccess ||
+      (err = pd->spec_slot.alloc_copy(slot.data(), slot.size() * 4)) != cudaSuccess)
     return cuda_fail(ctx, err, "attention plan upload");
   pd->view.groups = (const AttnGroup *)pd->groups.p;
   pd->view.group_specs = (const int32_t *)pd->group_specs.p;
   pd->view.spec_dist = (const int32_t *)pd->spec_dist.p;
   pd->view.distinct_n = (const int32_t *)pd->distinct_n.p;
   pd->view.distinct_off = (const int32_t *)pd->distinct_off.p;
+  pd->view.spec_slot = (const int32_t *)pd->spec_slot.p;
+  pd->view.n_slots = (int32_t)dn.size();
   pd->view.n_groups = (int32_t)groups.size();
   pd->view.words_per_warp = words_max + kAttnScratchWords;  // accumulators + request scratch
   for (const AttnGroup &gr : groups) {
@@ -367,21 +430,50 @@ extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const
         return fail(ctx, SP_E_UNSUPPORTED, "attention featurization: too many distinct SM-count groups");
       AttnPlan run = *plan;
       run.counters = ctx->counters;
-      e = launch_featurize_attention(cv, ds, pairs->spec_begin, specs->n, run, n_pairs, nullptr, nullptr,
-                                     specs->max_sms, fo, ctx->num_sms, stream);
+      // per-config results of the schedule kernel: st (4 B), L, U, and maxS/maxB per slot (8 B each)
+      const int64_t C = cfg->n_configs, ld = (C + 31) & ~(int64_t)31;
+      const size_t need = (size_t)ld * (4 + 8 + 8 + 16 * (size_t)run.n_slots);
+      if (need > ctx->attn_res_bytes) {
+        if (ctx->attn_res) cudaFree(ctx->attn_res);
+        ctx->attn_res = nullptr;
+        ctx->attn_res_bytes = 0;
+        cudaError_t me = cudaMalloc(&ctx->attn_res, need);
+        if (me != cudaSuccess) {
+          ctx->attn_res = nullptr;
+          return cuda_fail(ctx, me, "sp_featurize: attention result scratch");
+        }
+        ctx->attn_res_bytes = need;
+      }
+      char *base = (char *)ctx->attn_res;
+      AttnResults res;
+      res.ld = ld;
+      res.L = (int64_t *)base;
+      res.U = (uint64_t *)(base + 8 * ld);
+      res.mS = (int64_t *)(base + 16 * ld);
+      res.mB = res.mS + (size_t)run.n_slots * ld;
+      res.st = (int32_t *)(res.mB + (size_t)run.n_slots * ld);
+      e = launch_featurize_attention(cv, ds, pairs->spec_begin, pairs->spec_end, specs->n, run, res, n_pairs,
+                                     nullptr, nullptr, specs->max_sms, fo, ctx->num_sms, stream, ctx->hook());
     } else {
       if (specs->max_sms > kAttnMaxSms)
         return fail(ctx, SP_E_UNSUPPORTED, "attention featurization supports at most 4096 SMs per spec");
       AttnPlan none{};
-      e = launch_featurize_attention(cv, ds, 0, specs->n, none, n_pairs, pairs->cfg_idx, pairs->spec_idx,
-                                     specs->max_sms, fo, ctx->num_sms, stream);
+      AttnResults nores{};
+      e = launch_featurize_attention(cv, ds, 0, specs->n, specs->n, none, nores, n_pairs, pairs->cfg_idx,
+                                     pairs->spec_idx, specs->max_sms, fo, ctx->num_sms, stream, ctx->hook());
     }
   } else if (pairs->kind == SP_PAIRS_CROSS) {
+    const LaunchHook h = ctx->hook();
+    h.on_begin("featurize_uniform_cross", stream);
     e = launch_featurize_uniform(fam, cv, ds, pairs->spec_begin, pairs->spec_end, n_pairs, nullptr, nullptr,
                                  fo, stream);
+    h.on_end(stream);
   } else {
+    const LaunchHook h = ctx->hook();
+    h.on_begin("featurize_uniform_list", stream);
     e = launch_featurize_uniform(fam, cv, ds, 0, specs->n, n_pairs, pairs->cfg_idx, pairs->spec_idx, fo,
                                  stream);
+    h.on_end(stream);
   }
   if (e) return cuda_fail(ctx, e, "sp_featurize: launch");
   return SP_OK;
@@ -517,10 +609,58 @@ extern "C" sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_fea
   ctx->err.clear();
   cudaSetDevice(ctx->device);
   int e;
-  if (model->precision == SP_MLP_BF16 || model->precision == SP_MLP_FP16)
+  const LaunchHook h = ctx->hook();
+  if (model->precision == SP_MLP_BF16 || model->precision == SP_MLP_FP16) {
+    h.on_begin("predict_tcgen05", stream);
     e = launch_predict_tcgen05(model->m16, *in, latency_us, efficiency, ctx->num_sms, stream);
-  else
+  } else {
+    h.on_begin("predict_simt", stream);
     e = launch_predict_simt(model->m32, *in, latency_us, efficiency, ctx->num_sms, stream);
+  }
+  h.on_end(stream);
   if (e) return cuda_fail(ctx, e, "sp_predict: launch");
   return SP_OK;
+}
+
+// ------------------------------------------------------------- accounting
+
+extern "C" sp_status sp_set_profiling(sp_ctx *ctx, int32_t enable) {
+  if (!ctx) return fail(nullptr, SP_E_ARG, "sp_set_profiling: ctx is NULL");
+  std::lock_guard<std::mutex> lk(ctx->prof_mu);
+  ctx->prof = enable != 0;
+  return SP_OK;
+}
+
+extern "C" int32_t sp_profile_read(sp_ctx *ctx, sp_kernel_stat *out, int32_t max, int32_t reset) {
+  if (!ctx) {
+    fail(nullptr, SP_E_ARG, "sp_profile_read: ctx is NULL");
+    return -1;
+  }
+  std::lock_guard<std::mutex> lk(ctx->prof_mu);
+  cudaSetDevice(ctx->device);
+  int32_t rc = 0;
+  for (auto &p : ctx->pending) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(p.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, p.a, p.b);
+    if (e != cudaSuccess) {
+      cuda_fail(ctx, e, "sp_profile_read");
+      rc = -1;
+    } else {
+      ctx->kstats[p.kernel].ms += ms;
+    }
+    ctx->ev_pool.push_back(p.a);
+    ctx->ev_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+  if (rc < 0) return rc;
+  int32_t n = 0;
+  for (auto &kv : ctx->kstats) {
+    auto it = ctx->knames.find(kv.first);
+    if (it == ctx->knames.end()) it = ctx->knames.emplace(kv.first, strdup(kv.first.c_str())).first;
+    if (out && n < max) out[n] = sp_kernel_stat{it->second, kv.second.launches, kv.second.ms};
+    ++n;
+  }
+  if (reset) ctx->kstats.clear();
+  return n;
 }

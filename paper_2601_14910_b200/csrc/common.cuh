@@ -31,6 +31,8 @@ struct FastDiv {
     return (uint32_t)(t >> s);
   }
   __device__ __forceinline__ uint32_t mod(uint32_t n) const { return n - div(n) * d; }
+  // n < 2^31: the sum umulhi(n, m) + n < 2n stays in 32 bits
+  __device__ __forceinline__ uint32_t div31(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
 };
 
 // Footprint of one task (O2 inputs) and the per-pair accumulated demands.

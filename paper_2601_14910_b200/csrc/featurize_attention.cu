@@ -29,7 +29,7 @@ namespace sp {
 namespace {
 
 #ifndef SP_ATTN_MINB
-#define SP_ATTN_MINB 3
+#define SP_ATTN_MINB 4  // 32 warps/SM (64 regs): measured best of 3..6 on cfg2
 #endif
 
 constexpr int kWarps = 8;           // warps per block
@@ -254,6 +254,9 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
     return warp_sum_u64(us);
   }
   const FastDiv fbq = make_fd((uint32_t)a.bq);
+  // causal without split-KV and g | BQ: kv_need is affine in the q-block index
+  const uint32_t a_per = (uint32_t)(a.bq / a.g);
+  const bool lin = !split && a.causal && a.bq % a.g == 0 && (int64_t)a.bq * 33 < (1ll << 30);
   const FastDiv fchunk = split ? make_fd((uint32_t)a.chunk) : FastDiv{1u, 1u, 0u};
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);  // shared-window byte address
   const uint32_t lm_le = lanemask_le();
@@ -348,6 +351,17 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       const uint32_t nxt = bcur + 1 < nreq ? s_start[bcur + 1] : total;
       if (k0 + 32 <= nxt) {
         const uint32_t r1 = s_a1[bcur], r2 = s_a2[bcur], r3 = s_a3[bcur], ruf = s_uf[bcur], rul = s_ul[bcur];
+        if (lin && r2 < (1u << 30)) {
+          // causal, g | BQ: kv_need(kl) = min(kv, kv - q + (kl+1)*BQ/g) = kv - max(t, 0) with
+          // t = q - (kl+1)*BQ/g stepping by -32*BQ/g (R10-R11; exact for the last q-block too,
+          // where the min takes kv).  q < 2^30 and 33*BQ < 2^30 keep t in int32.
+          int32_t t = (int32_t)r2 - (int32_t)(k0 + lane - st + 1u) * (int32_t)a_per;
+          for (; k0 + 32 <= nxt; k0 += 32) {
+            const uint32_t need = r3 - (uint32_t)max(t, 0);  // >= kv - q + 1 >= 1
+            add(k0 + lane, fbkv.div31(need - 1u) + 1u, true);
+            t -= 32 * (int32_t)a_per;
+          }
+        } else
         for (; k0 + 32 <= nxt; k0 += 32) {
           const uint32_t k = k0 + lane;
           add(k, unit(k - st, r1, r2, r3, ruf, rul), true);
@@ -488,11 +502,11 @@ __device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const A
 }
 
 // Whole per-config pipeline for one distinct set; per-distinct maxima go to
-// mS[d], mB[d] (the warp's shared-memory stash, written by lane 0).
+// mS[d * ms], mB[d * ms] (written by lane 0).
 template <int ND, bool SMALL>
 __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, uint32_t *scr, const int32_t (&N)[ND],
                            const int32_t (&off)[ND], const FastDiv *fdN, int32_t minN, int lane, int64_t &L,
-                           uint64_t &U, int64_t *mS, int64_t *mB) {
+                           uint64_t &U, int64_t *mS, int64_t *mB, int64_t ms) {
   const FastDiv fg = make_fd((uint32_t)a.g);
   L = count_tasks(a, lane, fg);
   if (L > kI32Max || L * a.nkv > kI32Max) return SP_PAIR_E_RANGE;
@@ -503,8 +517,8 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, uint32_t 
     if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
     if (lane == 0)
       for (int d = 0; d < ND; ++d) {
-        mS[d] = (int64_t)umax;
-        mB[d] = (int64_t)a.bq + 2 * (int64_t)a.bkv * umax;
+        mS[d * ms] = (int64_t)umax;
+        mB[d * ms] = (int64_t)a.bq + 2 * (int64_t)a.bkv * umax;
       }
     __syncwarp();
     return 0;
@@ -519,8 +533,8 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, uint32_t 
     const DistinctMax m = s32 ? fold<uint32_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane)
                               : fold<uint64_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
     if (lane == 0) {
-      mS[d] = m.maxS;
-      mB[d] = m.maxB;
+      mS[d * ms] = m.maxS;
+      mB[d * ms] = m.maxB;
     }
   }
   __syncwarp();
@@ -544,20 +558,20 @@ __device__ __forceinline__ AttnCfg load_cfg_lane(const ConfigView &v, int64_t c)
 }
 
 // Per-warp shared-memory region: [stash of 32 configs | request scratch | accumulators].
-constexpr int kStashWords = 32 + 64 + 64 + 32 * kMaxDistinct * 2 * 2;  // status, L, U, maxS[8], maxB[8]
-static_assert(kStashWords + 224 == kAttnScratchWords, "api.cu sizes the warp region with kAttnScratchWords");
 // fold()'s duplicate of the last region (N <= kFoldDupMax, reads to 2N + 31) must fit in the request scratch
-static_assert(224 >= kFoldDupMax + 32, "fold duplicate overruns the warp region");
+static_assert(kAttnScratchWords >= kFoldDupMax + 32, "fold duplicate overruns the warp region");
 
 // CROSS mode.  Warps take chunks of 32 consecutive configs from a per-group
-// work counter (dynamic: per-config cost is heavy-tailed), run every config of
-// the chunk, stash its per-distinct results, then write the chunk's records
-// with lane j owning config c0 + j, so each SoA row store of a spec is 32
-// consecutive elements (full sectors, no partial-write read-modify-write).
+// Schedule kernel (cross mode): warps pull chunks of 32 configs; per config
+// the head-0 task stream is accumulated once per distinct SM count of the
+// launch group and folded into per-distinct maxima, written to the context's
+// result scratch (res.mS/mB[slot][c], res.st/L/U[c]).  The records are written
+// by attn_emit_cross: keeping the emit code (128-bit range checks, fp64
+// cycle conversions) out of this kernel keeps its hot code inside the
+// instruction cache (ncu: stalled_no_instructions was its top stall).
 template <int ND, bool SMALL>
-__global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) featurize_attention_cross(ConfigView cfg,
-                                                                            const DevSpec *__restrict__ specs,
-                                                                            int g0, AttnPlan plan, FeatOut out) {
+__global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) attn_schedule_cross(ConfigView cfg, AttnPlan plan,
+                                                                             AttnResults res) {
   extern __shared__ uint32_t smem[];
   __shared__ FastDiv s_fd[kMaxDistinct];
   const AttnGroup grp = plan.groups[blockIdx.y];
@@ -574,18 +588,13 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) featurize_attention
   if (threadIdx.x < ND) s_fd[threadIdx.x] = make_fd((uint32_t)N[threadIdx.x]);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t *region = smem + (size_t)warp * plan.words_per_warp;
-  uint32_t *s_st = region;
-  int64_t *s_L = reinterpret_cast<int64_t *>(region + 32);
-  uint64_t *s_U = reinterpret_cast<uint64_t *>(region + 96);
-  int64_t *s_mS = reinterpret_cast<int64_t *>(region + 160);
-  int64_t *s_mB = s_mS + 32 * kMaxDistinct;
-  // warp region: [stash][accumulators: words_per_warp - kAttnScratchWords][request scratch]
-  uint32_t *acc = region + kStashWords;
+  // warp region: [accumulators: words_per_warp - kAttnScratchWords][request scratch]
+  uint32_t *acc = smem + (size_t)warp * plan.words_per_warp;
   uint32_t *scr = acc + (plan.words_per_warp - kAttnScratchWords);
   const int64_t C = cfg.n_configs;
   const int64_t n_chunks = (C + 31) / 32;
   int *counter = plan.counters + blockIdx.y;
+  int64_t *mS = res.mS + (int64_t)grp.distinct_first * res.ld, *mB = res.mB + (int64_t)grp.distinct_first * res.ld;
   for (;;) {
     int64_t chunk = 0;
     if (lane == 0) chunk = atomicAdd(counter, 1);
@@ -594,32 +603,40 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) featurize_attention
     const int64_t c0 = chunk * 32;
     const int nc = (int)min((int64_t)32, C - c0);
     for (int j = 0; j < nc; ++j) {
-      const AttnCfg a = load_cfg(cfg, c0 + j, lane);
+      const int64_t c = c0 + j;
+      const AttnCfg a = load_cfg(cfg, c, lane);
       int st = a.status;
       int64_t L = 0;
       uint64_t U = 0;
       if (st == 0)
-        st = attn_config<ND, SMALL>(a, acc, words, scr, N, off, s_fd, minN, lane, L, U, s_mS + j * kMaxDistinct,
-                                    s_mB + j * kMaxDistinct);
-      if (lane == 0) {
-        s_st[j] = (uint32_t)st;
-        s_L[j] = L;
-        s_U[j] = U;
+        st = attn_config<ND, SMALL>(a, acc, words, scr, N, off, s_fd, minN, lane, L, U, mS + c, mB + c, res.ld);
+      // the per-config fields do not depend on the group: group 0 writes them
+      if (lane == 0 && blockIdx.y == 0) {
+        res.st[c] = st;
+        res.L[c] = L;
+        res.U[c] = U;
       }
     }
-    __syncwarp();
-    if (lane < nc) {
-      const int64_t c = c0 + lane;
-      const AttnCfg al = load_cfg_lane(cfg, c);
-      const int st = (int)s_st[lane];
-      for (int j = 0; j < grp.n_specs; ++j) {
-        const int g = __ldg(plan.group_specs + grp.spec_first + j);
-        const int dsel = __ldg(plan.spec_dist + grp.spec_first + j) - grp.distinct_first;
-        const DistinctMax m{s_mS[lane * kMaxDistinct + dsel], s_mB[lane * kMaxDistinct + dsel]};
-        attn_emit(out, (int64_t)(g - g0) * C + c, al, st, s_L[lane], s_U[lane], m, specs[g]);
-      }
-    }
-    __syncwarp();
+  }
+}
+
+// Emit kernel (cross mode): thread per config, specs of the range in turn;
+// consecutive threads write consecutive records of one spec (full sectors).
+__global__ void __launch_bounds__(256) attn_emit_cross(ConfigView cfg, const DevSpec *__restrict__ specs, int g0,
+                                                       int n_specs, const int32_t *__restrict__ spec_slot,
+                                                       AttnResults res, FeatOut out) {
+  const int64_t C = cfg.n_configs;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int st = __ldg(res.st + c);
+  const AttnCfg al = st ? AttnCfg{} : load_cfg_lane(cfg, c);
+  const int64_t L = __ldg(res.L + c);
+  const uint64_t U = __ldg(res.U + c);
+  for (int j = 0; j < n_specs; ++j) {
+    const int64_t slot = __ldg(spec_slot + j);
+    DistinctMax m{0, 0};
+    if (!st) m = DistinctMax{__ldg(res.mS + slot * res.ld + c), __ldg(res.mB + slot * res.ld + c)};
+    attn_emit(out, (int64_t)j * C + c, al, st, L, U, m, specs[g0 + j]);
   }
 }
 
@@ -635,7 +652,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
   __shared__ int64_t s_m[kWarps][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *region = smem + (size_t)warp * words_per_warp;
-  uint32_t *acc = region + kStashWords, *scr = acc + (words_per_warp - kAttnScratchWords);
+  uint32_t *acc = region, *scr = acc + (words_per_warp - kAttnScratchWords);
   for (int64_t p = (int64_t)blockIdx.x * kWarps + warp; p < n_pairs; p += (int64_t)gridDim.x * kWarps) {
     const int64_t c = __ldg(cfg_idx + p);
     const int32_t g = __ldg(spec_idx + p);
@@ -654,10 +671,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
     if (st == 0) {
       if (N[0] >= 32)
         st = attn_config<1, false>(a, acc, words, scr, N, off, s_fd + warp, N[0], lane, L, U, &s_m[warp][0],
-                                   &s_m[warp][1]);
+                                   &s_m[warp][1], 1);
       else
         st = attn_config<1, true>(a, acc, words, scr, N, off, s_fd + warp, N[0], lane, L, U, &s_m[warp][0],
-                                  &s_m[warp][1]);
+                                  &s_m[warp][1], 1);
     }
     if (lane == 0) attn_emit(out, p, a, st, L, U, DistinctMax{s_m[warp][0], s_m[warp][1]}, specs[g]);
     __syncwarp();
@@ -665,16 +682,16 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
 }
 
 template <int ND, bool SMALL>
-int launch_cross(const ConfigView &cfg, const DevSpec *specs, int g0, const AttnPlan &plan, const FeatOut &out,
-                 int num_device_sms, cudaStream_t st, int group_y0, int n_groups) {
+int launch_cross(const ConfigView &cfg, const AttnPlan &plan, const AttnResults &res, int num_device_sms,
+                 cudaStream_t st, int group_y0, int n_groups, const LaunchHook &hook) {
   const size_t smem = (size_t)kWarps * plan.words_per_warp * 4;
-  cudaError_t e = cudaFuncSetAttribute(featurize_attention_cross<ND, SMALL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(attn_schedule_cross<ND, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return (int)e;
   // chunks of 32 configs are handed out dynamically: launch about as many
   // warps as can be resident, never more than there are chunks
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, featurize_attention_cross<ND, SMALL>, kWarps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_schedule_cross<ND, SMALL>, kWarps * 32, smem);
   if (e != cudaSuccess) return (int)e;
   const int64_t chunks = (cfg.n_configs + 31) / 32;
   int64_t want = (chunks + kWarps - 1) / kWarps;
@@ -683,31 +700,33 @@ int launch_cross(const ConfigView &cfg, const DevSpec *specs, int g0, const Attn
   sub.groups = plan.groups + group_y0;
   sub.counters = plan.counters + group_y0;
   dim3 grid((unsigned)(want < cap ? want : cap), (unsigned)n_groups);
-  featurize_attention_cross<ND, SMALL><<<grid, kWarps * 32, smem, st>>>(cfg, specs, g0, sub, out);
+  hook.on_begin("attn_schedule_cross", st);
+  attn_schedule_cross<ND, SMALL><<<grid, kWarps * 32, smem, st>>>(cfg, sub, res);
+  hook.on_end(st);
   return (int)cudaGetLastError();
 }
 
 template <bool SMALL>
-int launch_nd(int nd, const ConfigView &cfg, const DevSpec *specs, int g0, const AttnPlan &plan,
-              const FeatOut &out, int sms, cudaStream_t st, int y0, int ny) {
+int launch_nd(int nd, const ConfigView &cfg, const AttnPlan &plan, const AttnResults &res, int sms,
+              cudaStream_t st, int y0, int ny, const LaunchHook &hook) {
   switch (nd) {
-    case 1: return launch_cross<1, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
-    case 2: return launch_cross<2, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
-    case 3: return launch_cross<3, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
-    case 4: return launch_cross<4, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
-    case 5: return launch_cross<5, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
-    case 6: return launch_cross<6, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
-    case 7: return launch_cross<7, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
-    default: return launch_cross<8, SMALL>(cfg, specs, g0, plan, out, sms, st, y0, ny);
+    case 1: return launch_cross<1, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
+    case 2: return launch_cross<2, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
+    case 3: return launch_cross<3, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
+    case 4: return launch_cross<4, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
+    case 5: return launch_cross<5, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
+    case 6: return launch_cross<6, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
+    case 7: return launch_cross<7, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
+    default: return launch_cross<8, SMALL>(cfg, plan, res, sms, st, y0, ny, hook);
   }
 }
 
 }  // namespace
 
-int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
-                               const AttnPlan &plan, int64_t n_pairs, const int64_t *cfg_idx,
-                               const int32_t *spec_idx, int32_t max_sms, const FeatOut &out,
-                               int num_device_sms, void *stream) {
+int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
+                               int n_specs, const AttnPlan &plan, const AttnResults &res, int64_t n_pairs,
+                               const int64_t *cfg_idx, const int32_t *spec_idx, int32_t max_sms,
+                               const FeatOut &out, int num_device_sms, void *stream, const LaunchHook &hook) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (cfg_idx == nullptr) {
     if (cfg.n_configs == 0 || plan.n_groups == 0) return 0;
@@ -719,23 +738,30 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
       const bool small = plan.host_small[y];
       int y1 = y + 1;
       while (y1 < plan.n_groups && plan.host_nd[y1] == nd && plan.host_small[y1] == small) ++y1;
-      int e = small ? launch_nd<true>(nd, cfg, specs, spec_begin, plan, out, num_device_sms, st, y, y1 - y)
-                    : launch_nd<false>(nd, cfg, specs, spec_begin, plan, out, num_device_sms, st, y, y1 - y);
+      int e = small ? launch_nd<true>(nd, cfg, plan, res, num_device_sms, st, y, y1 - y, hook)
+                    : launch_nd<false>(nd, cfg, plan, res, num_device_sms, st, y, y1 - y, hook);
       if (e) return e;
       y = y1;
     }
-    return 0;
+    const unsigned blocks = (unsigned)((cfg.n_configs + 255) / 256);
+    hook.on_begin("attn_emit_cross", st);
+    attn_emit_cross<<<blocks, 256, 0, st>>>(cfg, specs, spec_begin, spec_end - spec_begin, plan.spec_slot, res,
+                                            out);
+    hook.on_end(st);
+    return (int)cudaGetLastError();
   }
   if (n_pairs == 0) return 0;
-  const int words = ((max_sms + 3) & ~3) + kAttnScratchWords;  // stash + request scratch + accumulators
+  const int words = ((max_sms + 3) & ~3) + kAttnScratchWords;  // accumulators + request scratch
   const size_t smem = (size_t)kWarps * words * 4;
   cudaError_t e = cudaFuncSetAttribute(featurize_attention_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return (int)e;
   int64_t want = (n_pairs + kWarps - 1) / kWarps;
   int64_t cap = (int64_t)num_device_sms * 8;
+  hook.on_begin("featurize_attention_list", st);
   featurize_attention_list<<<(unsigned)(want < cap ? want : cap), kWarps * 32, smem, st>>>(
       cfg, specs, n_specs, words, n_pairs, cfg_idx, spec_idx, out);
+  hook.on_end(st);
   return (int)cudaGetLastError();
 }
 

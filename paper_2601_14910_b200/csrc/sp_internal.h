@@ -77,9 +77,8 @@ struct AttnGroup {
   int32_t distinct_first;  // index into distinct_n / distinct_off
   int32_t n_distinct;
 };
-// per-warp shared memory before the accumulators: the stash of 32 configs'
-// results (32 + 64 + 64 + 32*8*4 words) and the request scratch (7 x 32 words)
-constexpr int kAttnScratchWords = 1184 + 224;
+// per-warp shared memory after the accumulators: the request scratch (7 x 32 words)
+constexpr int kAttnScratchWords = 224;
 constexpr int kAttnMaxGroups = 4096;  // work counters per launch (sp_ctx scratch)
 struct AttnPlan {
   const AttnGroup *groups;     // DEVICE [n_groups]
@@ -92,11 +91,31 @@ struct AttnPlan {
   const int32_t *host_nd;      // HOST [n_groups]: distinct count per group (kernel template)
   const uint8_t *host_small;   // HOST [n_groups]: group holds an SM count < 32 (atomic path)
   int *counters;               // DEVICE [n_groups] work counters (context scratch, zeroed per launch)
+  const int32_t *spec_slot;    // DEVICE, per spec of the range: its distinct slot (absolute)
+  int32_t n_slots;             // distinct slots over all groups
 };
-int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin,
-                               int n_specs, const AttnPlan &plan, int64_t n_pairs, const int64_t *cfg_idx,
-                               const int32_t *spec_idx, int32_t max_sms, const FeatOut &out,
-                               int num_device_sms, void *stream);
+// Per-config results of the schedule kernel (context scratch, cross mode):
+// st/L/U [C], mS/mB [n_slots][ld].
+struct AttnResults {
+  int32_t *st;
+  int64_t *L;
+  uint64_t *U;
+  int64_t *mS, *mB;
+  int64_t ld;
+};
+// Optional per-launch hook (kernel accounting, sp_set_profiling): begin/end
+// bracket one kernel launch on the launch stream.
+struct LaunchHook {
+  void (*begin)(void *self, const char *kernel, void *stream);
+  void (*end)(void *self, void *stream);
+  void *self;
+  void on_begin(const char *k, void *st) const { if (begin) begin(self, k, st); }
+  void on_end(void *st) const { if (end) end(self, st); }
+};
+int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
+                               int n_specs, const AttnPlan &plan, const AttnResults &res, int64_t n_pairs,
+                               const int64_t *cfg_idx, const int32_t *spec_idx, int32_t max_sms,
+                               const FeatOut &out, int num_device_sms, void *stream, const LaunchHook &hook);
 
 // MLP predictor.
 struct MlpFp32 {        // DEVICE pointers, fp32

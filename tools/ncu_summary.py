@@ -98,14 +98,17 @@ def main():
             if k in m:
                 lines.append(f"| {k} | {m[k]:.6g} |")
         dram = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
-        name = "featurize_attention_cross" if "attention" in m.get("kernel", "") else (
-            "featurize_uniform_cross" if "uniform" in m.get("kernel", "") else None)
+        kn = m.get("kernel", "")
+        name = "attn_schedule_cross" if "attn_schedule" in kn else (
+            "featurize_uniform_cross" if "uniform" in kn else None)
         if tag == "predict":
             for p in ("fp16", "bf16"):
                 tw[f"predict_tcgen05_{p}_dram_bytes"] = dram
         elif name:
             tw[f"{name}_dram_bytes"] = dram
-            tw["featurize_inst_executed"] = m.get("smsp__inst_executed.sum")
+            tw[f"{name}_inst_executed"] = m.get("smsp__inst_executed.sum")
+            tw.pop("featurize_inst_executed", None)
+            tw.pop("featurize_attention_cross_dram_bytes", None)
         tw[f"{tag}_ncu_duration_s"] = m.get("gpu__time_duration.sum")
     tw["source"] = f"profiles/ncu_{r}_{w}.md"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)

@@ -12,7 +12,7 @@ mkdir -p "$OUT"
 BENCH="python bench.py --workload $W --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" $BENCH \
   > "$OUT/launches_bench.log" 2>&1 || true
-FEAT=featurize_attention_cross
+FEAT=attn_schedule_cross
 [ "$W" != "cfg2" ] && FEAT=featurize_uniform_cross
 ncu --set full --clock-control none --import-source on -k regex:$FEAT -s 3 -c 1 -o "$OUT/featurize" $BENCH \
   > "$OUT/featurize.log" 2>&1 || true
