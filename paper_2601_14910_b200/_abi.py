@@ -81,7 +81,7 @@ def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"libsynperf.so not found at {LIB_PATH}; build it with "
-            "`python -m paper_2601_14910_b200.build` (there is no CPU fallback)")
+            "`python paper_2601_14910_b200/build.py` or `python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
     L = C.CDLL(LIB_PATH)
     vp, i32, i64, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
     sig = {

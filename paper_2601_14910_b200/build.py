@@ -1,6 +1,8 @@
 """Build libsynperf.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-    python -m paper_2601_14910_b200.build [--force]
+    python paper_2601_14910_b200/build.py [--force]
+
+(Run by path: importing the package loads the library this script builds.)
 """
 from __future__ import annotations
 

@@ -20,8 +20,9 @@ def declared_functions():
 
 @pytest.fixture(scope="module")
 def libsp():
-    from paper_2601_14910_b200 import build
+    from __graft_entry__ import _build_module
 
+    build = _build_module()
     build.build()
     return C.CDLL(build.LIB)
 
@@ -85,7 +86,8 @@ def test_sass_is_sm100a(libsp):
     cuobj = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
     if not os.path.exists(cuobj):
         pytest.skip("cuobjdump not available")
-    from paper_2601_14910_b200 import build
+    from __graft_entry__ import _build_module
 
+    build = _build_module()
     out = subprocess.run([cuobj, "--list-elf", build.LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in out
