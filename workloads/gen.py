@@ -252,3 +252,76 @@ def shuffle(b: ConfigBatch, seed: int) -> tuple[ConfigBatch, np.ndarray]:
     """Seeded permutation of configs (cost balance before sharding)."""
     perm = np.random.default_rng(seed).permutation(b.n_configs)
     return b.subset(perm), perm
+
+
+# ---- BASELINE config 4: serving request traces (inputs of the E2E composition) ----
+
+# (layers, hidden, heads, kv heads, head dim, intermediate, vocab) -> a dict per model
+def serving_model(name: str, tp: int = 1, pp: int = 1) -> dict:
+    L, h, nh, nkv, hd, inter, vocab = MODEL_CARDS[name]
+    return dict(n_layers=L, hidden=h, n_heads=nh, n_kv_heads=nkv, head_dim=hd,
+                intermediate=inter, vocab=vocab, tp=tp, pp=pp)
+
+
+# §VI-E (P:583): arxiv_* inputs average 2,630 tokens, splitwise_* 982; outputs 5..4,056;
+# static batches named arxiv_8 / splitwise_64 etc. (P:583, Table VIII)
+TRACE_DATASETS = {"arxiv": 2630.0, "splitwise": 982.0}
+TRACE_BATCHES = (8, 12, 16, 48, 64)
+
+
+@dataclass
+class RequestTraces:
+    """R static batches of requests: batch r holds requests
+    [req_off[r], req_off[r+1]) with input / output token counts."""
+    req_off: np.ndarray  # int64 [R+1]
+    input_len: np.ndarray  # int32 [n_requests]
+    output_len: np.ndarray  # int32 [n_requests]
+
+    @property
+    def n_traces(self) -> int:
+        return len(self.req_off) - 1
+
+    def trace(self, r: int):
+        a, b = int(self.req_off[r]), int(self.req_off[r + 1])
+        return self.input_len[a:b], self.output_len[a:b]
+
+    def subset(self, idx) -> "RequestTraces":
+        ins, outs, off = [], [], [0]
+        for r in idx:
+            i, o = self.trace(int(r))
+            ins.append(i)
+            outs.append(o)
+            off.append(off[-1] + len(i))
+        return RequestTraces(np.array(off, np.int64), np.concatenate(ins).astype(np.int32),
+                             np.concatenate(outs).astype(np.int32))
+
+
+def gen_serving_traces(n_traces: int, seed: int, batches=TRACE_BATCHES, out_max: int = 4056,
+                       in_max: int = 20000, sigma: float = 0.6) -> RequestTraces:
+    """BASELINE config 4 traces: trace r is a static batch of size
+    batches[r % len(batches)] drawn from dataset arxiv (even r) or splitwise
+    (odd r).  Input lengths ~ lognormal with the dataset's mean,
+    clipped to [16, in_max]; output lengths ~ logU[5, out_max]."""
+    rng = np.random.default_rng(seed)
+    names = list(TRACE_DATASETS)
+    ins, outs, off = [], [], [0]
+    for r in range(n_traces):
+        bs = int(batches[r % len(batches)])
+        mean = TRACE_DATASETS[names[r % len(names)]]
+        mu = np.log(mean) - sigma * sigma / 2
+        i = np.clip(np.round(rng.lognormal(mu, sigma, bs)), 16, in_max).astype(np.int32)
+        o = _logu_int(rng, 5, out_max, bs).astype(np.int32)
+        ins.append(i)
+        outs.append(o)
+        off.append(off[-1] + bs)
+    return RequestTraces(np.array(off, np.int64), np.concatenate(ins), np.concatenate(outs))
+
+
+def make_traces(batches: list) -> RequestTraces:
+    """Hand-built traces: [[(input_len, output_len), ...] per batch]."""
+    ins, outs, off = [], [], [0]
+    for b in batches:
+        ins += [int(i) for i, _ in b]
+        outs += [int(o) for _, o in b]
+        off.append(off[-1] + len(b))
+    return RequestTraces(np.array(off, np.int64), np.array(ins, np.int32), np.array(outs, np.int32))

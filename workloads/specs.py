@@ -150,3 +150,28 @@ def hypothetical_sweep_specs(n: int | None = None) -> np.ndarray:
     out["bw_global_gbps"] = grid[:, 1]
     out["bw_l2_gbps"] = 2.5 * grid[:, 1]
     return out
+
+
+# ---- communication calibration tables (inputs of the E2E composition) ----
+# The paper profiles All-Reduce / Send-Recv per topology and regresses latency on
+# volume; no profile is published.  These are synthetic alpha-beta tables
+# ("a synthetic alpha-beta generator produces desk-scale tables"):
+# latency = alpha + algorithmic bytes / link GB/s at 2^10 .. 2^30 bytes.
+# Link bandwidths are public interconnect figures (NVLink for the SXM parts,
+# PCIe otherwise): realism "parity unpinned".
+LINK_GBPS = {"A40": 56.0, "A100": 300.0, "RTX 6000 Ada": 25.0, "L20": 25.0, "H20": 450.0,
+             "H800": 200.0, "RTX A6000": 56.0, "L40": 25.0, "H100": 450.0, "H200": 450.0,
+             "RTX PRO 6000 S": 50.0}
+COMM_POINTS = np.array([2.0 ** k for k in range(10, 31)])
+
+
+def synthetic_comm_tables(spec_arr: np.ndarray, tp: int, alpha_us: float = 8.0) -> dict:
+    """{"bytes": [P], "allreduce_us": [G][P], "sendrecv_us": [G][P]} (fp64).
+    Ring all-reduce moves 2(tp-1)/tp of the buffer per GPU; send/recv moves it once."""
+    names = [n.decode() if isinstance(n, bytes) else str(n) for n in spec_arr["name"]]
+    bw = np.array([LINK_GBPS.get(n, 450.0) for n in names]) * 1e3  # bytes per us
+    ar_factor = 2.0 * (tp - 1) / tp if tp > 1 else 0.0
+    b = COMM_POINTS
+    ar = alpha_us + ar_factor * b[None, :] / bw[:, None]
+    sr = 0.5 * alpha_us + b[None, :] / bw[:, None]
+    return {"bytes": b.copy(), "allreduce_us": ar, "sendrecv_us": sr}
