@@ -38,8 +38,12 @@ WORKLOADS = {
     "cfg1": "1,000 GEMM configs x 1 GPU spec (A100, Table VI)",
     "cfg2": "FlashAttention prefill/decode sweep, 1e6 configs x the paper's 11 GPU specs",
     "cfg3": "fused MoE Triton config space, 1e6 configs x 11 GPU specs",
+    "cfg4": "E2E serving iterations: Llama-3-8B + Qwen2.5-14B over 256 static-batch request traces "
+            "(arxiv/splitwise-like), per-kernel predictions composed per step, x 11 GPU specs",
     "cfg5": "1,000 serving GEMMs x 100,000 hypothetical GPU specs (1e8 pairs), sharded by spec",
 }
+E2E_MODELS = ("llama3-8b", "qwen2.5-14b")
+E2E_FAMILIES = (gen.GEMM, gen.ATTENTION, gen.RMSNORM, gen.SILU_MUL)
 
 
 def build_workload(name: str, rank: int, world: int, scale: float = 1.0):
@@ -154,9 +158,39 @@ def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int =
     return n / dt, n, dt, O.num_threads()
 
 
+def oracle_e2e_rate(traces, sa, mlps, target_s: float, seed: int = 0):
+    """Times the literal E2E oracle (oracle/e2e.py) on random serving steps:
+    every invocation of the sampled steps featurised + predicted on every spec
+    and summed.  Returns (step-spec predictions/s, pairs/s, n_steps, secs, threads)."""
+    from oracle import e2e as E
+    from oracle import oracle as O
+
+    O.build()
+    rng = np.random.default_rng(seed)
+    kf = E.kernel_latency_fn(sa, mlps, O)
+    steps = []
+    t0 = time.perf_counter()
+    n_pairs = 0
+    while time.perf_counter() - t0 < target_s or not steps:
+        name = E2E_MODELS[len(steps) % len(E2E_MODELS)]
+        m = E.ServingModel(**gen.serving_model(name))
+        r = int(rng.integers(0, traces.n_traces))
+        ins, outs = traces.trace(r)
+        st = E.steps_of_trace(ins, outs)
+        pf, req = st[int(rng.integers(0, len(st)))]
+        invs = E.forward_pass(m, req, pf)
+        E.predict_e2e([invs], len(sa), kf, None)
+        n_pairs += len(invs) * len(sa)
+        steps.append((name, r))
+    dt = time.perf_counter() - t0
+    return len(steps) * len(sa) / dt, n_pairs / dt, len(steps), dt, O.num_threads()
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if args.workload == "cfg4":
+        return run_reference_e2e(args)
     b, sa, rng_, _ = build_workload(args.workload, 0, 1, args.scale)
     model = models.random_mlp(b.family, 42)
     budget = 150.0 / max(1, args.steps + args.warmup)
@@ -190,6 +224,36 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
                    "pairs_per_step": n_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_e2e(args):
+    traces = gen.gen_serving_traces(256, 1004)
+    sa = specs.paper_gpu_specs()
+    mlps = {f: models.random_mlp(f, 42 + f) for f in E2E_FAMILIES}
+    per_step = min(10.0, 150.0 / max(1, args.steps + args.warmup))
+    times, rates = [], []
+    for s in range(args.warmup + args.steps):
+        sps, pps, n, dt, threads = oracle_e2e_rate(traces, sa, mlps, per_step, seed=100 + s)
+        if s >= args.warmup:
+            times.append(dt)
+            rates.append((sps, pps, n))
+    tot = float(np.sum(times))
+    value = float(np.sum([r[1] * t for r, t in zip(rates, times)]) / tot)
+    steps_ps = float(np.sum([r[0] * t for r, t in zip(rates, times)]) / tot)
+    sample = (f"random serving steps of the cfg4 traces (Llama-3-8B / Qwen2.5-14B), every invocation "
+              f"featurised + predicted literally on 11 specs, ~{per_step:.0f} s per step, fp64")
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg4", "description": WORKLOADS["cfg4"]},
+        "step_predictions_per_s": steps_ps,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -338,6 +402,180 @@ def run_gpu(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_gpu_e2e(args, rank, world, local_rank):
+    """cfg4: one step = for each serving model, re-expand the plan on the GPU
+    (sp_e2e_plan_expand), featurise + predict the four families' batches x 11
+    specs, and compose per-step / per-trace latencies (sp_e2e_compose) [+ the
+    all-gather of per-trace totals when N > 1].  Weak scaling: every rank has
+    its own 256 traces."""
+    import torch
+
+    import paper_2601_14910_b200 as sp
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = sp.Context(local_rank)
+    n_tr = max(1, int(256 * args.scale))
+    traces = gen.gen_serving_traces(n_tr, 1004 + 7919 * rank)
+    sa = specs.paper_gpu_specs()
+    G = len(sa)
+    specs_h = ctx.load_gpu_specs(sa)
+    mlps = {f: models.random_mlp(f, 42 + f) for f in E2E_FAMILIES}
+    mdl = {f: ctx.load_model(mlps[f], args.precision) for f in E2E_FAMILIES}
+    stream = torch.cuda.current_stream()
+    plans = [ctx.e2e_plan(gen.serving_model(n), traces, stream) for n in E2E_MODELS]
+    infos = [p.info() for p in plans]
+    pairs_per_step = sum(G * p["n_configs"][f] for p in infos for f in E2E_FAMILIES)
+    step_preds = sum(G * p["n_steps"] for p in infos)
+    invocations = 0
+    for name, p in zip(E2E_MODELS, plans):
+        L = gen.serving_model(name)["n_layers"]
+        invocations += G * p.info()["n_steps"] * (8 * L + 2)
+    tot_all = torch.empty((len(plans), G, n_tr), dtype=torch.float64, device=dev)
+    gathered = torch.empty(world * tot_all.numel(), dtype=torch.float64, device=dev) if dist else None
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        for i, p in enumerate(plans):
+            p.expand(stream)
+            r = ctx.predict_e2e(p, specs_h, mdl, None, (0, G), step_latencies=True, stream=stream)
+            tot_all[i].copy_(r.trace_us)
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered, tot_all.view(-1))
+        if ev is not None:
+            ev[1].record(stream)
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if torch.isnan(tot_all).any():
+        raise SystemExit("NaN trace latency")
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.profile_read(reset=True)
+    ctx.set_profiling(True)
+    with ClockSampler(local_rank) as clk:
+        for s in range(args.steps):
+            flush.zero_()
+            step(evs[s])
+        torch.cuda.synchronize()
+    ctx.set_profiling(False)
+    kst = ctx.profile_read(reset=True)
+    if dist is not None:
+        dist.barrier()
+    t_step = np.array([e[0].elapsed_time(e[1]) for e in evs])
+    tot_ms = float(t_step.sum())
+    if dist is not None:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = pairs_per_step * world * args.steps / (tot_ms * 1e-3)
+
+    # ---- e2e through the public host API: host traces in, host per-trace latencies out
+    for _ in range(2):
+        for n in E2E_MODELS:
+            ctx.predict_e2e_host(gen.serving_model(n), traces, specs_h, mdl)
+    e_steps = max(1, min(args.steps, args.e2e_steps))
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        for n in E2E_MODELS:
+            ctx.predict_e2e_host(gen.serving_model(n), traces, specs_h, mdl)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    h2d = len(E2E_MODELS) * (traces.req_off.nbytes + traces.input_len.nbytes + traces.output_len.nbytes)
+    d2h = len(E2E_MODELS) * G * n_tr * 8 * (1 + 5)
+    e2e = {"value": pairs_per_step * world * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "steps": e_steps,
+           "api": "Context.predict_e2e_host (host request traces -> H2D -> GPU expansion -> "
+                  "sp_featurize/sp_predict x 4 families -> sp_e2e_compose -> D2H per-trace latencies)"}
+
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json")) or {}
+    roof = roofline_e2e(infos, G, kst, peaks, prof, tot_ms, args)
+    line = {
+        "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": {"bf16": "bf16", "fp16": "f16", "fp32": "f32"}[args.precision],
+        "data": "synthetic (seeded request traces and MLP weights, workloads/)",
+        "config": {
+            "workload": "cfg4", "description": WORKLOADS["cfg4"], "traces_per_gpu": n_tr,
+            "requests_per_gpu": int(traces.req_off[-1]), "models": list(E2E_MODELS), "specs": G,
+            "serving_steps_per_gpu": int(sum(p["n_steps"] for p in infos)),
+            "pairs_per_gpu": pairs_per_step, "mlp_precision": args.precision,
+            "parallelism": f"dp{world}" + ("+allgather" if gathered is not None else ""),
+            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+        },
+        "step_predictions_per_s": step_preds * world * args.steps / (tot_ms * 1e-3),
+        "invocations_per_s": invocations * world * args.steps / (tot_ms * 1e-3),
+        "roofline": roof,
+        "kernels": {k: {"launches": n, "avg_ms": t / max(n, 1)} for k, (n, t) in sorted(kst.items())},
+        "e2e": e2e,
+        "gpu_launches": int(sum(n for n, _ in kst.values())),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sps, pps, n, dt, thr = oracle_e2e_rate(traces, sa, mlps, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": pps, "unit": UNIT, "cores": thr, "kind": "oracle",
+            "step_predictions_per_s": sps,
+            "sample": f"{n} random serving steps, every invocation featurised + predicted literally "
+                      f"on 11 specs (fp64 oracle), {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def roofline_e2e(infos, G, kst, peaks, prof, tot_ms, args):
+    """Dominant kernel of a cfg4 step; its algorithmic work summed over the
+    step's launches (different batch sizes per family) / its summed device time."""
+    kernel, (launches, total) = max(kst.items(), key=lambda kv: kv[1][1])
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    long_region = tot_ms > 1000.0
+    wp = prof.get("cfg4", {}) or {}
+    steps = args.steps
+    if kernel.startswith("predict"):
+        flop = steps * sum(G * p["n_configs"][f] * MLP_FLOP_PER_PAIR[models.N_IN[f]]
+                           for p in infos for f in E2E_FAMILIES)
+        achieved = flop / (total * 1e-3) / 1e12
+        key = "bf16_tflops_sustained" if long_region else "bf16_tflops"
+        peak, bound, unit, src = peaks.get(key), "tensor", "TFLOP/s", f"MEASURED_PEAKS.json {key}"
+        per_unit = "MLP FLOP/pair (87,680 F=11; 89,728 F=15) x pairs of all launches"
+    elif kernel == "attn_schedule_cross":
+        instr = wp.get("attn_schedule_cross_inst_executed")  # per step (ncu, all launches of one step)
+        achieved = None if instr is None else instr * steps / (total * 1e-3) / 1e9
+        peak = 4 * 148 * sm_mhz * 1e6 / 1e9
+        bound, unit, src = "alu", "Ginstr/s", "4 warp-instr/clk/SM x 148 x sm_max_mhz (DESIGN.md §6)"
+        per_unit = "warp instructions per step (ncu smsp__inst_executed.sum summed over the step's launches)"
+    else:
+        nbytes = steps * sum(G * p["n_configs"][f] for p in infos for f in E2E_FAMILIES) * RECORD_BYTES
+        achieved = nbytes / (total * 1e-3) / 1e9
+        peak, bound, unit, src = peaks.get("hbm_gbs"), "hbm", "GB/s", "MEASURED_PEAKS.json hbm_gbs"
+        per_unit = f"{RECORD_BYTES} B/pair written"
+    return {"kernel": kernel, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": (achieved / peak) if (achieved is not None and peak) else None,
+            "traffic": wp.get(f"{kernel}_dram_bytes"), "avg_launch_ms": total / max(launches, 1),
+            "launches": launches, "per_unit": per_unit, "peak_source": src}
+
+
 def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling, n_specs):
     """Same metric through Context.predict_host with pinned host buffers: every
     step copies the configs H2D and the fp32 latencies D2H."""
@@ -445,6 +683,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.workload == "cfg4":
+        run_gpu_e2e(args, rank, world, local_rank)
         return
     run_gpu(args, rank, world, local_rank)
 

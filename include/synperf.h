@@ -317,6 +317,145 @@ typedef struct sp_kernel_stat {
 sp_status sp_set_profiling(sp_ctx *ctx, int32_t enable);
 int32_t sp_profile_read(sp_ctx *ctx, sp_kernel_stat *out, int32_t max, int32_t reset);
 
+/* ===================================================================
+ * End-to-end serving composition (PAPER §V-D; SURVEY §8(f) NEXT-1,
+ * BASELINE config 4).  A Workload Generator turns a model and a batch of
+ * requests into "a sequence of kernel invocations that represents a real
+ * inference scenario"; kernels run "sequentially without overlap" and the
+ * end-to-end latency is "the sum of all predicted kernel durations";
+ * All-Reduce (TP) and Send/Recv (PP) latencies come from a regression over
+ * profiled (volume, latency) points.  Readings E1..E9
+ * fix what the paper leaves open:
+ *   E1 per layer: RMSNorm, QKV GEMM, Attention, O GEMM, [AllReduce], RMSNorm,
+ *      GateUp GEMM, SiLU&Mul, Down GEMM, [AllReduce]; then final RMSNorm and
+ *      LM-head GEMM once per forward pass; pp-1 Send/Recv per forward pass
+ *      (SPEC S:556).
+ *   E2 static batch: step 0 prefills every request (qlen = kvlen = input_len,
+ *      causal); decode step k = 1 .. max(output_len)-1 runs the requests with
+ *      output_len > k in batch order, qlen 1, kvlen = input_len + k.
+ *   E3 token count M = sum of qlen over the step's requests; the LM head runs
+ *      on one row per sequence.
+ *   E4 GEMM tiles by M: <= 64 -> 64x128 (BK 64, 4 stages, 4 warps, 128 regs);
+ *      <= 256 -> 128x128 (4 stages, 8 warps, 168 regs); else 128x256
+ *      (3 stages, 8 warps, 232 regs).
+ *   E5 attention (FA2): heads nh/tp, nkv/tp; prefill BQ 128, BKV 64, causal,
+ *      4 warps, 168 regs; decode BQ 16, BKV 64, non-causal, 4 warps, 64 regs,
+ *      kv_chunk 1024 if n_active*nkv/tp < 128 else unsplit.
+ *   E6 RMSNorm (dim = hidden) and SiLU&Mul (dim = intermediate/tp):
+ *      clamp(ceil(dim/256), 1, 32) warps, 32 regs.
+ *   E7 comm bytes M*hidden*2; latency interpolated linearly in ln(bytes)
+ *      over the spec's calibration points, clamped flat at both ends.
+ *   E8 per trace: sum over its steps; breakdown by category (Table I).
+ *   E9 bf16 everywhere (2 bytes per element).
+ * The expansion runs on the GPU; the resulting config batches go through
+ * sp_featurize / sp_predict like any other; sp_e2e_compose sums them.
+ * =================================================================== */
+
+/* SPEC ModelConfig + ParallelConfig: a dense SwiGLU transformer. */
+typedef struct sp_serving_model {
+  int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, intermediate, vocab;
+  int32_t tp;     /* tensor parallel degree >= 1: heads, kv heads, intermediate, vocab divisible */
+  int32_t pp;     /* pipeline parallel degree >= 1: n_layers divisible */
+  int32_t dtype;  /* SP_BF16 (E9) */
+} sp_serving_model;
+
+/* Breakdown categories of sp_e2e_compose (Table I's kernel classes). */
+enum { SP_E2E_CAT_GEMM = 0, SP_E2E_CAT_ATTENTION = 1, SP_E2E_CAT_RMSNORM = 2,
+       SP_E2E_CAT_SILU_MUL = 3, SP_E2E_CAT_COMM = 4, SP_E2E_NCAT = 5 };
+
+typedef struct sp_e2e_plan sp_e2e_plan;
+
+/* Sizes of an expanded plan.  Config batches (sp_e2e_plan_batch):
+ *   SP_ATTENTION: one config per step, steps of trace r contiguous
+ *                 (n_steps configs, n_ragged int32 (qlen, kvlen) entries);
+ *   SP_GEMM:      4 * n_slots + max_batch configs: kind k in {QKV, O, GateUp,
+ *                 Down} at k*n_slots + slot, LM head at 4*n_slots + (seqs-1);
+ *   SP_RMSNORM, SP_SILU_MUL: n_slots configs.
+ * A slot is a token count: slot j < max_batch holds M = j+1 (decode steps);
+ * slot max_batch + r holds trace r's prefill M = sum of its input lengths. */
+typedef struct sp_e2e_info {
+  int32_t n_traces;
+  int32_t max_batch;   /* largest number of requests in a trace */
+  int64_t n_requests;
+  int64_t n_steps;     /* sum over traces of max(output_len) */
+  int64_t n_ragged;    /* 2 * sum of output_len */
+  int64_t n_slots;     /* max_batch + n_traces */
+  int64_t n_configs[5];  /* per sp_family; 0 for SP_FUSED_MOE */
+} sp_e2e_info;
+
+/*
+ * Builds the invocation plan of R request traces (E1-E9) for `model`.
+ *   req_off:    HOST int64 [n_traces+1], trace r = requests [req_off[r], req_off[r+1])
+ *   input_len, output_len: HOST int32 [req_off[n_traces]]
+ * Copies the requests to the device on `stream` and expands them there (one
+ * warp per step); the plan owns all device memory it needs (allocated here,
+ * reused by later sp_e2e_plan_update calls that fit).  Errors: SP_E_ARG (NULL,
+ * counts, divisibility of heads / kv heads / intermediate / vocab by tp or of
+ * layers by pp, dtype != SP_BF16), SP_E_DATA (a trace without requests, a
+ * length < 1, or a token count >= 2^31), SP_E_INTERNAL (CUDA).
+ * The plan is valid for use on `stream` once the call returns (stream order).
+ */
+sp_status sp_e2e_plan_create(sp_ctx *ctx, const sp_serving_model *model, int32_t n_traces,
+                             const int64_t *req_off, const int32_t *input_len,
+                             const int32_t *output_len, void *stream, sp_e2e_plan **out);
+/* Re-expands new traces into an existing plan (same model), growing its
+ * buffers only if needed.  Same arguments and errors as sp_e2e_plan_create. */
+sp_status sp_e2e_plan_update(sp_e2e_plan *plan, int32_t n_traces, const int64_t *req_off,
+                             const int32_t *input_len, const int32_t *output_len, void *stream);
+/* Re-runs the expansion kernels from the requests already resident in the
+ * plan (no host work, no copy): the device-side step of a timed loop. */
+sp_status sp_e2e_plan_expand(sp_e2e_plan *plan, void *stream);
+void sp_free_e2e_plan(sp_e2e_plan *plan);
+sp_status sp_e2e_plan_info(const sp_e2e_plan *plan, sp_e2e_info *out);
+/* The plan's config batch of one family (DEVICE pointers owned by the plan,
+ * valid until the next update / free).  SP_E_ARG for SP_FUSED_MOE. */
+sp_status sp_e2e_plan_batch(const sp_e2e_plan *plan, int32_t family, sp_config_batch *out);
+
+/* Communication estimator (SPEC CommModel S:545): per spec, one
+ * calibration table per collective at this plan's world size, all on the same
+ * byte grid.  HOST fp64 arrays: bytes [n_points] strictly increasing > 0;
+ * allreduce_us, sendrecv_us [n_specs][n_points] finite, >= 0, non-decreasing
+ * in bytes.  Spec g of the table = spec g of the sp_specs handle used
+ * with it.  SP_E_DATA on a table violating these rules. */
+typedef struct sp_comm_desc {
+  int32_t n_specs;
+  int32_t n_points;   /* 1 .. 64 */
+  const double *bytes;
+  const double *allreduce_us;
+  const double *sendrecv_us;
+} sp_comm_desc;
+typedef struct sp_comm_model sp_comm_model;
+sp_status sp_load_comm_model(sp_ctx *ctx, const sp_comm_desc *desc, sp_comm_model **out);
+void sp_free_comm_model(sp_comm_model *comm);
+
+/* Per-family predicted latencies of the plan's batches (DEVICE fp32), each
+ * spec-major over specs [spec_begin, spec_end) as sp_predict writes them after
+ * sp_featurize with SP_PAIRS_CROSS: lat[(g - spec_begin) * n_configs + c]. */
+typedef struct sp_e2e_latencies {
+  const float *gemm;
+  const float *attention;
+  const float *rmsnorm;
+  const float *silu_mul;
+} sp_e2e_latencies;
+
+/*
+ * Composition (E8): for every spec g of [spec_begin, spec_end) and step
+ * s, the step latency is the sum of its invocations' latencies
+ *   L*(2 rms + qkv + attn + o + gate_up + silu + down + 2 [tp>1] allreduce)
+ *   + (pp-1) sendrecv + rms + lm_head,
+ * and trace r's latency the sum of its steps (fp64).  Outputs (DEVICE,
+ * caller-owned, each may be NULL):
+ *   step_us   fp32 [G][n_steps]
+ *   trace_us  fp64 [G][n_traces]               (total)
+ *   trace_cat fp64 [G][n_traces][SP_E2E_NCAT]  (breakdown; sums to trace_us)
+ * G = spec_end - spec_begin.  comm may be NULL when tp == pp == 1; it must
+ * cover spec_end specs otherwise.  A NaN latency (a pair with status != 0)
+ * propagates.  Asynchronous on `stream`; no allocation.
+ */
+sp_status sp_e2e_compose(sp_ctx *ctx, const sp_e2e_plan *plan, int32_t spec_begin, int32_t spec_end,
+                         const sp_comm_model *comm, const sp_e2e_latencies *lat, float *step_us,
+                         double *trace_us, double *trace_cat, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

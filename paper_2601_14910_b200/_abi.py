@@ -63,6 +63,31 @@ class sp_features(C.Structure):
     ]
 
 
+class sp_serving_model(C.Structure):
+    _fields_ = [(k, C.c_int32) for k in ("n_layers", "hidden", "n_heads", "n_kv_heads", "head_dim",
+                                         "intermediate", "vocab", "tp", "pp", "dtype")]
+
+
+class sp_e2e_info(C.Structure):
+    _fields_ = [("n_traces", C.c_int32), ("max_batch", C.c_int32), ("n_requests", C.c_int64),
+                ("n_steps", C.c_int64), ("n_ragged", C.c_int64), ("n_slots", C.c_int64),
+                ("n_configs", C.c_int64 * 5)]
+
+
+class sp_comm_desc(C.Structure):
+    _fields_ = [("n_specs", C.c_int32), ("n_points", C.c_int32), ("bytes", C.c_void_p),
+                ("allreduce_us", C.c_void_p), ("sendrecv_us", C.c_void_p)]
+
+
+class sp_e2e_latencies(C.Structure):
+    _fields_ = [("gemm", C.c_void_p), ("attention", C.c_void_p), ("rmsnorm", C.c_void_p),
+                ("silu_mul", C.c_void_p)]
+
+
+SP_E2E_NCAT = 5
+E2E_CATEGORIES = ["gemm", "attention", "rmsnorm", "silu_mul", "comm"]
+
+
 class sp_kernel_stat(C.Structure):
     _fields_ = [("kernel", C.c_char_p), ("launches", C.c_int64), ("total_ms", C.c_double)]
 
@@ -99,6 +124,15 @@ def _load():
         "sp_predict": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "sp_set_profiling": (C.c_int, [vp, i32]),
         "sp_profile_read": (i32, [vp, C.POINTER(sp_kernel_stat), i32, i32]),
+        "sp_e2e_plan_create": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, C.POINTER(vp)]),
+        "sp_e2e_plan_update": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+        "sp_e2e_plan_expand": (C.c_int, [vp, vp]),
+        "sp_free_e2e_plan": (None, [vp]),
+        "sp_e2e_plan_info": (C.c_int, [vp, C.POINTER(sp_e2e_info)]),
+        "sp_e2e_plan_batch": (C.c_int, [vp, i32, C.POINTER(sp_config_batch)]),
+        "sp_load_comm_model": (C.c_int, [vp, C.POINTER(sp_comm_desc), C.POINTER(vp)]),
+        "sp_free_comm_model": (None, [vp]),
+        "sp_e2e_compose": (C.c_int, [vp, vp, i32, i32, vp, C.POINTER(sp_e2e_latencies), vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -111,4 +145,6 @@ lib = _load()
 
 EXPORTED = ["sp_create", "sp_destroy", "sp_last_error", "sp_version", "sp_device_sms",
             "sp_load_gpu_specs", "sp_free_specs", "sp_specs_count", "sp_load_model",
-            "sp_free_model", "sp_featurize", "sp_predict", "sp_set_profiling", "sp_profile_read"]
+            "sp_free_model", "sp_featurize", "sp_predict", "sp_set_profiling", "sp_profile_read",
+            "sp_e2e_plan_create", "sp_e2e_plan_update", "sp_e2e_plan_expand", "sp_free_e2e_plan", "sp_e2e_plan_info",
+            "sp_e2e_plan_batch", "sp_load_comm_model", "sp_free_comm_model", "sp_e2e_compose"]

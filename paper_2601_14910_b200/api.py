@@ -159,6 +159,97 @@ class Model:
             self._h = None
 
 
+class CommModel:
+    """sp_comm_model: per-spec All-Reduce / Send-Recv calibration tables."""
+
+    def __init__(self, ctx: "Context", handle: int, n_specs: int):
+        self._ctx, self._h, self.n_specs = ctx, handle, n_specs
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.sp_free_comm_model(self._h)
+            self._h = None
+
+
+class PlanBatch:
+    """A config batch owned by an E2EPlan (device pointers into the plan)."""
+
+    def __init__(self, s: _abi.sp_config_batch):
+        self._s = s
+        self.family = int(s.family)
+
+    @property
+    def n_configs(self) -> int:
+        return int(self._s.n_configs)
+
+    def c_struct(self) -> _abi.sp_config_batch:
+        return self._s
+
+
+class E2EPlan:
+    """sp_e2e_plan: the Workload Generator's invocation plan of a set of request
+    traces for one serving model, expanded on the GPU."""
+
+    FAMILIES = (_abi.SP_GEMM, _abi.SP_ATTENTION, _abi.SP_RMSNORM, _abi.SP_SILU_MUL)
+
+    def __init__(self, ctx: "Context", handle: int, model: dict):
+        self._ctx, self._h, self.model = ctx, handle, dict(model)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.sp_free_e2e_plan(self._h)
+            self._h = None
+
+    def info(self) -> dict:
+        inf = _abi.sp_e2e_info()
+        self._ctx._check(lib.sp_e2e_plan_info(self._h, C.byref(inf)))
+        return {"n_traces": inf.n_traces, "max_batch": inf.max_batch, "n_requests": inf.n_requests,
+                "n_steps": inf.n_steps, "n_ragged": inf.n_ragged, "n_slots": inf.n_slots,
+                "n_configs": {f: int(inf.n_configs[f]) for f in range(5)}}
+
+    def batch(self, family: int) -> PlanBatch:
+        s = _abi.sp_config_batch()
+        self._ctx._check(lib.sp_e2e_plan_batch(self._h, int(family), C.byref(s)))
+        return PlanBatch(s)
+
+    def expand(self, stream=None) -> "E2EPlan":
+        """Re-run the expansion kernels on the resident requests (sp_e2e_plan_expand)."""
+        self._ctx._check(lib.sp_e2e_plan_expand(self._h, _stream_ptr(stream)))
+        return self
+
+    def update(self, traces, stream=None) -> "E2EPlan":
+        off, ins, outs = _trace_arrays(traces)
+        self._ctx._check(lib.sp_e2e_plan_update(self._h, len(off) - 1, off.ctypes.data, ins.ctypes.data,
+                                                outs.ctypes.data, _stream_ptr(stream)))
+        return self
+
+
+def _trace_arrays(traces):
+    off = np.ascontiguousarray(traces.req_off, dtype=np.int64)
+    ins = np.ascontiguousarray(traces.input_len, dtype=np.int32)
+    outs = np.ascontiguousarray(traces.output_len, dtype=np.int32)
+    return off, ins, outs
+
+
+@dataclass
+class E2EResult:
+    """Device outputs of Context.predict_e2e for specs [g0, g1)."""
+
+    step_us: torch.Tensor | None   # fp32 [G, n_steps]
+    trace_us: torch.Tensor         # fp64 [G, n_traces]
+    trace_cat: torch.Tensor        # fp64 [G, n_traces, 5] (gemm, attention, rmsnorm, silu_mul, comm)
+    latency: dict                  # family -> fp32 [G * n_configs] per-kernel predictions
+    n_pairs: int                   # (config, spec) pairs featurised and predicted
+
+
 class Context:
     """sp_ctx on one CUDA device."""
 
@@ -250,6 +341,163 @@ class Context:
                                    _stream_ptr(stream)))
         return latency
 
+    # -- end-to-end serving composition (PAPER §V-D; include/synperf.h sp_e2e_*)
+
+    def load_comm_model(self, comm: dict) -> CommModel:
+        """comm: {"bytes": [P], "allreduce_us": [G][P], "sendrecv_us": [G][P]} (fp64)."""
+        b = np.ascontiguousarray(comm["bytes"], dtype=np.float64)
+        ar = np.ascontiguousarray(comm["allreduce_us"], dtype=np.float64)
+        sr = np.ascontiguousarray(comm["sendrecv_us"], dtype=np.float64)
+        d = _abi.sp_comm_desc()
+        d.n_specs, d.n_points = int(ar.shape[0]), int(b.shape[0])
+        d.bytes, d.allreduce_us, d.sendrecv_us = b.ctypes.data, ar.ctypes.data, sr.ctypes.data
+        h = C.c_void_p()
+        self._check(lib.sp_load_comm_model(self._h, C.byref(d), C.byref(h)))
+        return CommModel(self, h.value, d.n_specs)
+
+    def e2e_plan(self, model: dict, traces, stream=None) -> E2EPlan:
+        """model: n_layers, hidden, n_heads, n_kv_heads, head_dim, intermediate, vocab, tp, pp;
+        traces: .req_off int64 [R+1], .input_len / .output_len int32 (host)."""
+        m = _abi.sp_serving_model()
+        for k in ("n_layers", "hidden", "n_heads", "n_kv_heads", "head_dim", "intermediate", "vocab"):
+            setattr(m, k, int(model[k]))
+        m.tp, m.pp, m.dtype = int(model.get("tp", 1)), int(model.get("pp", 1)), 0
+        off, ins, outs = _trace_arrays(traces)
+        h = C.c_void_p()
+        self._check(lib.sp_e2e_plan_create(self._h, C.byref(m), len(off) - 1, off.ctypes.data,
+                                           ins.ctypes.data, outs.ctypes.data, _stream_ptr(stream),
+                                           C.byref(h)))
+        return E2EPlan(self, h.value, model)
+
+    def e2e_compose(self, plan: E2EPlan, spec_range, comm: CommModel | None, lat: dict,
+                    step_us=None, trace_us=None, trace_cat=None, stream=None) -> None:
+        """sp_e2e_compose: lat maps family -> fp32 device latencies (spec-major)."""
+        L = _abi.sp_e2e_latencies()
+        for f, name in ((_abi.SP_GEMM, "gemm"), (_abi.SP_ATTENTION, "attention"),
+                        (_abi.SP_RMSNORM, "rmsnorm"), (_abi.SP_SILU_MUL, "silu_mul")):
+            t = lat[f]
+            assert t.dtype == torch.float32 and t.is_contiguous()
+            setattr(L, name, t.data_ptr())
+
+        def ptr(t, dt):
+            if t is None:
+                return None
+            assert t.dtype == dt and t.is_contiguous()
+            return t.data_ptr()
+
+        g0, g1 = spec_range
+        self._check(lib.sp_e2e_compose(self._h, plan.handle, int(g0), int(g1),
+                                       comm.handle if comm is not None else None, C.byref(L),
+                                       ptr(step_us, torch.float32), ptr(trace_us, torch.float64),
+                                       ptr(trace_cat, torch.float64), _stream_ptr(stream)))
+
+    def predict_e2e(self, plan: E2EPlan, specs: Specs, models: dict, comm: CommModel | None = None,
+                    spec_range=None, step_latencies: bool = True, stream=None) -> E2EResult:
+        """Featurise + predict every config batch of the plan on specs
+        [g0, g1) (one sp_featurize + sp_predict per family) and compose the
+        per-step and per-trace latencies (sp_e2e_compose).  Device in, device
+        out; feature buffers are cached on the context."""
+        g0, g1 = spec_range if spec_range is not None else (0, len(specs))
+        G = g1 - g0
+        inf = plan.info()
+        dev = self.torch_device
+        cache = self.__dict__.setdefault("_e2e_cache", {})
+        lat = {}
+        n_pairs = 0
+        for f in E2EPlan.FAMILIES:
+            b = plan.batch(f)
+            n = G * b.n_configs
+            n_pairs += n
+            key = (f, max(n, 1))
+            ent = cache.get(f)
+            if ent is None or ent[0] < n:
+                ent = (max(n, 1), Features.empty(f, max(n, 1), dev),
+                       torch.empty(max(n, 1), dtype=torch.float32, device=dev))
+                cache[f] = ent
+            feats = ent[1]
+            feats.n_pairs = n
+            self.featurize(b, specs, feats, cross(g0, g1), stream)
+            self.predict(models[f], feats, ent[2], None, stream)
+            lat[f] = ent[2][:max(n, 1)]
+        R, S = inf["n_traces"], inf["n_steps"]
+        step = torch.empty((G, S), dtype=torch.float32, device=dev) if step_latencies else None
+        tot = torch.empty((G, R), dtype=torch.float64, device=dev)
+        cat = torch.empty((G, R, _abi.SP_E2E_NCAT), dtype=torch.float64, device=dev)
+        self.e2e_compose(plan, (g0, g1), comm, lat, step, tot, cat, stream)
+        return E2EResult(step, tot, cat, lat, n_pairs)
+
+    def predict_e2e_host(self, model: dict, traces, specs: Specs, models: dict,
+                         comm: CommModel | None = None, spec_range=None, stream=None):
+        """The user-facing end-to-end call: host request traces in, host
+        per-trace latencies out.  Uploads the requests (sp_e2e_plan_update on
+        a cached plan), runs predict_e2e and copies back trace totals and the
+        category breakdown: (trace_us [G, R], trace_cat [G, R, 5]) numpy fp64."""
+        plans = self.__dict__.setdefault("_e2e_plans", {})
+        key = tuple(sorted((k, int(v)) for k, v in model.items()))
+        plan = plans.get(key)
+        if plan is None:
+            plan = plans[key] = self.e2e_plan(model, traces, stream)
+        else:
+            plan.update(traces, stream)
+        r = self.predict_e2e(plan, specs, models, comm, spec_range, step_latencies=False, stream=stream)
+        tot = torch.empty(r.trace_us.shape, dtype=torch.float64, pin_memory=True)
+        cat = torch.empty(r.trace_cat.shape, dtype=torch.float64, pin_memory=True)
+        tot.copy_(r.trace_us, non_blocking=True)
+        cat.copy_(r.trace_cat, non_blocking=True)
+        (stream or torch.cuda.current_stream(self.torch_device)).synchronize()
+        return tot.numpy(), cat.numpy()
+
+    def _predict_host_by_spec(self, fam, fh, rh, oh, specs, model, g0, g1, out_t, chunks, stream):
+        """predict_host for a wide spec range: the configs go H2D once, then
+        spec slices [ga, gb) are featurised + predicted while the previous
+        slice's latencies -- a contiguous run of the spec-major output -- go D2H."""
+        G, C = g1 - g0, int(fh.shape[1])
+        bounds = [g0 + G * i // chunks for i in range(chunks + 1)]
+        gmax = max(b - a for a, b in zip(bounds, bounds[1:]))
+        dev = self.torch_device
+        key = ("spec", fam, tuple(fh.shape), C, gmax, 0 if rh is None else rh.numel())
+        cache = getattr(self, "_host_cache", None)
+        if cache is None or cache["key"] != key:
+            cache = {
+                "key": key,
+                "fields": torch.empty(tuple(fh.shape), dtype=torch.int32, device=dev),
+                "ragged": None if rh is None else torch.empty(max(rh.numel(), 1), dtype=torch.int32, device=dev),
+                "roff": None if oh is None else torch.empty(C, dtype=torch.int64, device=dev),
+                "feats": Features.empty(fam, gmax * C, dev),
+                "lat": [torch.empty(gmax * C, dtype=torch.float32, device=dev) for _ in range(2)],
+                "d2h": torch.cuda.Stream(dev),
+            }
+            self._host_cache = cache
+        comp = stream or torch.cuda.current_stream(dev)
+        s_d2h = cache["d2h"]
+        cache["fields"].copy_(fh, non_blocking=True)
+        if rh is not None:
+            cache["ragged"][:rh.numel()].copy_(rh, non_blocking=True)
+        if oh is not None:
+            cache["roff"].copy_(oh, non_blocking=True)
+        db = DeviceBatch(fam, cache["fields"], cache["ragged"], cache["roff"])
+        feats = cache["feats"]
+        done = []
+        for i, (ga, gb) in enumerate(zip(bounds, bounds[1:])):
+            n = (gb - ga) * C
+            lat = cache["lat"][i % 2]
+            if i >= 2:
+                comp.wait_event(done[i - 2])
+            feats.n_pairs = n
+            self.featurize(db, specs, feats, cross(ga, gb), comp)
+            self.predict(model, feats, lat, None, comp)
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev)
+                out_t[(ga - g0) * C:(gb - g0) * C].copy_(lat[:n], non_blocking=True)
+                ev2 = torch.cuda.Event()
+                ev2.record(s_d2h)
+                done.append(ev2)
+        s_d2h.synchronize()
+        comp.wait_stream(s_d2h)
+        return out_t[:G * C].numpy()
+
     # -- end-to-end: host configs in, host latencies out
     def predict_host(self, batch, specs: Specs, model: Model, spec_range=None,
                      out: np.ndarray | torch.Tensor | None = None, chunks: int = 4,
@@ -282,6 +530,9 @@ class Context:
             out_t = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
         if n == 0:
             return out_t[:0].numpy()
+        if G >= 64 and G >= 4 * chunks:  # wide spec axis (e.g. config 5): pipeline over specs
+            return self._predict_host_by_spec(fam, fh, rh, oh, specs, model, g0, g1, out_t,
+                                              max(chunks, 8), stream)
         chunks = max(1, min(chunks, C))
         bounds = [C * i // chunks for i in range(chunks + 1)]
         cmax = max(b1 - b0 for b0, b1 in zip(bounds, bounds[1:]))

@@ -280,3 +280,19 @@ def test_featurize_deterministic(sp, ctx):
     _, c = gpu_features(sp, ctx, b, sa)
     for x, y in zip(a, c):
         assert np.array_equal(x, y, equal_nan=True)
+
+
+@pytest.mark.parametrize("fam", ["attention", "gemm"])
+def test_predict_host_wide_spec_axis(sp, ctx, fam):
+    """>= 64 specs: predict_host pipelines over spec slices (contiguous D2H
+    runs of the spec-major output); identical to the device path."""
+    b = FAMILY_BATCHES[fam]()
+    sa = specs.hypothetical_sweep_specs(300)
+    sh = ctx.load_gpu_specs(sa)
+    m = ctx.load_model(models.random_mlp(b.family, 6), "fp16")
+    f, _ = gpu_features(sp, ctx, b, sa, specs_handle=sh)
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    ctx.predict(m, f, lat)
+    torch.cuda.synchronize()
+    got = ctx.predict_host(b, sh, m)
+    assert np.array_equal(got, lat.cpu().numpy(), equal_nan=True)
