@@ -57,72 +57,100 @@ struct ExpandArgs {
   int32_t nh, nkv, hd, hidden, inter, vocab, qkv_n;
 };
 
-// E2 + E5: warp per step, grid-stride.
+constexpr int kStepsPerWarp = 32;
+
+// E2 + E5: each warp expands kStepsPerWarp consecutive steps (one binary search
+// for the first step's trace, then a walk across trace boundaries).  Lanes hold
+// the current trace's first 64 requests in registers; larger batches read the
+// rest through L1.
 __global__ void __launch_bounds__(256) e2e_expand_kernel(ExpandArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = warp; s < a.n_steps; s += nwarps) {
-    // trace of step s: last r with step_off[r] <= s
+  for (int64_t s_first = warp * kStepsPerWarp; s_first < a.n_steps; s_first += nwarps * kStepsPerWarp) {
+    const int64_t s_last = min(a.n_steps, s_first + kStepsPerWarp);
+    // trace of the first step: last r with step_off[r] <= s_first
     int lo = 0, hi = a.n_traces - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(a.step_off + mid) <= s) lo = mid; else hi = mid - 1;
+      if (__ldg(a.step_off + mid) <= s_first) lo = mid; else hi = mid - 1;
     }
-    const int r = lo;
-    const int32_t k = (int32_t)(s - __ldg(a.step_off + r));
-    const int64_t b0 = __ldg(a.req_off + r), nb = __ldg(a.req_off + r + 1) - b0;
-    int64_t roff = __ldg(a.rag_off + r);
-    int32_t bs;
-    if (k == 0) {  // prefill: every request, qlen = kvlen = input_len, batch order
-      for (int64_t b = lane; b < nb; b += 32) {
-        const int32_t q = __ldg(a.in_len + b0 + b);
-        a.attn_ragged[roff + 2 * b] = q;
-        a.attn_ragged[roff + 2 * b + 1] = q;
+    int r = lo;
+    int64_t t_begin = __ldg(a.step_off + r), t_end = __ldg(a.step_off + r + 1);
+    int64_t b0 = __ldg(a.req_off + r), nb = __ldg(a.req_off + r + 1) - b0;
+    int32_t in0 = 0, out0 = 0, in1 = 0, out1 = 0;  // requests lane, lane + 32
+    auto load_trace = [&]() {
+      in0 = lane < nb ? __ldg(a.in_len + b0 + lane) : 0;
+      out0 = lane < nb ? __ldg(a.out_len + b0 + lane) : 0;
+      in1 = lane + 32 < nb ? __ldg(a.in_len + b0 + lane + 32) : 0;
+      out1 = lane + 32 < nb ? __ldg(a.out_len + b0 + lane + 32) : 0;
+    };
+    load_trace();
+    for (int64_t s = s_first; s < s_last; ++s) {
+      while (s >= t_end) {  // next trace (steps of a trace are contiguous; empty traces cannot occur)
+        ++r;
+        t_begin = t_end;
+        t_end = __ldg(a.step_off + r + 1);
+        b0 = __ldg(a.req_off + r);
+        nb = __ldg(a.req_off + r + 1) - b0;
+        load_trace();
       }
-      bs = (int32_t)nb;
-    } else {
-      // entries before this step: n (prefill) + sum_b min(out_b - 1, k - 1) (decode steps 1..k-1)
-      int64_t before = 0;
-      for (int64_t b = lane; b < nb; b += 32) before += min(__ldg(a.out_len + b0 + b) - 1, k - 1);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
-      roff += 2 * (nb + before);
-      int32_t pos = 0;
-      for (int64_t b = 0; b < nb; b += 32) {
-        const bool in = b + lane < nb;
-        const int32_t o = in ? __ldg(a.out_len + b0 + b + lane) : 0;
-        const bool act = in && o > k;
-        const unsigned m = __ballot_sync(0xffffffffu, act);
-        if (act) {
-          const int32_t p = pos + __popc(m & ((1u << lane) - 1u));
-          a.attn_ragged[roff + 2 * p] = 1;
-          a.attn_ragged[roff + 2 * p + 1] = __ldg(a.in_len + b0 + b + lane) + k;
+      const int32_t k = (int32_t)(s - t_begin);
+      int64_t roff = __ldg(a.rag_off + r);
+      int32_t bs;
+      if (k == 0) {  // prefill: every request, qlen = kvlen = input_len, batch order
+        for (int64_t b = lane; b < nb; b += 32) {
+          const int32_t q = b < 32 ? in0 : (b < 64 ? in1 : __ldg(a.in_len + b0 + b));
+          *reinterpret_cast<int2 *>(a.attn_ragged + roff + 2 * b) = make_int2(q, q);
         }
-        pos += __popc(m);
+        bs = (int32_t)nb;
+      } else {
+        // entries before this step: nb (prefill) + sum_b min(out_b - 1, k - 1) (decode steps 1..k-1)
+        int64_t before = 0;
+        for (int64_t b = lane; b < nb; b += 32) {
+          const int32_t o = b < 32 ? out0 : (b < 64 ? out1 : __ldg(a.out_len + b0 + b));
+          before += min(o - 1, k - 1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+        roff += 2 * (nb + before);
+        int32_t pos = 0;
+        for (int64_t b = 0; b < nb; b += 32) {
+          const int64_t bi = b + lane;
+          const bool in = bi < nb;
+          const int32_t o = !in ? 0 : (bi < 32 ? out0 : (bi < 64 ? out1 : __ldg(a.out_len + b0 + bi)));
+          const bool act = in && o > k;
+          const unsigned m = __ballot_sync(0xffffffffu, act);
+          if (act) {
+            const int32_t q = bi < 32 ? in0 : (bi < 64 ? in1 : __ldg(a.in_len + b0 + bi));
+            const int32_t p = pos + __popc(m & ((1u << lane) - 1u));
+            *reinterpret_cast<int2 *>(a.attn_ragged + roff + 2 * p) = make_int2(1, q + k);
+          }
+          pos += __popc(m);
+        }
+        bs = pos;
       }
-      bs = pos;
-    }
-    if (lane < SP_NFIELDS_ATTENTION) {
-      const bool pf = k == 0;
-      int32_t v;
-      switch (lane) {
-        case 0: v = bs; break;                                        // BS
-        case 1: v = a.nh; break;                                      // NH
-        case 2: v = a.nkv; break;                                     // NKV
-        case 3: v = a.hd; break;                                      // HD
-        case 4: v = pf ? 128 : 16; break;                             // BQ
-        case 5: v = 64; break;                                        // BKV
-        case 6: v = pf ? 0 : ((int64_t)bs * a.nkv < 128 ? 1024 : 0); break;  // KV_CHUNK
-        case 7: v = pf ? 1 : 0; break;                                // CAUSAL
-        case 8: v = 4; break;                                         // WARPS
-        case 9: v = pf ? 168 : 64; break;                             // REGS
-        case 10: v = 0; break;                                        // SMEM (default footprint)
-        default: v = SP_BF16; break;                                  // DTYPE
+      if (lane < SP_NFIELDS_ATTENTION) {
+        const bool pf = k == 0;
+        int32_t v;
+        switch (lane) {
+          case 0: v = bs; break;                                        // BS
+          case 1: v = a.nh; break;                                      // NH
+          case 2: v = a.nkv; break;                                     // NKV
+          case 3: v = a.hd; break;                                      // HD
+          case 4: v = pf ? 128 : 16; break;                             // BQ
+          case 5: v = 64; break;                                        // BKV
+          case 6: v = pf ? 0 : ((int64_t)bs * a.nkv < 128 ? 1024 : 0); break;  // KV_CHUNK
+          case 7: v = pf ? 1 : 0; break;                                // CAUSAL
+          case 8: v = 4; break;                                         // WARPS
+          case 9: v = pf ? 168 : 64; break;                             // REGS
+          case 10: v = 0; break;                                        // SMEM (default footprint)
+          default: v = SP_BF16; break;                                  // DTYPE
+        }
+        a.attn_fields[(int64_t)lane * a.n_steps + s] = v;
       }
-      a.attn_fields[(int64_t)lane * a.n_steps + s] = v;
+      if (lane == 0) a.attn_roff[s] = roff;
     }
-    if (lane == 0) a.attn_roff[s] = roff;
   }
 }
 
@@ -460,7 +488,7 @@ static sp_status plan_launch(sp_e2e_plan *p, void *stream) {
   cudaError_t e;
   cudaSetDevice(ctx->device);
   const LaunchHook hk = ctx->hook();
-  const int64_t warps_needed = inf.n_steps;
+  const int64_t warps_needed = (inf.n_steps + kStepsPerWarp - 1) / kStepsPerWarp;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((warps_needed + 7) / 8, (int64_t)ctx->num_sms * 16));
   hk.on_begin("e2e_expand", stream);
   e2e_expand_kernel<<<blocks, 256, 0, st>>>(a);

@@ -81,9 +81,63 @@ __device__ UniformCfg gemm_cfg(const ConfigView &v, int64_t c) {
   return u;
 }
 
+// Histogram pass of a fused-MoE config (R16): sum of the per-expert token
+// counts, any negative count, and sum_e ceil(t_e/BM).
+struct MoeHist {
+  int64_t sum = 0;
+  int64_t mblocks = 0;
+  int neg = 0;
+};
+
+// Warp-cooperative histogram pass for the (up to) 32 configs of a warp, lane j
+// holding config c0 + j: the warp walks its configs one at a time, its lanes
+// reading 32 consecutive counts per iteration (coalesced) and reducing with
+// shuffles.  Lane j receives config j's result.  All 32 lanes must call it.
+__device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c, bool valid) {
+  const int lane = threadIdx.x & 31;
+  int64_t off = -1;
+  int32_t E = 0, bm = 0;
+  if (valid && v.ragged_off) {
+    off = __ldg(v.ragged_off + c);
+    E = fld(v, 1, c);
+    bm = fld(v, 5, c);
+  }
+  MoeHist mine;
+  unsigned need = __ballot_sync(0xffffffffu, off >= 0 && E >= 1 && bm >= 1);
+  while (need) {
+    const int j = __ffs(need) - 1;
+    need &= need - 1;
+    const int64_t oj = __shfl_sync(0xffffffffu, off, j);
+    const int32_t Ej = __shfl_sync(0xffffffffu, E, j);
+    const uint32_t bmj = (uint32_t)__shfl_sync(0xffffffffu, bm, j);
+    const int32_t *h = v.ragged + oj;
+    int64_t sum = 0, mb = 0;
+    int neg = 0;
+    for (int32_t e = lane; e < Ej; e += 32) {
+      const int32_t te = __ldg(h + e);
+      neg |= te < 0;
+      sum += te;
+      mb += te > 0 ? ((uint32_t)te + bmj - 1u) / bmj : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      mb += __shfl_xor_sync(0xffffffffu, mb, o);
+    }
+    neg = __any_sync(0xffffffffu, neg);
+    if (lane == j) {
+      mine.sum = sum;
+      mine.mblocks = mb;
+      mine.neg = neg;
+    }
+  }
+  return mine;
+}
+
 // Fused MoE (R16): t_e from the histogram or the balanced split; tasks are
 // padded BM x BN x H_pad tiles: T = sum_e ceil(t_e/BM) * ceil(N/BN).
-__device__ UniformCfg moe_cfg(const ConfigView &v, int64_t c) {
+// `hist`: this config's histogram pass (moe_hist_warp), or nullptr to walk it here.
+__device__ UniformCfg moe_cfg(const ConfigView &v, int64_t c, const MoeHist *hist) {
   UniformCfg u{};
   const int64_t M = fld(v, 0, c), E = fld(v, 1, c), topk = fld(v, 2, c), H = fld(v, 3, c),
                 N = fld(v, 4, c), bm = fld(v, 5, c), bn = fld(v, 6, c), bk = fld(v, 7, c),
@@ -97,7 +151,10 @@ __device__ UniformCfg moe_cfg(const ConfigView &v, int64_t c) {
   if (mt > kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
   const int64_t off = v.ragged_off ? __ldg(v.ragged_off + c) : -1;
   unsigned __int128 mblocks = 0;
-  if (off >= 0) {
+  if (off >= 0 && hist) {
+    if (hist->neg || hist->sum != mt) { u.status = SP_PAIR_E_HIST; return u; }
+    mblocks = (unsigned __int128)hist->mblocks;
+  } else if (off >= 0) {
     const int32_t *h = v.ragged + off;
     int64_t sum = 0;
     for (int64_t e = 0; e < E; ++e) {
@@ -147,10 +204,11 @@ __device__ UniformCfg rowwise_cfg(const ConfigView &v, int64_t c, bool silu) {
   return u;
 }
 
-__device__ __forceinline__ UniformCfg config_of(int fam, const ConfigView &v, int64_t c) {
+__device__ __forceinline__ UniformCfg config_of(int fam, const ConfigView &v, int64_t c,
+                                                const MoeHist *hist = nullptr) {
   switch (fam) {
     case SP_GEMM: return gemm_cfg(v, c);
-    case SP_FUSED_MOE: return moe_cfg(v, c);
+    case SP_FUSED_MOE: return moe_cfg(v, c, hist);
     case SP_RMSNORM: return rowwise_cfg(v, c, false);
     default: return rowwise_cfg(v, c, true);
   }
@@ -188,8 +246,10 @@ __global__ void __launch_bounds__(kThreads) featurize_uniform_cross(int fam, Con
   }
   __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  MoeHist hist;
+  if (fam == SP_FUSED_MOE) hist = moe_hist_warp(cfg, c, c < cfg.n_configs);
   if (c >= cfg.n_configs) return;
-  const UniformCfg u = config_of(fam, cfg, c);
+  const UniformCfg u = config_of(fam, cfg, c, fam == SP_FUSED_MOE ? &hist : nullptr);
   const int pipes = family_pipes(fam);
   const int64_t C = cfg.n_configs;
   for (int g = gt0; g < gt1; ++g) uniform_pair(out, (int64_t)(g - g0) * C + c, u, s_spec[g - gt0], pipes);

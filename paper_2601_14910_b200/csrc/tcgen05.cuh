@@ -84,6 +84,17 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t mbar, uint32_t parity) 
         : "memory");
   } while (!done);
 }
+// try_wait without a suspend-time hint (the hardware's default time limit).
+__device__ __forceinline__ void mbar_wait_try(uint32_t mbar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
 // Non-blocking probe of a phase.
 __device__ __forceinline__ bool mbar_test(uint32_t mbar, uint32_t parity) {
   uint32_t done;

@@ -37,17 +37,21 @@ def raw_metrics(rep):
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return {}
-    h, units, vals = rows[0], rows[1], rows[2]
+    h, units = rows[0], rows[1]
     m = {}
-    for k, u, v in zip(h, units, vals):
-        if k in KEYS:
-            try:
-                x = float(v.replace(",", ""))
-            except ValueError:
-                continue
-            m[k] = x * SCALE.get(u, 1.0) if u in SCALE else x
-            m[k + ".unit"] = u
-    m["kernel"] = next((v for k, v in zip(h, vals) if k == "Kernel Name"), "")
+    for vals in rows[2:]:  # one row per captured launch: additive counters are summed
+        for k, u, v in zip(h, units, vals):
+            if k in KEYS:
+                try:
+                    x = float(v.replace(",", ""))
+                except ValueError:
+                    continue
+                x = x * SCALE.get(u, 1.0) if u in SCALE else x
+                additive = k.endswith(".sum") and "per_" not in k
+                m[k] = m.get(k, 0.0) + x if additive else x
+                m[k + ".unit"] = u
+        m["kernel"] = next((v for k, v in zip(h, vals) if k == "Kernel Name"), "")
+    m["launches_captured"] = len(rows) - 2
     return m
 
 
@@ -74,7 +78,9 @@ def launches(path):
 def main():
     r = sys.argv[1] if len(sys.argv) > 1 else "r01"
     w = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
-    d = os.path.join(ROOT, "gpurun_out", f"prof_{r}")
+    d = os.path.join(ROOT, "gpurun_out", f"prof_{r}_{w}")
+    if not os.path.isdir(d):
+        d = os.path.join(ROOT, "gpurun_out", f"prof_{r}")
     lines = [f"# ncu evidence, round {r}, workload {w}", "",
              "Captured with tools/profile_round.sh on one B200 (`--clock-control none`).",
              "Launch times are cold-cache and serialised (compare shares, not absolutes).", ""]
@@ -92,7 +98,10 @@ def main():
         if not os.path.exists(rep):
             continue
         m = raw_metrics(rep)
-        lines += ["", f"## `ncu --set full`: {tag} ({m.get('kernel', '')[:90]})", "", "| counter | value |",
+        nl = int(m.get("launches_captured", 1))
+        lines += ["", f"## `ncu --set full`: {tag} ({m.get('kernel', '')[:90]})",
+                  "" if nl == 1 else f"\n{nl} launches captured (one step); additive counters summed.", "",
+                  "| counter | value |",
                   "|---|---|"]
         for k in KEYS:
             if k in m:
