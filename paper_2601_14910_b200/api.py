@@ -563,7 +563,8 @@ class Context:
         for i, (c0, c1) in enumerate(zip(bounds, bounds[1:])):
             nc = c1 - c0
             with torch.cuda.stream(s_h2d):
-                cache["fields"][:, c0:c1].copy_(fh[:, c0:c1], non_blocking=True)
+                for fi in range(nf):  # contiguous row pieces: async DMA from pinned memory
+                    cache["fields"][fi, c0:c1].copy_(fh[fi, c0:c1], non_blocking=True)
                 if cache["roff"] is not None:
                     cache["roff"][c0:c1].copy_(oh[c0:c1], non_blocking=True)
                     valid = o[c0:c1] >= 0
