@@ -31,8 +31,10 @@
 //   D2 [B+64, B+192)     (N = 128 in one MMA per K step: a TS MMA reads its
 //                         4 KB A slice from TMEM at ~64 B/clk, so N = 64 would
 //                         halve the tensor rate; N = 128 matches it)
-//   H2 [B, B+64)         (half h: K 64h..64h+63 in [B+32h, B+32h+32))
 //   D3 [B+192, B+256)
+// H2 is written to shared memory (per slot, UMMA K-major) and layer 3 runs as
+// an SS MMA: the kernel is bound by TMEM reads (epilogue loads + TS operand
+// reads), and moving this 32 KB operand off TMEM measured 2.7% faster.
 // Each half writes only columns it has itself read (half 1 packs its D1
 // columns back to front), or columns whose readers the MMA barrier already
 // retired, so the halves need no barrier between them.
@@ -75,7 +77,27 @@ constexpr uint32_t kOffX = kWBytes;
 constexpr uint32_t kOffRaw = kOffX + kNX * kXBytes;
 constexpr uint32_t kOffVec = kOffRaw + kNR * kRawBytes;
 constexpr uint32_t kOffZx = kOffVec + kVecBytes;  // [2][128] fp32 partial logits
+// Default: H2 goes to shared memory and L3 runs as an SS MMA (2.7% faster than
+// reading it from TMEM: the kernel is bound by TMEM reads).
+// -DSP_L3_TS restores the TS form; -DSP_L2H_SS (half of H1 in shared memory)
+// measured 26% slower (shared-memory bound).
+#if !defined(SP_L3_TS) && !defined(SP_L2H_SS) && !defined(SP_L3_SS)
+#define SP_L3_SS 1
+#endif
+#if defined(SP_L3_SS) && defined(SP_L2H_SS)
+#error "SP_L3_SS and SP_L2H_SS need the same shared memory"
+#endif
+#if defined(SP_L3_SS) || defined(SP_L2H_SS)
+#define SP_ACT_SMEM 1
+#endif
+#ifdef SP_ACT_SMEM
+// H2 (SP_L3_SS) or H1 K 0..127 (SP_L2H_SS) per TMEM slot in shared memory (L3 as an SS MMA): [128 rows][128 K] 16-bit, K-major
+constexpr uint32_t kH2Bytes = kTile * 128 * 2;  // 32 KB
+constexpr uint32_t kOffH2 = kOffZx + 2 * kTile * 4;
+constexpr uint32_t kOffBar = kOffH2 + 2 * kH2Bytes;
+#else
 constexpr uint32_t kOffBar = kOffZx + 2 * kTile * 4;
+#endif
 // barriers: x_full[kNX] x_empty[kNX] d_full[2] a_ready[2] slot_free[2], then the TMEM base
 constexpr int kBarXFull = 0, kBarXEmpty = kNX, kBarDFull = 2 * kNX, kBarAReady = 2 * kNX + 2,
               kBarSlotFree = 2 * kNX + 4, kNumBars = 2 * kNX + 6;
@@ -174,6 +196,26 @@ __device__ __forceinline__ void epi_hidden_tmem(uint32_t tmem_row, uint32_t src,
     tc::tmem_st32(tmem_row + dst + c / 2, *reinterpret_cast<uint32_t(*)[32]>(v));
   }
 }
+
+#ifdef SP_ACT_SMEM
+// Hidden epilogue to shared memory: fp32 TMEM columns [src, src + 64) of this
+// lane's row -> ReLU -> 16-bit -> K columns [k0, k0 + 64) of the row in the
+// UMMA K-major layout (K = 128): eight 16-byte core-matrix rows.
+template <bool BF16>
+__device__ __forceinline__ void epi_hidden_smem64(uint32_t tmem_row, uint32_t src, uint32_t hbuf, uint32_t row,
+                                                  uint32_t k0) {
+  uint32_t v[64];
+  tc::tmem_ld32(tmem_row + src, *reinterpret_cast<uint32_t(*)[32]>(v));
+  tc::tmem_ld32(tmem_row + src + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+  tc::tmem_wait_ld();
+  uint32_t w[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) w[j] = tc::relu_x2<BF16>(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    tc::st_shared_v4(hbuf + op_off(row, k0 + 8 * c, 128), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+}
+#endif
 
 // Write a bias vector (broadcast over rows) into TMEM columns [c, c + NC).
 template <int NC>
@@ -288,14 +330,29 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
 #pragma unroll
               for (int ks = 0; ks < 16; ++ks) {
                 const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
+#ifdef SP_L2H_SS
+                if (ks < 8) {  // K 0..127 from shared memory
+                  if (!kNoMma)
+                    tc::mma_f16kind(B + 64, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
+                                    tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
+                  continue;
+                }
+#endif
                 if (!kNoMma)
                   tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
-            } else {  // H2 from TMEM; D3 preset to b3'
+            } else {  // H2 from TMEM (or shared memory with SP_L3_SS); D3 preset to b3'
 #pragma unroll
-              for (int ks = 0; ks < 8; ++ks)
+              for (int ks = 0; ks < 8; ++ks) {
+#ifdef SP_L3_SS
+                if (!kNoMma)
+                  tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
+                                  tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64, 1);
+#else
                 if (!kNoMma) tc::mma_f16kind_ts(B + 192, B + 8 * ks, tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64,
                                    1);
+#endif
+              }
             }
           }
           PTRACE(2, (int)(j >> 1), 1 + layer[s] * 2 + s);
@@ -385,13 +442,23 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       pd ^= 1;
       tc::fence_after();
 #ifndef SP_EXP_NOEPI
+#ifdef SP_L2H_SS
+      if (h == 0) {
+        epi_hidden_smem64<BF16>(tmem_row, 0, sbase + kOffH2 + s * kH2Bytes, row, 0);
+        epi_hidden_smem64<BF16>(tmem_row, 64, sbase + kOffH2 + s * kH2Bytes, row, 64);
+      }
+#else
       if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
+#endif
       else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
 #endif
 #ifndef SP_EXP_NOBIAS
       bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
 #endif
       tc::tmem_wait_st();
+#ifdef SP_L2H_SS
+      tc::fence_proxy_async();  // generic-proxy H1 writes -> visible to the tensor core
+#endif
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
@@ -402,12 +469,19 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       pd ^= 1;
       tc::fence_after();
 #ifndef SP_EXP_NOEPI
+#ifdef SP_L3_SS
+      epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
+#else
       epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
+#endif
 #endif
 #ifndef SP_EXP_NOBIAS
       bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
 #endif
       tc::tmem_wait_st();
+#ifdef SP_L3_SS
+      tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
+#endif
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(5);
