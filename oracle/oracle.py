@@ -18,6 +18,9 @@ SRC = os.path.join(HERE, "synperf_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
 CLAMPED = 1
+# scheduler modes (flags bits 4..5): cyclic RR is 0
+SCHED_GREEDY = 1 << 4   # hardware RR with greedy retirement
+SCHED_MINHEAP = 2 << 4  # persistent kernel, software MinHeap
 
 N_INTS, N_FLTS = 11, 12
 INT_NAMES = ["n_tasks", "occupancy", "waves", "tot_T", "tot_F", "tot_X", "max_T", "max_F",
@@ -55,6 +58,11 @@ def lib():
                                     C.c_int, C.c_int64, C.c_void_p, C.c_int64]
         L.orc_schedule_rr.restype = None
         L.orc_schedule_rr.argtypes = [C.c_int64, C.c_int64, C.c_void_p]
+        L.orc_schedule_greedy.restype = None
+        L.orc_schedule_greedy.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
+        L.orc_schedule_minheap.restype = None
+        L.orc_schedule_minheap.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                           C.c_void_p]
         L.orc_mlp_input.restype = C.c_int
         L.orc_mlp_input.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_num_threads.restype = C.c_int
@@ -124,6 +132,23 @@ def schedule_rr(n_tasks: int, n_sm: int) -> np.ndarray:
     out = np.zeros(n_tasks, np.int64)
     lib().orc_schedule_rr(n_tasks, n_sm, _ptr(out))
     return out
+
+
+def schedule_greedy(costs, n_sm: int, occ: int) -> np.ndarray:
+    """sm_of[t] under the GREEDY scheduler for explicit integer task costs."""
+    c = np.ascontiguousarray(costs, dtype=np.int64)
+    out = np.zeros(len(c), np.int64)
+    lib().orc_schedule_greedy(_ptr(c), len(c), n_sm, occ, _ptr(out))
+    return out
+
+
+def schedule_minheap(costs, n_sm: int, occ: int) -> tuple[np.ndarray, np.ndarray]:
+    """(worker_of[t], sm_of[t]) under the MINHEAP scheduler for explicit costs."""
+    c = np.ascontiguousarray(costs, dtype=np.int64)
+    w = np.zeros(len(c), np.int64)
+    out = np.zeros(len(c), np.int64)
+    lib().orc_schedule_minheap(_ptr(c), len(c), n_sm, occ, _ptr(w), _ptr(out))
+    return w, out
 
 
 class _Mlp(C.Structure):

@@ -18,6 +18,18 @@
  *      ceil(T / (N_SM * occ)).
  *   O3 Scheduling Simulator M, Eq.2: hardware round-robin, task t
  *      dealt to SM (t mod N_SM) (R5), accumulated into explicit per-SM arrays.
+ *      Scheduler modes (flags >> 4):
+ *        1 GREEDY  hardware RR with retirement ("a new task is assigned
+ *                  to an SM when an existing task finishes"): the
+ *                  first N_SM*occ tasks are dealt cyclically, then each task
+ *                  goes to the SM with the least accumulated busy time;
+ *        2 MINHEAP persistent kernel with a software MinHeap scheduler (P:281,
+ *                  P:427 FlashInfer FA3): W = min(N_SM*occ, T)
+ *                  workers pinned round-robin to SMs, each task to the worker
+ *                  with the least accumulated busy time.
+ *      Busy time of a task = max over the family's pipes of its theoretical
+ *      cycles ops_p / Th_p, kept exact as an integer in units of
+ *      1/lcm(Th_p) cycle; ties go to the lowest index.
  *   O4 GPU totals: summed over the task list itself, independently of the
  *      per-SM arrays, so conservation (sum_j S_j = total) is a real check.
  *   O5 Max-SM: max_j S_j per quantity independently (R7).
@@ -74,6 +86,8 @@ typedef struct {
 
 /* oracle flags */
 #define ORC_CLAMPED 1 /* SPEC's clamped edge tiles (R2 alternative), oracle-only */
+#define ORC_SCHED_SHIFT 4 /* scheduler mode in bits 4..5: 0 RR, 1 GREEDY, 2 MINHEAP */
+enum { SCHED_RR = 0, SCHED_GREEDY = 1, SCHED_MINHEAP = 2 };
 
 /* output slots (SURVEY §8 uniform record) */
 enum { I_NTASKS, I_OCC, I_WAVES, I_TOT_T, I_TOT_F, I_TOT_X, I_MAX_T, I_MAX_F, I_MAX_X,
@@ -110,11 +124,27 @@ typedef struct {
   i128 *sm_sum;       /* [n_sm][4] explicit per-SM sums  S_j(X) */
   int64_t *sm_count;  /* [n_sm] tasks per SM */
   i128 total[4];      /* sum over the task list */
+  int mode;           /* SCHED_*; non-RR modes collect the task list first */
+  i128 *list;         /* [cap][4] task demands in task order (GREEDY / MINHEAP) */
+  int64_t cap;
 } orc_sched;
 
-/* One task tau_t with demands d[4]: Eq.2 cyclic dealing (R5) + O4 totals. */
+/* One task tau_t with demands d[4]: Eq.2 cyclic dealing (R5) + O4 totals.
+ * GREEDY / MINHEAP: the task is recorded and dealt later (schedule_list). */
 static void emit_task(orc_sched *s, i128 ops_t, i128 ops_f, i128 ops_x, i128 bytes) {
   i128 d[4] = {ops_t, ops_f, ops_x, bytes};
+  if (s->mode != SCHED_RR) {
+    if (s->t == s->cap) {
+      s->cap = s->cap ? 2 * s->cap : 1024;
+      s->list = (i128 *)realloc(s->list, (size_t)s->cap * 4 * sizeof(i128));
+    }
+    for (int q = 0; q < 4; ++q) {
+      s->list[s->t * 4 + q] = d[q];
+      if (s->total[q] < SAT128) s->total[q] += d[q];
+    }
+    s->t += 1;
+    return;
+  }
   int64_t j = s->t % s->n_sm; /* M: task t -> SM (t mod N_SM) */
   for (int q = 0; q < 4; ++q) {
     /* saturate far above int64 (only the > INT64_MAX decision matters there) */
@@ -370,6 +400,86 @@ static void set_error(int64_t *ints, double *flts) {
   for (int k = 0; k < N_F; ++k) flts[k] = NAN;
 }
 
+/* ---------------- O3 non-cyclic schedulers (NEXT-2) ---------------- */
+
+static int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t r = a % b;
+    a = b;
+    b = r;
+  }
+  return a;
+}
+
+/* GREEDY: tasks 0..N*occ-1 dealt cyclically (the RR rounds until every SM is
+ * saturated), then task t to the SM with the least busy time (ties: lowest
+ * SM).  cost[t] = busy time of task t.  Writes sm_of[t]. */
+static void greedy_assign(const i128 *cost, int64_t n, int64_t n_sm, int64_t occ, int64_t *sm_of) {
+  i128 *busy = (i128 *)calloc((size_t)n_sm, sizeof(i128));
+  for (int64_t t = 0; t < n; ++t) {
+    int64_t j;
+    if (t < n_sm * occ) {
+      j = t % n_sm;
+    } else {
+      j = 0;
+      for (int64_t k = 1; k < n_sm; ++k)
+        if (busy[k] < busy[j]) j = k;
+    }
+    busy[j] += cost[t];
+    sm_of[t] = j;
+  }
+  free(busy);
+}
+
+/* MINHEAP: W = min(N*occ, n) workers, worker w resident on SM (w mod N);
+ * task t to the worker with the least accumulated busy time (ties: lowest
+ * worker) -- a linear scan gives the heap's answer.  Writes worker_of[t]
+ * and sm_of[t]. */
+static void minheap_assign(const i128 *cost, int64_t n, int64_t n_sm, int64_t occ, int64_t *worker_of,
+                           int64_t *sm_of) {
+  int64_t W = n_sm * occ < n ? n_sm * occ : n;
+  if (W < 1) W = 1;
+  i128 *load = (i128 *)calloc((size_t)W, sizeof(i128));
+  for (int64_t t = 0; t < n; ++t) {
+    int64_t w = 0;
+    for (int64_t k = 1; k < W; ++k)
+      if (load[k] < load[w]) w = k;
+    load[w] += cost[t];
+    if (worker_of) worker_of[t] = w;
+    sm_of[t] = w % n_sm;
+  }
+  free(load);
+}
+
+/* Deal the recorded task list of s with scheduler `mode` into the per-SM
+ * arrays.  th[p] = pipe throughputs (ops/clk/SM), pipes = Table V bitmask. */
+static void schedule_list(orc_sched *s, int mode, int64_t occ, const int64_t *th, int pipes) {
+  int64_t lc = 1; /* lcm of the pipes' throughputs: busy time in 1/lc cycles is an integer */
+  for (int p = 0; p < 3; ++p)
+    if (pipes & (1 << p)) lc = lc / gcd64(lc, th[p]) * th[p];
+  i128 *cost = (i128 *)malloc((size_t)(s->t ? s->t : 1) * sizeof(i128));
+  int64_t *sm_of = (int64_t *)malloc((size_t)(s->t ? s->t : 1) * sizeof(int64_t));
+  for (int64_t t = 0; t < s->t; ++t) {
+    i128 c = 0;
+    for (int p = 0; p < 3; ++p) {
+      if (!(pipes & (1 << p))) continue;
+      i128 v = s->list[t * 4 + p] * (i128)(lc / th[p]); /* ops_p / Th_p cycles, in 1/lc units */
+      if (v > c) c = v;
+    }
+    cost[t] = c;
+  }
+  if (mode == SCHED_GREEDY) greedy_assign(cost, s->t, s->n_sm, occ, sm_of);
+  else minheap_assign(cost, s->t, s->n_sm, occ, NULL, sm_of);
+  for (int64_t t = 0; t < s->t; ++t) {
+    int64_t j = sm_of[t];
+    for (int q = 0; q < 4; ++q)
+      if (s->sm_sum[j * 4 + q] < SAT128) s->sm_sum[j * 4 + q] += s->list[t * 4 + q];
+    s->sm_count[j] += 1;
+  }
+  free(cost);
+  free(sm_of);
+}
+
 /* One (config, spec) pair through O1..O7.  ints[N_I], flts[N_F]. */
 static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const orc_spec *sp,
                           int flags, int64_t *ints, double *flts) {
@@ -391,6 +501,7 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
   s.n_sm = sp->num_sms;
   s.sm_sum = (i128 *)calloc((size_t)s.n_sm * 4, sizeof(i128));
   s.sm_count = (int64_t *)calloc((size_t)s.n_sm, sizeof(int64_t));
+  s.mode = (flags >> ORC_SCHED_SHIFT) & 3;
 
   switch (fam) { /* O1 + O3 + O4 */
     case FAM_GEMM: decompose_gemm(x, flags, &s); break;
@@ -398,6 +509,11 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
     case FAM_RMSNORM: decompose_rmsnorm(x, &s); break;
     case FAM_SILU: decompose_silu(x, &s); break;
     case FAM_ATTENTION: decompose_attention(x, rag, flags, &s); break;
+  }
+  if (s.mode != SCHED_RR) { /* O3 for GREEDY / MINHEAP over the recorded task list */
+    int64_t th_sched[3] = {tensor_th, sp->th_fma, sp->th_xu};
+    schedule_list(&s, s.mode, occupancy(fam, x, sp), th_sched, pipes_of(fam));
+    free(s.list);
   }
 
   /* O5: per-quantity max over SMs (R7) */
@@ -524,6 +640,22 @@ int orc_featurize(int fam, int64_t n_configs, const int32_t *fields, int64_t fie
  * sm_of[t] = SM of task t (Eq.2 partition). */
 void orc_schedule_rr(int64_t n_tasks, int64_t n_sm, int64_t *sm_of) {
   for (int64_t t = 0; t < n_tasks; ++t) sm_of[t] = t % n_sm;
+}
+
+/* The two non-cyclic schedulers on an explicit cost list (tests pin them with
+ * SPEC S:191-193's examples): sm_of[t] (and worker_of[t] for MINHEAP). */
+void orc_schedule_greedy(const int64_t *cost, int64_t n, int64_t n_sm, int64_t occ, int64_t *sm_of) {
+  i128 *c = (i128 *)malloc((size_t)(n ? n : 1) * sizeof(i128));
+  for (int64_t t = 0; t < n; ++t) c[t] = cost[t];
+  greedy_assign(c, n, n_sm, occ, sm_of);
+  free(c);
+}
+void orc_schedule_minheap(const int64_t *cost, int64_t n, int64_t n_sm, int64_t occ, int64_t *worker_of,
+                          int64_t *sm_of) {
+  i128 *c = (i128 *)malloc((size_t)(n ? n : 1) * sizeof(i128));
+  for (int64_t t = 0; t < n; ++t) c[t] = cost[t];
+  minheap_assign(c, n, n_sm, occ, worker_of, sm_of);
+  free(c);
 }
 
 /* Per-task demand list of one config on one spec (tests: conservation,
