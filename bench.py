@@ -311,7 +311,7 @@ def run_gpu(args, rank, world, local_rank):
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        ctx.featurize(db, specs_h, feats, pairs, stream)
+        ctx.featurize(db, specs_h, feats, pairs, stream, scheduler=args.scheduler)
         if ev is not None:
             ev[1].record(stream)
         ctx.predict(model, feats, lat, None, stream)
@@ -380,6 +380,7 @@ def run_gpu(args, rank, world, local_rank):
             "workload": args.workload, "description": WORKLOADS[args.workload],
             "pairs_per_gpu": n_pairs, "configs_per_gpu": b.n_configs, "specs": g1 - g0,
             "family": gen.FAMILY_NAMES[b.family], "mlp_precision": precision,
+            "scheduler": args.scheduler,
             "parallelism": f"dp{world}" + ("+allgather" if gathered is not None else ""),
             "l2": "flushed between timed steps (256 MiB write, outside the events)",
         },
@@ -672,6 +673,8 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--scale", type=float, default=1.0, help="workload size multiplier (testing)")
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"])
+    ap.add_argument("--scheduler", default="rr", choices=["rr", "greedy", "minheap"],
+                    help="Scheduling Simulator variant (sp_featurize_sched; default cyclic RR)")
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -287,6 +287,34 @@ sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *
                        const sp_pairing *pairs, const sp_features *out, void *stream);
 
 /*
+ * Scheduling Simulator variants ("supporting the two main scheduling
+ * paradigms").  sp_featurize uses SP_SCHED_RR.
+ *   SP_SCHED_RR      hardware round-robin as cyclic dealing, task t -> SM
+ *                    (t mod N_SM) (R5).  Exact for uniform tasks.
+ *   SP_SCHED_GREEDY  hardware round-robin with retirement ("a new task
+ *                    is assigned to an SM when an existing task finishes";
+ *                    SPEC S:183): the first N_SM*occ tasks are dealt
+ *                    cyclically, then each task goes to the SM with the least
+ *                    accumulated busy time.
+ *   SP_SCHED_MINHEAP persistent kernel with a software MinHeap tile scheduler
+ *                    (P:281, P:427 FlashInfer FA3): W = min(N_SM*occ,
+ *                    T) workers, worker w resident on SM (w mod N_SM); each
+ *                    task goes to the worker with the least accumulated busy time.
+ * Busy time of a task = max over the family's pipes of ops_p / Th_p;
+ * ties go to the lowest SM / worker index.  For the uniform-task
+ * families (GEMM, fused MoE, RMSNorm, SiLU&Mul) all three give the cyclic
+ * partition, so they share the closed form.  Attention under GREEDY / MINHEAP
+ * is simulated task by task (one warp per pair): exact, but ~100x slower than
+ * SP_SCHED_RR; SP_E_UNSUPPORTED if the scheduler state of the spec range
+ * (N_SM, or N_SM x max CTAs/SM, 12 bytes each) exceeds a warp's shared memory.
+ */
+typedef enum sp_scheduler { SP_SCHED_RR = 0, SP_SCHED_GREEDY = 1, SP_SCHED_MINHEAP = 2 } sp_scheduler;
+
+sp_status sp_featurize_sched(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs,
+                             const sp_pairing *pairs, int32_t scheduler, const sp_features *out,
+                             void *stream);
+
+/*
  * Predictor stage, steps a10..a12: for each pair p < in->n_pairs,
  * x = normalised Table IV vector of in (O8-O9), e = sigmoid(MLP(x)),
  * latency_us[p] = t_theory_us[p] / e.  efficiency may be NULL.  Pairs with

@@ -321,13 +321,19 @@ class Context:
 
     # -- feature stage (a2..a9)
     def featurize(self, batch: DeviceBatch, specs: Specs, out: Features, pairs=None,
-                  stream=None) -> Features:
+                  stream=None, scheduler: str = "rr") -> Features:
+        """sp_featurize (scheduler "rr") or sp_featurize_sched ("greedy", "minheap")."""
         if pairs is None:
             pairs = cross(0, len(specs))
         cb = batch.c_struct()
         fs = out.c_struct()
-        self._check(lib.sp_featurize(self._h, C.byref(cb), specs.handle, C.byref(pairs),
-                                     C.byref(fs), _stream_ptr(stream)))
+        if scheduler == "rr":
+            self._check(lib.sp_featurize(self._h, C.byref(cb), specs.handle, C.byref(pairs),
+                                         C.byref(fs), _stream_ptr(stream)))
+        else:
+            self._check(lib.sp_featurize_sched(self._h, C.byref(cb), specs.handle, C.byref(pairs),
+                                               _abi.SCHEDULERS[scheduler], C.byref(fs),
+                                               _stream_ptr(stream)))
         return out
 
     # -- predictor stage (a10..a12)

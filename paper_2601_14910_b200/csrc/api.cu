@@ -293,7 +293,15 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
 
 extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs_c,
                                   const sp_pairing *pairs, const sp_features *out, void *stream) {
+  return sp_featurize_sched(ctx, cfg, specs_c, pairs, SP_SCHED_RR, out, stream);
+}
+
+extern "C" sp_status sp_featurize_sched(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs_c,
+                                        const sp_pairing *pairs, int32_t scheduler, const sp_features *out,
+                                        void *stream) {
   if (!ctx) return fail(nullptr, SP_E_ARG, "sp_featurize: ctx is NULL");
+  if (scheduler != SP_SCHED_RR && scheduler != SP_SCHED_GREEDY && scheduler != SP_SCHED_MINHEAP)
+    return fail(ctx, SP_E_ARG, "sp_featurize_sched: unknown scheduler");
   if (!cfg || !specs_c || !pairs || !out) return fail(ctx, SP_E_ARG, "sp_featurize: NULL argument");
   sp_specs *specs = const_cast<sp_specs *>(specs_c);
   const int fam = cfg->family;
@@ -332,7 +340,20 @@ extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const
   FeatOut fo{out->ints, out->flts, out->status, out->ld};
   const DevSpec *ds = (const DevSpec *)specs->dev.p;
   int e;
-  if (fam == SP_ATTENTION) {
+  if (fam == SP_ATTENTION && scheduler != SP_SCHED_RR) {
+    // sequential scheduler simulation: per-warp shared memory for the largest target set
+    const bool cross = pairs->kind == SP_PAIRS_CROSS;
+    const int b = cross ? pairs->spec_begin : 0, en = cross ? pairs->spec_end : specs->n;
+    int64_t max_targets = 1;
+    for (int g = b; g < en; ++g) {
+      const int64_t n = specs->host[g].num_sms;
+      max_targets = std::max(max_targets, scheduler == SP_SCHED_GREEDY ? n : n * specs->host[g].max_ctas_per_sm);
+    }
+    if (attention_sim_smem_bytes(max_targets) > 227 * 1024)
+      return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_sched: scheduler state of these specs exceeds shared memory");
+    e = launch_attention_sim(scheduler, cv, ds, b, en, specs->n, n_pairs, cross ? nullptr : pairs->cfg_idx,
+                             cross ? nullptr : pairs->spec_idx, max_targets, fo, ctx->num_sms, stream, ctx->hook());
+  } else if (fam == SP_ATTENTION) {
     if (pairs->kind == SP_PAIRS_CROSS) {
       const AttnPlan *plan = nullptr;
       sp_status st = attn_plan(ctx, specs, pairs->spec_begin, pairs->spec_end, &plan);

@@ -23,6 +23,8 @@
 // The kernel is bound by integer issue, not by HBM.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace sp {
@@ -33,6 +35,7 @@ namespace {
 #endif
 
 constexpr int kWarps = 8;           // warps per block
+constexpr int kSimWarps = 4;        // warps per block of the scheduler-simulation kernel
 constexpr int kMaxDistinct = 8;     // distinct SM counts per group (api.cu plans accordingly)
 constexpr int64_t kI32Max = 2147483647LL;
 constexpr int64_t kU32Max = 4294967295LL;
@@ -681,6 +684,187 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
   }
 }
 
+// ---------------------------------------------------------------------------
+// Non-cyclic schedulers: SP_SCHED_GREEDY (hardware RR
+// with retirement: the first N*occ tasks dealt cyclically, then each task to
+// the SM with the least busy time) and SP_SCHED_MINHEAP
+// (persistent kernel: W = min(N*occ, T) workers pinned round-robin to SMs,
+// each task to the least-loaded worker).  Ties: lowest index.
+//
+// A task's busy time max(Tensor/Th_T, XU/Th_X) is u * max(4 BQ hd BKV / Th_T,
+// BQ (BKV+1) / Th_X): both pipes scale with its kv units u, so the greedy
+// order is decided by u-sums alone -- exact integers, no spec throughput.
+// The decisions are sequential, so one warp walks one pair's full task list
+// (all kv-heads, R4 order) and keeps the per-target loads in shared memory
+// with a two-level min structure: per 32-entry group, its least (load, index);
+// a task costs one scan of the group minima, one update and one group rescan,
+// each a warp reduction.  This is the modelling path for persistent kernels
+// (FlashInfer FA3); it is ~100x slower per pair than the cyclic path.
+struct SimRegion {
+  uint64_t *load;   // [W]
+  uint32_t *count;  // [W]
+  uint64_t *gmin;   // [G] least load of each 32-entry group
+  uint32_t *gidx;   // [G] its index
+};
+
+// Warp-wide least (load, idx): least load, then lowest index among equals.
+__device__ __forceinline__ void warp_argmin(uint64_t &ld, uint32_t &ix) {
+  const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(ld >> 32));
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(ld >> 32) == hi ? (uint32_t)ld : 0xffffffffu);
+  const bool win = (uint32_t)(ld >> 32) == hi && (uint32_t)ld == lo;
+  ix = __reduce_min_sync(0xffffffffu, win ? ix : 0xffffffffu);
+  ld = ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ void group_rescan(const SimRegion &r, uint32_t W, uint32_t g, int lane) {
+  const uint32_t i = g * 32 + lane;
+  uint64_t ld = i < W ? r.load[i] : ~0ull;
+  uint32_t ix = i < W ? i : 0xffffffffu;
+  warp_argmin(ld, ix);
+  if (lane == 0) {
+    r.gmin[g] = ld;
+    r.gidx[g] = ix;
+  }
+  __syncwarp();
+}
+
+template <int MODE>  // 1 GREEDY, 2 MINHEAP
+__device__ void attn_sim_pair(const AttnCfg &a, const SimRegion &r, uint32_t N, uint32_t occ, int lane, int64_t &L,
+                              uint64_t &U, DistinctMax &m, int &st) {
+  const FastDiv fg = make_fd((uint32_t)a.g);
+  L = count_tasks(a, lane, fg);
+  if (L > kI32Max || L * a.nkv > kI32Max) { st = SP_PAIR_E_RANGE; return; }
+  const uint32_t T = (uint32_t)(L * a.nkv);
+  const uint64_t slots = (uint64_t)N * occ;
+  const uint32_t W = MODE == 1 ? N : (uint32_t)(slots < T ? slots : T);
+  const uint32_t R = MODE == 1 ? (uint32_t)(slots < T ? slots : T) : W;  // tasks placed without a search
+  const uint32_t G = (W + 31) / 32;
+  for (uint32_t i = lane; i < W; i += 32) {
+    r.load[i] = 0;
+    r.count[i] = 0;
+  }
+  __syncwarp();
+  uint32_t t = 0, tgt = 0;  // task index; its cyclic target while t < R (tgt = t mod N, or t)
+  uint64_t usum = 0;
+  auto place = [&](uint32_t u) {
+    if (t < R) {
+      if (lane == 0) {
+        r.load[tgt] += u;
+        r.count[tgt] += 1;
+      }
+      ++tgt;
+      if (MODE == 1 && tgt == N) tgt = 0;
+      if (++t == R && R < T) {  // all resident slots taken: build the group minima
+        __syncwarp();
+        for (uint32_t g = 0; g < G; ++g) group_rescan(r, W, g, lane);
+      }
+      return;
+    }
+    uint64_t ld = ~0ull;
+    uint32_t ix = 0xffffffffu;
+    for (uint32_t g = lane; g < G; g += 32) {
+      const uint64_t v = r.gmin[g];
+      const uint32_t vi = r.gidx[g];
+      if (v < ld || (v == ld && vi < ix)) { ld = v; ix = vi; }
+    }
+    warp_argmin(ld, ix);
+    if (lane == 0) {
+      r.load[ix] += u;
+      r.count[ix] += 1;
+    }
+    __syncwarp();
+    group_rescan(r, W, ix / 32, lane);
+    ++t;
+  };
+  // the task stream (R4): kv-head outermost, then request, q-block, kv-chunk
+  for (int32_t h = 0; h < a.nkv; ++h) {
+    for (int64_t b = 0; b < a.bs; ++b) {
+      const uint32_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
+      const uint64_t rows = (uint64_t)q * a.g, nqb = (rows + a.bq - 1) / a.bq;
+      for (uint64_t i = 0; i < nqb; ++i) {
+        const uint32_t need = kv_need(i, a.bq, rows, q, kv, a.causal, fg);
+        if (a.chunk == 0) {
+          const uint32_t u = (uint32_t)((need + a.bkv - 1) / a.bkv);
+          if (h == 0) usum += u;
+          place(u);
+        } else {
+          for (uint64_t c0 = 0; c0 < need; c0 += a.chunk) {
+            const uint32_t u = (uint32_t)((min((uint64_t)a.chunk, need - c0) + a.bkv - 1) / a.bkv);
+            if (h == 0) usum += u;
+            place(u);
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  U = usum;
+  if (U > (uint64_t)kU32Max) { st = SP_PAIR_E_RANGE; return; }
+  // per-SM task count n_j and unit sum S_j (MINHEAP: sum of the SM's workers)
+  int64_t mS = 0, mB = 0;
+  for (uint32_t j = lane; j < N; j += 32) {
+    uint64_t S = 0, n = 0;
+    for (uint32_t w = j; w < W; w += N) {
+      S += r.load[w];
+      n += r.count[w];
+    }
+    mS = max(mS, (int64_t)S);
+    mB = max(mB, (int64_t)a.bq * (int64_t)n + 2 * (int64_t)a.bkv * (int64_t)S);
+  }
+  m.maxS = warp_max64(mS);
+  m.maxB = warp_max64(mB);
+  st = 0;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kSimWarps * 32) attn_sched_sim(ConfigView cfg, const DevSpec *__restrict__ specs,
+                                                               int g0, int n_specs, int64_t n_pairs,
+                                                               const int64_t *__restrict__ cfg_idx,
+                                                               const int32_t *__restrict__ spec_idx,
+                                                               int64_t words_per_warp, FeatOut out) {
+  extern __shared__ uint64_t sim_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  uint64_t *base = sim_smem + (size_t)warp * words_per_warp;
+  const int64_t C = cfg.n_configs;
+  for (int64_t p = (int64_t)blockIdx.x * nw + warp; p < n_pairs; p += (int64_t)gridDim.x * nw) {
+    int64_t c;
+    int32_t g;
+    if (cfg_idx) {
+      c = __ldg(cfg_idx + p);
+      g = __ldg(spec_idx + p);
+      if (c < 0 || c >= C || g < 0 || g >= n_specs) {
+        if (lane == 0) emit_error(out, p, SP_PAIR_E_INDEX);
+        continue;
+      }
+    } else {
+      c = p % C;
+      g = g0 + (int32_t)(p / C);
+    }
+    const DevSpec &sp = specs[g];
+    const AttnCfg a = load_cfg(cfg, c, lane);
+    int st = a.status;
+    int64_t L = 0;
+    uint64_t U = 0;
+    DistinctMax m{0, 0};
+    if (st == 0) {
+      const uint32_t N = (uint32_t)sp.num_sms;
+      const uint32_t occ = (uint32_t)occupancy(a.fp, sp);
+      const uint64_t W = MODE == 1 ? N : (uint64_t)N * occ;  // upper bound of the targets
+      SimRegion r;
+      r.load = base;
+      r.count = reinterpret_cast<uint32_t *>(base + W);
+      r.gmin = base + W + (W + 1) / 2;
+      r.gidx = reinterpret_cast<uint32_t *>(r.gmin + (W + 31) / 32);
+      attn_sim_pair<MODE>(a, r, N, occ, lane, L, U, m, st);
+    }
+    if (lane == 0) attn_emit(out, p, a, st, L, U, m, sp);
+    __syncwarp();
+  }
+}
+
+// 64-bit words of shared memory one warp needs for W targets.
+__host__ __device__ constexpr int64_t sim_words(int64_t W) { return W + (W + 1) / 2 + 2 * ((W + 31) / 32) + 2; }
+
 template <int ND, bool SMALL>
 int launch_cross(const ConfigView &cfg, const AttnPlan &plan, const AttnResults &res, int num_device_sms,
                  cudaStream_t st, int group_y0, int n_groups, const LaunchHook &hook) {
@@ -722,6 +906,33 @@ int launch_nd(int nd, const ConfigView &cfg, const AttnPlan &plan, const AttnRes
 }
 
 }  // namespace
+
+int launch_attention_sim(int mode, const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
+                         int n_specs, int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx,
+                         int64_t max_targets, const FeatOut &out, int num_device_sms, void *stream,
+                         const LaunchHook &hook) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (n_pairs == 0) return 0;
+  const int64_t words = sim_words(max_targets);
+  const int64_t budget = 227 * 1024;
+  const int nw = (int)std::min<int64_t>(kSimWarps, budget / (words * 8));
+  if (nw < 1) return (int)cudaErrorInvalidValue;  // the caller checks attention_sim_smem_bytes first
+  const size_t smem = (size_t)nw * words * 8;
+  void (*kern)(ConfigView, const DevSpec *, int, int, int64_t, const int64_t *, const int32_t *, int64_t, FeatOut) =
+      mode == SP_SCHED_GREEDY ? attn_sched_sim<1> : attn_sched_sim<2>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  int64_t want = (n_pairs + nw - 1) / nw;
+  int64_t cap = (int64_t)num_device_sms * 16;
+  hook.on_begin(mode == SP_SCHED_GREEDY ? "attn_sched_greedy" : "attn_sched_minheap", st);
+  kern<<<(unsigned)(want < cap ? want : cap), nw * 32, smem, st>>>(
+      cfg, specs, spec_begin, cfg_idx ? n_specs : spec_end - spec_begin, n_pairs, cfg_idx, spec_idx, words, out);
+  hook.on_end(st);
+  return (int)cudaGetLastError();
+}
+
+// shared memory one warp of the simulation kernel needs (<= 227 KB or unsupported)
+int64_t attention_sim_smem_bytes(int64_t max_targets) { return sim_words(max_targets) * 8; }
 
 int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
                                int n_specs, const AttnPlan &plan, const AttnResults &res, int64_t n_pairs,

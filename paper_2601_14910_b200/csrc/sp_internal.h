@@ -117,6 +117,15 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
                                const int64_t *cfg_idx, const int32_t *spec_idx, int32_t max_sms,
                                const FeatOut &out, int num_device_sms, void *stream, const LaunchHook &hook);
 
+// Attention under SP_SCHED_GREEDY / SP_SCHED_MINHEAP: warp per pair, sequential
+// scheduler simulation (CROSS when cfg_idx == nullptr, else LIST).  max_targets =
+// largest SM count (GREEDY) or SM count x max CTAs/SM (MINHEAP) over the specs.
+int launch_attention_sim(int mode, const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
+                         int n_specs, int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx,
+                         int64_t max_targets, const FeatOut &out, int num_device_sms, void *stream,
+                         const LaunchHook &hook);
+int64_t attention_sim_smem_bytes(int64_t max_targets);  // per warp
+
 // MLP predictor.
 struct MlpFp32 {        // DEVICE pointers, fp32
   const float *w1t;     // [n_in][256]  (transposed: k-major)
