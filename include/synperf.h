@@ -325,6 +325,37 @@ sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_features *in, 
                      float *efficiency, void *stream);
 
 /*
+ * Performance-gap diagnosis (PAPER §VII).  A
+ * second estimator trained with quantile loss at q = 0.8 predicts the
+ * "Potential Performance Ceiling" efficiency y_p80; it is an
+ * ordinary sp_model run through sp_predict (its `efficiency` output).  For
+ * every pair, with measured latency m:
+ *   y_actual = t_theory_us / m          (efficiency, P:489's definition)
+ *   gap      = y_p80 - y_actual          ("perf_gap")
+ *   underperforming <=> gap > 0.1        (strict)
+ * all in fp32 (IEEE division and subtraction).  Pairs with status != 0, a
+ * NaN operand or m <= 0 are skipped (counted in neither total).
+ *   in:        features of the pairs (t_theory_us = flts[11], status)
+ *   eff_p80:   DEVICE fp32 [n_pairs], sp_predict's efficiency of the P80 model
+ *   measured_us: DEVICE fp32 [n_pairs]
+ *   pairs:     how pair p maps to a spec: SP_PAIRS_CROSS (spec = spec_begin +
+ *              p / n_configs, spec-major as sp_featurize writes) or
+ *              SP_PAIRS_LIST (spec_idx[p]); G = number of spec slots
+ *              (CROSS: spec_end - spec_begin; LIST: n_specs below)
+ *   n_configs: configs per spec (CROSS); n_specs: slots (LIST)
+ * Outputs (DEVICE, caller-owned, zeroed by the call; gap may be NULL):
+ *   gap        fp32 [n_pairs] (NaN for skipped pairs)
+ *   counts     int64 [G][2]: {valid pairs, underperforming pairs} per spec
+ *   hist       int64 [G][n_bins]: gap histogram on [gap_lo, gap_hi), the end
+ *              bins also collect the gaps below / above (the CDF of Fig. 7)
+ * Asynchronous on `stream`.
+ */
+#define SP_GAP_THRESHOLD 0.1f
+sp_status sp_perf_gap(sp_ctx *ctx, const sp_features *in, const float *eff_p80, const float *measured_us,
+                      const sp_pairing *pairs, int64_t n_configs, int32_t n_specs, int32_t n_bins,
+                      float gap_lo, float gap_hi, float *gap, int64_t *counts, int64_t *hist, void *stream);
+
+/*
  * Kernel accounting, for measurement (bench.py's roofline and launch count,
  * DESIGN.md section 6).  Every kernel launched by sp_featurize / sp_predict is
  * counted per kernel name.  With profiling enabled (off by default) each such

@@ -347,6 +347,28 @@ class Context:
                                    _stream_ptr(stream)))
         return latency
 
+    # -- performance-gap diagnosis (PAPER §VII-B)
+    def perf_gap(self, feats: Features, eff_p80: torch.Tensor, measured_us: torch.Tensor, pairs=None,
+                 n_configs: int = 0, n_specs: int = 0, n_bins: int = 100, gap_lo: float = -0.5,
+                 gap_hi: float = 0.5, want_gap: bool = True, stream=None):
+        """sp_perf_gap: returns (gap fp32 [n] or None, counts int64 [G, 2] = {valid,
+        underperforming}, hist int64 [G, n_bins]) as device tensors."""
+        if pairs is None:
+            pairs = cross(0, n_specs)
+        G = (pairs.spec_end - pairs.spec_begin) if pairs.kind == _abi.SP_PAIRS_CROSS else n_specs
+        dev = self.torch_device
+        n = feats.n_pairs
+        gap = torch.empty(max(n, 1), dtype=torch.float32, device=dev) if want_gap else None
+        counts = torch.empty((max(G, 1), 2), dtype=torch.int64, device=dev)
+        hist = torch.empty((max(G, 1), n_bins), dtype=torch.int64, device=dev)
+        fs = feats.c_struct()
+        self._check(lib.sp_perf_gap(self._h, C.byref(fs), eff_p80.data_ptr(), measured_us.data_ptr(),
+                                    C.byref(pairs), int(n_configs), int(n_specs), int(n_bins),
+                                    float(gap_lo), float(gap_hi),
+                                    gap.data_ptr() if gap is not None else None, counts.data_ptr(),
+                                    hist.data_ptr(), _stream_ptr(stream)))
+        return (gap[:n] if gap is not None else None), counts[:G], hist[:G]
+
     # -- end-to-end serving composition (PAPER §V-D; include/synperf.h sp_e2e_*)
 
     def load_comm_model(self, comm: dict) -> CommModel:

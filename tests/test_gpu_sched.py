@@ -112,3 +112,44 @@ def test_unsupported_scheduler_state(sp, ctx):
     s = tiny_spec(4096, 32)
     with pytest.raises(sp.SynPerfError, match="SP_E_UNSUPPORTED"):
         run(sp, ctx, b, s, "minheap")
+
+
+# ---------------------------------------------------------------- NEXT-3 gap diagnosis
+
+@pytest.mark.parametrize("kind", ["cross", "list"])
+def test_perf_gap_parity(sp, ctx, orc, kind):
+    """sp_perf_gap vs oracle/gap.py: fp32 gap bit-exact, counts and histogram exact."""
+    from oracle import gap as OG
+    from workloads import models
+
+    b = gen.gen_moe(400, 31)
+    sa = specs.paper_gpu_specs()
+    sh = ctx.load_gpu_specs(sa)
+    db = sp.DeviceBatch.from_host(b, ctx.torch_device)
+    G = len(sa)
+    n = G * b.n_configs
+    f = sp.Features.empty(b.family, n, ctx.torch_device)
+    ctx.featurize(db, sh, f)
+    p80m = ctx.load_model(models.random_mlp(b.family, 77), "fp16")
+    lat = torch.empty(n, dtype=torch.float32, device="cuda")
+    eff = torch.empty(n, dtype=torch.float32, device="cuda")
+    ctx.predict(p80m, f, lat, eff)
+    _, gf, gs = sp.features_to_host(f)
+    rng = np.random.default_rng(9)
+    meas = (gf[11] / rng.uniform(0.05, 1.0, n)).astype(np.float32)  # measured latencies
+    meas[rng.uniform(0, 1, n) < 0.01] = 0.0  # some invalid measurements
+    meas_d = torch.from_numpy(meas).cuda()
+    if kind == "cross":
+        gap, counts, hist = ctx.perf_gap(f, eff, meas_d, sp.cross(0, G), n_configs=b.n_configs, n_bins=64)
+        spec_of = np.arange(n) // b.n_configs
+    else:
+        spec_of = rng.integers(0, 5, n)
+        pl = sp.pair_list(torch.arange(n, dtype=torch.int64).cuda(),
+                          torch.from_numpy(spec_of.astype(np.int32)).cuda())
+        gap, counts, hist = ctx.perf_gap(f, eff, meas_d, pl, n_specs=5, n_bins=64)
+    torch.cuda.synchronize()
+    og, oc, oh = OG.perf_gap(gf[11], gs, eff.cpu().numpy(), meas, spec_of, int(counts.shape[0]), n_bins=64)
+    assert np.array_equal(gap.cpu().numpy(), og, equal_nan=True)
+    assert np.array_equal(counts.cpu().numpy(), oc)
+    assert np.array_equal(hist.cpu().numpy(), oh)
+    assert oc[:, 1].sum() > 0 and oc[:, 0].sum() < n
