@@ -536,7 +536,9 @@ class Context:
 
         The configs are split into `chunks` slices pipelined over three
         streams: the H2D of slice i+1 and the D2H of slice i-1 overlap the
-        kernels of slice i.  Device buffers are cached across calls."""
+        kernels of slice i (the ragged request / histogram data is copied
+        whole, ahead of the first slice).  Device buffers are cached across
+        calls."""
         g0, g1 = spec_range if spec_range is not None else (0, len(specs))
         G = g1 - g0
         fam = int(batch.family)
@@ -583,10 +585,11 @@ class Context:
         s_h2d, s_d2h = cache["h2d"], cache["d2h"]
         s_h2d.wait_stream(comp)
         out2d = out_t[:n].view(G, C)
-        if rh is not None and oh is not None:
-            o = oh.numpy()
-            lens = (2 * fh[0].numpy().astype(np.int64) if fam == _abi.SP_ATTENTION
-                    else fh[1].numpy().astype(np.int64))  # attention: 2*bs; MoE: E
+        if rh is not None and rh.numel() > 0:
+            # the ragged data goes first, in one copy: locating each slice's own
+            # ragged range on the host costs more than the copy it would overlap
+            with torch.cuda.stream(s_h2d):
+                cache["ragged"][:rh.numel()].copy_(rh, non_blocking=True)
         d2h_done = []
         for i, (c0, c1) in enumerate(zip(bounds, bounds[1:])):
             nc = c1 - c0
@@ -595,11 +598,6 @@ class Context:
                     cache["fields"][fi, c0:c1].copy_(fh[fi, c0:c1], non_blocking=True)
                 if cache["roff"] is not None:
                     cache["roff"][c0:c1].copy_(oh[c0:c1], non_blocking=True)
-                    valid = o[c0:c1] >= 0
-                    if valid.any():
-                        r0 = int(o[c0:c1][valid].min())
-                        r1 = int((o[c0:c1][valid] + lens[c0:c1][valid]).max())
-                        cache["ragged"][r0:r1].copy_(rh[r0:r1], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(s_h2d)
             comp.wait_event(ev)

@@ -1,0 +1,80 @@
+"""Throughput of the §8(f) variants on one B200 (one JSON line each):
+  * sp_featurize_sched GREEDY / MINHEAP on a slice of BASELINE config 2
+    (attention x 11 GPUs; sequential scheduler simulation, warp per pair);
+  * sp_perf_gap (P80 gap diagnosis) over BASELINE config 3 (fused MoE x 11,
+    the paper applies it to its fused-MoE dataset).
+Device-timed with CUDA events, median of --reps after warm-up.
+
+    python tools/bench_variants.py [--reps 5] [--scale 0.02]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2601_14910_b200 as sp  # noqa: E402
+from workloads import models  # noqa: E402
+
+
+def timed(fn, reps):
+    for _ in range(2):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--scale", type=float, default=0.02, help="fraction of config 2 for the scheduler variants")
+    args = ap.parse_args()
+    ctx = sp.Context(0)
+    # ---- scheduler variants on a config-2 slice
+    b, sa, (g0, g1), _ = bench.build_workload("cfg2", 0, 1, args.scale)
+    sh = ctx.load_gpu_specs(sa)
+    db = sp.DeviceBatch.from_host(b, "cuda:0")
+    n = (g1 - g0) * b.n_configs
+    f = sp.Features.empty(b.family, n, "cuda:0")
+    for mode in ("rr", "greedy", "minheap"):
+        ms = timed(lambda: ctx.featurize(db, sh, f, sp.cross(g0, g1), scheduler=mode), args.reps)
+        print(json.dumps({"variant": f"featurize_{mode}", "workload": f"cfg2 x{args.scale}", "pairs": n,
+                          "ms": ms, "pairs_per_s": n / (ms * 1e-3)}), flush=True)
+    # ---- gap diagnosis over config 3
+    b, sa, (g0, g1), _ = bench.build_workload("cfg3", 0, 1, 1.0)
+    sh = ctx.load_gpu_specs(sa)
+    db = sp.DeviceBatch.from_host(b, "cuda:0")
+    n = (g1 - g0) * b.n_configs
+    f = sp.Features.empty(b.family, n, "cuda:0")
+    ctx.featurize(db, sh, f)
+    m = ctx.load_model(models.random_mlp(b.family, 80), "fp16")
+    lat = torch.empty(n, dtype=torch.float32, device="cuda:0")
+    eff = torch.empty(n, dtype=torch.float32, device="cuda:0")
+    ctx.predict(m, f, lat, eff)
+    meas = lat * torch.empty_like(lat).uniform_(1.0, 3.0)  # synthetic "measured" latencies
+    pr = sp.cross(g0, g1)
+    ms = timed(lambda: ctx.perf_gap(f, eff, meas, pr, n_configs=b.n_configs), args.reps)
+    _, counts, _ = ctx.perf_gap(f, eff, meas, pr, n_configs=b.n_configs)
+    c = counts.cpu().numpy()
+    nbytes = n * (4 + 1 + 4 + 4 + 4)  # t_theory, status, y_p80, measured read; gap written
+    print(json.dumps({"variant": "perf_gap", "workload": "cfg3", "pairs": n, "ms": ms,
+                      "pairs_per_s": n / (ms * 1e-3), "achieved_gbs": nbytes / (ms * 1e-3) / 1e9,
+                      "underperforming": int(c[:, 1].sum()), "valid": int(c[:, 0].sum())}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
