@@ -225,7 +225,7 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
   Ns.erase(std::unique(Ns.begin(), Ns.end()), Ns.end());
   if (!Ns.empty() && Ns.back() > kAttnMaxSms)
     return fail(ctx, SP_E_UNSUPPORTED, "attention featurization supports at most 4096 SMs per spec");
-  const int budget = std::max(kAttnWordBudget, Ns.empty() ? 0 : ((Ns.back() + 3) & ~3));
+  const int budget = std::max(kAttnWordBudget, Ns.empty() ? 0 : ((Ns.back() + kAttnSlack + 3) & ~3));
   std::vector<AttnGroup> groups;
   std::vector<int32_t> gspecs, sdist, dn, doff;
   size_t i = 0;
@@ -234,10 +234,10 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
     AttnGroup gr{};
     gr.distinct_first = (int32_t)dn.size();
     int words = 0;
-    while (i < Ns.size() && gr.n_distinct < kAttnMaxDistinct && words + Ns[i] <= budget) {
+    while (i < Ns.size() && gr.n_distinct < kAttnMaxDistinct && words + Ns[i] + kAttnSlack <= budget) {
       dn.push_back(Ns[i]);
       doff.push_back(words);
-      words += Ns[i];
+      words += Ns[i] + kAttnSlack;  // + the lazy-wrap overflow of the region
       ++gr.n_distinct;
       ++i;
     }
@@ -280,7 +280,7 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
   pd->view.words_per_warp = words_max + kAttnScratchWords;  // accumulators + request scratch
   for (const AttnGroup &gr : groups) {
     pd->nd.push_back(gr.n_distinct);
-    pd->small.push_back(dn[gr.distinct_first] < 32);  // Ns ascending: first is the smallest
+    pd->small.push_back(dn[gr.distinct_first] < kAttnLazyMinN);  // Ns ascending: first is the smallest
   }
   pd->view.host_nd = pd->nd.data();
   pd->view.host_small = pd->small.data();

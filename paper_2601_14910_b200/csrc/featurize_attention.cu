@@ -328,7 +328,11 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       const FastDiv f{r1, r2, r3};  // chunk index kl mod n_ch: full chunks, then the last one
       return f.mod(kl) == f.d - 1u ? rul : ruf;
     };
-    // one step: lane task base + k0 + lane gets u (0 for idle lanes)
+    // one step: lane task base + k0 + lane gets u (0 for idle lanes).  The
+    // residue pointers wrap lazily: each region has kAttnSlack words past N, so
+    // a pointer may run up to 2 steps (index <= N + 31) before wrap() brings it
+    // back below N (N >= 64 on this path): the wrap test is paid every other
+    // step (ncu: it was 18% of the kernel's instructions when paid every step).
     auto add = [&](uint32_t k, uint32_t u, bool active) {
       usum += u;
       if (SMALL) {
@@ -341,10 +345,15 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
           // one ATOMS.ADD instead of load + add + store: the kernel is issue bound
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(p[d]), "r"(u) : "memory");
           p[d] += 128u;
-          p[d] = p[d] >= hi[d] ? p[d] - 4u * (uint32_t)N[d] : p[d];
         }
       }
       __syncwarp();
+    };
+    auto wrap = [&]() {
+      if (!SMALL) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) p[d] = p[d] >= hi[d] ? p[d] - 4u * (uint32_t)N[d] : p[d];
+      }
     };
     uint32_t bcur = 0;  // chunk-local request holding task k0
     uint32_t k0 = 0;
@@ -359,15 +368,32 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
           // t = q - (kl+1)*BQ/g stepping by -32*BQ/g (R10-R11; exact for the last q-block too,
           // where the min takes kv).  q < 2^30 and 33*BQ < 2^30 keep t in int32.
           int32_t t = (int32_t)r2 - (int32_t)(k0 + lane - st + 1u) * (int32_t)a_per;
-          for (; k0 + 32 <= nxt; k0 += 32) {
-            const uint32_t need = r3 - (uint32_t)max(t, 0);  // >= kv - q + 1 >= 1
-            add(k0 + lane, fbkv.div31(need - 1u) + 1u, true);
+          for (; k0 + 64 <= nxt; k0 += 64) {
+            const uint32_t need0 = r3 - (uint32_t)max(t, 0);  // >= kv - q + 1 >= 1
+            add(k0 + lane, fbkv.div31(need0 - 1u) + 1u, true);
             t -= 32 * (int32_t)a_per;
+            const uint32_t need1 = r3 - (uint32_t)max(t, 0);
+            add(k0 + 32 + lane, fbkv.div31(need1 - 1u) + 1u, true);
+            t -= 32 * (int32_t)a_per;
+            wrap();
           }
-        } else
-        for (; k0 + 32 <= nxt; k0 += 32) {
-          const uint32_t k = k0 + lane;
-          add(k, unit(k - st, r1, r2, r3, ruf, rul), true);
+          if (k0 + 32 <= nxt) {
+            const uint32_t need = r3 - (uint32_t)max(t, 0);
+            add(k0 + lane, fbkv.div31(need - 1u) + 1u, true);
+            wrap();
+            k0 += 32;
+          }
+        } else {
+          for (; k0 + 64 <= nxt; k0 += 64) {
+            add(k0 + lane, unit(k0 + lane - st, r1, r2, r3, ruf, rul), true);
+            add(k0 + 32 + lane, unit(k0 + 32 + lane - st, r1, r2, r3, ruf, rul), true);
+            wrap();
+          }
+          if (k0 + 32 <= nxt) {
+            add(k0 + lane, unit(k0 + lane - st, r1, r2, r3, ruf, rul), true);
+            wrap();
+            k0 += 32;
+          }
         }
         if (k0 >= total) break;
         if (k0 == nxt) { ++bcur; continue; }
@@ -381,10 +407,16 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       const uint32_t bl = min(bcur + __popc(M & lm_le), nreq - 1);
       const uint32_t u = unit(k - s_start[bl], s_a1[bl], s_a2[bl], s_a3[bl], s_uf[bl], s_ul[bl]);
       add(k, active ? u : 0u, active);
+      wrap();
       bcur += __popc(M) + (__any_sync(0xffffffffu, has && start == k0 + 32) ? 1u : 0u);
       k0 += 32;
     }
     base += total;
+    __syncwarp();
+  }
+  if (!SMALL) {  // fold the lazy-wrap overflow A[N, N+32) back onto A[0, 32)
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[off[d] + lane] += acc[off[d] + N[d] + lane];
     __syncwarp();
   }
   return warp_sum_u64(usum);
@@ -585,7 +617,7 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) attn_schedule_cross
     N[d] = __ldg(plan.distinct_n + grp.distinct_first + d);
     off[d] = __ldg(plan.distinct_off + grp.distinct_first + d);
     minN = min(minN, N[d]);
-    words = max(words, off[d] + N[d]);
+    words = max(words, off[d] + N[d] + kAttnSlack);
   }
   words = (words + 3) & ~3;
   if (threadIdx.x < ND) s_fd[threadIdx.x] = make_fd((uint32_t)N[threadIdx.x]);
@@ -670,9 +702,9 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
     int st = a.status;
     int64_t L = 0;
     uint64_t U = 0;
-    const int words = (N[0] + 3) & ~3;
+    const int words = (N[0] + kAttnSlack + 3) & ~3;
     if (st == 0) {
-      if (N[0] >= 32)
+      if (N[0] >= kAttnLazyMinN)
         st = attn_config<1, false>(a, acc, words, scr, N, off, s_fd + warp, N[0], lane, L, U, &s_m[warp][0],
                                    &s_m[warp][1], 1);
       else
@@ -962,7 +994,7 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
     return (int)cudaGetLastError();
   }
   if (n_pairs == 0) return 0;
-  const int words = ((max_sms + 3) & ~3) + kAttnScratchWords;  // accumulators + request scratch
+  const int words = ((max_sms + kAttnSlack + 3) & ~3) + kAttnScratchWords;  // accumulators + request scratch
   const size_t smem = (size_t)kWarps * words * 4;
   cudaError_t e = cudaFuncSetAttribute(featurize_attention_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

@@ -79,6 +79,10 @@ struct AttnGroup {
 };
 // per-warp shared memory after the accumulators: the request scratch (7 x 32 words)
 constexpr int kAttnScratchWords = 224;
+// Lazy residue wrap (featurize_attention.cu accumulate): every accumulator
+// region has kAttnSlack words past its N; the non-atomic path needs N >= 64.
+constexpr int kAttnSlack = 32;
+constexpr int kAttnLazyMinN = 64;
 constexpr int kAttnMaxGroups = 4096;  // work counters per launch (sp_ctx scratch)
 struct AttnPlan {
   const AttnGroup *groups;     // DEVICE [n_groups]
@@ -89,7 +93,7 @@ struct AttnPlan {
   int32_t n_groups;
   int32_t words_per_warp;      // u32 accumulator words per warp
   const int32_t *host_nd;      // HOST [n_groups]: distinct count per group (kernel template)
-  const uint8_t *host_small;   // HOST [n_groups]: group holds an SM count < 32 (atomic path)
+  const uint8_t *host_small;   // HOST [n_groups]: group holds an SM count < kAttnLazyMinN (atomic path)
   int *counters;               // DEVICE [n_groups] work counters (context scratch, zeroed per launch)
   const int32_t *spec_slot;    // DEVICE, per spec of the range: its distinct slot (absolute)
   int32_t n_slots;             // distinct slots over all groups
