@@ -347,7 +347,9 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
           p[d] += 128u;
         }
       }
-      __syncwarp();
+      // distinct addresses per step and no reads until the loop ends (the
+      // __syncwarp after it orders them for the fold); the atomic path may diverge
+      if (SMALL) __syncwarp();
     };
     auto wrap = [&]() {
       if (!SMALL) {
@@ -496,7 +498,14 @@ __device__ DistinctMax fold(const AttnCfg &a, uint32_t *A, int32_t N, const Fast
       else m_hi = max(m_hi, S);
     }
   }
-  const int64_t lo = warp_max64((int64_t)m_lo), hi = warp_max64((int64_t)m_hi);
+  int64_t lo, hi;
+  if (sizeof(SumT) == 4) {  // one REDUX each instead of a 5-step 64-bit shuffle tree
+    lo = (int64_t)__reduce_max_sync(0xffffffffu, (uint32_t)m_lo);
+    hi = (int64_t)__reduce_max_sync(0xffffffffu, (uint32_t)m_hi);
+  } else {
+    lo = warp_max64((int64_t)m_lo);
+    hi = warp_max64((int64_t)m_hi);
+  }
   int64_t mB = 0;
   if (rn > 0) mB = (int64_t)a.bq * (qn + 1) + 2 * (int64_t)a.bkv * lo;
   if (rn < (uint32_t)N) mB = max(mB, (int64_t)a.bq * qn + 2 * (int64_t)a.bkv * hi);
