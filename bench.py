@@ -41,6 +41,8 @@ WORKLOADS = {
     "cfg4": "E2E serving iterations: Llama-3-8B + Qwen2.5-14B over 256 static-batch request traces "
             "(arxiv/splitwise-like), per-kernel predictions composed per step, x 11 GPU specs",
     "cfg5": "1,000 serving GEMMs x 100,000 hypothetical GPU specs (1e8 pairs), sharded by spec",
+    "scaledmm": "FP8 Scaled MM (block-wise quantisation) space of P:480, 1e6 configs x 11 GPU specs "
+                "(not a BASELINE config: NEXT-4 variant)",
 }
 E2E_MODELS = ("llama3-8b", "qwen2.5-14b")
 E2E_FAMILIES = (gen.GEMM, gen.ATTENTION, gen.RMSNORM, gen.SILU_MUL)
@@ -58,6 +60,10 @@ def build_workload(name: str, rank: int, world: int, scale: float = 1.0):
         return b, sa, (0, len(sa)), "weak"
     if name == "cfg3":
         b = gen.gen_moe(int(1_000_000 * scale), 1003 + 7919 * rank)
+        sa = specs.paper_gpu_specs()
+        return b, sa, (0, len(sa)), "weak"
+    if name == "scaledmm":
+        b = gen.gen_scaled_mm(int(1_000_000 * scale), 1006 + 7919 * rank)
         sa = specs.paper_gpu_specs()
         return b, sa, (0, len(sa)), "weak"
     if name == "cfg5":

@@ -41,7 +41,7 @@ typedef enum sp_status {
   SP_E_ARG = 1,         /* bad argument: NULL, size, family mismatch (SPEC S:604 exit 1) */
   SP_E_DATA = 2,        /* invalid data: spec or model values (SPEC S:604 exit 2) */
   SP_E_INTERNAL = 3,    /* CUDA error or launch failure (SPEC S:604 exit 3) */
-  SP_E_UNSUPPORTED = 4  /* valid but not implemented (e.g. FP8 Scaled MM, NEXT-4) */
+  SP_E_UNSUPPORTED = 4  /* valid but not implemented (e.g. scheduler state beyond shared memory) */
 } sp_status;
 
 /* Per-pair status written by sp_featurize (one byte per pair).  A pair with a
@@ -65,13 +65,14 @@ typedef enum sp_pair_status {
 
 /* ---------------------------------------------------------------- families */
 
-/* Kernel categories of Table V.  Scaled MM (FP8) is NEXT-4. */
+/* Kernel categories of Table V. */
 typedef enum sp_family {
   SP_GEMM = 0,       /* cuBLAS GEMM, Tensor pipe */
   SP_ATTENTION = 1,  /* FlashInfer FA2 prefill/decode, Tensor + XU */
   SP_FUSED_MOE = 2,  /* SGLang fused MoE (Triton), Tensor */
   SP_RMSNORM = 3,    /* FlashInfer RMSNorm, FMA + XU */
-  SP_SILU_MUL = 4    /* FlashInfer SiLU&Mul, FMA + XU */
+  SP_SILU_MUL = 4,   /* FlashInfer SiLU&Mul, FMA + XU */
+  SP_SCALED_MM = 5   /* vLLM FP8 Scaled MM, block-wise quantisation, Tensor */
 } sp_family;
 
 typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_dtype;
@@ -88,6 +89,13 @@ typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_d
  *                    the balanced split q + [e < r], q = M*TOPK / E, r = M*TOPK % E (R16)
  * SP_RMSNORM (6):    SEQ, DIM, WARPS, REGS, SMEM, DTYPE
  * SP_SILU_MUL (6):   SEQ, DIM, WARPS, REGS, SMEM, DTYPE   (DIM = output width, R15)
+ * SP_SCALED_MM (11): M, N, K, TM, TN, BK, STAGES, WARPS, REGS, SMEM, DTYPE (= SP_FP8)
+ *                    GEMM's tiling (Table V lists the Tensor pipe only) with
+ *                    FP8 operands at the spec's th_tensor_fp8 and block-wise scales
+ *                    (reading R23): per task, A scales tm x ceil(K/128) and B scales
+ *                    ceil(tn/128) x ceil(K/128), fp32 each, on top of (tm+tn) x K_pad
+ *                    one-byte operands.  A spec without an FP8 tensor rate (sm_80/86)
+ *                    gives SP_PAIR_E_DTYPE.
  *
  * SMEM = per-task shared memory bytes, 0 = default footprint.
  * GROUP_M does not change any feature under cyclic dealing (it only permutes
@@ -95,7 +103,7 @@ typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_d
  */
 enum {
   SP_NFIELDS_GEMM = 11, SP_NFIELDS_ATTENTION = 12, SP_NFIELDS_FUSED_MOE = 14,
-  SP_NFIELDS_RMSNORM = 6, SP_NFIELDS_SILU_MUL = 6
+  SP_NFIELDS_RMSNORM = 6, SP_NFIELDS_SILU_MUL = 6, SP_NFIELDS_SCALED_MM = 11
 };
 
 /* -------------------------------------------------------------- hardware S */
@@ -201,7 +209,7 @@ typedef enum sp_precision {
  */
 typedef struct sp_mlp_desc {
   int32_t family;      /* sp_family the model was trained for */
-  int32_t n_in;        /* 4 * (#pipes) + 7: 11 (GEMM, MoE) or 15 */
+  int32_t n_in;        /* 4 * (#pipes) + 7: 11 (GEMM, MoE, Scaled MM) or 15 */
   int32_t precision;   /* sp_precision */
   int32_t reserved_;
   const float *mu, *sigma;              /* [n_in] */

@@ -59,7 +59,7 @@
 
 /* ---------------- input formats (defined by workloads/, documented in include/synperf.h) */
 
-enum { FAM_GEMM = 0, FAM_ATTENTION = 1, FAM_MOE = 2, FAM_RMSNORM = 3, FAM_SILU = 4 };
+enum { FAM_GEMM = 0, FAM_ATTENTION = 1, FAM_MOE = 2, FAM_RMSNORM = 3, FAM_SILU = 4, FAM_SCALED = 5 };
 enum { DT_BF16 = 0, DT_FP16 = 1, DT_FP32 = 2, DT_FP8 = 3 };
 
 /* per-pair status codes (include/synperf.h sp_pair_status) */
@@ -156,6 +156,23 @@ static void emit_task(orc_sched *s, i128 ops_t, i128 ops_f, i128 ops_x, i128 byt
 }
 
 /* ---------------- O1 decomposers (Eq.1, one per family) ---------------- */
+
+/* Scaled MM (Table V; FP8 with block-wise quantisation; reading
+ * R23): GEMM's output tiles, operands one byte each, and every task also
+ * loads its fp32 scales -- one per (row of A, 128-wide K block) and one per
+ * (128x128 block of B): tm*ceil(K/128) + ceil(tn/128)*ceil(K/128) floats. */
+static void decompose_scaled_mm(const int64_t *x, orc_sched *s) {
+  int64_t M = x[G_M], N = x[G_N], K = x[G_K], tm = x[G_TM], tn = x[G_TN], bk = x[G_BK];
+  int64_t kpad = cdiv(K, bk) * bk;
+  int64_t kblocks = cdiv(K, 128);
+  for (int64_t i = 0; i < cdiv(M, tm); ++i) {
+    for (int64_t j = 0; j < cdiv(N, tn); ++j) {
+      i128 operand_bytes = (i128)(tm + tn) * kpad * 1;               /* FP8: 1 byte per element */
+      i128 scale_bytes = ((i128)tm * kblocks + (i128)cdiv(tn, 128) * kblocks) * 4;  /* fp32 scales */
+      emit_task(s, (i128)2 * tm * tn * kpad, 0, 0, operand_bytes + scale_bytes);
+    }
+  }
+}
 
 /* GEMM (Table V; Eq.3 alpha = 2): output tiles row-major,
  * i over ceil(M/tm) outer, j over ceil(N/tn) inner (R4).  Padded (R2): every
@@ -261,7 +278,9 @@ static void decompose_attention(const int64_t *x, const int32_t *req, int flags,
 
 /* ---------------- domain checks (include/synperf.h "per-pair domain") ---- */
 
-static int is_tensor_family(int fam) { return fam == FAM_GEMM || fam == FAM_ATTENTION || fam == FAM_MOE; }
+static int is_tensor_family(int fam) {
+  return fam == FAM_GEMM || fam == FAM_ATTENTION || fam == FAM_MOE || fam == FAM_SCALED;
+}
 
 /* Validates one config; also computes its task count T (int64) and, for
  * attention, the per-kv-head kv-unit sum, to enforce the documented exact
@@ -269,6 +288,16 @@ static int is_tensor_family(int fam) { return fam == FAM_GEMM || fam == FAM_ATTE
 static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_out) {
   *T_out = 0;
   switch (fam) {
+    case FAM_SCALED: {
+      if (x[G_M] < 1 || x[G_N] < 1 || x[G_K] < 1) return ST_DIM;
+      if (x[G_TM] < 1 || x[G_TN] < 1 || x[G_BK] < 1 || x[G_STAGES] < 1) return ST_TILE;
+      if (x[G_WARPS] < 1 || x[G_REGS] < 1 || x[G_SMEM] < 0) return ST_RES;
+      if (x[G_DTYPE] != DT_FP8) return ST_DTYPE;
+      int64_t T = cdiv(x[G_M], x[G_TM]) * cdiv(x[G_N], x[G_TN]);
+      if (T > INT32_LIM) return ST_RANGE;
+      *T_out = T;
+      return ST_OK;
+    }
     case FAM_GEMM: {
       if (x[G_M] < 1 || x[G_N] < 1 || x[G_K] < 1) return ST_DIM;
       if (x[G_TM] < 1 || x[G_TN] < 1 || x[G_BK] < 1 || x[G_STAGES] < 1) return ST_TILE;
@@ -354,6 +383,10 @@ static int64_t occupancy(int fam, const int64_t *x, const orc_spec *sp) {
   i128 smem = 0;
   int64_t warps = 0, regs = 0;
   switch (fam) {
+    case FAM_SCALED: /* one-byte FP8 operand stages */
+      warps = x[G_WARPS]; regs = x[G_REGS];
+      smem = x[G_SMEM] > 0 ? (i128)x[G_SMEM] : (i128)x[G_STAGES] * (x[G_TM] + x[G_TN]) * x[G_BK] * 1;
+      break;
     case FAM_GEMM:
       warps = x[G_WARPS]; regs = x[G_REGS];
       smem = x[G_SMEM] > 0 ? (i128)x[G_SMEM]
@@ -389,7 +422,7 @@ static int64_t occupancy(int fam, const int64_t *x, const orc_spec *sp) {
 /* Pipes present per family (Table V): bit 0 Tensor, 1 FMA, 2 XU */
 static int pipes_of(int fam) {
   switch (fam) {
-    case FAM_GEMM: case FAM_MOE: return 1;
+    case FAM_GEMM: case FAM_MOE: case FAM_SCALED: return 1;
     case FAM_ATTENTION: return 1 | 4;
     default: return 2 | 4;
   }
@@ -487,8 +520,8 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
   int st = validate(fam, x, rag, &T);
   int64_t tensor_th = 0;
   if (st == ST_OK && is_tensor_family(fam)) {
-    int dt = (int)(fam == FAM_GEMM ? x[G_DTYPE] : fam == FAM_MOE ? x[E_DTYPE] : x[A_DTYPE]);
-    tensor_th = dt == DT_BF16 ? sp->th_tensor_bf16 : sp->th_tensor_fp16;
+    int dt = (int)((fam == FAM_GEMM || fam == FAM_SCALED) ? x[G_DTYPE] : fam == FAM_MOE ? x[E_DTYPE] : x[A_DTYPE]);
+    tensor_th = dt == DT_BF16 ? sp->th_tensor_bf16 : dt == DT_FP16 ? sp->th_tensor_fp16 : sp->th_tensor_fp8;
     if (tensor_th <= 0) st = ST_DTYPE;
   }
   if (st != ST_OK) {
@@ -505,6 +538,7 @@ static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const o
 
   switch (fam) { /* O1 + O3 + O4 */
     case FAM_GEMM: decompose_gemm(x, flags, &s); break;
+    case FAM_SCALED: decompose_scaled_mm(x, &s); break;
     case FAM_MOE: decompose_moe(x, rag, flags, &s); break;
     case FAM_RMSNORM: decompose_rmsnorm(x, &s); break;
     case FAM_SILU: decompose_silu(x, &s); break;
@@ -588,7 +622,7 @@ static void load_config(const int32_t *fields, int64_t ld, int64_t c, int nf, in
 
 static int n_fields_of(int fam) {
   switch (fam) {
-    case FAM_GEMM: return 11;
+    case FAM_GEMM: case FAM_SCALED: return 11;
     case FAM_ATTENTION: return 12;
     case FAM_MOE: return 14;
     default: return 6;
@@ -604,7 +638,7 @@ int orc_featurize(int fam, int64_t n_configs, const int32_t *fields, int64_t fie
                   const int32_t *ragged, const int64_t *ragged_off, const orc_spec *specs,
                   int64_t n_specs, int64_t n_pairs, const int64_t *cfg_idx, const int64_t *spec_idx, int flags,
                   int64_t *ints, double *flts, uint8_t *status, int nthreads) {
-  if (fam < 0 || fam > 4) return -1;
+  if (fam < 0 || fam > FAM_SCALED) return -1;
   int nf = n_fields_of(fam);
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -677,6 +711,7 @@ int64_t orc_task_list(int fam, const int32_t *fields, int64_t field_ld, int64_t 
   s.sm_count = (int64_t *)calloc((size_t)s.n_sm, sizeof(int64_t));
   switch (fam) {
     case FAM_GEMM: decompose_gemm(x, flags, &s); break;
+    case FAM_SCALED: decompose_scaled_mm(x, &s); break;
     case FAM_MOE: decompose_moe(x, rag, flags, &s); break;
     case FAM_RMSNORM: decompose_rmsnorm(x, &s); break;
     case FAM_SILU: decompose_silu(x, &s); break;

@@ -35,6 +35,7 @@ int nfields_of(int fam) {
     case SP_FUSED_MOE: return SP_NFIELDS_FUSED_MOE;
     case SP_RMSNORM: return SP_NFIELDS_RMSNORM;
     case SP_SILU_MUL: return SP_NFIELDS_SILU_MUL;
+    case SP_SCALED_MM: return SP_NFIELDS_SCALED_MM;
     default: return -1;
   }
 }
@@ -174,8 +175,8 @@ extern "C" sp_status sp_load_gpu_specs(sp_ctx *ctx, const sp_gpu_spec *host_spec
     d.regs_per_sm = s.regfile_per_sm_bytes / 4;
     d.max_warps = s.max_warps_per_sm;
     d.max_ctas = s.max_ctas_per_sm;
-    const int32_t th_t[2] = {s.th_tensor_bf16, s.th_tensor_fp16};
-    for (int k = 0; k < 2; ++k) {
+    const int32_t th_t[3] = {s.th_tensor_bf16, s.th_tensor_fp16, s.th_tensor_fp8};
+    for (int k = 0; k < 3; ++k) {
       d.tensor_ok[k] = th_t[k] > 0;
       d.cg_tensor[k] = th_t[k] > 0 ? 1.0 / (N * th_t[k]) : 0.0;
       d.cs_tensor[k] = th_t[k] > 0 ? 1.0 / th_t[k] : 0.0;

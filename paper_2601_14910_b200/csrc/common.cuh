@@ -67,7 +67,7 @@ __device__ __forceinline__ int64_t waves_of(int64_t T, int64_t nsm, int64_t occ)
 }
 
 // a7-a9: cycles from the exact integers in fp64, one rounding to fp32 (R20),
-// and the record store.  tdt = tensor dtype index (0 bf16, 1 fp16).
+// and the record store.  tdt = tensor dtype index (0 bf16, 1 fp16, 2 fp8).
 __device__ __forceinline__ void emit_pair(const FeatOut &o, int64_t p, const PairDemand &d,
                                           const Footprint &fp, const DevSpec &s, int pipes,
                                           int tdt) {

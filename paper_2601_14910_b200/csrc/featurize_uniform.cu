@@ -134,6 +134,33 @@ __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c,
   return mine;
 }
 
+// Scaled MM (reading R23): GEMM tiles with one-byte FP8 operands
+// at the spec's FP8 tensor rate, plus the block-wise fp32 scales each task
+// loads: A scales tm x ceil(K/128), B scales ceil(tn/128) x ceil(K/128).
+__device__ UniformCfg scaled_mm_cfg(const ConfigView &v, int64_t c) {
+  UniformCfg u{};
+  const int64_t M = fld(v, 0, c), N = fld(v, 1, c), K = fld(v, 2, c), tm = fld(v, 3, c),
+                tn = fld(v, 4, c), bk = fld(v, 5, c), stages = fld(v, 6, c), warps = fld(v, 7, c),
+                regs = fld(v, 8, c), smem = fld(v, 9, c), dt = fld(v, 10, c);
+  if (M < 1 || N < 1 || K < 1) { u.status = SP_PAIR_E_DIM; return u; }
+  if (tm < 1 || tn < 1 || bk < 1 || stages < 1) { u.status = SP_PAIR_E_TILE; return u; }
+  if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return u; }
+  if (dt != SP_FP8) { u.status = SP_PAIR_E_DTYPE; return u; }
+  const int64_t T = cdiv64(M, tm) * cdiv64(N, tn);
+  if (T > kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
+  u.T = T;
+  u.tdt = 2;
+  const int64_t kpad = cdiv64(K, bk) * bk, kb = cdiv64(K, 128);
+  unsigned __int128 task[4] = {(unsigned __int128)(2 * tm * tn) * kpad, 0, 0,
+                               (unsigned __int128)(tm + tn) * kpad +
+                                   ((unsigned __int128)tm + (unsigned __int128)cdiv64(tn, 128)) * kb * 4};
+  finish_totals(u, task);
+  u.fp.smem = smem > 0 ? smem : sat40((unsigned __int128)stages * (tm + tn) * bk);
+  u.fp.warps = warps;
+  u.fp.regs = regs;
+  return u;
+}
+
 // Fused MoE (R16): t_e from the histogram or the balanced split; tasks are
 // padded BM x BN x H_pad tiles: T = sum_e ceil(t_e/BM) * ceil(N/BN).
 // `hist`: this config's histogram pass (moe_hist_warp), or nullptr to walk it here.
@@ -210,6 +237,7 @@ __device__ __forceinline__ UniformCfg config_of(int fam, const ConfigView &v, in
     case SP_GEMM: return gemm_cfg(v, c);
     case SP_FUSED_MOE: return moe_cfg(v, c, hist);
     case SP_RMSNORM: return rowwise_cfg(v, c, false);
+    case SP_SCALED_MM: return scaled_mm_cfg(v, c);
     default: return rowwise_cfg(v, c, true);
   }
 }

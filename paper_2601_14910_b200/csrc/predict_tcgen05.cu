@@ -111,7 +111,7 @@ __host__ __device__ constexpr uint32_t op_off(uint32_t r, uint32_t k, uint32_t K
 // Table IV order (O8): per pipe present (Tensor, FMA, XU) [total ops, C^GPU,
 // max-SM ops, C^SM], then the 7 MIO features.  Record slot, +16 for a float slot.
 __host__ __device__ constexpr int in_slot(int fam, int k) {
-  const int pipes = (fam == SP_GEMM || fam == SP_FUSED_MOE) ? 1 : (fam == SP_ATTENTION ? 5 : 6);
+  const int pipes = (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM) ? 1 : (fam == SP_ATTENTION ? 5 : 6);
   int n = 0;
   for (int p = 0; p < 3; ++p) {
     if (!(pipes & (1 << p))) continue;
@@ -124,7 +124,9 @@ __host__ __device__ constexpr int in_slot(int fam, int k) {
   const int mio[7] = {I_BYTES, 16 + F_GLOB_G, 16 + F_L2_G, I_BYTES_MAX, 16 + F_GLOB_S, 16 + F_L2_S, 16 + F_SMEM_S};
   return k - n < 7 ? mio[k - n] : -1;
 }
-__host__ __device__ constexpr int n_in_of(int fam) { return (fam == SP_GEMM || fam == SP_FUSED_MOE) ? 11 : 15; }
+__host__ __device__ constexpr int n_in_of(int fam) {
+  return (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM) ? 11 : 15;
+}
 
 #ifdef SP_PRED_TRACE
 // Debug build only: clock64 stamps of CTA 0 (role r: 0 = slot-0 epilogue, 1 =
@@ -598,6 +600,7 @@ static cudaError_t launch_fam(int fam, const Params &P, unsigned grid, cudaStrea
     case SP_GEMM: kern = predict_tcgen05_kernel<BF16, SP_GEMM>; break;
     case SP_ATTENTION: kern = predict_tcgen05_kernel<BF16, SP_ATTENTION>; break;
     case SP_FUSED_MOE: kern = predict_tcgen05_kernel<BF16, SP_FUSED_MOE>; break;
+    case SP_SCALED_MM: kern = predict_tcgen05_kernel<BF16, SP_GEMM>; break;  // same Table IV layout
     case SP_RMSNORM: kern = predict_tcgen05_kernel<BF16, SP_RMSNORM>; break;
     default: kern = predict_tcgen05_kernel<BF16, SP_SILU_MUL>; break;
   }

@@ -20,7 +20,7 @@ enum FltSlot { F_CG_T, F_CG_F, F_CG_X, F_CS_T, F_CS_F, F_CS_X, F_GLOB_G, F_L2_G,
 
 // Pipes per family (Table V): bit 0 Tensor, bit 1 FMA, bit 2 XU.
 __host__ __device__ inline int family_pipes(int fam) {
-  return (fam == SP_GEMM || fam == SP_FUSED_MOE) ? 1 : (fam == SP_ATTENTION ? 5 : 6);
+  return (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM) ? 1 : (fam == SP_ATTENTION ? 5 : 6);
 }
 
 // Step a1: per-spec constants derived once on the host in fp64 (Eq.4-5).
@@ -31,10 +31,9 @@ struct alignas(16) DevSpec {
   int32_t regs_per_sm;   // 32-bit registers (R6)
   int32_t max_warps;
   int32_t max_ctas;
-  int32_t tensor_ok[2];  // tensor rate present for {bf16, fp16}
-  int32_t pad_;
-  double cg_tensor[2];   // 1 / (N_SM * Th_tensor)   (Eq.5)
-  double cs_tensor[2];   // 1 / Th_tensor           (Eq.4)
+  int32_t tensor_ok[3];  // tensor rate present for {bf16, fp16, fp8}
+  double cg_tensor[3];   // 1 / (N_SM * Th_tensor)   (Eq.5)
+  double cs_tensor[3];   // 1 / Th_tensor           (Eq.4)
   double cg_fma, cs_fma, cg_xu, cs_xu;
   double glob_g;         // f / (BW_glob * 1e3): bytes -> cycles at GPU level (R8)
   double l2_g;
@@ -43,7 +42,7 @@ struct alignas(16) DevSpec {
   double smem_s;         // 1 / smem bytes per clk
   double inv_f;          // 1 / f (cycles -> us)
 };
-static_assert(sizeof(DevSpec) == 144, "DevSpec layout");
+static_assert(sizeof(DevSpec) == 160, "DevSpec layout");
 
 // Device feature-record view.
 struct FeatOut {

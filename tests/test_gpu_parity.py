@@ -67,6 +67,7 @@ FAMILY_BATCHES = {
     "moe": lambda: gen.gen_moe(600, 1003),
     "rmsnorm": lambda: gen.gen_rowwise(gen.RMSNORM, 500, 1004),
     "silu": lambda: gen.gen_rowwise(gen.SILU_MUL, 500, 1005),
+    "scaled_mm": lambda: gen.gen_scaled_mm(500, 1006),
 }
 
 
@@ -76,7 +77,10 @@ def test_featurize_cross_parity(sp, ctx, orc, fam):
     sa = specs.paper_gpu_specs()
     _, g = gpu_features(sp, ctx, b, sa)
     o = orc.featurize(b, sa)
-    assert (o.status == 0).all()
+    if fam == "scaled_mm":  # no FP8 tensor rate on sm_80/86 (A40, A100, RTX A6000)
+        assert ((o.status == 0) | (o.status == 7)).all() and (o.status == 0).any()
+    else:
+        assert (o.status == 0).all()
     assert_feature_parity(g, o, fam)
 
 

@@ -480,3 +480,38 @@ def test_predict_exceeds_roof_and_is_deterministic(orc):
     ok = f.status == 0
     assert (lat[ok] > f.flts[11][ok]).all() and ((eff[ok] > 0) & (eff[ok] < 1)).all()
     assert np.array_equal(lat, lat2, equal_nan=True)
+
+
+# --------------------------------------------------------------- Scaled MM (FP8, NEXT-4)
+
+def test_scaled_mm_worked_example(orc):
+    g = GOLD["scaled_mm_256"]
+    b = one(gen.SCALED_MM, g["config"])
+    tl = orc.task_list(b)
+    assert len(tl) == g["n_tasks"]
+    assert (tl[:, 0] == g["ops_per_task"]).all() and (tl[:, 3] == g["bytes_per_task"]).all()
+    ints, flts, st = feats(orc, b, specs.spec_by_name("H100"))
+    assert st == 0 and ints["occupancy"] == g["occupancy"]
+    assert flts["cs_T"] == pytest.approx(g["cs_T"], rel=1e-12)
+    assert flts["cg_T"] == pytest.approx(g["cg_T"], rel=1e-9)
+
+
+def test_scaled_mm_relates_to_gemm(orc):
+    """Same tiling as a bf16 GEMM: equal task counts and Tensor ops; bytes =
+    GEMM bytes / 2 (one-byte operands) + the scale floats; no FP8 rate on
+    sm_80/86 (A40, A100, RTX A6000) -> dtype error."""
+    g = gen.gen_gemm(60, 5, m_range=(2, 5000), n_range=(384, 5000), k_range=(256, 5000))
+    g.fields[gen.FIELDS[gen.GEMM].index("BK")] = 128
+    s = gen.ConfigBatch(gen.SCALED_MM, g.fields.copy())
+    s.fields[gen.FIELDS[gen.SCALED_MM].index("DTYPE")] = gen.FP8
+    for c in range(g.n_configs):
+        tg, ts = orc.task_list(g, c), orc.task_list(s, c)
+        assert len(tg) == len(ts) and (tg[:, 0] == ts[:, 0]).all()
+        M, N, K, tm, tn = (int(g.fields[i, c]) for i in range(5))
+        kb = -(-K // 128)
+        assert (ts[:, 3] == tg[:, 3] // 2 + (tm * kb + -(-tn // 128) * kb) * 4).all()
+    sa = specs.paper_gpu_specs()
+    o = orc.featurize(s, sa)
+    no_fp8 = sa["th_tensor_fp8"] == 0
+    st = o.status.reshape(len(sa), -1)
+    assert (st[no_fp8] == 7).all() and (st[~no_fp8] == 0).all()

@@ -19,9 +19,9 @@ from dataclasses import dataclass
 import numpy as np
 
 # ---- family codes (include/synperf.h sp_family) ----
-GEMM, ATTENTION, FUSED_MOE, RMSNORM, SILU_MUL = 0, 1, 2, 3, 4
+GEMM, ATTENTION, FUSED_MOE, RMSNORM, SILU_MUL, SCALED_MM = 0, 1, 2, 3, 4, 5
 FAMILY_NAMES = {GEMM: "gemm", ATTENTION: "attention", FUSED_MOE: "fused_moe",
-                RMSNORM: "rmsnorm", SILU_MUL: "silu_mul"}
+                RMSNORM: "rmsnorm", SILU_MUL: "silu_mul", SCALED_MM: "scaled_mm"}
 
 # ---- dtype codes (include/synperf.h sp_dtype) ----
 BF16, FP16, FP32, FP8 = 0, 1, 2, 3
@@ -34,6 +34,7 @@ FIELDS = {
                 "WARPS", "REGS", "SMEM", "DTYPE"],
     RMSNORM: ["SEQ", "DIM", "WARPS", "REGS", "SMEM", "DTYPE"],
     SILU_MUL: ["SEQ", "DIM", "WARPS", "REGS", "SMEM", "DTYPE"],
+    SCALED_MM: ["M", "N", "K", "TM", "TN", "BK", "STAGES", "WARPS", "REGS", "SMEM", "DTYPE"],
 }
 N_FIELDS = {f: len(v) for f, v in FIELDS.items()}
 
@@ -198,6 +199,22 @@ def gen_moe(n: int, seed: int, zipf_a=1.1) -> ConfigBatch:
     cols = dict(M=M, E=E, TOPK=topk, H=H, N=N, BM=bm, BN=bn, BK=bk, GROUP_M=gm,
                 STAGES=stages, WARPS=warps, REGS=regs, SMEM=0, DTYPE=BF16)
     return ConfigBatch(FUSED_MOE, _pack(FUSED_MOE, cols, n), ragged, off)
+
+
+def gen_scaled_mm(n: int, seed: int) -> ConfigBatch:
+    """FP8 Scaled MM (block-wise quantisation) space of §V-B:
+    M ~ logU[2, 131072], N ~ logU[384, 8192], K ~ logU[256, 8192]; CUTLASS
+    block-scaled tiles (tm, tn) in {64x128, 128x128, 128x256}, BK 128, 3-5 stages."""
+    rng = np.random.default_rng(seed)
+    M = _logu_int(rng, 2, 131072, n)
+    N = _logu_int(rng, 384, 8192, n)
+    K = _logu_int(rng, 256, 8192, n)
+    tiles = np.array([(64, 128), (128, 128), (128, 256)])[rng.integers(0, 3, n)]
+    area = tiles[:, 0] * tiles[:, 1]
+    cols = dict(M=M, N=N, K=K, TM=tiles[:, 0], TN=tiles[:, 1], BK=128, STAGES=rng.choice([3, 4, 5], n),
+                WARPS=np.where(area <= 8192, 4, 8), REGS=np.where(area <= 16384, 168, 232), SMEM=0,
+                DTYPE=FP8)
+    return ConfigBatch(SCALED_MM, _pack(SCALED_MM, cols, n))
 
 
 def gen_rowwise(family: int, n: int, seed: int) -> ConfigBatch:
