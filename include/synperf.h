@@ -84,6 +84,10 @@ typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_d
  * SP_GEMM (11):      M, N, K, TM, TN, BK, STAGES, WARPS, REGS, SMEM, DTYPE
  * SP_ATTENTION (12): BS, NH, NKV, HD, BQ, BKV, KV_CHUNK, CAUSAL, WARPS, REGS, SMEM, DTYPE
  *                    ragged: 2*BS int32 per config, (qlen, kvlen) interleaved
+ *                    KV_CHUNK: 0 unsplit, > 0 split-KV chunk (R12), -1 the split-KV
+ *                    planner picks it per spec (non-causal only; reading R24: the
+ *                    smallest multiple of 16 whose work items nkv * sum_b nqb_b *
+ *                    ceil(kvlen_b / chunk) fit N_SM x occupancy, unsplit if none needed)
  * SP_FUSED_MOE (14): M, E, TOPK, H, N, BM, BN, BK, GROUP_M, STAGES, WARPS, REGS, SMEM, DTYPE
  *                    ragged: E int32 per-expert token counts; ragged_off = -1 means
  *                    the balanced split q + [e < r], q = M*TOPK / E, r = M*TOPK % E (R16)

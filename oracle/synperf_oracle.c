@@ -342,7 +342,7 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
     }
     case FAM_ATTENTION: {
       if (x[A_BS] < 1 || x[A_NH] < 1 || x[A_NKV] < 1 || x[A_HD] < 1) return ST_DIM;
-      if (x[A_BQ] < 1 || x[A_BKV] < 1 || x[A_CHUNK] < 0) return ST_TILE;
+      if (x[A_BQ] < 1 || x[A_BKV] < 1 || x[A_CHUNK] < 0) return ST_TILE; /* -1 is resolved before (R24) */
       if (x[A_WARPS] < 1 || x[A_REGS] < 1 || x[A_SMEM] < 0) return ST_RES;
       if (x[A_DTYPE] != DT_BF16 && x[A_DTYPE] != DT_FP16) return ST_DTYPE;
       if (x[A_NH] % x[A_NKV] != 0) return ST_HEADS;
@@ -513,11 +513,42 @@ static void schedule_list(orc_sched *s, int mode, int64_t occ, const int64_t *th
   free(sm_of);
 }
 
+/* R24 split-KV planner (FlashInfer's decode planner; the decomposition F
+ * depends on S): for a non-causal attention config with kv_chunk = -1
+ * on spec sp, max_grid = N_SM * occupancy work items; no split (0) if
+ * nkv * sum_b nqb_b >= max_grid, else the smallest chunk = 16c, c = 1, 2, ...,
+ * with nkv * sum_b nqb_b * ceil(kvlen_b / chunk) <= max_grid -- 0 again if that
+ * chunk covers the longest request.  A literal upward scan. */
+static int64_t plan_kv_chunk(const int64_t *x, const int32_t *rag, const orc_spec *sp, int64_t occ) {
+  int64_t g = x[A_NH] / x[A_NKV], max_grid = (int64_t)sp->num_sms * occ, w0 = 0, maxkv = 0;
+  for (int64_t b = 0; b < x[A_BS]; ++b) {
+    w0 += cdiv((int64_t)rag[2 * b] * g, x[A_BQ]);
+    if (rag[2 * b + 1] > maxkv) maxkv = rag[2 * b + 1];
+  }
+  if (w0 * x[A_NKV] >= max_grid) return 0;
+  for (int64_t c = 1;; ++c) {
+    int64_t chunk = 16 * c, items = 0;
+    for (int64_t b = 0; b < x[A_BS]; ++b) items += cdiv((int64_t)rag[2 * b] * g, x[A_BQ]) * cdiv(rag[2 * b + 1], chunk);
+    if (items * x[A_NKV] <= max_grid) return chunk >= maxkv ? 0 : chunk;
+  }
+}
+
 /* One (config, spec) pair through O1..O7.  ints[N_I], flts[N_F]. */
-static int featurize_pair(int fam, const int64_t *x, const int32_t *rag, const orc_spec *sp,
+static int featurize_pair(int fam, const int64_t *x_in, const int32_t *rag, const orc_spec *sp,
                           int flags, int64_t *ints, double *flts) {
-  int64_t T = 0;
-  int st = validate(fam, x, rag, &T);
+  int64_t T = 0, x[16];
+  memcpy(x, x_in, sizeof x);
+  int st;
+  if (fam == FAM_ATTENTION && x[A_CHUNK] == -1 && !x[A_CAUSAL]) {
+    x[A_CHUNK] = 0; /* domain checks first, with the unsplit extent */
+    st = validate(fam, x, rag, &T);
+    if (st == ST_OK) {
+      x[A_CHUNK] = plan_kv_chunk(x, rag, sp, occupancy(fam, x, sp));
+      st = validate(fam, x, rag, &T);
+    }
+  } else {
+    st = validate(fam, x, rag, &T);
+  }
   int64_t tensor_th = 0;
   if (st == ST_OK && is_tensor_family(fam)) {
     int dt = (int)((fam == FAM_GEMM || fam == FAM_SCALED) ? x[G_DTYPE] : fam == FAM_MOE ? x[E_DTYPE] : x[A_DTYPE]);

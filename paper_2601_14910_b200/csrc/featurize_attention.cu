@@ -79,6 +79,11 @@ struct AttnCfg {
   Footprint fp;
 };
 
+// PLANNER: accept kv_chunk = -1 (non-causal) for the split-KV planner (R24).
+// The cross schedule kernel uses PLANNER = false and reports such configs as
+// SP_PAIR_E_TILE; attn_planner_cross then rewrites their records (keeping the
+// hot kernel's code -- and its register allocation -- free of the planner).
+template <bool PLANNER = true>
 __device__ __forceinline__ AttnCfg load_cfg(const ConfigView &v, int64_t c, int lane) {
   AttnCfg a{};
   const int32_t f = lane < 12 ? __ldg(v.fields + (int64_t)lane * v.ld + c) : 0;
@@ -98,7 +103,11 @@ __device__ __forceinline__ AttnCfg load_cfg(const ConfigView &v, int64_t c, int 
   // validation, in the oracle's order (a config without requests first)
   if (off < 0) { a.status = SP_PAIR_E_DIM; return a; }
   if (a.bs < 1 || a.nh < 1 || a.nkv < 1 || a.hd < 1) { a.status = SP_PAIR_E_DIM; return a; }
-  if (a.bq < 1 || a.bkv < 1 || a.chunk < 0) { a.status = SP_PAIR_E_TILE; return a; }
+  // kv_chunk -1: the split-KV planner chooses it per spec (R24; non-causal only)
+  if (a.bq < 1 || a.bkv < 1 || a.chunk < (PLANNER ? -1 : 0) || (a.chunk == -1 && a.causal)) {
+    a.status = SP_PAIR_E_TILE;
+    return a;
+  }
   if (warps < 1 || regs < 1 || smem < 0) { a.status = SP_PAIR_E_RES; return a; }
   if (a.dt != SP_BF16 && a.dt != SP_FP16) { a.status = SP_PAIR_E_DTYPE; return a; }
   if (a.nh % a.nkv != 0) { a.status = SP_PAIR_E_HEADS; return a; }
@@ -136,6 +145,43 @@ __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b) {
   const uint64_t lim = 1ull << 40;
   const uint64_t s = a + b;
   return s > lim ? lim : s;
+}
+
+// Split-KV planner (R24; FlashInfer's decode planner, F depends on S):
+// with max_grid = N_SM * occ work items, no split if nkv * sum_b nqb_b already
+// reaches it; otherwise the smallest chunk 16c (c >= 1) with
+// nkv * sum_b nqb_b * ceil(kv_b / 16c) <= max_grid, and 0 (unsplit) if that
+// chunk covers the longest request.  Warp-cooperative binary search (the item
+// count is non-increasing in c).  Non-causal configs only.
+constexpr int32_t kPlannerPage = 16;
+
+__device__ int32_t plan_chunk(const AttnCfg &a, const DevSpec &sp, int lane) {
+  const uint64_t max_grid = (uint64_t)sp.num_sms * (uint64_t)occupancy(a.fp, sp);
+  uint64_t w0 = 0;
+  uint32_t maxkv = 0;
+  for (int64_t b = lane; b < a.bs; b += 32) {
+    const uint64_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
+    w0 += (q * a.g + a.bq - 1) / a.bq;
+    maxkv = max(maxkv, (uint32_t)kv);
+  }
+  w0 = warp_sum_u64(w0) * (uint64_t)a.nkv;
+  maxkv = warp_max_u32(maxkv);
+  if (w0 >= max_grid) return 0;
+  auto items = [&](uint32_t chunk) -> uint64_t {
+    uint64_t n = 0;
+    for (int64_t b = lane; b < a.bs; b += 32) {
+      const uint64_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
+      n += (q * a.g + a.bq - 1) / a.bq * ((kv + chunk - 1) / chunk);
+    }
+    return warp_sum_u64(n) * (uint64_t)a.nkv;
+  };
+  uint32_t lo = 1, hi = (maxkv + kPlannerPage - 1) / kPlannerPage;  // items(16*hi) = w0 < max_grid
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (items(mid * kPlannerPage) <= max_grid) hi = mid; else lo = mid + 1;
+  }
+  const uint32_t chunk = lo * kPlannerPage;
+  return chunk >= maxkv ? 0 : (int32_t)chunk;
 }
 
 // Pre-pass: per-head task count L (lanes over requests; causal split-KV walks
@@ -648,7 +694,7 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) attn_schedule_cross
     const int nc = (int)min((int64_t)32, C - c0);
     for (int j = 0; j < nc; ++j) {
       const int64_t c = c0 + j;
-      const AttnCfg a = load_cfg(cfg, c, lane);
+      const AttnCfg a = load_cfg<false>(cfg, c, lane);
       int st = a.status;
       int64_t L = 0;
       uint64_t U = 0;
@@ -684,6 +730,30 @@ __global__ void __launch_bounds__(256) attn_emit_cross(ConfigView cfg, const Dev
   }
 }
 
+// One (config, spec) pair through the per-pair cyclic path (LIST mode and
+// planner configs): accumulate + fold for the pair's own SM count; the
+// planner's chunk (R24) replaces kv_chunk = -1.  Lane 0 writes record p.
+__device__ void attn_one_pair(const ConfigView &cfg, int64_t c, const DevSpec &sp, int64_t p, uint32_t *acc,
+                              uint32_t *scr, FastDiv *fd, int64_t *sm, int lane, const FeatOut &out) {
+  const int32_t N[1] = {sp.num_sms}, off[1] = {0};
+  if (lane == 0) *fd = make_fd((uint32_t)N[0]);
+  __syncwarp();
+  AttnCfg a = load_cfg(cfg, c, lane);
+  int st = a.status;
+  int64_t L = 0;
+  uint64_t U = 0;
+  const int words = (N[0] + kAttnSlack + 3) & ~3;
+  if (st == 0) {
+    if (a.chunk == -1) a.chunk = plan_chunk(a, sp, lane);
+    if (N[0] >= kAttnLazyMinN)
+      st = attn_config<1, false>(a, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
+    else
+      st = attn_config<1, true>(a, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
+  }
+  if (lane == 0) attn_emit(out, p, a, st, L, U, DistinctMax{sm[0], sm[1]}, sp);
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(ConfigView cfg,
                                                                            const DevSpec *__restrict__ specs,
                                                                            int n_specs, int words_per_warp,
@@ -704,24 +774,36 @@ __global__ void __launch_bounds__(kWarps * 32, 2) featurize_attention_list(Confi
       if (lane == 0) emit_error(out, p, SP_PAIR_E_INDEX);
       continue;
     }
-    const int32_t N[1] = {specs[g].num_sms}, off[1] = {0};
-    if (lane == 0) s_fd[warp] = make_fd((uint32_t)N[0]);
-    __syncwarp();
-    const AttnCfg a = load_cfg(cfg, c, lane);
-    int st = a.status;
-    int64_t L = 0;
-    uint64_t U = 0;
-    const int words = (N[0] + kAttnSlack + 3) & ~3;
-    if (st == 0) {
-      if (N[0] >= kAttnLazyMinN)
-        st = attn_config<1, false>(a, acc, words, scr, N, off, s_fd + warp, N[0], lane, L, U, &s_m[warp][0],
-                                   &s_m[warp][1], 1);
-      else
-        st = attn_config<1, true>(a, acc, words, scr, N, off, s_fd + warp, N[0], lane, L, U, &s_m[warp][0],
-                                  &s_m[warp][1], 1);
+    attn_one_pair(cfg, c, specs[g], p, acc, scr, s_fd + warp, s_m[warp], lane, out);
+  }
+}
+
+// CROSS mode, planner configs (kv_chunk = -1): the cross kernels wrote them
+// as SP_PAIR_E_TILE (their chunk depends on the spec); this pass, launched
+// after attn_emit_cross on the same stream, rewrites their records.  A warp
+// takes 32 configs, skips the others with one ballot, and runs each planner
+// config through every spec of the range on the per-pair path.
+__global__ void __launch_bounds__(kWarps * 32, 2) attn_planner_cross(ConfigView cfg, const DevSpec *__restrict__ specs,
+                                                                     int g0, int n_specs, int words_per_warp,
+                                                                     FeatOut out) {
+  extern __shared__ uint32_t smem[];
+  __shared__ FastDiv s_fd[kWarps];
+  __shared__ int64_t s_m[kWarps][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *acc = smem + (size_t)warp * words_per_warp;
+  uint32_t *scr = acc + (words_per_warp - kAttnScratchWords);
+  const int64_t C = cfg.n_configs;
+  for (int64_t c0 = ((int64_t)blockIdx.x * kWarps + warp) * 32; c0 < C; c0 += (int64_t)gridDim.x * kWarps * 32) {
+    const int64_t cl = c0 + lane;
+    const bool plan = cl < C && __ldg(cfg.fields + (int64_t)CHUNK * cfg.ld + cl) == -1;
+    unsigned m = __ballot_sync(0xffffffffu, plan);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      for (int k = 0; k < n_specs; ++k)
+        attn_one_pair(cfg, c0 + j, specs[g0 + k], (int64_t)k * C + c0 + j, acc, scr, s_fd + warp, s_m[warp], lane,
+                      out);
     }
-    if (lane == 0) attn_emit(out, p, a, st, L, U, DistinctMax{s_m[warp][0], s_m[warp][1]}, specs[g]);
-    __syncwarp();
   }
 }
 
@@ -882,11 +964,12 @@ __global__ void __launch_bounds__(kSimWarps * 32) attn_sched_sim(ConfigView cfg,
       g = g0 + (int32_t)(p / C);
     }
     const DevSpec &sp = specs[g];
-    const AttnCfg a = load_cfg(cfg, c, lane);
+    AttnCfg a = load_cfg(cfg, c, lane);
     int st = a.status;
     int64_t L = 0;
     uint64_t U = 0;
     DistinctMax m{0, 0};
+    if (st == 0 && a.chunk == -1) a.chunk = plan_chunk(a, sp, lane);  // R24
     if (st == 0) {
       const uint32_t N = (uint32_t)sp.num_sms;
       const uint32_t occ = (uint32_t)occupancy(a.fp, sp);
@@ -999,6 +1082,19 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
     hook.on_begin("attn_emit_cross", st);
     attn_emit_cross<<<blocks, 256, 0, st>>>(cfg, specs, spec_begin, spec_end - spec_begin, plan.spec_slot, res,
                                             out);
+    hook.on_end(st);
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) return (int)le;
+    // planner configs (kv_chunk = -1): per pair, after the cross kernels skipped them
+    const int pw = ((max_sms + kAttnSlack + 3) & ~3) + kAttnScratchWords;
+    const size_t psmem = (size_t)kWarps * pw * 4;
+    le = cudaFuncSetAttribute(attn_planner_cross, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    if (le != cudaSuccess) return (int)le;
+    const int64_t pwant = (cfg.n_configs + 32 * kWarps - 1) / (32 * kWarps);
+    const int64_t pcap = (int64_t)num_device_sms * 4;
+    hook.on_begin("attn_planner_cross", st);
+    attn_planner_cross<<<(unsigned)(pwant < pcap ? pwant : pcap), kWarps * 32, psmem, st>>>(
+        cfg, specs, spec_begin, spec_end - spec_begin, pw, out);
     hook.on_end(st);
     return (int)cudaGetLastError();
   }

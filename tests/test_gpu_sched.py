@@ -153,3 +153,29 @@ def test_perf_gap_parity(sp, ctx, orc, kind):
     assert np.array_equal(counts.cpu().numpy(), oc)
     assert np.array_equal(hist.cpu().numpy(), oh)
     assert oc[:, 1].sum() > 0 and oc[:, 0].sum() < n
+
+
+# ---------------------------------------------------------------- R24 split-KV planner
+
+def planner_batch(seed, n=80):
+    """Decode configs, a third with kv_chunk = -1 (planner), mixed with fixed chunks."""
+    b = gen.gen_attention(0, n, seed, max_bs=12, kvlen_max=8000)
+    ch = b.fields[gen.FIELDS[gen.ATTENTION].index("KV_CHUNK")]
+    ch[::3] = -1
+    return b
+
+
+@pytest.mark.parametrize("mode", ["rr", "greedy", "minheap"])
+def test_planner_parity_cross(sp, ctx, orc, mode):
+    b = planner_batch(95)
+    base = specs.paper_gpu_specs()
+    sa = np.concatenate([base, np.concatenate([tiny_spec(n, o) for n, o in ((8, 1), (33, 2), (64, 1))])])
+    check(run(sp, ctx, b, sa, mode), orc.featurize(b, sa, flags=oflag(orc, mode)))
+
+
+def test_planner_parity_list(sp, ctx, orc):
+    b = planner_batch(96)
+    sa = specs.paper_gpu_specs()
+    rng = np.random.default_rng(5)
+    ci, si = rng.integers(0, b.n_configs, 400), rng.integers(0, len(sa), 400)
+    check(run(sp, ctx, b, sa, "rr", (ci, si)), orc.featurize(b, sa, ci, si))

@@ -515,3 +515,38 @@ def test_scaled_mm_relates_to_gemm(orc):
     no_fp8 = sa["th_tensor_fp8"] == 0
     st = o.status.reshape(len(sa), -1)
     assert (st[no_fp8] == 7).all() and (st[~no_fp8] == 0).all()
+
+
+# --------------------------------------------------------------- split-KV planner (R24, NEXT-2)
+
+@pytest.mark.parametrize("case", ["split", "nosplit"])
+def test_planner_worked_example(orc, case):
+    g = GOLD["planner_decode"]
+    c = g[case]
+    s = specs.spec_by_name("A100")
+    s["num_sms"] = c["n_sm"]
+    s["max_ctas_per_sm"] = c["occ"]
+    ints, _, st = feats(orc, one(gen.ATTENTION, g["config"], requests=g["requests"]), s)
+    assert st == 0
+    assert (ints["n_tasks"], ints["occupancy"], ints["tot_T"], ints["max_T"]) == (
+        c["n_tasks"], c["occ"], c["tot_T"], c["max_T"])
+
+
+def test_planner_equals_explicit_chunk(orc):
+    """The planner only picks kv_chunk: a planner config gives the same record
+    as the same config with that chunk written in (176 on the 64-SM spec)."""
+    g = GOLD["planner_decode"]
+    s = specs.spec_by_name("A100")
+    s["num_sms"] = 64
+    s["max_ctas_per_sm"] = 1
+    a = feats(orc, one(gen.ATTENTION, g["config"], requests=g["requests"]), s)
+    cfg = dict(g["config"], KV_CHUNK=176)
+    b = feats(orc, one(gen.ATTENTION, cfg, requests=g["requests"]), s)
+    assert a[0] == b[0] and a[2] == b[2] == 0
+
+
+def test_planner_rejects_causal(orc):
+    g = GOLD["planner_decode"]
+    cfg = dict(g["config"], CAUSAL=1)
+    _, _, st = feats(orc, one(gen.ATTENTION, cfg, requests=[[1, 1000], [1, 300]]), A100)
+    assert st == 2  # SP_PAIR_E_TILE
