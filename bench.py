@@ -43,6 +43,8 @@ WORKLOADS = {
     "cfg5": "1,000 serving GEMMs x 100,000 hypothetical GPU specs (1e8 pairs), sharded by spec",
     "scaledmm": "FP8 Scaled MM (block-wise quantisation) space of P:480, 1e6 configs x 11 GPU specs "
                 "(not a BASELINE config: NEXT-4 variant)",
+    "splitk": "split-K GEMM space (long K, few output tiles; reading R25), 1e6 configs x 11 GPU specs "
+              "(not a BASELINE config: NEXT-4 variant)",
 }
 E2E_MODELS = ("llama3-8b", "qwen2.5-14b")
 E2E_FAMILIES = (gen.GEMM, gen.ATTENTION, gen.RMSNORM, gen.SILU_MUL)
@@ -64,6 +66,10 @@ def build_workload(name: str, rank: int, world: int, scale: float = 1.0):
         return b, sa, (0, len(sa)), "weak"
     if name == "scaledmm":
         b = gen.gen_scaled_mm(int(1_000_000 * scale), 1006 + 7919 * rank)
+        sa = specs.paper_gpu_specs()
+        return b, sa, (0, len(sa)), "weak"
+    if name == "splitk":
+        b = gen.gen_gemm_splitk(int(1_000_000 * scale), 1007 + 7919 * rank)
         sa = specs.paper_gpu_specs()
         return b, sa, (0, len(sa)), "weak"
     if name == "cfg5":

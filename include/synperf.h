@@ -72,7 +72,9 @@ typedef enum sp_family {
   SP_FUSED_MOE = 2,  /* SGLang fused MoE (Triton), Tensor */
   SP_RMSNORM = 3,    /* FlashInfer RMSNorm, FMA + XU */
   SP_SILU_MUL = 4,   /* FlashInfer SiLU&Mul, FMA + XU */
-  SP_SCALED_MM = 5   /* vLLM FP8 Scaled MM, block-wise quantisation, Tensor */
+  SP_SCALED_MM = 5,  /* vLLM FP8 Scaled MM, block-wise quantisation, Tensor */
+  SP_GEMM_SPLITK = 6 /* cuBLAS split-K GEMM (tiling reverse-engineered from profiles, P:270;
+                        SURVEY 8(f) NEXT-4), Tensor; reading R25 */
 } sp_family;
 
 typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_dtype;
@@ -100,6 +102,15 @@ typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_d
  *                    ceil(tn/128) x ceil(K/128), fp32 each, on top of (tm+tn) x K_pad
  *                    one-byte operands.  A spec without an FP8 tensor rate (sm_80/86)
  *                    gives SP_PAIR_E_DTYPE.
+ * SP_GEMM_SPLITK (12): M, N, K, TM, TN, BK, SPLIT_K, STAGES, WARPS, REGS, SMEM, DTYPE
+ *                    reading R25: the kt = ceil(K/BK) k-tiles are cut into slices of
+ *                    kps = ceil(kt/SPLIT_K) k-tiles; S' = ceil(kt/kps) <= SPLIT_K
+ *                    non-empty slices, the last one holding kt - (S'-1)*kps.  Tasks
+ *                    are (slice z, tile i, tile j) with z outermost (cuBLAS's grid z,
+ *                    dispatched last), tiles row-major: T = S' * ceil(M/TM) * ceil(N/TN);
+ *                    task (z,.,.) = padded TM x TN x (k_z*BK) tile (Tensor 2*TM*TN*k_z*BK,
+ *                    bytes (TM+TN)*k_z*BK*bpe).  The fp32 partial-tile reduction is a
+ *                    separate kernel and is excluded (as the split-KV merge, R12).
  *
  * SMEM = per-task shared memory bytes, 0 = default footprint.
  * GROUP_M does not change any feature under cyclic dealing (it only permutes
@@ -107,7 +118,8 @@ typedef enum sp_dtype { SP_BF16 = 0, SP_FP16 = 1, SP_FP32 = 2, SP_FP8 = 3 } sp_d
  */
 enum {
   SP_NFIELDS_GEMM = 11, SP_NFIELDS_ATTENTION = 12, SP_NFIELDS_FUSED_MOE = 14,
-  SP_NFIELDS_RMSNORM = 6, SP_NFIELDS_SILU_MUL = 6, SP_NFIELDS_SCALED_MM = 11
+  SP_NFIELDS_RMSNORM = 6, SP_NFIELDS_SILU_MUL = 6, SP_NFIELDS_SCALED_MM = 11,
+  SP_NFIELDS_GEMM_SPLITK = 12
 };
 
 /* -------------------------------------------------------------- hardware S */
@@ -213,7 +225,7 @@ typedef enum sp_precision {
  */
 typedef struct sp_mlp_desc {
   int32_t family;      /* sp_family the model was trained for */
-  int32_t n_in;        /* 4 * (#pipes) + 7: 11 (GEMM, MoE, Scaled MM) or 15 */
+  int32_t n_in;        /* 4 * (#pipes) + 7: 11 (GEMM, MoE, Scaled MM, split-K GEMM) or 15 */
   int32_t precision;   /* sp_precision */
   int32_t reserved_;
   const float *mu, *sigma;              /* [n_in] */

@@ -59,7 +59,8 @@
 
 /* ---------------- input formats (defined by workloads/, documented in include/synperf.h) */
 
-enum { FAM_GEMM = 0, FAM_ATTENTION = 1, FAM_MOE = 2, FAM_RMSNORM = 3, FAM_SILU = 4, FAM_SCALED = 5 };
+enum { FAM_GEMM = 0, FAM_ATTENTION = 1, FAM_MOE = 2, FAM_RMSNORM = 3, FAM_SILU = 4, FAM_SCALED = 5,
+       FAM_SPLITK = 6 };
 enum { DT_BF16 = 0, DT_FP16 = 1, DT_FP32 = 2, DT_FP8 = 3 };
 
 /* per-pair status codes (include/synperf.h sp_pair_status) */
@@ -73,6 +74,7 @@ enum { G_M, G_N, G_K, G_TM, G_TN, G_BK, G_STAGES, G_WARPS, G_REGS, G_SMEM, G_DTY
 enum { A_BS, A_NH, A_NKV, A_HD, A_BQ, A_BKV, A_CHUNK, A_CAUSAL, A_WARPS, A_REGS, A_SMEM, A_DTYPE };
 enum { E_M, E_E, E_TOPK, E_H, E_N, E_BM, E_BN, E_BK, E_GROUPM, E_STAGES, E_WARPS, E_REGS, E_SMEM, E_DTYPE };
 enum { R_SEQ, R_DIM, R_WARPS, R_REGS, R_SMEM, R_DTYPE };
+enum { K_M, K_N, K_K, K_TM, K_TN, K_BK, K_SPLIT, K_STAGES, K_WARPS, K_REGS, K_SMEM, K_DTYPE };
 
 /* Table II record, byte layout of workloads/specs.py SPEC_DTYPE (112 B) */
 typedef struct {
@@ -171,6 +173,26 @@ static void decompose_scaled_mm(const int64_t *x, orc_sched *s) {
       i128 scale_bytes = ((i128)tm * kblocks + (i128)cdiv(tn, 128) * kblocks) * 4;  /* fp32 scales */
       emit_task(s, (i128)2 * tm * tn * kpad, 0, 0, operand_bytes + scale_bytes);
     }
+  }
+}
+
+/* Split-K GEMM (cuBLAS's split-K variants, tiling inferred from profiles
+ * P:270; Table V P:409 Tensor pipe; reading R25).  The K loop of kt =
+ * ceil(K/BK) k-tiles is cut into slices of kps = ceil(kt/SPLIT_K) k-tiles,
+ * slice z holding min(kps, kt - z*kps) of them; slices are enumerated while
+ * they hold at least one k-tile.  Grid order: slice z outermost (grid z is
+ * dispatched last), then output tiles row-major as in GEMM.  Each task is a
+ * padded tm x tn tile over its slice's k_z*BK extent.  The fp32 reduction of
+ * the partial tiles is another kernel and is not part of this one (R25). */
+static void decompose_gemm_splitk(const int64_t *x, orc_sched *s) {
+  int64_t M = x[K_M], N = x[K_N], K = x[K_K], tm = x[K_TM], tn = x[K_TN], bk = x[K_BK];
+  int64_t bpe = bytes_per_elem((int)x[K_DTYPE]);
+  int64_t kt = cdiv(K, bk), kps = cdiv(kt, x[K_SPLIT]);
+  for (int64_t z = 0; z * kps < kt; ++z) {
+    int64_t kz = imin(kps, kt - z * kps); /* k-tiles of slice z */
+    for (int64_t i = 0; i < cdiv(M, tm); ++i)
+      for (int64_t j = 0; j < cdiv(N, tn); ++j)
+        emit_task(s, (i128)2 * tm * tn * kz * bk, 0, 0, (i128)(tm + tn) * kz * bk * bpe);
   }
 }
 
@@ -279,7 +301,7 @@ static void decompose_attention(const int64_t *x, const int32_t *req, int flags,
 /* ---------------- domain checks (include/synperf.h "per-pair domain") ---- */
 
 static int is_tensor_family(int fam) {
-  return fam == FAM_GEMM || fam == FAM_ATTENTION || fam == FAM_MOE || fam == FAM_SCALED;
+  return fam == FAM_GEMM || fam == FAM_ATTENTION || fam == FAM_MOE || fam == FAM_SCALED || fam == FAM_SPLITK;
 }
 
 /* Validates one config; also computes its task count T (int64) and, for
@@ -306,6 +328,17 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
       int64_t T = cdiv(x[G_M], x[G_TM]) * cdiv(x[G_N], x[G_TN]);
       if (T > INT32_LIM) return ST_RANGE;
       *T_out = T;
+      return ST_OK;
+    }
+    case FAM_SPLITK: {
+      if (x[K_M] < 1 || x[K_N] < 1 || x[K_K] < 1) return ST_DIM;
+      if (x[K_TM] < 1 || x[K_TN] < 1 || x[K_BK] < 1 || x[K_SPLIT] < 1 || x[K_STAGES] < 1) return ST_TILE;
+      if (x[K_WARPS] < 1 || x[K_REGS] < 1 || x[K_SMEM] < 0) return ST_RES;
+      if (x[K_DTYPE] != DT_BF16 && x[K_DTYPE] != DT_FP16) return ST_DTYPE;
+      int64_t kt = cdiv(x[K_K], x[K_BK]), slices = cdiv(kt, cdiv(kt, x[K_SPLIT]));
+      i128 T = (i128)slices * cdiv(x[K_M], x[K_TM]) * cdiv(x[K_N], x[K_TN]);
+      if (T > INT32_LIM) return ST_RANGE;
+      *T_out = (int64_t)T;
       return ST_OK;
     }
     case FAM_MOE: {
@@ -392,6 +425,11 @@ static int64_t occupancy(int fam, const int64_t *x, const orc_spec *sp) {
       smem = x[G_SMEM] > 0 ? (i128)x[G_SMEM]
                            : (i128)x[G_STAGES] * (x[G_TM] + x[G_TN]) * x[G_BK] * bytes_per_elem((int)x[G_DTYPE]);
       break;
+    case FAM_SPLITK:
+      warps = x[K_WARPS]; regs = x[K_REGS];
+      smem = x[K_SMEM] > 0 ? (i128)x[K_SMEM]
+                           : (i128)x[K_STAGES] * (x[K_TM] + x[K_TN]) * x[K_BK] * bytes_per_elem((int)x[K_DTYPE]);
+      break;
     case FAM_MOE:
       warps = x[E_WARPS]; regs = x[E_REGS];
       smem = x[E_SMEM] > 0 ? (i128)x[E_SMEM]
@@ -422,7 +460,7 @@ static int64_t occupancy(int fam, const int64_t *x, const orc_spec *sp) {
 /* Pipes present per family (Table V): bit 0 Tensor, 1 FMA, 2 XU */
 static int pipes_of(int fam) {
   switch (fam) {
-    case FAM_GEMM: case FAM_MOE: case FAM_SCALED: return 1;
+    case FAM_GEMM: case FAM_MOE: case FAM_SCALED: case FAM_SPLITK: return 1;
     case FAM_ATTENTION: return 1 | 4;
     default: return 2 | 4;
   }
@@ -551,7 +589,10 @@ static int featurize_pair(int fam, const int64_t *x_in, const int32_t *rag, cons
   }
   int64_t tensor_th = 0;
   if (st == ST_OK && is_tensor_family(fam)) {
-    int dt = (int)((fam == FAM_GEMM || fam == FAM_SCALED) ? x[G_DTYPE] : fam == FAM_MOE ? x[E_DTYPE] : x[A_DTYPE]);
+    int dt = (int)((fam == FAM_GEMM || fam == FAM_SCALED) ? x[G_DTYPE]
+                   : fam == FAM_MOE                         ? x[E_DTYPE]
+                   : fam == FAM_SPLITK                      ? x[K_DTYPE]
+                                                            : x[A_DTYPE]);
     tensor_th = dt == DT_BF16 ? sp->th_tensor_bf16 : dt == DT_FP16 ? sp->th_tensor_fp16 : sp->th_tensor_fp8;
     if (tensor_th <= 0) st = ST_DTYPE;
   }
@@ -570,6 +611,7 @@ static int featurize_pair(int fam, const int64_t *x_in, const int32_t *rag, cons
   switch (fam) { /* O1 + O3 + O4 */
     case FAM_GEMM: decompose_gemm(x, flags, &s); break;
     case FAM_SCALED: decompose_scaled_mm(x, &s); break;
+    case FAM_SPLITK: decompose_gemm_splitk(x, &s); break;
     case FAM_MOE: decompose_moe(x, rag, flags, &s); break;
     case FAM_RMSNORM: decompose_rmsnorm(x, &s); break;
     case FAM_SILU: decompose_silu(x, &s); break;
@@ -654,7 +696,7 @@ static void load_config(const int32_t *fields, int64_t ld, int64_t c, int nf, in
 static int n_fields_of(int fam) {
   switch (fam) {
     case FAM_GEMM: case FAM_SCALED: return 11;
-    case FAM_ATTENTION: return 12;
+    case FAM_ATTENTION: case FAM_SPLITK: return 12;
     case FAM_MOE: return 14;
     default: return 6;
   }
@@ -669,7 +711,7 @@ int orc_featurize(int fam, int64_t n_configs, const int32_t *fields, int64_t fie
                   const int32_t *ragged, const int64_t *ragged_off, const orc_spec *specs,
                   int64_t n_specs, int64_t n_pairs, const int64_t *cfg_idx, const int64_t *spec_idx, int flags,
                   int64_t *ints, double *flts, uint8_t *status, int nthreads) {
-  if (fam < 0 || fam > FAM_SCALED) return -1;
+  if (fam < 0 || fam > FAM_SPLITK) return -1;
   int nf = n_fields_of(fam);
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -743,6 +785,7 @@ int64_t orc_task_list(int fam, const int32_t *fields, int64_t field_ld, int64_t 
   switch (fam) {
     case FAM_GEMM: decompose_gemm(x, flags, &s); break;
     case FAM_SCALED: decompose_scaled_mm(x, &s); break;
+    case FAM_SPLITK: decompose_gemm_splitk(x, &s); break;
     case FAM_MOE: decompose_moe(x, rag, flags, &s); break;
     case FAM_RMSNORM: decompose_rmsnorm(x, &s); break;
     case FAM_SILU: decompose_silu(x, &s); break;

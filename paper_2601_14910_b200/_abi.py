@@ -15,9 +15,9 @@ LIB_PATH = os.environ.get("SYNPERF_LIB") or os.path.join(os.path.dirname(os.path
 SP_OK, SP_E_ARG, SP_E_DATA, SP_E_INTERNAL, SP_E_UNSUPPORTED = 0, 1, 2, 3, 4
 STATUS_NAMES = {0: "SP_OK", 1: "SP_E_ARG", 2: "SP_E_DATA", 3: "SP_E_INTERNAL", 4: "SP_E_UNSUPPORTED"}
 # sp_family
-SP_GEMM, SP_ATTENTION, SP_FUSED_MOE, SP_RMSNORM, SP_SILU_MUL, SP_SCALED_MM = 0, 1, 2, 3, 4, 5
+SP_GEMM, SP_ATTENTION, SP_FUSED_MOE, SP_RMSNORM, SP_SILU_MUL, SP_SCALED_MM, SP_GEMM_SPLITK = range(7)
 NFIELDS = {SP_GEMM: 11, SP_ATTENTION: 12, SP_FUSED_MOE: 14, SP_RMSNORM: 6, SP_SILU_MUL: 6,
-           SP_SCALED_MM: 11}
+           SP_SCALED_MM: 11, SP_GEMM_SPLITK: 12}
 # sp_pairing_kind
 SP_PAIRS_CROSS, SP_PAIRS_LIST = 0, 1
 # sp_precision

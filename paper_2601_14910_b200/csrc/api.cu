@@ -36,6 +36,7 @@ int nfields_of(int fam) {
     case SP_RMSNORM: return SP_NFIELDS_RMSNORM;
     case SP_SILU_MUL: return SP_NFIELDS_SILU_MUL;
     case SP_SCALED_MM: return SP_NFIELDS_SCALED_MM;
+    case SP_GEMM_SPLITK: return SP_NFIELDS_GEMM_SPLITK;
     default: return -1;
   }
 }
@@ -397,13 +398,13 @@ extern "C" sp_status sp_featurize_sched(sp_ctx *ctx, const sp_config_batch *cfg,
     }
   } else if (pairs->kind == SP_PAIRS_CROSS) {
     const LaunchHook h = ctx->hook();
-    h.on_begin("featurize_uniform_cross", stream);
+    h.on_begin(fam == SP_GEMM_SPLITK ? "featurize_splitk_cross" : "featurize_uniform_cross", stream);
     e = launch_featurize_uniform(fam, cv, ds, pairs->spec_begin, pairs->spec_end, n_pairs, nullptr, nullptr,
                                  fo, stream);
     h.on_end(stream);
   } else {
     const LaunchHook h = ctx->hook();
-    h.on_begin("featurize_uniform_list", stream);
+    h.on_begin(fam == SP_GEMM_SPLITK ? "featurize_splitk_list" : "featurize_uniform_list", stream);
     e = launch_featurize_uniform(fam, cv, ds, 0, specs->n, n_pairs, pairs->cfg_idx, pairs->spec_idx, fo,
                                  stream);
     h.on_end(stream);

@@ -161,6 +161,56 @@ __device__ UniformCfg scaled_mm_cfg(const ConfigView &v, int64_t c) {
   return u;
 }
 
+// Split-K GEMM (reading R25; cuBLAS split-K): the kt = ceil(K/BK)
+// k-tiles are cut into S' = ceil(kt/kps) slices of kps = ceil(kt/SPLIT_K); the
+// task list is slice-major (grid z last), tiles row-major inside a slice.  Two
+// task classes: the Ta = (S'-1)*tiles tasks of full slices (kps k-tiles) come
+// first, then the `tiles` tasks of the last slice (kt - (S'-1)*kps k-tiles).
+struct SplitKCfg {
+  UniformCfg u;      // u.task = full-slice task, u.tot = totals over both classes
+  int64_t Ta;        // tasks of the full slices (a prefix of the task list)
+  int64_t taskb[4];  // last-slice task
+};
+
+__device__ SplitKCfg splitk_cfg(const ConfigView &v, int64_t c) {
+  SplitKCfg r{};
+  UniformCfg &u = r.u;
+  const int64_t M = fld(v, 0, c), N = fld(v, 1, c), K = fld(v, 2, c), tm = fld(v, 3, c),
+                tn = fld(v, 4, c), bk = fld(v, 5, c), split = fld(v, 6, c), stages = fld(v, 7, c),
+                warps = fld(v, 8, c), regs = fld(v, 9, c), smem = fld(v, 10, c), dt = fld(v, 11, c);
+  if (M < 1 || N < 1 || K < 1) { u.status = SP_PAIR_E_DIM; return r; }
+  if (tm < 1 || tn < 1 || bk < 1 || split < 1 || stages < 1) { u.status = SP_PAIR_E_TILE; return r; }
+  if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return r; }
+  if (dt != SP_BF16 && dt != SP_FP16) { u.status = SP_PAIR_E_DTYPE; return r; }
+  const int64_t kt = cdiv64(K, bk), kps = cdiv64(kt, split), slices = cdiv64(kt, kps);
+  const int64_t tiles = cdiv64(M, tm) * cdiv64(N, tn);  // <= 2^31 * 2^31 / 1: fits in int64
+  if ((unsigned __int128)tiles * (unsigned __int128)slices > (unsigned __int128)kI32Max) {
+    u.status = SP_PAIR_E_RANGE;
+    return r;
+  }
+  u.T = tiles * slices;
+  u.tdt = (int)dt;
+  r.Ta = tiles * (slices - 1);
+  const int64_t klast = kt - (slices - 1) * kps;
+  const unsigned __int128 ta[4] = {(unsigned __int128)(2 * tm * tn) * (kps * bk), 0, 0,
+                                   (unsigned __int128)(tm + tn) * (kps * bk) * 2};
+  const unsigned __int128 tb[4] = {(unsigned __int128)(2 * tm * tn) * (klast * bk), 0, 0,
+                                   (unsigned __int128)(tm + tn) * (klast * bk) * 2};
+  u.range_bad = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const unsigned __int128 t = ta[q] * (unsigned __int128)r.Ta + tb[q] * (unsigned __int128)tiles;
+    if (ta[q] > kI64Max || t > kI64Max) u.range_bad = 1;
+    u.task[q] = (int64_t)ta[q];
+    r.taskb[q] = (int64_t)tb[q];
+    u.tot[q] = (int64_t)t;
+  }
+  u.fp.smem = smem > 0 ? smem : sat40((unsigned __int128)stages * (tm + tn) * bk * 2);
+  u.fp.warps = warps;
+  u.fp.regs = regs;
+  return r;
+}
+
 // Fused MoE (R16): t_e from the histogram or the balanced split; tasks are
 // padded BM x BN x H_pad tiles: T = sum_e ceil(t_e/BM) * ceil(N/BN).
 // `hist`: this config's histogram pass (moe_hist_warp), or nullptr to walk it here.
@@ -260,6 +310,65 @@ __device__ __forceinline__ void uniform_pair(const FeatOut &out, int64_t p, cons
   emit_pair(out, p, d, u.fp, s, pipes, u.tdt < 0 ? 0 : u.tdt);
 }
 
+// Split-K pair: cyclic dealing of two contiguous task classes.  SM j holds
+// qa + [j < ra] full-slice tasks (ra = Ta mod N) and qb + [(j - Ta) mod N < rb]
+// last-slice tasks; since Ta = ra (mod N) the second set is the cyclic
+// interval [ra, ra + rb), which meets [0, ra) iff ra + rb > N.  Full-slice
+// demands dominate last-slice ones (k_last <= kps), so the busiest SM is
+//   qa*a + qb*b + (ra + rb > N ? a + b : ra > 0 ? a : rb > 0 ? b : 0)
+// for every quantity at once (all are proportional to the slice's k extent).
+__device__ __forceinline__ void splitk_pair(const FeatOut &out, int64_t p, const SplitKCfg &r,
+                                            const DevSpec &s) {
+  const UniformCfg &u = r.u;
+  if (u.status != 0) { emit_error(out, p, u.status); return; }
+  if (!s.tensor_ok[u.tdt]) { emit_error(out, p, SP_PAIR_E_DTYPE); return; }
+  if (u.range_bad) { emit_error(out, p, SP_PAIR_E_RANGE); return; }
+  const uint32_t N = (uint32_t)s.num_sms, Ta = (uint32_t)r.Ta, Tb = (uint32_t)(u.T - r.Ta);
+  const uint32_t qa = Ta / N, ra = Ta - qa * N, qb = Tb / N, rb = Tb - qb * N;
+  const int cls = ra + rb > N ? 3 : ra > 0 ? 1 : rb > 0 ? 2 : 0;  // bit 0: a, bit 1: b
+  PairDemand d;
+  d.T = u.T;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    d.tot[q] = u.tot[q];
+    d.mx[q] = (int64_t)(qa + (cls & 1)) * u.task[q] + (int64_t)(qb + (cls >> 1)) * r.taskb[q];
+  }
+  emit_pair(out, p, d, u.fp, s, 1, u.tdt);
+}
+
+__global__ void __launch_bounds__(kThreads) featurize_splitk_cross(ConfigView cfg,
+                                                                   const DevSpec *__restrict__ specs, int g0,
+                                                                   int g1, FeatOut out) {
+  __shared__ DevSpec s_spec[kSpecTile];
+  const int gt0 = g0 + blockIdx.y * kSpecTile;
+  const int gt1 = min(g1, gt0 + kSpecTile);
+  {
+    const int n_words = (gt1 - gt0) * (int)(sizeof(DevSpec) / 16);
+    const int4 *src = reinterpret_cast<const int4 *>(specs + gt0);
+    int4 *dst = reinterpret_cast<int4 *>(s_spec);
+    for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (c >= cfg.n_configs) return;
+  const SplitKCfg r = splitk_cfg(cfg, c);
+  const int64_t C = cfg.n_configs;
+  for (int g = gt0; g < gt1; ++g) splitk_pair(out, (int64_t)(g - g0) * C + c, r, s_spec[g - gt0]);
+}
+
+__global__ void __launch_bounds__(kThreads) featurize_splitk_list(ConfigView cfg, const DevSpec *__restrict__ specs,
+                                                                  int n_specs, int64_t n_pairs,
+                                                                  const int64_t *__restrict__ cfg_idx,
+                                                                  const int32_t *__restrict__ spec_idx,
+                                                                  FeatOut out) {
+  const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (p >= n_pairs) return;
+  const int64_t c = __ldg(cfg_idx + p);
+  const int32_t g = __ldg(spec_idx + p);
+  if (c < 0 || c >= cfg.n_configs || g < 0 || g >= n_specs) { emit_error(out, p, SP_PAIR_E_INDEX); return; }
+  splitk_pair(out, p, splitk_cfg(cfg, c), specs[g]);
+}
+
 __global__ void __launch_bounds__(kThreads) featurize_uniform_cross(int fam, ConfigView cfg,
                                                                     const DevSpec *__restrict__ specs,
                                                                     int g0, int g1, FeatOut out) {
@@ -308,12 +417,18 @@ int launch_featurize_uniform(int family, const ConfigView &cfg, const DevSpec *s
     if (cfg.n_configs == 0 || spec_end <= spec_begin) return 0;
     dim3 grid((unsigned)((cfg.n_configs + kThreads - 1) / kThreads),
               (unsigned)((spec_end - spec_begin + kSpecTile - 1) / kSpecTile));
-    featurize_uniform_cross<<<grid, kThreads, 0, st>>>(family, cfg, specs, spec_begin, spec_end, out);
+    if (family == SP_GEMM_SPLITK)
+      featurize_splitk_cross<<<grid, kThreads, 0, st>>>(cfg, specs, spec_begin, spec_end, out);
+    else
+      featurize_uniform_cross<<<grid, kThreads, 0, st>>>(family, cfg, specs, spec_begin, spec_end, out);
   } else {
     if (n_pairs == 0) return 0;
     unsigned blocks = (unsigned)((n_pairs + kThreads - 1) / kThreads);
-    featurize_uniform_list<<<blocks, kThreads, 0, st>>>(family, cfg, specs, spec_end, n_pairs, cfg_idx,
-                                                         spec_idx, out);
+    if (family == SP_GEMM_SPLITK)
+      featurize_splitk_list<<<blocks, kThreads, 0, st>>>(cfg, specs, spec_end, n_pairs, cfg_idx, spec_idx, out);
+    else
+      featurize_uniform_list<<<blocks, kThreads, 0, st>>>(family, cfg, specs, spec_end, n_pairs, cfg_idx,
+                                                           spec_idx, out);
   }
   return (int)cudaGetLastError();
 }

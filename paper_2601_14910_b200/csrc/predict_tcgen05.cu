@@ -111,7 +111,9 @@ __host__ __device__ constexpr uint32_t op_off(uint32_t r, uint32_t k, uint32_t K
 // Table IV order (O8): per pipe present (Tensor, FMA, XU) [total ops, C^GPU,
 // max-SM ops, C^SM], then the 7 MIO features.  Record slot, +16 for a float slot.
 __host__ __device__ constexpr int in_slot(int fam, int k) {
-  const int pipes = (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM) ? 1 : (fam == SP_ATTENTION ? 5 : 6);
+  const int pipes = (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM || fam == SP_GEMM_SPLITK)
+                        ? 1
+                        : (fam == SP_ATTENTION ? 5 : 6);
   int n = 0;
   for (int p = 0; p < 3; ++p) {
     if (!(pipes & (1 << p))) continue;
@@ -125,7 +127,7 @@ __host__ __device__ constexpr int in_slot(int fam, int k) {
   return k - n < 7 ? mio[k - n] : -1;
 }
 __host__ __device__ constexpr int n_in_of(int fam) {
-  return (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM) ? 11 : 15;
+  return (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM || fam == SP_GEMM_SPLITK) ? 11 : 15;
 }
 
 #ifdef SP_PRED_TRACE
@@ -600,7 +602,8 @@ static cudaError_t launch_fam(int fam, const Params &P, unsigned grid, cudaStrea
     case SP_GEMM: kern = predict_tcgen05_kernel<BF16, SP_GEMM>; break;
     case SP_ATTENTION: kern = predict_tcgen05_kernel<BF16, SP_ATTENTION>; break;
     case SP_FUSED_MOE: kern = predict_tcgen05_kernel<BF16, SP_FUSED_MOE>; break;
-    case SP_SCALED_MM: kern = predict_tcgen05_kernel<BF16, SP_GEMM>; break;  // same Table IV layout
+    case SP_SCALED_MM:    // same Table IV layout as GEMM
+    case SP_GEMM_SPLITK: kern = predict_tcgen05_kernel<BF16, SP_GEMM>; break;
     case SP_RMSNORM: kern = predict_tcgen05_kernel<BF16, SP_RMSNORM>; break;
     default: kern = predict_tcgen05_kernel<BF16, SP_SILU_MUL>; break;
   }

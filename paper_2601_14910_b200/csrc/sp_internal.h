@@ -20,7 +20,9 @@ enum FltSlot { F_CG_T, F_CG_F, F_CG_X, F_CS_T, F_CS_F, F_CS_X, F_GLOB_G, F_L2_G,
 
 // Pipes per family (Table V): bit 0 Tensor, bit 1 FMA, bit 2 XU.
 __host__ __device__ inline int family_pipes(int fam) {
-  return (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM) ? 1 : (fam == SP_ATTENTION ? 5 : 6);
+  return (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_SCALED_MM || fam == SP_GEMM_SPLITK)
+             ? 1
+             : (fam == SP_ATTENTION ? 5 : 6);
 }
 
 // Step a1: per-spec constants derived once on the host in fp64 (Eq.4-5).

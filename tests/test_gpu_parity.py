@@ -68,6 +68,7 @@ FAMILY_BATCHES = {
     "rmsnorm": lambda: gen.gen_rowwise(gen.RMSNORM, 500, 1004),
     "silu": lambda: gen.gen_rowwise(gen.SILU_MUL, 500, 1005),
     "scaled_mm": lambda: gen.gen_scaled_mm(500, 1006),
+    "gemm_splitk": lambda: gen.gen_gemm_splitk(600, 1007),
 }
 
 
@@ -153,6 +154,36 @@ def test_attention_edge_cases(sp, ctx, orc):
     o = orc.featurize(b, sa)
     assert set(np.unique(o.status)) >= {0, 1, 2, 3, 5, 6, 7}
     assert_feature_parity(g, o, "attention edges")
+
+
+def test_splitk_edge_cases(sp, ctx, orc):
+    """Split-K: the hand-derived golden cases (wrapping / disjoint task classes,
+    empty slices), SPLIT_K far above the k-tile count, a single k-tile, one
+    output tile, SPLIT_K = 0 (tile error) and a task count past 2^31 (range)."""
+    cols = {k: [] for k in gen.FIELDS[gen.GEMM_SPLITK]}
+
+    def add(**kw):
+        d = dict(M=256, N=256, K=1000, TM=128, TN=128, BK=64, SPLIT_K=3, STAGES=3, WARPS=8, REGS=168,
+                 SMEM=0, DTYPE=0)
+        d.update(kw)
+        for k in cols:
+            cols[k].append(d[k])
+
+    for sk, k in ((3, 1000), (7, 1000), (20, 1000), (2, 960)):
+        add(SPLIT_K=sk, K=k)
+    add(SPLIT_K=100000, K=53248)
+    add(SPLIT_K=16, K=64)                       # one k-tile: one slice
+    add(M=1, N=1, SPLIT_K=5)                    # one output tile
+    add(SPLIT_K=0)                              # SP_PAIR_E_TILE
+    add(M=131072, N=131072, TM=16, TN=16, K=65536, BK=16, SPLIT_K=64)  # T >= 2^31: SP_PAIR_E_RANGE
+    add(DTYPE=3)                                # FP8 is the Scaled MM family's: SP_PAIR_E_DTYPE
+    b = gen.make_batch(gen.GEMM_SPLITK, cols)
+    sa = np.concatenate([odd_specs(), specs.paper_gpu_specs()])
+    sa[0]["num_sms"], sa[1]["num_sms"] = 5, 8
+    _, g = gpu_features(sp, ctx, b, sa)
+    o = orc.featurize(b, sa)
+    assert set(np.unique(o.status)) == {0, 2, 7, 8}
+    assert_feature_parity(g, o, "split-K edges")
 
 
 def test_uniform_edge_cases(sp, ctx, orc):

@@ -550,3 +550,67 @@ def test_planner_rejects_causal(orc):
     cfg = dict(g["config"], CAUSAL=1)
     _, _, st = feats(orc, one(gen.ATTENTION, cfg, requests=[[1, 1000], [1, 300]]), A100)
     assert st == 2  # SP_PAIR_E_TILE
+
+
+# --------------------------------------------------------------- split-K GEMM (R25, NEXT-4)
+
+@pytest.mark.parametrize("k", range(4))
+def test_gemm_splitk_worked_example(orc, k):
+    """Hand-derived slices, task lists and busiest SM (golden gemm_splitk_1000):
+    covers the wrapping last-slice interval (SPLIT_K 3), empty slices (7, 20)
+    and disjoint classes (K 960, SPLIT_K 2 on 8 SMs)."""
+    g = GOLD["gemm_splitk_1000"]
+    c = g["cases"][k]
+    b = one(gen.GEMM_SPLITK, dict(g["config"], SPLIT_K=c["SPLIT_K"], K=c["K"]))
+    tl = orc.task_list(b)
+    assert (tl[:, 0] // g["ktile_ops"]).tolist() == c["task_ktiles"]
+    assert (tl[:, 3] // g["ktile_bytes"]).tolist() == c["task_ktiles"]
+    assert (tl[:, 0] % g["ktile_ops"] == 0).all() and (tl[:, 1:3] == 0).all()
+    ints, _, st = feats(orc, b, spec_with(num_sms=c["n_sm"]))
+    assert st == 0
+    for key in ("n_tasks", "tot_T", "max_T", "bytes", "bytes_max"):
+        assert ints[key] == c[key], key
+
+
+def test_gemm_splitk_one_is_gemm(orc):
+    """SPLIT_K = 1 is the plain GEMM (a different decomposer, decompose_gemm):
+    identical records on all 11 Table VI GPUs."""
+    g = gen.gen_gemm(80, 11, m_range=(2, 9000), n_range=(384, 9000), k_range=(256, 20000))
+    cols = {n: g.field(n) for n in gen.FIELDS[gen.GEMM]}
+    cols["SPLIT_K"] = np.ones(g.n_configs, dtype=np.int32)
+    s = gen.make_batch(gen.GEMM_SPLITK, cols)
+    sa = specs.paper_gpu_specs()
+    a, b = orc.featurize(g, sa), orc.featurize(s, sa)
+    assert np.array_equal(a.status, b.status) and np.array_equal(a.ints, b.ints)
+    assert np.array_equal(a.flts, b.flts, equal_nan=True)
+
+
+def test_gemm_splitk_invariants(orc):
+    """Splitting K moves work between tasks, never creates it: Tensor ops and
+    bytes totals equal the unsplit GEMM's; T = tiles x non-empty slices; the
+    busiest SM is at least the mean and at most ceil(T/N) full-slice tasks."""
+    b = gen.gen_gemm_splitk(150, 12)
+    sa = specs.paper_gpu_specs()
+    o = orc.featurize(b, sa)
+    assert (o.status == 0).all()
+    C = b.n_configs
+    one_split = gen.ConfigBatch(gen.GEMM_SPLITK, b.fields.copy())
+    one_split.fields[gen.FIELDS[gen.GEMM_SPLITK].index("SPLIT_K")] = 1
+    o1 = orc.featurize(one_split, sa)
+    names = orc.INT_NAMES
+    for key in ("tot_T", "bytes"):
+        k = names.index(key)
+        assert np.array_equal(o.ints[k], o1.ints[k])
+    M, N, K, tm, tn, bk, S = (b.field(n).astype(np.int64) for n in ("M", "N", "K", "TM", "TN", "BK", "SPLIT_K"))
+    kt = -(-K // bk)
+    kps = -(-kt // S)
+    slices = -(-kt // kps)
+    tiles = (-(-M // tm)) * (-(-N // tn))
+    T = o.ints[names.index("n_tasks")].reshape(len(sa), C)
+    assert (T == tiles * slices).all()
+    nsm = sa["num_sms"].astype(np.int64)[:, None]
+    mx = o.ints[names.index("max_T")].reshape(len(sa), C)
+    tot = o.ints[names.index("tot_T")].reshape(len(sa), C)
+    full = 2 * tm * tn * kps * bk
+    assert (mx * nsm >= tot).all()
+    assert (mx <= -(-T // nsm) * full).all()

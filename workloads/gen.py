@@ -19,9 +19,10 @@ from dataclasses import dataclass
 import numpy as np
 
 # ---- family codes (include/synperf.h sp_family) ----
-GEMM, ATTENTION, FUSED_MOE, RMSNORM, SILU_MUL, SCALED_MM = 0, 1, 2, 3, 4, 5
+GEMM, ATTENTION, FUSED_MOE, RMSNORM, SILU_MUL, SCALED_MM, GEMM_SPLITK = 0, 1, 2, 3, 4, 5, 6
 FAMILY_NAMES = {GEMM: "gemm", ATTENTION: "attention", FUSED_MOE: "fused_moe",
-                RMSNORM: "rmsnorm", SILU_MUL: "silu_mul", SCALED_MM: "scaled_mm"}
+                RMSNORM: "rmsnorm", SILU_MUL: "silu_mul", SCALED_MM: "scaled_mm",
+                GEMM_SPLITK: "gemm_splitk"}
 
 # ---- dtype codes (include/synperf.h sp_dtype) ----
 BF16, FP16, FP32, FP8 = 0, 1, 2, 3
@@ -35,6 +36,8 @@ FIELDS = {
     RMSNORM: ["SEQ", "DIM", "WARPS", "REGS", "SMEM", "DTYPE"],
     SILU_MUL: ["SEQ", "DIM", "WARPS", "REGS", "SMEM", "DTYPE"],
     SCALED_MM: ["M", "N", "K", "TM", "TN", "BK", "STAGES", "WARPS", "REGS", "SMEM", "DTYPE"],
+    GEMM_SPLITK: ["M", "N", "K", "TM", "TN", "BK", "SPLIT_K", "STAGES", "WARPS", "REGS", "SMEM",
+                  "DTYPE"],
 }
 N_FIELDS = {f: len(v) for f, v in FIELDS.items()}
 
@@ -215,6 +218,26 @@ def gen_scaled_mm(n: int, seed: int) -> ConfigBatch:
                 WARPS=np.where(area <= 8192, 4, 8), REGS=np.where(area <= 16384, 168, 232), SMEM=0,
                 DTYPE=FP8)
     return ConfigBatch(SCALED_MM, _pack(SCALED_MM, cols, n))
+
+
+def gen_gemm_splitk(n: int, seed: int) -> ConfigBatch:
+    """Split-K GEMMs: the GEMM space of §V-B restricted to the shapes
+    cuBLAS splits -- few output tiles against a long K (M ~ logU[1, 4096],
+    N ~ logU[384, 16384], K ~ logU[1024, 53248]) -- with the GEMM tile set and
+    SPLIT_K ~ U{1..16} (1 = no split; values above the k-tile count exercise
+    the empty-slice rule of reading R25)."""
+    rng = np.random.default_rng(seed)
+    M = _logu_int(rng, 1, 4096, n)
+    N = _logu_int(rng, 384, 16384, n)
+    K = _logu_int(rng, 1024, 53248, n)
+    tiles = np.array([(64, 64), (64, 128), (128, 64), (128, 128), (128, 256), (256, 128)])[rng.integers(0, 6, n)]
+    area = tiles[:, 0] * tiles[:, 1]
+    cols = dict(M=M, N=N, K=K, TM=tiles[:, 0], TN=tiles[:, 1], BK=rng.choice([32, 64], n),
+                SPLIT_K=rng.integers(1, 17, n), STAGES=rng.choice([3, 4, 5], n),
+                WARPS=np.where(area <= 8192, 4, 8),
+                REGS=np.where(area <= 8192, 128, np.where(area <= 16384, 168, 232)), SMEM=0,
+                DTYPE=rng.choice([BF16, FP16], n))
+    return ConfigBatch(GEMM_SPLITK, _pack(GEMM_SPLITK, cols, n))
 
 
 def gen_rowwise(family: int, n: int, seed: int) -> ConfigBatch:

@@ -20,7 +20,7 @@ from __future__ import annotations
 import numpy as np
 
 HIDDEN = (256, 128, 64)
-N_IN = {0: 11, 1: 15, 2: 11, 3: 15, 4: 15, 5: 11}  # family -> Table IV width (4*pipes + 7)
+N_IN = {0: 11, 1: 15, 2: 11, 3: 15, 4: 15, 5: 11, 6: 11}  # family -> Table IV width (4*pipes + 7)
 
 
 def _he_uniform(rng, fan_out, fan_in):
