@@ -539,6 +539,89 @@ sp_status sp_e2e_compose(sp_ctx *ctx, const sp_e2e_plan *plan, int32_t spec_begi
                          const sp_comm_model *comm, const sp_e2e_latencies *lat, float *step_us,
                          double *trace_us, double *trace_cat, void *stream);
 
+/* ===================================================================
+ * Estimator training on the GPU (PAPER §V-C; §VII-A P:670;
+ * SURVEY §8(f) NEXT-4).  One minibatch step of the per-category MLP:
+ *   target  t = t_theory_us / measured_us        (execution efficiency)
+ *   input   x = normalised Table IV vector        (O8-O9 with the model's mu/sigma, R17)
+ *   forward, per hidden layer: z = h W^T + b, a = relu(z),
+ *           batch-statistics BatchNorm a_hat = (a - mean)/sqrt(var + eps) (biased var),
+ *           y = gamma a_hat + beta, inverted Dropout(p) -> h; e = sigmoid(h3 . w4 + b4)
+ *   loss    MAPE mean |e - t| / max(t, 1e-6) or pinball(q)
+ *   update  AdamW: decoupled weight decay on every parameter, bias-corrected
+ *           moments; running BN statistics with momentum and unbiased variance.
+ * Readings T1..T9 fix what the paper leaves open.  The dropout
+ * keep mask is counter-based (T3): splitmix64 finaliser of seed + ctr*0x9E3779B97F4A7C15,
+ * ctr = ((step*4 + layer)*2^20 + row)*2^8 + col; keep iff bits 63..40 >= round(p*2^24).
+ * Arithmetic is fp32 (CUDA cores); reductions run in a fixed order, so a step is
+ * deterministic.  Oracle: oracle/train.py (fp64).
+ * =================================================================== */
+
+typedef enum sp_loss { SP_LOSS_MAPE = 0, SP_LOSS_PINBALL = 1 } sp_loss;
+
+typedef struct sp_train_config {
+  int32_t loss;          /* sp_loss */
+  float quantile;        /* pinball q in (0,1); 0.8 for the P80 ceiling */
+  float lr;              /* 1e-3 */
+  float weight_decay;    /* decoupled; 0.01 (T5: the paper gives no value) */
+  float beta1, beta2, adam_eps;  /* 0.9, 0.999, 1e-8 */
+  float dropout;         /* p in [0,1); 0.1 */
+  float bn_momentum;     /* 0.1 */
+  int32_t max_batch;     /* largest minibatch, 2 .. 2^20 (sizes the trainer's buffers) */
+  uint64_t seed;         /* dropout generator seed (T3) */
+} sp_train_config;
+
+typedef struct sp_trainer sp_trainer;
+
+/* Creates a trainer on ctx's device from HOST initial weights (desc: same
+ * layout and checks as sp_load_model; precision is ignored, training is fp32;
+ * mu/sigma are the fixed input normalisation).  Allocates its device buffers
+ * once (parameters, AdamW moments, activations for max_batch rows).
+ * SP_E_ARG / SP_E_DATA on bad arguments, SP_E_INTERNAL on allocation failure. */
+sp_status sp_train_create(sp_ctx *ctx, const sp_mlp_desc *init, const sp_train_config *cfg,
+                          sp_trainer **out);
+void sp_train_destroy(sp_trainer *tr);
+
+/* One training step over the minibatch rows batch_idx[0..B) (DEVICE int64
+ * pair indices into `in`, which must have the model's family; every indexed
+ * pair must have status 0 and measured_us > 0).  measured_us: DEVICE fp32
+ * [in->n_pairs].  loss_out: DEVICE fp32 [1] receiving the pre-update batch
+ * loss, or NULL.  Advances the trainer's step counter (the dropout counter).
+ * Asynchronous on `stream`; no allocation.  SP_E_ARG if B < 2 or B > max_batch. */
+sp_status sp_train_step(sp_trainer *tr, const sp_features *in, const float *measured_us,
+                        const int64_t *batch_idx, int64_t B, float *loss_out, void *stream);
+
+/* Eval-mode loss (running statistics, no dropout) over rows idx[0..n) (DEVICE
+ * int64), processed in chunks of max_batch: the validation loss that early
+ * stopping monitors.  loss_out: DEVICE fp32 [1].  Asynchronous. */
+sp_status sp_train_eval(sp_trainer *tr, const sp_features *in, const float *measured_us,
+                        const int64_t *idx, int64_t n, float *loss_out, void *stream);
+
+/* Number of floats sp_train_export writes: P + 2*(256+128+64), with
+ * P = 256*n_in + 3*256 + 128*256 + 3*128 + 64*128 + 3*64 + 64 + 1 trainable
+ * parameters in the order w1 b1 g1 be1 w2 b2 g2 be2 w3 b3 g3 be3 w4 b4
+ * (weights row-major [out][in]), followed by the running statistics
+ * m1 v1 m2 v2 m3 v3. */
+int64_t sp_train_export_count(const sp_trainer *tr);
+
+/* Waits for the trainer's pending work on `stream` and copies the current
+ * parameters and running statistics into host_out[sp_train_export_count]. */
+sp_status sp_train_export(sp_trainer *tr, float *host_out, void *stream);
+
+/* Waits for the trainer's pending work on `stream` and copies the gradients of
+ * the last sp_train_step (the P trainable parameters, same order) into
+ * host_out[P]; P = sp_train_export_count - 2*(256+128+64).  For testing and
+ * diagnosis. */
+sp_status sp_train_export_grads(sp_trainer *tr, float *host_out, void *stream);
+
+/* Normalisation statistics (R17; reading T7): per input feature k of the
+ * family's Table IV vector, mean and population standard deviation of
+ * ln(1 + v_k) over pairs idx[0..n) (DEVICE int64) of `in`, accumulated in fp64
+ * in a fixed order.  Writes HOST mu_out[n_in], sigma_out[n_in]; synchronises
+ * `stream`. */
+sp_status sp_fit_norm(sp_ctx *ctx, const sp_features *in, const int64_t *idx, int64_t n, float *mu_out,
+                      float *sigma_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

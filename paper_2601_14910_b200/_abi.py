@@ -92,6 +92,21 @@ SP_E2E_NCAT = 5
 E2E_CATEGORIES = ["gemm", "attention", "rmsnorm", "silu_mul", "comm"]
 
 
+# sp_loss
+SP_LOSS_MAPE, SP_LOSS_PINBALL = 0, 1
+LOSSES = {"mape": SP_LOSS_MAPE, "pinball": SP_LOSS_PINBALL}
+
+
+class sp_train_config(C.Structure):
+    _fields_ = [("loss", C.c_int32), ("quantile", C.c_float), ("lr", C.c_float),
+                ("weight_decay", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("adam_eps", C.c_float), ("dropout", C.c_float), ("bn_momentum", C.c_float),
+                ("max_batch", C.c_int32), ("seed", C.c_uint64)]
+
+
+assert C.sizeof(sp_train_config) == 48
+
+
 class sp_kernel_stat(C.Structure):
     _fields_ = [("kernel", C.c_char_p), ("launches", C.c_int64), ("total_ms", C.c_double)]
 
@@ -139,6 +154,14 @@ def _load():
         "sp_load_comm_model": (C.c_int, [vp, C.POINTER(sp_comm_desc), C.POINTER(vp)]),
         "sp_free_comm_model": (None, [vp]),
         "sp_e2e_compose": (C.c_int, [vp, vp, i32, i32, vp, C.POINTER(sp_e2e_latencies), vp, vp, vp, vp]),
+        "sp_train_create": (C.c_int, [vp, vp, C.POINTER(sp_train_config), C.POINTER(vp)]),
+        "sp_train_destroy": (None, [vp]),
+        "sp_train_step": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
+        "sp_train_eval": (C.c_int, [vp, vp, vp, vp, i64, vp, vp]),
+        "sp_train_export_count": (i64, [vp]),
+        "sp_train_export": (C.c_int, [vp, vp, vp]),
+        "sp_train_export_grads": (C.c_int, [vp, vp, vp]),
+        "sp_fit_norm": (C.c_int, [vp, vp, vp, i64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -153,4 +176,6 @@ EXPORTED = ["sp_create", "sp_destroy", "sp_last_error", "sp_version", "sp_device
             "sp_load_gpu_specs", "sp_free_specs", "sp_specs_count", "sp_load_model",
             "sp_free_model", "sp_featurize", "sp_featurize_sched", "sp_predict", "sp_perf_gap", "sp_set_profiling", "sp_profile_read",
             "sp_e2e_plan_create", "sp_e2e_plan_update", "sp_e2e_plan_expand", "sp_free_e2e_plan", "sp_e2e_plan_info",
-            "sp_e2e_plan_batch", "sp_load_comm_model", "sp_free_comm_model", "sp_e2e_compose"]
+            "sp_e2e_plan_batch", "sp_load_comm_model", "sp_free_comm_model", "sp_e2e_compose",
+            "sp_train_create", "sp_train_destroy", "sp_train_step", "sp_train_eval", "sp_train_export_count",
+            "sp_train_export", "sp_train_export_grads", "sp_fit_norm"]

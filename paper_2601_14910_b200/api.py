@@ -159,6 +159,110 @@ class Model:
             self._h = None
 
 
+class Trainer:
+    """sp_trainer: on-GPU training of one per-category estimator (PAPER §V-C
+    P:486-491).  Argument marshalling only; the step runs in
+    csrc/train.cu."""
+
+    PARAM_ORDER = ["w1", "b1", "g1", "be1", "w2", "b2", "g2", "be2", "w3", "b3", "g3", "be3", "w4", "b4"]
+
+    def __init__(self, ctx: "Context", init: dict, loss: str = "mape", quantile: float = 0.8,
+                 lr: float = 1e-3, weight_decay: float = 0.01, betas=(0.9, 0.999), adam_eps: float = 1e-8,
+                 dropout: float = 0.1, bn_momentum: float = 0.1, max_batch: int = 256, seed: int = 0):
+        self._ctx, self.family, self.n_in = ctx, int(init["family"]), int(init["n_in"])
+        self.bn_eps = float(init.get("bn_eps", 1e-5))
+        self.mu = np.asarray(init["mu"], np.float32).copy()
+        self.sigma = np.asarray(init["sigma"], np.float32).copy()
+        d, keep = ctx._mlp_desc(init, "fp32")
+        c = _abi.sp_train_config()
+        c.loss = _abi.LOSSES[loss]
+        c.quantile, c.lr, c.weight_decay = quantile, lr, weight_decay
+        c.beta1, c.beta2, c.adam_eps = betas[0], betas[1], adam_eps
+        c.dropout, c.bn_momentum, c.max_batch, c.seed = dropout, bn_momentum, int(max_batch), int(seed)
+        h = C.c_void_p()
+        ctx._check(lib.sp_train_create(ctx._h, C.byref(d), C.byref(c), C.byref(h)))
+        del keep
+        self._h = h.value
+        self.max_batch = int(max_batch)
+        self.loss_dev = torch.zeros(1, dtype=torch.float32, device=ctx.torch_device)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.sp_train_destroy(self._h)
+            self._h = None
+
+    def step(self, feats: "Features", measured_us: torch.Tensor, batch_idx: torch.Tensor, stream=None) -> torch.Tensor:
+        """sp_train_step over pairs batch_idx (int64, device); returns the device loss scalar."""
+        fs = feats.c_struct()
+        self._ctx._check(lib.sp_train_step(self._h, C.byref(fs), measured_us.data_ptr(), batch_idx.data_ptr(),
+                                           int(batch_idx.numel()), self.loss_dev.data_ptr(), _stream_ptr(stream)))
+        return self.loss_dev
+
+    def eval_loss(self, feats: "Features", measured_us: torch.Tensor, idx: torch.Tensor, stream=None) -> torch.Tensor:
+        out = torch.empty(1, dtype=torch.float32, device=self._ctx.torch_device)
+        fs = feats.c_struct()
+        self._ctx._check(lib.sp_train_eval(self._h, C.byref(fs), measured_us.data_ptr(), idx.data_ptr(),
+                                           int(idx.numel()), out.data_ptr(), _stream_ptr(stream)))
+        return out
+
+    def export(self, stream=None) -> dict:
+        """Current weights + running statistics as a model dict (sp_load_model's layout)."""
+        n = int(lib.sp_train_export_count(self._h))
+        buf = np.empty(n, np.float32)
+        self._ctx._check(lib.sp_train_export(self._h, buf.ctypes.data, _stream_ptr(stream)))
+        m = {"family": self.family, "n_in": self.n_in, "bn_eps": np.float32(self.bn_eps),
+             "mu": self.mu.copy(), "sigma": self.sigma.copy()}
+        m.update(self._split(buf))
+        o = n - 2 * (256 + 128 + 64)  # running statistics follow the P parameters
+        m["b4"] = np.float32(m["b4"][0])
+        for l, width in zip((1, 2, 3), (256, 128, 64)):
+            m[f"m{l}"] = buf[o:o + width].copy()
+            m[f"v{l}"] = buf[o + width:o + 2 * width].copy()
+            o += 2 * width
+        return m
+
+    def _split(self, buf: np.ndarray) -> dict:
+        shapes = {"w1": (256, self.n_in), "w2": (128, 256), "w3": (64, 128), "w4": (64,), "b4": (1,)}
+        out, o = {}, 0
+        for k in self.PARAM_ORDER:
+            shp = shapes[k] if k in shapes else ({"1": 256, "2": 128, "3": 64}[k[-1]],)
+            cnt = int(np.prod(shp))
+            out[k] = buf[o:o + cnt].reshape(shp).copy()
+            o += cnt
+        return out
+
+    def export_grads(self, stream=None) -> dict:
+        """Gradients of the last step, per parameter (sp_train_export_grads)."""
+        n = int(lib.sp_train_export_count(self._h)) - 2 * (256 + 128 + 64)
+        buf = np.empty(n, np.float32)
+        self._ctx._check(lib.sp_train_export_grads(self._h, buf.ctypes.data, _stream_ptr(stream)))
+        return self._split(buf)
+
+    def fit(self, feats: "Features", measured_us: torch.Tensor, train_idx: torch.Tensor, val_idx: torch.Tensor,
+            max_epochs: int = 100, patience: int = 20, batch: int | None = None, seed: int = 0) -> dict:
+        """Early-stopped training loop ("Early stopping ... monitoring validation loss"):
+        shuffled minibatches (seeded permutation of train_idx on the device), one eval
+        loss per epoch, best-validation snapshot returned with the loss history."""
+        bs = batch or self.max_batch
+        g = torch.Generator(device=self._ctx.torch_device)
+        g.manual_seed(seed)
+        best, best_m, bad, hist = float("inf"), None, 0, []
+        n = int(train_idx.numel())
+        for _ in range(max_epochs):
+            perm = train_idx[torch.randperm(n, generator=g, device=train_idx.device)]
+            for i in range(0, n - bs + 1, bs):
+                self.step(feats, measured_us, perm[i:i + bs])
+            v = float(self.eval_loss(feats, measured_us, val_idx).item())
+            hist.append(v)
+            if v < best:
+                best, best_m, bad = v, self.export(), 0
+            else:
+                bad += 1
+                if bad > patience:
+                    break
+        return {"model": best_m, "best_val_loss": best, "val_history": hist}
+
+
 class CommModel:
     """sp_comm_model: per-spec All-Reduce / Send-Recv calibration tables."""
 
@@ -301,6 +405,34 @@ class Context:
         return Specs(self, h.value, len(arr))
 
     # -- estimator
+    def _mlp_desc(self, model: dict, precision: str):
+        d = _abi.sp_mlp_desc()
+        d.family = int(model["family"])
+        d.n_in = int(model["n_in"])
+        d.precision = _abi.PRECISIONS[precision]
+        keep = []
+        for k in _abi.MLP_ARRAYS:
+            a = np.ascontiguousarray(model[k], dtype=np.float32)
+            keep.append(a)
+            setattr(d, k, a.ctypes.data)
+        d.b4 = float(model["b4"])
+        d.bn_eps = float(model.get("bn_eps", 1e-5))
+        return d, keep
+
+    def trainer(self, init: dict, **cfg) -> Trainer:
+        """sp_train_create: on-GPU estimator training from the initial weights `init`."""
+        return Trainer(self, init, **cfg)
+
+    def fit_norm(self, feats: "Features", idx: torch.Tensor, stream=None):
+        """sp_fit_norm: (mu, sigma) fp32 [n_in] of ln(1+v) over pairs idx (R17, T7)."""
+        n_in = 11 if feats.family in (_abi.SP_GEMM, _abi.SP_FUSED_MOE, _abi.SP_SCALED_MM,
+                                      _abi.SP_GEMM_SPLITK) else 15
+        mu, sg = np.empty(n_in, np.float32), np.empty(n_in, np.float32)
+        fs = feats.c_struct()
+        self._check(lib.sp_fit_norm(self._h, C.byref(fs), idx.data_ptr(), int(idx.numel()), mu.ctypes.data,
+                                    sg.ctypes.data, _stream_ptr(stream)))
+        return mu, sg
+
     def load_model(self, model: dict, precision: str = "fp16") -> Model:
         """precision: "fp16" / "bf16" (tcgen05 tensor-core path) or "fp32" (CUDA cores)."""
         d = _abi.sp_mlp_desc()

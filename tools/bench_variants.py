@@ -2,7 +2,10 @@
   * sp_featurize_sched GREEDY / MINHEAP on a slice of BASELINE config 2
     (attention x 11 GPUs; sequential scheduler simulation, warp per pair);
   * sp_perf_gap (P80 gap diagnosis) over BASELINE config 3 (fused MoE x 11,
-    the paper applies it to its fused-MoE dataset).
+    the paper applies it to its fused-MoE dataset, P:677);
+  * sp_train_step (on-GPU estimator training, NEXT-4) on config-3 features at
+    minibatch 256 (the SPEC default) and 4096: steps/s, samples/s, per-kernel
+    device times (sp_set_profiling) and FLOP rate (6 x forward MACs per sample).
 Device-timed with CUDA events, median of --reps after warm-up.
 
     python tools/bench_variants.py [--reps 5] [--scale 0.02]
@@ -74,6 +77,32 @@ def main():
     print(json.dumps({"variant": "perf_gap", "workload": "cfg3", "pairs": n, "ms": ms,
                       "pairs_per_s": n / (ms * 1e-3), "achieved_gbs": nbytes / (ms * 1e-3) / 1e9,
                       "underperforming": int(c[:, 1].sum()), "valid": int(c[:, 0].sum())}), flush=True)
+    # ---- estimator training on the same features
+    valid = torch.nonzero(torch.from_numpy(sp.features_to_host(f)[2] == 0)).view(-1).cuda()
+    n_in = 11
+    flop = 6 * (n_in * 256 + 256 * 128 + 128 * 64 + 64)  # fwd 2 x MACs, bwd 2 x that (dX + dW)
+    for B in (256, 4096):
+        tr = ctx.trainer(models.random_mlp(b.family, 81), max_batch=B, seed=3)
+        g = torch.Generator(device="cuda:0")
+        g.manual_seed(0)
+        batches = [valid[torch.randint(0, valid.numel(), (B,), generator=g, device="cuda:0")] for _ in range(50)]
+
+        def run():
+            for bi in batches:
+                tr.step(f, meas, bi)
+
+        ctx.set_profiling(True)
+        ctx.profile_read(reset=True)
+        ms = timed(run, args.reps) / len(batches)
+        kst = ctx.profile_read(reset=True)
+        ctx.set_profiling(False)
+        ms_np = timed(run, args.reps) / len(batches)  # without the per-launch events
+        print(json.dumps({"variant": "train_step", "workload": "cfg3 features", "batch": B,
+                          "ms_per_step": ms_np, "steps_per_s": 1e3 / ms_np, "samples_per_s": B * 1e3 / ms_np,
+                          "tflops": flop * B / (ms_np * 1e-3) / 1e12,
+                          "launches_per_step": sum(v[0] for v in kst.values()) / ((args.reps + 2) * len(batches)),
+                          "kernels_ms_per_step": {k: v[1] / ((args.reps + 2) * len(batches)) for k, v in kst.items()}}),
+              flush=True)
 
 
 if __name__ == "__main__":
