@@ -339,6 +339,24 @@ sp_status sp_featurize_sched(sp_ctx *ctx, const sp_config_batch *cfg, const sp_s
                              void *stream);
 
 /*
+ * Feature-stage options.  sp_featurize_ex(.., scheduler, 0, ..)
+ * is sp_featurize_sched.
+ *   SP_FEAT_CLAMPED  SPEC's clamped edge tiles, the alternative
+ *                    to the padded reading R2: an edge tile of a GEMM (fused
+ *                    MoE) computes and loads only its in-range rows and columns,
+ *                    ma x na over the exact K (H): Tensor 2*ma*na*K, bytes
+ *                    (ma+na)*K*bpe.  Tasks are then non-uniform; the busiest SM
+ *                    is found exactly (cyclic dealing of runs of equal tasks,
+ *                    one warp per pair).  GEMM and fused MoE with SP_SCHED_RR
+ *                    only (SP_E_UNSUPPORTED otherwise); <= 4096 SMs per spec.
+ */
+#define SP_FEAT_CLAMPED 1u
+
+sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs,
+                          const sp_pairing *pairs, int32_t scheduler, uint32_t flags, const sp_features *out,
+                          void *stream);
+
+/*
  * Predictor stage, steps a10..a12: for each pair p < in->n_pairs,
  * x = normalised Table IV vector of in (O8-O9), e = sigmoid(MLP(x)),
  * latency_us[p] = t_theory_us[p] / e.  efficiency may be NULL.  Pairs with

@@ -24,6 +24,7 @@ SP_PAIRS_CROSS, SP_PAIRS_LIST = 0, 1
 SP_MLP_FP32, SP_MLP_BF16, SP_MLP_FP16 = 0, 1, 2
 PRECISIONS = {"fp32": SP_MLP_FP32, "bf16": SP_MLP_BF16, "fp16": SP_MLP_FP16}
 SP_STRICT = 1
+SP_FEAT_CLAMPED = 1
 # sp_scheduler
 SP_SCHED_RR, SP_SCHED_GREEDY, SP_SCHED_MINHEAP = 0, 1, 2
 SCHEDULERS = {"rr": SP_SCHED_RR, "greedy": SP_SCHED_GREEDY, "minheap": SP_SCHED_MINHEAP}
@@ -141,6 +142,7 @@ def _load():
         "sp_free_model": (None, [vp]),
         "sp_featurize": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "sp_featurize_sched": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
+        "sp_featurize_ex": (C.c_int, [vp, vp, vp, vp, i32, u32, vp, vp]),
         "sp_predict": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "sp_perf_gap": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, i32, C.c_float, C.c_float, vp, vp, vp, vp]),
         "sp_set_profiling": (C.c_int, [vp, i32]),
@@ -174,7 +176,7 @@ lib = _load()
 
 EXPORTED = ["sp_create", "sp_destroy", "sp_last_error", "sp_version", "sp_device_sms",
             "sp_load_gpu_specs", "sp_free_specs", "sp_specs_count", "sp_load_model",
-            "sp_free_model", "sp_featurize", "sp_featurize_sched", "sp_predict", "sp_perf_gap", "sp_set_profiling", "sp_profile_read",
+            "sp_free_model", "sp_featurize", "sp_featurize_sched", "sp_featurize_ex", "sp_predict", "sp_perf_gap", "sp_set_profiling", "sp_profile_read",
             "sp_e2e_plan_create", "sp_e2e_plan_update", "sp_e2e_plan_expand", "sp_free_e2e_plan", "sp_e2e_plan_info",
             "sp_e2e_plan_batch", "sp_load_comm_model", "sp_free_comm_model", "sp_e2e_compose",
             "sp_train_create", "sp_train_destroy", "sp_train_step", "sp_train_eval", "sp_train_export_count",

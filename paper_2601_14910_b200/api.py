@@ -453,13 +453,18 @@ class Context:
 
     # -- feature stage (a2..a9)
     def featurize(self, batch: DeviceBatch, specs: Specs, out: Features, pairs=None,
-                  stream=None, scheduler: str = "rr") -> Features:
-        """sp_featurize (scheduler "rr") or sp_featurize_sched ("greedy", "minheap")."""
+                  stream=None, scheduler: str = "rr", clamped: bool = False) -> Features:
+        """sp_featurize (scheduler "rr"), sp_featurize_sched ("greedy", "minheap"), or
+        sp_featurize_ex with SP_FEAT_CLAMPED (clamped edge tiles, GEMM / fused MoE)."""
         if pairs is None:
             pairs = cross(0, len(specs))
         cb = batch.c_struct()
         fs = out.c_struct()
-        if scheduler == "rr":
+        if clamped:
+            self._check(lib.sp_featurize_ex(self._h, C.byref(cb), specs.handle, C.byref(pairs),
+                                            _abi.SCHEDULERS[scheduler], _abi.SP_FEAT_CLAMPED, C.byref(fs),
+                                            _stream_ptr(stream)))
+        elif scheduler == "rr":
             self._check(lib.sp_featurize(self._h, C.byref(cb), specs.handle, C.byref(pairs),
                                          C.byref(fs), _stream_ptr(stream)))
         else:

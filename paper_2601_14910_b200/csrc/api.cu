@@ -301,9 +301,16 @@ extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const
 extern "C" sp_status sp_featurize_sched(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs_c,
                                         const sp_pairing *pairs, int32_t scheduler, const sp_features *out,
                                         void *stream) {
+  return sp_featurize_ex(ctx, cfg, specs_c, pairs, scheduler, 0u, out, stream);
+}
+
+extern "C" sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs_c,
+                                     const sp_pairing *pairs, int32_t scheduler, uint32_t flags,
+                                     const sp_features *out, void *stream) {
   if (!ctx) return fail(nullptr, SP_E_ARG, "sp_featurize: ctx is NULL");
   if (scheduler != SP_SCHED_RR && scheduler != SP_SCHED_GREEDY && scheduler != SP_SCHED_MINHEAP)
     return fail(ctx, SP_E_ARG, "sp_featurize_sched: unknown scheduler");
+  if (flags & ~SP_FEAT_CLAMPED) return fail(ctx, SP_E_ARG, "sp_featurize_ex: unknown flag");
   if (!cfg || !specs_c || !pairs || !out) return fail(ctx, SP_E_ARG, "sp_featurize: NULL argument");
   sp_specs *specs = const_cast<sp_specs *>(specs_c);
   const int fam = cfg->family;
@@ -342,7 +349,20 @@ extern "C" sp_status sp_featurize_sched(sp_ctx *ctx, const sp_config_batch *cfg,
   FeatOut fo{out->ints, out->flts, out->status, out->ld};
   const DevSpec *ds = (const DevSpec *)specs->dev.p;
   int e;
-  if (fam == SP_ATTENTION && scheduler != SP_SCHED_RR) {
+  if (flags & SP_FEAT_CLAMPED) {
+    if (fam != SP_GEMM && fam != SP_FUSED_MOE)
+      return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_ex: clamped edge tiles are implemented for GEMM and fused MoE");
+    if (scheduler != SP_SCHED_RR)
+      return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_ex: clamped edge tiles use the cyclic (RR) scheduler");
+    if (specs->max_sms > 4096) return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_ex: clamped mode supports <= 4096 SMs");
+    const bool cross = pairs->kind == SP_PAIRS_CROSS;
+    const LaunchHook h = ctx->hook();
+    h.on_begin("featurize_clamped", stream);
+    e = launch_featurize_clamped(fam, cv, ds, cross ? pairs->spec_begin : 0, specs->n, n_pairs,
+                                 cross ? nullptr : pairs->cfg_idx, cross ? nullptr : pairs->spec_idx, specs->max_sms,
+                                 fo, ctx->num_sms, stream);
+    h.on_end(stream);
+  } else if (fam == SP_ATTENTION && scheduler != SP_SCHED_RR) {
     // sequential scheduler simulation: per-warp shared memory for the largest target set
     const bool cross = pairs->kind == SP_PAIRS_CROSS;
     const int b = cross ? pairs->spec_begin : 0, en = cross ? pairs->spec_end : specs->n;

@@ -14,6 +14,9 @@
 // 137 B/pair record written to HBM.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <climits>
+
 #include "common.cuh"
 
 namespace sp {
@@ -407,6 +410,173 @@ __global__ void __launch_bounds__(kThreads) featurize_uniform_list(int fam, Conf
   uniform_pair(out, p, u, specs[g], family_pipes(fam));
 }
 
+// ------------------------------------------------------------------ clamped edge tiles
+
+// SPEC's clamped reading of edge tiles (the alternative to R2's
+// padded tiles): an edge tile computes and loads only its
+// in-range rows/columns, over the exact K (GEMM) or H (fused MoE).  Tasks are no
+// longer uniform, so the busiest SM is not ceil(T/N) tasks.  The task list is a
+// sequence of runs of equal tasks (per output-tile row: nt-1 full-width tiles,
+// then the edge tile), and cyclic dealing sends a run [start, start+len) of
+// weight w to SM j  q*w + w*[(j - start) mod N < r]  times (q = len/N, r = len%N).
+// A warp per pair adds the q*w parts to a constant and the cyclic intervals to a
+// per-warp difference array in shared memory (64-bit atomics: order-free
+// integer sums), then a prefix scan gives every S_j and the max.  O(rows + N).
+struct ClampRuns {
+  unsigned __int128 tot[2] = {0, 0};  // this lane's totals: Tensor ops, bytes
+  int64_t cst[2] = {0, 0};            // this lane's q*w parts
+};
+
+__device__ __forceinline__ void add_run(ClampRuns &cr, int64_t *D, int N, int64_t start, int64_t len,
+                                        int64_t w_ops, int64_t w_bytes) {
+  const int64_t w[2] = {w_ops, w_bytes};
+  const int64_t q = len / N, r = len - q * N;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    cr.tot[k] += (unsigned __int128)len * (unsigned __int128)w[k];
+    cr.cst[k] += q * w[k];
+    if (r == 0) continue;
+    unsigned long long *d = reinterpret_cast<unsigned long long *>(D + k * (N + 1));
+    const int a = (int)(start % N), b = a + (int)r;
+    atomicAdd(d + a, (unsigned long long)w[k]);
+    if (b <= N) {
+      atomicAdd(d + b, (unsigned long long)(-w[k]));
+    } else {
+      atomicAdd(d, (unsigned long long)w[k]);
+      atomicAdd(d + (b - N), (unsigned long long)(-w[k]));
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One pair, whole warp.  D: this warp's 2*(N_max+1) int64 scratch.
+__device__ void clamped_pair(int fam, const ConfigView &v, int64_t c, const DevSpec &s, const FeatOut &out,
+                             int64_t p, int64_t *D) {
+  const int lane = threadIdx.x & 31;
+  const UniformCfg u = config_of(fam, v, c);  // status, T, footprint, dtype (padded totals unused)
+  if (u.status != 0 || (u.tdt >= 0 && !s.tensor_ok[u.tdt])) {
+    if (lane == 0) emit_error(out, p, u.status != 0 ? u.status : SP_PAIR_E_DTYPE);
+    return;
+  }
+  const int N = s.num_sms;
+  for (int i = lane; i < 2 * (N + 1); i += 32) D[i] = 0;
+  __syncwarp();
+  ClampRuns cr;
+  if (fam == SP_GEMM) {
+    const int64_t M = fld(v, 0, c), Nn = fld(v, 1, c), K = fld(v, 2, c), tm = fld(v, 3, c), tn = fld(v, 4, c);
+    const int64_t bpe = bytes_per_elem((int)fld(v, 10, c));
+    const int64_t mt = cdiv64(M, tm), nt = cdiv64(Nn, tn), wl = Nn - (nt - 1) * tn;
+    for (int64_t i = lane; i < mt; i += 32) {
+      const int64_t h = min(tm, M - i * tm), t0 = i * nt;
+      if (nt > 1) add_run(cr, D, N, t0, nt - 1, 2 * h * tn * K, (h + tn) * K * bpe);
+      add_run(cr, D, N, t0 + nt - 1, 1, 2 * h * wl * K, (h + wl) * K * bpe);
+    }
+  } else {  // fused MoE: expert-major, m-block, n-block
+    const int64_t M = fld(v, 0, c), E = fld(v, 1, c), topk = fld(v, 2, c), H = fld(v, 3, c), Nn = fld(v, 4, c),
+                  bm = fld(v, 5, c), bn = fld(v, 6, c);
+    const int64_t bpe = bytes_per_elem((int)fld(v, 13, c));
+    const int64_t nt = cdiv64(Nn, bn), wl = Nn - (nt - 1) * bn;
+    const int64_t off = v.ragged_off ? __ldg(v.ragged_off + c) : -1;
+    const int64_t mtk = M * topk, qq = mtk / E, rr = mtk - qq * E;
+    int64_t base = 0;  // m-blocks of the experts before this chunk
+    for (int64_t e0 = 0; e0 < E; e0 += 32) {
+      const int64_t e = e0 + lane;
+      const int64_t te = e < E ? (off >= 0 ? (int64_t)__ldg(v.ragged + off + e) : qq + (e < rr ? 1 : 0)) : 0;
+      const int64_t mb = cdiv64(te, bm);
+      int64_t incl = mb;  // inclusive warp scan of the m-block counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int64_t first = base + incl - mb;
+      for (int64_t j = 0; j < mb; ++j) {
+        const int64_t ma = min(bm, te - j * bm), t0 = (first + j) * nt;
+        if (nt > 1) add_run(cr, D, N, t0, nt - 1, 2 * ma * bn * H, (ma + bn) * H * bpe);
+        add_run(cr, D, N, t0 + nt - 1, 1, 2 * ma * wl * H, (ma + wl) * H * bpe);
+      }
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  // totals (128-bit) and the exact-range rule (R22)
+  int bad = 0;
+  int64_t tot[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    unsigned long long lo = (unsigned long long)cr.tot[k], hi = (unsigned long long)(cr.tot[k] >> 64);
+    unsigned __int128 t = 0;
+    for (int l = 0; l < 32; ++l) {
+      const unsigned long long a = __shfl_sync(0xffffffffu, lo, l), b = __shfl_sync(0xffffffffu, hi, l);
+      t += ((unsigned __int128)b << 64) | a;
+    }
+    bad |= t > kI64Max;
+    tot[k] = (int64_t)t;
+  }
+  const int64_t cst[2] = {warp_sum64(cr.cst[0]), warp_sum64(cr.cst[1])};
+  __syncwarp();
+  // S_j = cst + prefix(D)[j]; lanes own contiguous chunks of the N SMs
+  const int chunk = (N + 31) / 32, j0 = min(N, lane * chunk), j1 = min(N, j0 + chunk);
+  int64_t mx[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int64_t *d = D + k * (N + 1);
+    int64_t part = 0;
+    for (int j = j0; j < j1; ++j) part += d[j];
+    int64_t incl = part;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int64_t run = cst[k] + incl - part, best = INT64_MIN;
+    for (int j = j0; j < j1; ++j) {
+      run += d[j];
+      best = max(best, run);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    mx[k] = best;
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  if (bad) { emit_error(out, p, SP_PAIR_E_RANGE); return; }
+  PairDemand d;
+  d.T = u.T;
+  d.tot[0] = tot[0]; d.tot[1] = 0; d.tot[2] = 0; d.tot[3] = tot[1];
+  d.mx[0] = mx[0]; d.mx[1] = 0; d.mx[2] = 0; d.mx[3] = mx[1];
+  emit_pair(out, p, d, u.fp, s, 1, u.tdt);
+}
+
+__global__ void featurize_clamped(int fam, ConfigView cfg, const DevSpec *__restrict__ specs, int g0, int n_specs,
+                                  int64_t n_pairs, const int64_t *__restrict__ cfg_idx,
+                                  const int32_t *__restrict__ spec_idx, int max_sms, FeatOut out) {
+  extern __shared__ int64_t s_diff[];
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t *D = s_diff + (size_t)warp * 2 * (max_sms + 1);
+  for (int64_t p = (int64_t)blockIdx.x * nw + warp; p < n_pairs; p += (int64_t)gridDim.x * nw) {
+    int64_t c;
+    int g;
+    if (cfg_idx) {
+      c = __ldg(cfg_idx + p);
+      g = __ldg(spec_idx + p);
+      if (c < 0 || c >= cfg.n_configs || g < 0 || g >= n_specs) {
+        if ((threadIdx.x & 31) == 0) emit_error(out, p, SP_PAIR_E_INDEX);
+        continue;
+      }
+    } else {
+      g = g0 + (int)(p / cfg.n_configs);
+      c = p - (int64_t)(g - g0) * cfg.n_configs;
+    }
+    clamped_pair(fam, cfg, c, specs[g], out, p, D);
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 int launch_featurize_uniform(int family, const ConfigView &cfg, const DevSpec *specs, int spec_begin,
@@ -430,6 +600,23 @@ int launch_featurize_uniform(int family, const ConfigView &cfg, const DevSpec *s
       featurize_uniform_list<<<blocks, kThreads, 0, st>>>(family, cfg, specs, spec_end, n_pairs, cfg_idx,
                                                            spec_idx, out);
   }
+  return (int)cudaGetLastError();
+}
+
+int launch_featurize_clamped(int family, const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
+                             int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx, int max_sms,
+                             const FeatOut &out, int num_device_sms, void *stream) {
+  if (n_pairs == 0) return 0;
+  const size_t per_warp = (size_t)2 * (max_sms + 1) * sizeof(int64_t);
+  const int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per_warp));
+  const size_t smem = per_warp * warps;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(featurize_clamped, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const int64_t blocks = std::min<int64_t>((n_pairs + warps - 1) / warps, (int64_t)num_device_sms * 16);
+  featurize_clamped<<<(unsigned)blocks, 32 * warps, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      family, cfg, specs, spec_begin, n_specs, n_pairs, cfg_idx, spec_idx, max_sms, out);
   return (int)cudaGetLastError();
 }
 

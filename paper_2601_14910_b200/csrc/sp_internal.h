@@ -66,6 +66,10 @@ struct ConfigView {
 // All return cudaError_t cast to int (0 = success).
 
 // Uniform families (GEMM, fused MoE, RMSNorm, SiLU&Mul): closed-form schedule.
+// Clamped edge tiles (NEXT-4), GEMM and fused MoE; warp per pair.
+int launch_featurize_clamped(int family, const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
+                             int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx, int max_sms,
+                             const FeatOut &out, int num_device_sms, void *stream);
 int launch_featurize_uniform(int family, const ConfigView &cfg, const DevSpec *specs,
                              int spec_begin, int spec_end, int64_t n_pairs, const int64_t *cfg_idx,
                              const int32_t *spec_idx, const FeatOut &out, void *stream);

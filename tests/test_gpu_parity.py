@@ -331,3 +331,74 @@ def test_predict_host_wide_spec_axis(sp, ctx, fam):
     torch.cuda.synchronize()
     got = ctx.predict_host(b, sh, m)
     assert np.array_equal(got, lat.cpu().numpy(), equal_nan=True)
+
+
+# ------------------------------------------------------------- clamped edge tiles (SP_FEAT_CLAMPED, NEXT-4)
+
+@pytest.mark.parametrize("fam", ["gemm", "moe"])
+def test_clamped_parity(sp, ctx, orc, fam):
+    """Clamped edge tiles vs the oracle's CLAMPED flag: CROSS over Table VI and
+    the odd SM counts, and a LIST with out-of-range indices."""
+    b = FAMILY_BATCHES[fam]()
+    for sa in (specs.paper_gpu_specs(), odd_specs()):
+        sh = ctx.load_gpu_specs(sa)
+        db = sp.DeviceBatch.from_host(b, ctx.torch_device)
+        f = sp.Features.empty(b.family, len(sa) * b.n_configs, ctx.torch_device)
+        ctx.featurize(db, sh, f, clamped=True)
+        torch.cuda.synchronize()
+        o = orc.featurize(b, sa, flags=orc.CLAMPED)
+        assert (o.status == 0).mean() > 0.9
+        assert_feature_parity(sp.features_to_host(f), o, fam + " clamped")
+    rng = np.random.default_rng(8)
+    ci, si = rng.integers(0, b.n_configs, 500), rng.integers(0, len(sa), 500)
+    ci[0], si[1] = -1, len(sa)
+    pr = sp.pair_list(torch.from_numpy(ci.astype(np.int64)).cuda(), torch.from_numpy(si.astype(np.int32)).cuda())
+    f = sp.Features.empty(b.family, 500, ctx.torch_device)
+    ctx.featurize(db, sh, f, pr, clamped=True)
+    torch.cuda.synchronize()
+    assert_feature_parity(sp.features_to_host(f), orc.featurize(b, sa, cfg_idx=ci, spec_idx=si, flags=orc.CLAMPED),
+                          fam + " clamped list")
+
+
+def test_clamped_edge_cases(sp, ctx, orc):
+    """Single tile, exact multiples (clamped = padded when K is a multiple of BK),
+    one row of tiles, huge M (many rows), and the golden MoE case; unsupported
+    families / schedulers are refused."""
+    cols = {k: [] for k in gen.FIELDS[gen.GEMM]}
+
+    def add(**kw):
+        d = dict(M=256, N=256, K=256, TM=128, TN=128, BK=64, STAGES=3, WARPS=8, REGS=168, SMEM=0, DTYPE=0)
+        d.update(kw)
+        for k in cols:
+            cols[k].append(d[k])
+
+    add(M=100, N=100, K=100)          # one clamped tile
+    add()                             # exact multiples
+    add(M=1, N=152064, K=4096)        # one row of 1188 tiles
+    add(M=131072, N=130, K=300)       # 1024 rows, edge column of 2
+    add(M=0)                          # dimension error
+    b = gen.make_batch(gen.GEMM, cols)
+    sa = np.concatenate([odd_specs(), specs.paper_gpu_specs()])
+    sh = ctx.load_gpu_specs(sa)
+    db = sp.DeviceBatch.from_host(b, ctx.torch_device)
+    f = sp.Features.empty(b.family, len(sa) * b.n_configs, ctx.torch_device)
+    ctx.featurize(db, sh, f, clamped=True)
+    torch.cuda.synchronize()
+    assert_feature_parity(sp.features_to_host(f), orc.featurize(b, sa, flags=orc.CLAMPED), "clamped edges")
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))["moe_clamped_tiny"]
+    mb = gen.make_batch(gen.FUSED_MOE, {k: [v] for k, v in g["config"].items()}, g["hist"], [0])
+    s3 = specs.spec_by_name("A100")
+    s3["num_sms"] = g["n_sm"]
+    f = sp.Features.empty(mb.family, 1, ctx.torch_device)
+    ctx.featurize(sp.DeviceBatch.from_host(mb, ctx.torch_device), ctx.load_gpu_specs(s3), f, clamped=True)
+    gi, _, gs = sp.features_to_host(f)
+    assert gs[0] == 0 and (gi[6, 0], gi[10, 0], gi[3, 0], gi[9, 0]) == (g["max_T"], g["bytes_max"], g["tot_T"], g["bytes"])
+    att = FAMILY_BATCHES["attention"]()
+    fa = sp.Features.empty(att.family, len(sa) * att.n_configs, ctx.torch_device)
+    with pytest.raises(sp.SynPerfError):
+        ctx.featurize(sp.DeviceBatch.from_host(att, ctx.torch_device), sh, fa, clamped=True)
+    f = sp.Features.empty(b.family, len(sa) * b.n_configs, ctx.torch_device)
+    with pytest.raises(sp.SynPerfError):
+        ctx.featurize(db, sh, f, clamped=True, scheduler="greedy")

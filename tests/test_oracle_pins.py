@@ -614,3 +614,30 @@ def test_gemm_splitk_invariants(orc):
     full = 2 * tm * tn * kps * bk
     assert (mx * nsm >= tot).all()
     assert (mx <= -(-T // nsm) * full).all()
+
+
+# --------------------------------------------------------------- clamped edge tiles (NEXT-4 on the GPU)
+
+def test_moe_clamped_worked_example(orc):
+    g = GOLD["moe_clamped_tiny"]
+    b = one(gen.FUSED_MOE, g["config"], hist=g["hist"])
+    tl = orc.task_list(b, flags=orc.CLAMPED)
+    assert tl[:, 0].tolist() == g["task_ops"] and tl[:, 3].tolist() == g["task_bytes"]
+    ints, _, st = feats(orc, b, spec_with(num_sms=g["n_sm"]), flags=orc.CLAMPED)
+    assert st == 0
+    for key in ("tot_T", "max_T", "bytes", "bytes_max"):
+        assert ints[key] == g[key], key
+
+
+def test_clamped_totals_are_exact_element_counts(orc):
+    """Clamped tiles count only in-range elements: total Tensor ops = 2*M*N*K
+    (GEMM) and 2*(M*topk)*N*H (fused MoE, every routed token row once)."""
+    gm = gen.gen_gemm(40, 17, m_range=(2, 3000), n_range=(384, 3000), k_range=(256, 3000))
+    o = orc.featurize(gm, A100, flags=orc.CLAMPED)
+    M, N, K = (gm.field(n).astype(np.int64) for n in ("M", "N", "K"))
+    assert (o.ints[orc.INT_NAMES.index("tot_T")] == 2 * M * N * K).all()
+    mo = gen.gen_moe(40, 18)
+    o = orc.featurize(mo, A100, flags=orc.CLAMPED)
+    ok = o.status == 0
+    M, tk, N, H = (mo.field(n).astype(np.int64) for n in ("M", "TOPK", "N", "H"))
+    assert ok.any() and (o.ints[orc.INT_NAMES.index("tot_T")][ok] == (2 * M * tk * N * H)[ok]).all()

@@ -1,6 +1,8 @@
 """Throughput of the §8(f) variants on one B200 (one JSON line each):
   * sp_featurize_sched GREEDY / MINHEAP on a slice of BASELINE config 2
     (attention x 11 GPUs; sequential scheduler simulation, warp per pair);
+  * sp_featurize_ex SP_FEAT_CLAMPED (clamped edge tiles) vs the padded closed
+    form, GEMM and fused MoE x 11 GPUs;
   * sp_perf_gap (P80 gap diagnosis) over BASELINE config 3 (fused MoE x 11,
     the paper applies it to its fused-MoE dataset);
   * sp_train_step (on-GPU estimator training, NEXT-4) on config-3 features at
@@ -57,6 +59,18 @@ def main():
         ms = timed(lambda: ctx.featurize(db, sh, f, sp.cross(g0, g1), scheduler=mode), args.reps)
         print(json.dumps({"variant": f"featurize_{mode}", "workload": f"cfg2 x{args.scale}", "pairs": n,
                           "ms": ms, "pairs_per_s": n / (ms * 1e-3)}), flush=True)
+    # ---- clamped edge tiles (SP_FEAT_CLAMPED): GEMM (config-1 shapes) and fused MoE (config 3), x 11 GPUs
+    from workloads import gen, specs as wspecs
+    for name, bb in (("gemm 1e5 x 11", gen.gen_gemm(100_000, 1001)), ("cfg3 x0.1", bench.build_workload("cfg3", 0, 1, 0.1)[0])):
+        sa2 = wspecs.paper_gpu_specs()
+        sh2 = ctx.load_gpu_specs(sa2)
+        db2 = sp.DeviceBatch.from_host(bb, "cuda:0")
+        n2 = len(sa2) * bb.n_configs
+        f2 = sp.Features.empty(bb.family, n2, "cuda:0")
+        for clamped in (False, True):
+            ms = timed(lambda: ctx.featurize(db2, sh2, f2, clamped=clamped), args.reps)
+            print(json.dumps({"variant": "featurize_clamped" if clamped else "featurize_padded", "workload": name,
+                              "pairs": n2, "ms": ms, "pairs_per_s": n2 / (ms * 1e-3)}), flush=True)
     # ---- gap diagnosis over config 3
     b, sa, (g0, g1), _ = bench.build_workload("cfg3", 0, 1, 1.0)
     sh = ctx.load_gpu_specs(sa)
