@@ -46,6 +46,7 @@ WORKLOADS = {
     "splitk": "split-K GEMM space (long K, few output tiles; reading R25), 1e6 configs x 11 GPU specs "
               "(not a BASELINE config: NEXT-4 variant)",
 }
+FUSABLE = (gen.GEMM, gen.FUSED_MOE, gen.RMSNORM, gen.SILU_MUL, gen.SCALED_MM)
 E2E_MODELS = ("llama3-8b", "qwen2.5-14b")
 E2E_FAMILIES = (gen.GEMM, gen.ATTENTION, gen.RMSNORM, gen.SILU_MUL)
 
@@ -320,13 +321,22 @@ def run_gpu(args, rank, world, local_rank):
         gathered = torch.empty(world * padded, dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    # fused feature + predictor pass (sp_featurize_predict) for the uniform families
+    fused = (args.fused == "on" or (args.fused == "auto" and b.family in FUSABLE)) and \
+        args.scheduler == "rr" and precision != "fp32"
+
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        ctx.featurize(db, specs_h, feats, pairs, stream, scheduler=args.scheduler)
-        if ev is not None:
-            ev[1].record(stream)
-        ctx.predict(model, feats, lat, None, stream)
+        if fused:
+            ctx.featurize_predict(db, specs_h, model, feats, lat, None, pairs, stream)
+            if ev is not None:
+                ev[1].record(stream)
+        else:
+            ctx.featurize(db, specs_h, feats, pairs, stream, scheduler=args.scheduler)
+            if ev is not None:
+                ev[1].record(stream)
+            ctx.predict(model, feats, lat, None, stream)
         if ev is not None:
             ev[2].record(stream)
         if gathered is not None:  # the single exchange: ncclAllGather of fp32 predictions
@@ -396,7 +406,7 @@ def run_gpu(args, rank, world, local_rank):
             "parallelism": f"dp{world}" + ("+allgather" if gathered is not None else ""),
             "l2": "flushed between timed steps (256 MiB write, outside the events)",
         },
-        "stage_ms": {"featurize": feat_ms, "predict": pred_ms,
+        "stage_ms": {("featurize+predict (fused)" if fused else "featurize"): feat_ms, "predict": pred_ms,
                      "allgather": float((t_step - t_feat - t_pred).mean())},
         "roofline": roof,
         "kernels": {k: {"launches": n, "avg_ms": t / max(n, 1)} for k, (n, t) in sorted(kst.items())},
@@ -654,7 +664,7 @@ def roofline(args, b, n_pairs, n_in, precision, kst, peaks, prof, tot_ms):
             peak, bound, src = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12, "alu", \
                 "148 SMs x 128 FP32 lanes x 2 FLOP x sm_max_mhz (DESIGN.md §6)"
         unit, per_unit = "TFLOP/s", f"{MLP_FLOP_PER_PAIR[n_in]} FLOP/pair x {per_launch_pairs} pairs"
-        traffic = wp.get(f"predict_tcgen05_{precision}_dram_bytes")
+        traffic = wp.get(f"{kernel}_{precision}_dram_bytes")
     elif kernel == "attn_schedule_cross":
         # integer-issue roofline: warp instructions per launch (ncu capture of this workload)
         instr = wp.get("attn_schedule_cross_inst_executed")
@@ -687,6 +697,8 @@ def main():
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"])
     ap.add_argument("--scheduler", default="rr", choices=["rr", "greedy", "minheap"],
                     help="Scheduling Simulator variant (sp_featurize_sched; default cyclic RR)")
+    ap.add_argument("--fused", default="auto", choices=["auto", "on", "off"],
+                    help="sp_featurize_predict for the uniform families (auto) or never (off)")
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

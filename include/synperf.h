@@ -367,6 +367,23 @@ sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_features *in, 
                      float *efficiency, void *stream);
 
 /*
+ * Fused feature + predictor stage (SURVEY §8(b) "fused"): the result of
+ * sp_featurize followed by sp_predict -- the same feature records in `out`,
+ * bit for bit, and the same latencies -- with the record computation moved into
+ * the predictor's producer warps, so the records are written while the tensor
+ * cores run the MLP instead of in a separate HBM-bound pass.  Applies to the
+ * uniform-task families (GEMM, fused MoE, RMSNorm, SiLU&Mul, Scaled MM) with
+ * SP_PAIRS_CROSS and a 16-bit (tcgen05) model; anything else runs the two
+ * calls in sequence.  A small per-config pre-pass (96 B per config, in a
+ * context-owned grow-only scratch: the first call with more configs than
+ * before allocates) runs first.  Asynchronous on `stream`; errors as
+ * sp_featurize and sp_predict.
+ */
+sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs,
+                               const sp_pairing *pairs, const sp_model *model, const sp_features *out,
+                               float *latency_us, float *efficiency, void *stream);
+
+/*
  * Performance-gap diagnosis (PAPER §VII).  A
  * second estimator trained with quantile loss at q = 0.8 predicts the
  * "Potential Performance Ceiling" efficiency y_p80; it is an

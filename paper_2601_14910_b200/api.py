@@ -484,6 +484,22 @@ class Context:
                                    _stream_ptr(stream)))
         return latency
 
+    def featurize_predict(self, batch: DeviceBatch, specs: Specs, model: Model, out: Features,
+                          latency: torch.Tensor, efficiency: torch.Tensor | None = None, pairs=None,
+                          stream=None) -> torch.Tensor:
+        """sp_featurize_predict: the records of sp_featurize and the latencies of sp_predict in
+        one fused pass (uniform families, CROSS, 16-bit model; otherwise the two calls)."""
+        if pairs is None:
+            pairs = cross(0, len(specs))
+        assert latency.dtype == torch.float32 and latency.is_contiguous()
+        cb = batch.c_struct()
+        fs = out.c_struct()
+        self._check(lib.sp_featurize_predict(self._h, C.byref(cb), specs.handle, C.byref(pairs), model.handle,
+                                             C.byref(fs), latency.data_ptr(),
+                                             efficiency.data_ptr() if efficiency is not None else None,
+                                             _stream_ptr(stream)))
+        return latency
+
     # -- performance-gap diagnosis (PAPER §VII-B)
     def perf_gap(self, feats: Features, eff_p80: torch.Tensor, measured_us: torch.Tensor, pairs=None,
                  n_configs: int = 0, n_specs: int = 0, n_bins: int = 100, gap_lo: float = -0.5,
@@ -581,8 +597,7 @@ class Context:
                 cache[f] = ent
             feats = ent[1]
             feats.n_pairs = n
-            self.featurize(b, specs, feats, cross(g0, g1), stream)
-            self.predict(models[f], feats, ent[2], None, stream)
+            self.featurize_predict(b, specs, models[f], feats, ent[2], None, cross(g0, g1), stream)
             lat[f] = ent[2][:max(n, 1)]
         R, S = inf["n_traces"], inf["n_steps"]
         step = torch.empty((G, S), dtype=torch.float32, device=dev) if step_latencies else None
@@ -649,8 +664,7 @@ class Context:
             if i >= 2:
                 comp.wait_event(done[i - 2])
             feats.n_pairs = n
-            self.featurize(db, specs, feats, cross(ga, gb), comp)
-            self.predict(model, feats, lat, None, comp)
+            self.featurize_predict(db, specs, model, feats, lat, None, cross(ga, gb), comp)
             ev = torch.cuda.Event()
             ev.record(comp)
             with torch.cuda.stream(s_d2h):
@@ -668,7 +682,7 @@ class Context:
                      out: np.ndarray | torch.Tensor | None = None, chunks: int = 4,
                      stream=None) -> np.ndarray:
         """The user-facing call.  Host config arrays (numpy or torch; pinned
-        memory gives asynchronous copies) -> H2D -> sp_featurize -> sp_predict
+        memory gives asynchronous copies) -> H2D -> sp_featurize_predict (fused, or sp_featurize -> sp_predict)
         -> D2H of fp32 latencies in spec-major order [spec][config].
 
         The configs are split into `chunks` slices pipelined over three
@@ -745,8 +759,7 @@ class Context:
             lat = cache["lat"][i % 2]
             if i >= 2:  # the D2H that read this buffer two slices ago must be done
                 comp.wait_event(d2h_done[i - 2])
-            self.featurize(db, specs, feats, cross(g0, g1), comp)
-            self.predict(model, feats, lat, None, comp)
+            self.featurize_predict(db, specs, model, feats, lat, None, cross(g0, g1), comp)
             ev2 = torch.cuda.Event()
             ev2.record(comp)
             with torch.cuda.stream(s_d2h):

@@ -433,6 +433,77 @@ extern "C" sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, co
   return SP_OK;
 }
 
+// --------------------------------------------------------- fused featurize -> predict
+
+extern "C" sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs,
+                                          const sp_pairing *pairs, const sp_model *model, const sp_features *out,
+                                          float *latency_us, float *efficiency, void *stream) {
+  if (!ctx) return fail(nullptr, SP_E_ARG, "sp_featurize_predict: ctx is NULL");
+  if (!cfg || !specs || !pairs || !model || !out) return fail(ctx, SP_E_ARG, "sp_featurize_predict: NULL argument");
+  if (model->family != cfg->family) return fail(ctx, SP_E_ARG, "sp_featurize_predict: config/model family mismatch");
+  const int fam = cfg->family;
+  const bool fusable = (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_RMSNORM || fam == SP_SILU_MUL ||
+                        fam == SP_SCALED_MM) &&
+                       pairs->kind == SP_PAIRS_CROSS &&
+                       (model->precision == SP_MLP_BF16 || model->precision == SP_MLP_FP16);
+  if (!fusable) {  // the two-kernel path (attention, split-K, pair lists, the fp32 predictor)
+    sp_status st = sp_featurize(ctx, cfg, specs, pairs, out, stream);
+    if (st != SP_OK) return st;
+    return sp_predict(ctx, model, out, latency_us, efficiency, stream);
+  }
+  // argument checks of sp_featurize (CROSS)
+  if (cfg->n_fields != nfields_of(fam))
+    return fail(ctx, SP_E_ARG, "sp_featurize_predict: n_fields does not match the family's field count");
+  if (cfg->n_configs < 0 || cfg->field_ld < cfg->n_configs)
+    return fail(ctx, SP_E_ARG, "sp_featurize_predict: bad n_configs / field_ld");
+  if (cfg->n_configs > 0 && !cfg->fields) return fail(ctx, SP_E_ARG, "sp_featurize_predict: fields is NULL");
+  if (fam == SP_FUSED_MOE && cfg->ragged_off && !cfg->ragged)
+    return fail(ctx, SP_E_ARG, "sp_featurize_predict: MoE ragged_off without ragged");
+  if (out->family != fam) return fail(ctx, SP_E_ARG, "sp_featurize_predict: out->family != cfg->family");
+  if (pairs->spec_begin < 0 || pairs->spec_end > specs->n || pairs->spec_begin > pairs->spec_end)
+    return fail(ctx, SP_E_ARG, "sp_featurize_predict: spec range out of bounds");
+  const int64_t n_pairs = (int64_t)(pairs->spec_end - pairs->spec_begin) * cfg->n_configs;
+  if (out->n_pairs != n_pairs || out->ld < n_pairs)
+    return fail(ctx, SP_E_ARG, "sp_featurize_predict: out->n_pairs / ld do not match the pairing");
+  if (n_pairs == 0) return SP_OK;
+  if (!out->ints || !out->flts || !out->status || !latency_us)
+    return fail(ctx, SP_E_ARG, "sp_featurize_predict: NULL buffer");
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  const int64_t C = cfg->n_configs, ldc = (C + 31) & ~(int64_t)31;
+  const size_t need = (size_t)ldc * kPreFields * sizeof(uint64_t);
+  if (need > ctx->pre_bytes) {
+    if (ctx->pre) cudaFree(ctx->pre);
+    ctx->pre = nullptr;
+    ctx->pre_bytes = 0;
+    cudaError_t me = cudaMalloc(&ctx->pre, need);
+    if (me != cudaSuccess) {
+      ctx->pre = nullptr;
+      return cuda_fail(ctx, me, "sp_featurize_predict: pre-pass scratch");
+    }
+    ctx->pre_bytes = need;
+  }
+  ConfigView cv{cfg->fields, cfg->ragged, cfg->ragged_off, cfg->n_configs, cfg->field_ld};
+  const LaunchHook h = ctx->hook();
+  h.on_begin("uniform_prepass", stream);
+  int e = launch_uniform_prepass(fam, cv, (uint64_t *)ctx->pre, ldc, stream);
+  h.on_end(stream);
+  if (e) return cuda_fail(ctx, e, "sp_featurize_predict: pre-pass launch");
+  FusedIn fi;
+  fi.pre = (const uint64_t *)ctx->pre;
+  fi.ldc = ldc;
+  fi.C = C;
+  fi.g0 = pairs->spec_begin;
+  fi.specs = (const DevSpec *)specs->dev.p;
+  fi.out = FeatOut{out->ints, out->flts, out->status, out->ld};
+  fi.n_pairs = n_pairs;
+  h.on_begin("predict_tcgen05_fused", stream);
+  e = launch_predict_tcgen05_fused(model->m16, fi, latency_us, efficiency, ctx->num_sms, stream);
+  h.on_end(stream);
+  if (e) return cuda_fail(ctx, e, "sp_featurize_predict: launch");
+  return SP_OK;
+}
+
 // -------------------------------------------------------------------- model
 
 static bool all_finite(const float *p, size_t n) {

@@ -68,9 +68,11 @@ __device__ __forceinline__ int64_t waves_of(int64_t T, int64_t nsm, int64_t occ)
 
 // a7-a9: cycles from the exact integers in fp64, one rounding to fp32 (R20),
 // and the record store.  tdt = tensor dtype index (0 bf16, 1 fp16, 2 fp8).
+// fv (optional): receives the 12 float slots as stored (the fused predictor
+// normalises them without reading the record back).
 __device__ __forceinline__ void emit_pair(const FeatOut &o, int64_t p, const PairDemand &d,
                                           const Footprint &fp, const DevSpec &s, int pipes,
-                                          int tdt) {
+                                          int tdt, float *fv = nullptr) {
   const int64_t ld = o.ld;
   int64_t occ = occupancy(fp, s);
   int64_t *I = o.ints + p;
@@ -95,18 +97,14 @@ __device__ __forceinline__ void emit_pair(const FeatOut &o, int64_t p, const Pai
   const double glob_g = B * s.glob_g, l2_g = B * s.l2_g;
   double roof = fmax(glob_g, l2_g);
   roof = fmax(roof, fmax(cg[0], fmax(cg[1], cg[2])));
-  F[F_CG_T * ld] = (float)cg[0];
-  F[F_CG_F * ld] = (float)cg[1];
-  F[F_CG_X * ld] = (float)cg[2];
-  F[F_CS_T * ld] = (float)cs[0];
-  F[F_CS_F * ld] = (float)cs[1];
-  F[F_CS_X * ld] = (float)cs[2];
-  F[F_GLOB_G * ld] = (float)glob_g;
-  F[F_L2_G * ld] = (float)l2_g;
-  F[F_GLOB_S * ld] = (float)(Bm * s.glob_s);
-  F[F_L2_S * ld] = (float)(Bm * s.l2_s);
-  F[F_SMEM_S * ld] = (float)(Bm * s.smem_s);
-  F[F_TTHEORY * ld] = (float)(roof * s.inv_f);
+  const float f[kNumFlts] = {(float)cg[0], (float)cg[1], (float)cg[2], (float)cs[0], (float)cs[1], (float)cs[2],
+                             (float)glob_g, (float)l2_g, (float)(Bm * s.glob_s), (float)(Bm * s.l2_s),
+                             (float)(Bm * s.smem_s), (float)(roof * s.inv_f)};
+#pragma unroll
+  for (int k = 0; k < kNumFlts; ++k) {
+    F[k * ld] = f[k];
+    if (fv) fv[k] = f[k];
+  }
   o.status[p] = 0;
 }
 

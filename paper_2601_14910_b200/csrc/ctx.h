@@ -21,6 +21,8 @@ struct sp_ctx {
   int *counters = nullptr;  // DEVICE work counters of the attention kernel (kAttnMaxGroups)
   void *attn_res = nullptr;  // DEVICE per-config attention results (AttnResults), grow-only
   size_t attn_res_bytes = 0;
+  void *pre = nullptr;  // DEVICE config pre-pass of the fused path (kPreFields u64 per config), grow-only
+  size_t pre_bytes = 0;
   std::string err;
   // kernel accounting (sp_set_profiling / sp_profile_read)
   struct KStat {
@@ -42,6 +44,7 @@ struct sp_ctx {
   ~sp_ctx() {
     if (counters) cudaFree(counters);
     if (attn_res) cudaFree(attn_res);
+    if (pre) cudaFree(pre);
     for (auto &p : pending) {
       cudaEventDestroy(p.a);
       cudaEventDestroy(p.b);

@@ -410,6 +410,30 @@ __global__ void __launch_bounds__(kThreads) featurize_uniform_list(int fam, Conf
   uniform_pair(out, p, u, specs[g], family_pipes(fam));
 }
 
+// ------------------------------------------------------------------ config pre-pass (fused path)
+
+// Spec-independent part of a uniform-family config for the fused
+// featurize -> predict kernel: u64 SoA [kPreFields][ldc] (layout in
+// sp_internal.h).  Thread per config; fused-MoE histograms by warp as above.
+__global__ void __launch_bounds__(kThreads) uniform_prepass(int fam, ConfigView cfg, uint64_t *__restrict__ pre,
+                                                            int64_t ldc) {
+  const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  MoeHist hist;
+  if (fam == SP_FUSED_MOE) hist = moe_hist_warp(cfg, c, c < cfg.n_configs);
+  if (c >= cfg.n_configs) return;
+  const UniformCfg u = config_of(fam, cfg, c, fam == SP_FUSED_MOE ? &hist : nullptr);
+  uint64_t *o = pre + c;
+  o[0] = (uint64_t)(uint32_t)u.status | ((uint64_t)u.range_bad << 8) | ((uint64_t)(u.tdt + 1) << 16);
+  o[1 * ldc] = (uint64_t)u.T;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    o[(2 + q) * ldc] = (uint64_t)u.task[q];
+    o[(6 + q) * ldc] = (uint64_t)u.tot[q];
+  }
+  o[10 * ldc] = (uint64_t)u.fp.smem;
+  o[11 * ldc] = (uint64_t)(uint32_t)u.fp.warps | ((uint64_t)(uint32_t)u.fp.regs << 32);
+}
+
 // ------------------------------------------------------------------ clamped edge tiles
 
 // SPEC's clamped reading of edge tiles (the alternative to R2's
@@ -600,6 +624,13 @@ int launch_featurize_uniform(int family, const ConfigView &cfg, const DevSpec *s
       featurize_uniform_list<<<blocks, kThreads, 0, st>>>(family, cfg, specs, spec_end, n_pairs, cfg_idx,
                                                            spec_idx, out);
   }
+  return (int)cudaGetLastError();
+}
+
+int launch_uniform_prepass(int family, const ConfigView &cfg, uint64_t *pre, int64_t ldc, void *stream) {
+  if (cfg.n_configs == 0) return 0;
+  uniform_prepass<<<(unsigned)((cfg.n_configs + kThreads - 1) / kThreads), kThreads, 0,
+                    reinterpret_cast<cudaStream_t>(stream)>>>(family, cfg, pre, ldc);
   return (int)cudaGetLastError();
 }
 

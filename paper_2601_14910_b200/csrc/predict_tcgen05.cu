@@ -535,6 +535,370 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
   }
 }
 
+// ---- fused feature + predictor kernel (sp_featurize_predict): the same MMA
+// issuer and epilogue, with 8 producer warps in two groups that take alternate
+// tiles and derive each pair's record from its config pre-pass and spec.
+// Layout: as the kernel above up to H2 (raw staging: 2 groups x kFNR stages of
+// kPreFields u64 per row = the same 48 KB), then the producer -> epilogue side
+// ring (t_theory, status per row of kNS tiles) and the barriers.
+constexpr int kFProdWarps = 8;
+constexpr int kFMmaWarp = kEpiWarps + kFProdWarps;
+constexpr int kFThreads = (kFMmaWarp + 1) * 32;
+constexpr int kFNR = 2;
+constexpr uint32_t kFRawBytes = kPreFields * kTile * 8;
+static_assert(2 * kFNR * kFRawBytes <= kNR * kRawBytes, "fused raw staging fits the unfused one");
+constexpr int kNS = 8;  // the producer of tile j + kNS waited for tile j + kNS - kNX's layer-1 MMA,
+                        // which needed tile j's slot freed: the ring never overruns
+constexpr uint32_t kFOffSide = kOffBar;
+constexpr uint32_t kFOffBar = kFOffSide + kNS * kTile * 5;
+constexpr int kBarSideFull = kNumBars, kFNumBars = kNumBars + kNS;
+constexpr uint32_t kFSmemBytes = kFOffBar + kFNumBars * 8 + 16;
+static_assert(kFSmemBytes <= 232448, "shared memory budget (fused)");
+
+struct FusedParams {
+  MlpBf16 m;
+  FusedIn fz;
+  float *latency;
+  float *eff;
+  int64_t n_tiles;
+};
+
+// Integer Table IV slot value of a pair's demands.
+__device__ __forceinline__ int64_t int_slot_value(const PairDemand &d, int sl) {
+  return sl == I_BYTES ? d.tot[3] : sl == I_BYTES_MAX ? d.mx[3] : sl >= I_MAX_T ? d.mx[sl - I_MAX_T] : d.tot[sl - I_TOT_T];
+}
+
+template <bool BF16, int FAM>
+__global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(FusedParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sbase = tc::smem_u32(smem);
+  float *vec = reinterpret_cast<float *>(smem + kOffVec);
+  float *zx = reinterpret_cast<float *>(smem + kOffZx);
+  const uint32_t bar0 = sbase + kFOffBar;
+  auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kFOffBar + kFNumBars * 8);
+
+  // ---- one-time setup: weights + vectors to smem, barriers, TMEM
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(P.m.wpack);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem);
+    for (int i = threadIdx.x; i < (int)(kWBytes / 16); i += kFThreads) dst[i] = __ldg(src + i);
+    for (int i = threadIdx.x; i < kVecFloats; i += kFThreads) vec[i] = __ldg(P.m.vecs + i);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kNX; ++i) {
+      tc::mbar_init(bar(kBarXFull + i), kProdWarps * 32);
+      tc::mbar_init(bar(kBarXEmpty + i), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(bar(kBarDFull + s), 1);
+      tc::mbar_init(bar(kBarAReady + s), 256);
+      tc::mbar_init(bar(kBarSlotFree + s), 256);
+    }
+    for (int i = 0; i < kNS; ++i) tc::mbar_init(bar(kBarSideFull + i), kProdWarps * 32);
+    tc::mbar_init_fence();
+  }
+  if (warp == kFMmaWarp) tc::tmem_alloc<512>(tc::smem_u32(tmem_slot));
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t G = gridDim.x;
+  const int64_t n_local = P.n_tiles > (int64_t)blockIdx.x ? (P.n_tiles - blockIdx.x + G - 1) / G : 0;
+  if (warp == kFMmaWarp) {
+    // ================= MMA issuer (one thread) =================
+    // Per TMEM slot s (CTA tiles j = s, s+2, ...): layer 0 needs the X tile
+    // (x_full) and the slot's previous tile fully read (slot_free); layers 1, 2
+    // need the epilogue's activations (a_ready).  Issue whatever is ready.
+    if (lane == 0) {
+      const uint32_t i1 = tc::idesc_f16kind_f32(128, 256, BF16), i128 = tc::idesc_f16kind_f32(128, 128, BF16),
+                     i64 = tc::idesc_f16kind_f32(128, 64, BF16);
+      int64_t js[2] = {0, 1};
+      int layer[2] = {0, 0};
+      uint32_t pa[2] = {0, 0}, pf[2] = {0, 0};
+      while (js[0] < n_local || js[1] < n_local) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int64_t j = js[s];
+          if (j >= n_local) continue;
+          const uint32_t B = tmem + (uint32_t)(s * 256);
+          if (layer[s] == 0) {
+            const int xi = (int)(j % kNX);
+            if (!tc::mbar_test(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u)) continue;
+            if (j >= 2 && !tc::mbar_test(bar(kBarSlotFree + s), pf[s])) continue;
+            if (j >= 2) pf[s] ^= 1;
+            tc::fence_after();
+            // X from smem; b1 rides on X's constant-1 column
+            if (!kNoMma) tc::mma_f16kind(B, tc::smem_desc(sbase + kOffX + xi * kXBytes, 128, 16 * kK1),
+                            tc::smem_desc(sbase + kOffW1, 128, 16 * kK1), i1, 0);
+            tc::commit(bar(kBarXEmpty + xi));
+          } else {
+            if (!tc::mbar_test(bar(kBarAReady + s), pa[s])) continue;
+            pa[s] ^= 1;
+            tc::fence_after();
+            if (layer[s] == 1) {  // H1 from TMEM; D2 preset to b2'
+#pragma unroll
+              for (int ks = 0; ks < 16; ++ks) {
+                const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
+#ifdef SP_L2H_SS
+                if (ks < 8) {  // K 0..127 from shared memory
+                  if (!kNoMma)
+                    tc::mma_f16kind(B + 64, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
+                                    tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
+                  continue;
+                }
+#endif
+                if (!kNoMma)
+                  tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
+              }
+            } else {  // H2 from TMEM (or shared memory with SP_L3_SS); D3 preset to b3'
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks) {
+#ifdef SP_L3_SS
+                if (!kNoMma)
+                  tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
+                                  tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64, 1);
+#else
+                if (!kNoMma) tc::mma_f16kind_ts(B + 192, B + 8 * ks, tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64,
+                                   1);
+#endif
+              }
+            }
+          }
+          PTRACE(2, (int)(j >> 1), 1 + layer[s] * 2 + s);
+          tc::commit(bar(kBarDFull + s));
+          if (++layer[s] == 3) {
+            layer[s] = 0;
+            js[s] += 2;
+          }
+        }
+      }
+    }
+  } else if (warp >= kEpiWarps) {
+    // ================= producers (two groups of 4 warps, alternate tiles) =================
+    // Per row: the pair's config pre-pass (kPreFields u64, cp.async kFNR tiles of
+    // the group ahead), its spec, then a4-a9 (uniform tasks: the busiest SM holds
+    // ceil(T/N) tasks) with the record written exactly as sp_featurize writes it,
+    // and a10 on the values just computed.
+    const int gid = (warp - kEpiWarps) >> 2;
+    const uint32_t row = (uint32_t)((warp - kEpiWarps) & 3) * 32 + lane;
+    const uint32_t raw_base = sbase + kOffRaw + (uint32_t)gid * kFNR * kFRawBytes;
+    const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + kOffRaw + gid * kFNR * kFRawBytes);
+    float na[15], nc[15];
+#pragma unroll
+    for (int f = 0; f < 15; ++f) {
+      na[f] = vec[kVNA + f];
+      nc[f] = vec[kVNC + f];
+    }
+    const FusedIn &fz = P.fz;
+    const double invC = 1.0 / (double)fz.C;
+    // p = q*C + r with q from the fp64 reciprocal, corrected by one (p < 2^52)
+    auto split = [&](int64_t p, int64_t &q, int64_t &r) {
+      q = (int64_t)((double)p * invC);
+      r = p - q * fz.C;
+      if (r < 0) { --q; r += fz.C; }
+      if (r >= fz.C) { ++q; r -= fz.C; }
+    };
+    auto issue = [&](int64_t j) {
+      if (j < n_local) {
+        int64_t p = (blockIdx.x + j * G) * kTile + row, q, c;
+        if (p >= fz.n_pairs) p = 0;  // tail rows: harmless copy, nothing stored
+        split(p, q, c);
+        const uint32_t dst = raw_base + (uint32_t)((j >> 1) % kFNR) * kFRawBytes + row * 8;
+#pragma unroll
+        for (int f = 0; f < kPreFields; ++f) cp_async8(dst + f * kTile * 8, fz.pre + (int64_t)f * fz.ldc + c);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int jj = 0; jj < kFNR - 1; ++jj) issue(gid + 2 * jj);
+    for (int64_t j = gid; j < n_local; j += 2) {
+      issue(j + 2 * (kFNR - 1));
+      asm volatile("cp.async.wait_group %0;" ::"n"(kFNR - 1) : "memory");
+      const uint64_t *rj = raw + (size_t)((j >> 1) % kFNR) * (kFRawBytes / 8) + row;
+      const int64_t p = (blockIdx.x + j * G) * kTile + row;
+      float xv[16];
+#pragma unroll
+      for (int f = 0; f < 16; ++f) xv[f] = 0.f;
+      float side_t = 0.f;
+      uint32_t side_s = 1;
+      if (p < fz.n_pairs) {
+        int64_t q, c;
+        split(p, q, c);
+        const uint64_t w0 = rj[0];
+        int st = (int)(w0 & 0xff);
+        const int tdt = (int)((w0 >> 16) & 0xff) - 1;
+        const DevSpec &sp = fz.specs[fz.g0 + q];
+        if (st == 0 && tdt >= 0 && !sp.tensor_ok[tdt]) st = SP_PAIR_E_DTYPE;
+        if (st == 0 && ((w0 >> 8) & 1)) st = SP_PAIR_E_RANGE;
+        if (st != 0) {
+          emit_error(fz.out, p, st);
+          side_s = (uint32_t)st;
+        } else {
+          PairDemand d;
+          d.T = (int64_t)rj[kTile];
+          const int64_t per_sm = (int64_t)(((uint32_t)d.T + (uint32_t)sp.num_sms - 1u) / (uint32_t)sp.num_sms);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            d.tot[qq] = (int64_t)rj[(6 + qq) * kTile];
+            d.mx[qq] = per_sm * (int64_t)rj[(2 + qq) * kTile];
+          }
+          const uint64_t wr = rj[11 * kTile];
+          const Footprint fp{(int64_t)rj[10 * kTile], (int64_t)(uint32_t)wr, (int64_t)(wr >> 32)};
+          float fv[kNumFlts];
+          emit_pair(fz.out, p, d, fp, sp, family_pipes(FAM), tdt < 0 ? 0 : tdt, fv);
+          side_s = 0;
+          side_t = fv[F_TTHEORY];
+#pragma unroll
+          for (int f = 0; f < n_in_of(FAM); ++f) {
+            const int sl = in_slot(FAM, f);
+            const float v = sl >= 16 ? fv[sl - 16] : (float)int_slot_value(d, sl);
+            xv[f] = fmaf(lg2_ftz(1.f + v), na[f], nc[f]);
+          }
+        }
+      }
+      xv[15] = 1.f;
+      uint32_t xp[8];
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) xp[qq] = tc::pack_x2<BF16>(xv[2 * qq], xv[2 * qq + 1]);
+      const int xi = (int)(j % kNX);
+      if (j >= kNX) tc::mbar_wait_sleep(bar(kBarXEmpty + xi), (uint32_t)((j / kNX) - 1) & 1u);
+      const uint32_t xb = sbase + kOffX + (uint32_t)xi * kXBytes;
+      tc::st_shared_v4(xb + op_off(row, 0, kK1), xp[0], xp[1], xp[2], xp[3]);
+      tc::st_shared_v4(xb + op_off(row, 8, kK1), xp[4], xp[5], xp[6], xp[7]);
+      const int si = (int)(j % kNS);
+      reinterpret_cast<float *>(smem + kFOffSide)[si * kTile + row] = side_t;
+      (smem + kFOffSide + kNS * kTile * 4)[si * kTile + row] = (uint8_t)side_s;
+      tc::fence_proxy_async();
+      tc::mbar_arrive(bar(kBarXFull + xi));
+      tc::mbar_arrive(bar(kBarSideFull + si));
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else {
+    // ================= epilogue warpgroups =================
+    const int grp = warp >> 2;                    // 0..3
+    const int s = grp >> 1, h = grp & 1;          // tile slot, column half
+    const uint32_t row = (warp & 3) * 32 + lane;  // TMEM lane == tile row
+    const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * 256);
+    const float *w4 = vec + kVW4;
+    const int64_t n_pairs = P.fz.n_pairs;
+    const uint32_t bar_d = bar(kBarDFull + s), bar_a = bar(kBarAReady + s), bar_f = bar(kBarSlotFree + s);
+    uint32_t pd = 0;
+    const bool tr = (warp & 7) == 0 && lane == 0;  // half-0 warp 0 of each slot
+    (void)tr;
+    for (int64_t j = s; j < n_local; j += 2) {
+      const int64_t p = (blockIdx.x + j * G) * kTile + row;
+      const int it = (int)(j >> 1);
+      (void)it;
+      EPT(0);
+      // output-side inputs, loaded now and used after layer 3
+      float t_theory = 0.f;
+      uint32_t stbyte = 1;
+      if (h == 0 && p < n_pairs) {  // from this tile's producers (the record itself is in flight)
+        const int si = (int)(j % kNS);
+        tc::mbar_wait_sleep(bar(kBarSideFull + si), (uint32_t)(j / kNS) & 1u);
+        t_theory = reinterpret_cast<const float *>(smem + kFOffSide)[si * kTile + row];
+        stbyte = (smem + kFOffSide + kNS * kTile * 4)[si * kTile + row];
+      }
+      // layer 1: D1 half h -> H1 (half 0 -> [0, 64), half 1 -> [192, 256));
+      // preset D2 columns 64h..64h+63 (TMEM [64+64h, 128+64h), read by this half) = b2'[64h..]
+      EPI_WAIT(bar_d, pd);
+      EPT(2);
+      pd ^= 1;
+      tc::fence_after();
+#ifndef SP_EXP_NOEPI
+#ifdef SP_L2H_SS
+      if (h == 0) {
+        epi_hidden_smem64<BF16>(tmem_row, 0, sbase + kOffH2 + s * kH2Bytes, row, 0);
+        epi_hidden_smem64<BF16>(tmem_row, 64, sbase + kOffH2 + s * kH2Bytes, row, 64);
+      }
+#else
+      if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
+#endif
+      else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
+#endif
+#ifndef SP_EXP_NOBIAS
+      bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
+#endif
+      tc::tmem_wait_st();
+#ifdef SP_L2H_SS
+      tc::fence_proxy_async();  // generic-proxy H1 writes -> visible to the tensor core
+#endif
+      tc::fence_before();
+      tc::mbar_arrive(bar_a);
+      EPT(3);
+      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 packed in [32h, 32h+32) (H1 is retired);
+      // preset D3 columns 32h.. [192+32h, 224+32h) = b3'[32h..]
+      EPI_WAIT(bar_d, pd);
+      EPT(4);
+      pd ^= 1;
+      tc::fence_after();
+#ifndef SP_EXP_NOEPI
+#ifdef SP_L3_SS
+      epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
+#else
+      epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
+#endif
+#endif
+#ifndef SP_EXP_NOBIAS
+      bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
+#endif
+      tc::tmem_wait_st();
+#ifdef SP_L3_SS
+      tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
+#endif
+      tc::fence_before();
+      tc::mbar_arrive(bar_a);
+      EPT(5);
+      // layer 3 + output layer: z = b4' + sum_j w4'_j relu(D3_j); this half sums 32 columns
+      EPI_WAIT(bar_d, pd);
+      EPT(6);
+      pd ^= 1;
+      tc::fence_after();
+      uint32_t v[32];
+      tc::tmem_ld32(tmem_row + 192 + 32 * h, v);
+      tc::tmem_wait_ld();
+      tc::fence_before();
+      tc::mbar_arrive(bar_f);  // the slot's TMEM may take the next tile
+      float zz[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < 32; q += 4) {
+        const float4 w = *reinterpret_cast<const float4 *>(w4 + 32 * h + q);
+        zz[0] = fmaf(w.x, fmaxf(__uint_as_float(v[q + 0]), 0.f), zz[0]);
+        zz[1] = fmaf(w.y, fmaxf(__uint_as_float(v[q + 1]), 0.f), zz[1]);
+        zz[2] = fmaf(w.z, fmaxf(__uint_as_float(v[q + 2]), 0.f), zz[2]);
+        zz[3] = fmaf(w.w, fmaxf(__uint_as_float(v[q + 3]), 0.f), zz[3]);
+      }
+      const float zp = (zz[0] + zz[1]) + (zz[2] + zz[3]);
+      if (h == 1) zx[s * kTile + row] = zp;
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + s) : "memory");  // the slot's two halves
+      if (h == 0 && p < n_pairs) {
+        const float z = P.m.b4 + zp + zx[s * kTile + row];
+        float lat, e;
+        if (stbyte != 0) {
+          lat = e = __int_as_float(0x7fc00000);
+        } else {
+          const float ez = __expf(-z);
+          e = 1.f / (1.f + ez);
+          lat = t_theory * (1.f + ez);
+        }
+        P.latency[p] = lat;
+        if (P.eff) P.eff[p] = e;
+      }
+      EPT(7);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == kFMmaWarp) {
+    tc::fence_after();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host side
@@ -635,6 +999,38 @@ int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *laten
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   return (int)(m.bf16 ? launch_fam<true>(m.family, P, (unsigned)grid, st)
                       : launch_fam<false>(m.family, P, (unsigned)grid, st));
+}
+
+template <bool BF16>
+static cudaError_t launch_fused(int fam, const FusedParams &P, unsigned grid, cudaStream_t st) {
+  void (*kern)(FusedParams) = nullptr;
+  switch (fam) {
+    case SP_GEMM:
+    case SP_SCALED_MM: kern = predict_tcgen05_fused_kernel<BF16, SP_GEMM>; break;
+    case SP_FUSED_MOE: kern = predict_tcgen05_fused_kernel<BF16, SP_FUSED_MOE>; break;
+    case SP_RMSNORM: kern = predict_tcgen05_fused_kernel<BF16, SP_RMSNORM>; break;
+    case SP_SILU_MUL: kern = predict_tcgen05_fused_kernel<BF16, SP_SILU_MUL>; break;
+    default: return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmemBytes);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kFThreads, kFSmemBytes, st>>>(P);
+  return cudaGetLastError();
+}
+
+int launch_predict_tcgen05_fused(const MlpBf16 &m, const FusedIn &fi, float *latency, float *eff,
+                                 int num_device_sms, void *stream) {
+  if (fi.n_pairs == 0) return 0;
+  FusedParams P{};
+  P.m = m;
+  P.fz = fi;
+  P.latency = latency;
+  P.eff = eff;
+  P.n_tiles = (fi.n_pairs + kTile - 1) / kTile;
+  const int64_t grid = P.n_tiles < num_device_sms ? P.n_tiles : num_device_sms;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return (int)(m.bf16 ? launch_fused<true>(m.family, P, (unsigned)grid, st)
+                      : launch_fused<false>(m.family, P, (unsigned)grid, st));
 }
 
 }  // namespace sp

@@ -66,6 +66,15 @@ struct ConfigView {
 // All return cudaError_t cast to int (0 = success).
 
 // Uniform families (GEMM, fused MoE, RMSNorm, SiLU&Mul): closed-form schedule.
+// Fused featurize -> predict (uniform families GEMM, fused MoE, RMSNorm,
+// SiLU&Mul, Scaled MM; SURVEY §8(b) "fused"): the spec-independent part of each
+// config, u64 SoA [kPreFields][ldc]:
+//   0 status | range_bad << 8 | (tensor dtype + 1) << 16    1 T
+//   2..5 per-task Tensor, FMA, XU ops, bytes                6..9 totals
+//   10 smem per task    11 warps | regs << 32
+constexpr int kPreFields = 12;
+int launch_uniform_prepass(int family, const ConfigView &cfg, uint64_t *pre, int64_t ldc, void *stream);
+
 // Clamped edge tiles (NEXT-4), GEMM and fused MoE; warp per pair.
 int launch_featurize_clamped(int family, const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
                              int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx, int max_sms,
@@ -167,5 +176,19 @@ bool pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const st
                     std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4);
 int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *latency, float *eff,
                            int num_device_sms, void *stream);
+// The fused kernel: producers derive each pair's record from the pre-pass and
+// its spec (writing `out`, the same bytes sp_featurize writes), then the MLP
+// runs as in sp_predict.  Pairs: CROSS, p = (g - g0) * C + c.
+struct FusedIn {
+  const uint64_t *pre;
+  int64_t ldc;
+  int64_t C;
+  int g0;
+  const DevSpec *specs;
+  FeatOut out;
+  int64_t n_pairs;
+};
+int launch_predict_tcgen05_fused(const MlpBf16 &m, const FusedIn &fi, float *latency, float *eff,
+                                 int num_device_sms, void *stream);
 
 }  // namespace sp

@@ -402,3 +402,38 @@ def test_clamped_edge_cases(sp, ctx, orc):
     f = sp.Features.empty(b.family, len(sa) * b.n_configs, ctx.torch_device)
     with pytest.raises(sp.SynPerfError):
         ctx.featurize(db, sh, f, clamped=True, scheduler="greedy")
+
+
+# ------------------------------------------------------------- fused featurize -> predict (sp_featurize_predict)
+
+@pytest.mark.parametrize("fam", ["gemm", "moe", "rmsnorm", "silu", "scaled_mm", "attention", "gemm_splitk"])
+@pytest.mark.parametrize("prec", ["fp16", "bf16"])
+def test_featurize_predict_equals_two_calls(sp, ctx, fam, prec):
+    """The fused call writes the same records, bit for bit, and the same latencies
+    and efficiencies as sp_featurize + sp_predict (full and partial spec ranges,
+    odd SM counts; pair counts that are not multiples of the 128-row tile)."""
+    b = FAMILY_BATCHES[fam]()
+    b = b.subset(np.arange(min(333, b.n_configs)))
+    m = ctx.load_model(models.random_mlp(b.family, 12), prec)
+    db = sp.DeviceBatch.from_host(b, ctx.torch_device)
+    for sa, (g0, g1) in ((specs.paper_gpu_specs(), (0, 11)), (specs.paper_gpu_specs(), (3, 9)), (odd_specs(), (0, 8))):
+        sh = ctx.load_gpu_specs(sa)
+        n = (g1 - g0) * b.n_configs
+        outs = []
+        for fused in (False, True):
+            f = sp.Features.empty(b.family, n, ctx.torch_device)
+            lat = torch.full((n,), -1.0, dtype=torch.float32, device="cuda")
+            eff = torch.full((n,), -1.0, dtype=torch.float32, device="cuda")
+            if fused:
+                ctx.featurize_predict(db, sh, m, f, lat, eff, sp.cross(g0, g1))
+            else:
+                ctx.featurize(db, sh, f, sp.cross(g0, g1))
+                ctx.predict(m, f, lat, eff)
+            torch.cuda.synchronize()
+            outs.append((sp.features_to_host(f), lat.cpu().numpy(), eff.cpu().numpy()))
+        (gi0, gf0, gs0), l0, e0 = outs[0]
+        (gi1, gf1, gs1), l1, e1 = outs[1]
+        assert np.array_equal(gs0, gs1) and np.array_equal(gi0, gi1), fam
+        assert np.array_equal(gf0.view(np.uint32), gf1.view(np.uint32)), fam
+        assert np.array_equal(l0.view(np.uint32), l1.view(np.uint32)), fam
+        assert np.array_equal(e0.view(np.uint32), e1.view(np.uint32)), fam
