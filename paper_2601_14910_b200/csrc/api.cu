@@ -494,6 +494,10 @@ extern "C" sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cf
   fi.ldc = ldc;
   fi.C = C;
   fi.g0 = pairs->spec_begin;
+  fi.n_specs = pairs->spec_end - pairs->spec_begin;
+  fi.inv_c = 0.0;
+  // config-major tiles when the pre-pass would not stay in L2 across the spec sweep
+  fi.cmajor = fi.n_specs > 1 && need > ((size_t)32 << 20) ? 1 : 0;
   fi.specs = (const DevSpec *)specs->dev.p;
   fi.out = FeatOut{out->ints, out->flts, out->status, out->ld};
   fi.n_pairs = n_pairs;

@@ -563,6 +563,30 @@ struct FusedParams {
   int64_t n_tiles;
 };
 
+// Fused tile -> pairs.  Config-major (fz.cmajor, a large config pre-pass): tile
+// t covers configs [128 cb, 128 cb + 128) of spec g0 + gs, t = cb * n_specs + gs,
+// so the n_specs tiles that read one block of the pre-pass run at about the same
+// time and share it through L2 (spec-major order re-reads all of it from DRAM
+// once per spec).  Otherwise pair-linear as sp_predict: p = 128 t + row (no
+// partial tiles; the pre-pass stays in L2 anyway).  Returns false past the end.
+__device__ __forceinline__ bool fused_tile_pair(const FusedIn &fz, int64_t t, uint32_t row, int64_t &p, int64_t &c,
+                                                int &gs) {
+  if (fz.cmajor) {
+    const int64_t cb = t / fz.n_specs;
+    gs = (int)(t - cb * fz.n_specs);
+    c = cb * kTile + row;
+    p = (int64_t)gs * fz.C + c;
+    return c < fz.C;
+  }
+  p = t * kTile + row;
+  int64_t q = (int64_t)((double)p * fz.inv_c);  // p = q C + c, fp64 estimate corrected by one
+  c = p - q * fz.C;
+  if (c < 0) { --q; c += fz.C; }
+  if (c >= fz.C) { ++q; c -= fz.C; }
+  gs = (int)q;
+  return p < fz.n_pairs;
+}
+
 // Integer Table IV slot value of a pair's demands.
 __device__ __forceinline__ int64_t int_slot_value(const PairDemand &d, int sl) {
   return sl == I_BYTES ? d.tot[3] : sl == I_BYTES_MAX ? d.mx[3] : sl >= I_MAX_T ? d.mx[sl - I_MAX_T] : d.tot[sl - I_TOT_T];
@@ -694,19 +718,11 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       nc[f] = vec[kVNC + f];
     }
     const FusedIn &fz = P.fz;
-    const double invC = 1.0 / (double)fz.C;
-    // p = q*C + r with q from the fp64 reciprocal, corrected by one (p < 2^52)
-    auto split = [&](int64_t p, int64_t &q, int64_t &r) {
-      q = (int64_t)((double)p * invC);
-      r = p - q * fz.C;
-      if (r < 0) { --q; r += fz.C; }
-      if (r >= fz.C) { ++q; r -= fz.C; }
-    };
     auto issue = [&](int64_t j) {
       if (j < n_local) {
-        int64_t p = (blockIdx.x + j * G) * kTile + row, q, c;
-        if (p >= fz.n_pairs) p = 0;  // tail rows: harmless copy, nothing stored
-        split(p, q, c);
+        int64_t p, c;
+        int gs;
+        if (!fused_tile_pair(fz, blockIdx.x + j * G, row, p, c, gs)) c = 0;  // tail rows: harmless copy
         const uint32_t dst = raw_base + (uint32_t)((j >> 1) % kFNR) * kFRawBytes + row * 8;
 #pragma unroll
         for (int f = 0; f < kPreFields; ++f) cp_async8(dst + f * kTile * 8, fz.pre + (int64_t)f * fz.ldc + c);
@@ -719,19 +735,19 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       issue(j + 2 * (kFNR - 1));
       asm volatile("cp.async.wait_group %0;" ::"n"(kFNR - 1) : "memory");
       const uint64_t *rj = raw + (size_t)((j >> 1) % kFNR) * (kFRawBytes / 8) + row;
-      const int64_t p = (blockIdx.x + j * G) * kTile + row;
+      int64_t p, c;
+      int gs;
+      const bool live = fused_tile_pair(fz, blockIdx.x + j * G, row, p, c, gs);
       float xv[16];
 #pragma unroll
       for (int f = 0; f < 16; ++f) xv[f] = 0.f;
       float side_t = 0.f;
       uint32_t side_s = 1;
-      if (p < fz.n_pairs) {
-        int64_t q, c;
-        split(p, q, c);
+      if (live) {
         const uint64_t w0 = rj[0];
         int st = (int)(w0 & 0xff);
         const int tdt = (int)((w0 >> 16) & 0xff) - 1;
-        const DevSpec &sp = fz.specs[fz.g0 + q];
+        const DevSpec &sp = fz.specs[fz.g0 + gs];
         if (st == 0 && tdt >= 0 && !sp.tensor_ok[tdt]) st = SP_PAIR_E_DTYPE;
         if (st == 0 && ((w0 >> 8) & 1)) st = SP_PAIR_E_RANGE;
         if (st != 0) {
@@ -784,20 +800,21 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
     const uint32_t row = (warp & 3) * 32 + lane;  // TMEM lane == tile row
     const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(s * 256);
     const float *w4 = vec + kVW4;
-    const int64_t n_pairs = P.fz.n_pairs;
     const uint32_t bar_d = bar(kBarDFull + s), bar_a = bar(kBarAReady + s), bar_f = bar(kBarSlotFree + s);
     uint32_t pd = 0;
     const bool tr = (warp & 7) == 0 && lane == 0;  // half-0 warp 0 of each slot
     (void)tr;
     for (int64_t j = s; j < n_local; j += 2) {
-      const int64_t p = (blockIdx.x + j * G) * kTile + row;
+      int64_t p, c_unused;
+      int gs_unused;
+      const bool live = fused_tile_pair(P.fz, blockIdx.x + j * G, row, p, c_unused, gs_unused);
       const int it = (int)(j >> 1);
       (void)it;
       EPT(0);
       // output-side inputs, loaded now and used after layer 3
       float t_theory = 0.f;
       uint32_t stbyte = 1;
-      if (h == 0 && p < n_pairs) {  // from this tile's producers (the record itself is in flight)
+      if (h == 0 && live) {  // from this tile's producers (the record itself is in flight)
         const int si = (int)(j % kNS);
         tc::mbar_wait_sleep(bar(kBarSideFull + si), (uint32_t)(j / kNS) & 1u);
         t_theory = reinterpret_cast<const float *>(smem + kFOffSide)[si * kTile + row];
@@ -875,7 +892,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       const float zp = (zz[0] + zz[1]) + (zz[2] + zz[3]);
       if (h == 1) zx[s * kTile + row] = zp;
       asm volatile("bar.sync %0, 256;" ::"r"(1 + s) : "memory");  // the slot's two halves
-      if (h == 0 && p < n_pairs) {
+      if (h == 0 && live) {
         const float z = P.m.b4 + zp + zx[s * kTile + row];
         float lat, e;
         if (stbyte != 0) {
@@ -1026,7 +1043,8 @@ int launch_predict_tcgen05_fused(const MlpBf16 &m, const FusedIn &fi, float *lat
   P.fz = fi;
   P.latency = latency;
   P.eff = eff;
-  P.n_tiles = (fi.n_pairs + kTile - 1) / kTile;
+  P.fz.inv_c = 1.0 / (double)fi.C;
+  P.n_tiles = fi.cmajor ? fi.n_specs * ((fi.C + kTile - 1) / kTile) : (fi.n_pairs + kTile - 1) / kTile;
   const int64_t grid = P.n_tiles < num_device_sms ? P.n_tiles : num_device_sms;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   return (int)(m.bf16 ? launch_fused<true>(m.family, P, (unsigned)grid, st)

@@ -183,6 +183,9 @@ struct FusedIn {
   const uint64_t *pre;
   int64_t ldc;
   int64_t C;
+  int64_t n_specs;  // spec_end - spec_begin
+  double inv_c;     // 1 / C (set by the launcher)
+  int cmajor;       // config-major tile order (large pre-pass, see predict_tcgen05.cu)
   int g0;
   const DevSpec *specs;
   FeatOut out;

@@ -109,10 +109,13 @@ def main():
         dram = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
         kn = m.get("kernel", "")
         name = "attn_schedule_cross" if "attn_schedule" in kn else (
-            "featurize_uniform_cross" if "uniform" in kn else None)
+            "uniform_prepass" if "uniform_prepass" in kn else (
+                "featurize_splitk_cross" if "splitk" in kn else (
+                    "featurize_uniform_cross" if "uniform" in kn else None)))
         if tag == "predict":
+            pk = "predict_tcgen05_fused" if "fused" in kn else "predict_tcgen05"
             for p in ("fp16", "bf16"):
-                tw[f"predict_tcgen05_{p}_dram_bytes"] = dram
+                tw[f"{pk}_{p}_dram_bytes"] = dram
         elif name:
             tw[f"{name}_dram_bytes"] = dram
             tw[f"{name}_inst_executed"] = m.get("smsp__inst_executed.sum")

@@ -17,7 +17,8 @@ SKIP=3; COUNT=1; PSKIP=3
 case "$W" in
   cfg2) ;;
   cfg4) SKIP=6; COUNT=2; PSKIP=25 ;;  # a step: 2 attention launches; predict 25 = 1st timed step's Llama attention
-  *) FEAT=featurize_uniform_cross ;;
+  splitk) FEAT=featurize_splitk_cross ;;
+  *) FEAT=uniform_prepass ;;  # uniform families run the fused pass: pre-pass + predict_tcgen05_fused
 esac
 ncu --set full --clock-control none --import-source on -k regex:$FEAT -s $SKIP -c $COUNT -o "$OUT/featurize" $BENCH \
   > "$OUT/featurize.log" 2>&1 || true
