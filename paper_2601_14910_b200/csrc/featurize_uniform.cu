@@ -93,9 +93,11 @@ struct MoeHist {
 };
 
 // Warp-cooperative histogram pass for the (up to) 32 configs of a warp, lane j
-// holding config c0 + j: the warp walks its configs one at a time, its lanes
-// reading 32 consecutive counts per iteration (coalesced) and reducing with
-// shuffles.  Lane j receives config j's result.  All 32 lanes must call it.
+// holding config c0 + j: the warp takes its configs four at a time, its lanes
+// reading 32 consecutive counts per config (coalesced; the first 128 counts of
+// all four configs are loaded before any is reduced, so four histograms are in
+// flight instead of one), and reduces with shuffles.  Lane j receives config
+// j's result.  All 32 lanes must call it.
 __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c, bool valid) {
   const int lane = threadIdx.x & 31;
   int64_t off = -1;
@@ -108,30 +110,51 @@ __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c,
   MoeHist mine;
   unsigned need = __ballot_sync(0xffffffffu, off >= 0 && E >= 1 && bm >= 1);
   while (need) {
-    const int j = __ffs(need) - 1;
-    need &= need - 1;
-    const int64_t oj = __shfl_sync(0xffffffffu, off, j);
-    const int32_t Ej = __shfl_sync(0xffffffffu, E, j);
-    const uint32_t bmj = (uint32_t)__shfl_sync(0xffffffffu, bm, j);
-    const int32_t *h = v.ragged + oj;
-    int64_t sum = 0, mb = 0;
-    int neg = 0;
-    for (int32_t e = lane; e < Ej; e += 32) {
-      const int32_t te = __ldg(h + e);
-      neg |= te < 0;
-      sum += te;
-      mb += te > 0 ? ((uint32_t)te + bmj - 1u) / bmj : 0u;
+    int jj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      jj[q] = need ? __ffs(need) - 1 : -1;
+      need &= need - 1;
+    }
+    int64_t oj[4];
+    int32_t Ej[4];
+    int32_t t[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // issue every load first
+      const int src = jj[q] < 0 ? 0 : jj[q];
+      oj[q] = __shfl_sync(0xffffffffu, off, src);
+      Ej[q] = jj[q] < 0 ? 0 : __shfl_sync(0xffffffffu, E, src);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int32_t e = lane + 32 * r;
+        t[q][r] = e < Ej[q] ? __ldg(v.ragged + oj[q] + e) : 0;
+      }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      mb += __shfl_xor_sync(0xffffffffu, mb, o);
-    }
-    neg = __any_sync(0xffffffffu, neg);
-    if (lane == j) {
-      mine.sum = sum;
-      mine.mblocks = mb;
-      mine.neg = neg;
+    for (int q = 0; q < 4; ++q) {
+      if (jj[q] < 0) break;  // warp-uniform
+      const uint32_t bmj = (uint32_t)__shfl_sync(0xffffffffu, bm, jj[q]);
+      int64_t sum = 0, mb = 0;
+      int neg = 0;
+      auto take = [&](int32_t te) {
+        neg |= te < 0;
+        sum += te;
+        mb += te > 0 ? ((uint32_t)te + bmj - 1u) / bmj : 0u;
+      };
+#pragma unroll
+      for (int r = 0; r < 4; ++r) take(t[q][r]);
+      for (int32_t e = lane + 128; e < Ej[q]; e += 32) take(__ldg(v.ragged + oj[q] + e));  // E > 128
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        mb += __shfl_xor_sync(0xffffffffu, mb, o);
+      }
+      neg = __any_sync(0xffffffffu, neg);
+      if (lane == jj[q]) {
+        mine.sum = sum;
+        mine.mblocks = mb;
+        mine.neg = neg;
+      }
     }
   }
   return mine;
