@@ -437,3 +437,38 @@ def test_featurize_predict_equals_two_calls(sp, ctx, fam, prec):
         assert np.array_equal(gf0.view(np.uint32), gf1.view(np.uint32)), fam
         assert np.array_equal(l0.view(np.uint32), l1.view(np.uint32)), fam
         assert np.array_equal(e0.view(np.uint32), e1.view(np.uint32)), fam
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg5"])
+def test_full_size_sampled_fused(sp, ctx, orc, cfg):
+    """BASELINE configs 3 (1e6 fused-MoE configs x 11 GPUs) and 5 (1,000 serving
+    GEMMs x 100,000 hypothetical specs = 1e8 pairs) at full size through
+    sp_featurize_predict -- the launch configuration bench.py times for them --
+    with 2,000 sampled pairs checked one by one against the oracle: records
+    (ints bit-exact, floats 1e-5) and fp16 latencies (1e-2)."""
+    if cfg == "cfg3":
+        b, sa = gen.gen_moe(1_000_000, 1003), specs.paper_gpu_specs()
+    else:
+        b, sa = gen.gen_serving_gemms(1000, 1005), specs.hypothetical_sweep_specs(100_000)
+    sh = ctx.load_gpu_specs(sa)
+    model = models.random_mlp(b.family, 42)
+    m = ctx.load_model(model, "fp16")
+    n = len(sa) * b.n_configs
+    f = sp.Features.empty(b.family, n, ctx.torch_device)
+    lat = torch.empty(n, dtype=torch.float32, device="cuda")
+    ctx.featurize_predict(sp.DeviceBatch.from_host(b, ctx.torch_device), sh, m, f, lat)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(4)
+    p = rng.integers(0, n, 2000)
+    ci, si = p % b.n_configs, p // b.n_configs
+    o = orc.featurize(b, sa, cfg_idx=ci, spec_idx=si)
+    pt = torch.from_numpy(p).cuda()
+    g = (f.ints[:, pt].cpu().numpy(), f.flts[:, pt].cpu().numpy(), f.status[pt].cpu().numpy())
+    assert_feature_parity(g, o, cfg + " full-size sample")
+    olat, _, _ = orc.predict(model, o)
+    gl = lat[pt].cpu().numpy()
+    ok = ~np.isnan(olat)
+    assert ok.mean() > 0.9 and np.array_equal(np.isnan(gl), ~ok)
+    np.testing.assert_allclose(gl[ok], olat[ok], rtol=LAT_RTOL_BF16)
+    del f, lat
+    torch.cuda.empty_cache()
