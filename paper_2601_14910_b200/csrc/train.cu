@@ -6,15 +6,16 @@
 // backward, running statistics, AdamW.  Readings T1..T9 in DESIGN.md §3c.
 //
 // fp32 on CUDA cores.  The work per step is small (B x ~44k MAC forward, twice
-// that backward) and a chain of dependent stages, so the design goal is few
-// launches with every reduction in a fixed order (deterministic steps):
-//   gather | 3 x (sgemm + bn_fwd) | out_fwd + out_red | bn_bwd3, dW3, dH2,
-//   bn_bwd2, dW2, dH1, bn_bwd1, dW1 | adamw                    (18 launches)
-// Column statistics (BatchNorm) use one block per 32 columns with 16 row lanes
-// summing rows r = lane (mod 16) in increasing order, then a fixed-order lane
-// fold.  GEMMs are 64x64x16 shared-memory tiles, 4x4 outputs per thread.
-// tcgen05 would need TF32 operands and 128-row tiles for a 256-row batch; at
-// these sizes the step is launch- and latency-bound, not tensor-bound.
+// that backward) and a chain of dependent stages; every reduction runs in a
+// fixed order, so steps are deterministic:
+//   gather | 3 x (sgemm, bn_stats, bn_apply) | out_fwd + out_red |
+//   3 x (bn_bwd_stats + bn_bwd_apply, dW sgemm [+ split-K reduce], dX sgemm) | adamw
+// BatchNorm kernels split the batch rows into up to 64 chunks (grid columns/32
+// x chunks; per-chunk partial sums merged in chunk order by the consumer), and
+// GEMMs whose tile grid would not fill the GPU -- the dW products, K = batch
+// rows -- are split along K into slices summed in order.  GEMMs are 64x64x16
+// shared-memory tiles, 4x4 outputs per thread.  tcgen05 would need TF32
+// operands; at these sizes the step is latency-bound, not tensor-bound.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -96,14 +97,20 @@ __global__ void train_gather(sp_features f, int pipes, int n_in, const float *__
 // A(m,k) = A[m*sam + k*sak], B(k,n) = B[k*sbk + n*sbn].  k summed in order.
 __global__ void __launch_bounds__(256) train_sgemm(int M, int N, int K, const float *__restrict__ A,
                                                    int64_t sam, int64_t sak, const float *__restrict__ Bm,
-                                                   int64_t sbk, int64_t sbn, const float *__restrict__ bias,
-                                                   float *__restrict__ C) {
+                                                   int64_t sbk, int64_t sbn, const float *bias, float *C) {
   __shared__ float As[kGemmK][kGemmT + 4];
   __shared__ float Bs[kGemmK][kGemmT + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int m0 = blockIdx.y * kGemmT, n0 = blockIdx.x * kGemmT;
+  // split-K: slice blockIdx.z covers k in [kb, ke) and writes its own partial C
+  const int kslice = (K + (int)gridDim.z - 1) / (int)gridDim.z;
+  const int kb = (int)blockIdx.z * kslice, ke = min(K, kb + kslice);
+  if (gridDim.z > 1) {
+    C += (int64_t)blockIdx.z * M * N;
+    bias = nullptr;
+  }
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += kGemmK) {
+  for (int k0 = kb; k0 < ke; k0 += kGemmK) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int e = tid + i * 256;
@@ -111,8 +118,8 @@ __global__ void __launch_bounds__(256) train_sgemm(int M, int N, int K, const fl
       const int am = sak == 1 ? e >> 4 : e & 63, ak = sak == 1 ? e & 15 : e >> 6;
       const int bn = sbk == 1 ? e >> 4 : e & 63, bk = sbk == 1 ? e & 15 : e >> 6;
       const int gm = m0 + am, gk = k0 + ak, gn = n0 + bn, gk2 = k0 + bk;
-      As[ak][am] = (gm < M && gk < K) ? __ldg(A + gm * sam + gk * sak) : 0.f;
-      Bs[bk][bn] = (gn < N && gk2 < K) ? __ldg(Bm + gk2 * sbk + gn * sbn) : 0.f;
+      As[ak][am] = (gm < M && gk < ke) ? __ldg(A + gm * sam + gk * sak) : 0.f;
+      Bs[bk][bn] = (gn < N && gk2 < ke) ? __ldg(Bm + gk2 * sbk + gn * sbn) : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -155,96 +162,166 @@ __device__ __forceinline__ float fold_lanes(float (*sm)[kColThreadsX + 1], float
   return s;
 }
 
-// Hidden-layer epilogue, forward.  Train (T2): a = relu(z), batch mean and
-// biased variance (two passes), a_hat, y = gamma a_hat + beta, inverted
-// dropout (T3); running statistics (T6).  Eval: running statistics, no dropout.
-__global__ void __launch_bounds__(512) train_bn_fwd(int B, int w, const float *__restrict__ z,
-                                                    const float *__restrict__ gamma,
-                                                    const float *__restrict__ beta, float *__restrict__ rmean,
-                                                    float *__restrict__ rvar, float *__restrict__ ahat,
-                                                    float *__restrict__ h, float *__restrict__ inv_std, float eps,
-                                                    float mom, int train, DropParams dp, int layer) {
+// Row chunks of the BatchNorm kernels: block (32 columns x 16 row lanes),
+// grid (columns / 32, R chunks); each statistic is a per-chunk partial in
+// scratch, merged by the consumer in chunk order (deterministic).
+__host__ __device__ inline int bn_chunks(int B) { return B <= 256 ? 1 : (B + 255) / 256 < 64 ? (B + 255) / 256 : 64; }
+__device__ __forceinline__ void chunk_rows(int B, int R, int rc, int &r0, int &r1) {
+  const int per = (B + R - 1) / R;
+  r0 = min(B, rc * per);
+  r1 = min(B, r0 + per);
+}
+
+// Forward statistics (T2), shifted sums: with K = relu(z[0][c]), per chunk
+// S1 = sum (a - K), S2 = sum (a - K)^2 (the shift keeps S2 - S1^2/B free of
+// cancellation).  part: [2][R][w].
+__global__ void __launch_bounds__(512) train_bn_stats(int B, int w, int R, const float *__restrict__ z,
+                                                      float *__restrict__ part) {
   __shared__ float sm[kColThreadsY][kColThreadsX + 1];
-  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y, rc = blockIdx.y;
   const int c = blockIdx.x * kColThreadsX + tx;
   const bool ok = c < w;
-  const float g = ok ? gamma[c] : 0.f, b = ok ? beta[c] : 0.f;
+  int r0, r1;
+  chunk_rows(B, R, rc, r0, r1);
+  float s1 = 0.f, s2 = 0.f;
+  if (ok) {
+    const float K = fmaxf(z[c], 0.f);
+    for (int r = r0 + ty; r < r1; r += kColThreadsY) {
+      const float d = fmaxf(z[(int64_t)r * w + c], 0.f) - K;
+      s1 += d;
+      s2 = fmaf(d, d, s2);
+    }
+  }
+  s1 = fold_lanes(sm, s1);
+  s2 = fold_lanes(sm, s2);
+  if (ok && ty == 0) {
+    part[(int64_t)rc * w + c] = s1;
+    part[(int64_t)(R + rc) * w + c] = s2;
+  }
+}
+
+// Hidden-layer epilogue, forward.  Train (T2): merge the chunk statistics into
+// the batch mean and biased variance, a_hat, y = gamma a_hat + beta, inverted
+// dropout (T3); chunk 0 updates the running statistics (T6).  Eval: running
+// statistics, no dropout.
+__global__ void __launch_bounds__(512) train_bn_apply(int B, int w, int R, const float *__restrict__ z,
+                                                      const float *__restrict__ part, const float *__restrict__ gamma,
+                                                      const float *__restrict__ beta, float *__restrict__ rmean,
+                                                      float *__restrict__ rvar, float *__restrict__ ahat,
+                                                      float *__restrict__ h, float *__restrict__ inv_std, float eps,
+                                                      float mom, int train, DropParams dp, int layer) {
+  const int tx = threadIdx.x, ty = threadIdx.y, rc = blockIdx.y;
+  const int c = blockIdx.x * kColThreadsX + tx;
+  if (c >= w) return;
+  int r0, r1;
+  chunk_rows(B, R, rc, r0, r1);
+  const float g = gamma[c], b = beta[c];
   if (!train) {
-    if (!ok) return;
     const float m = rmean[c], inv = 1.0f / sqrtf(rvar[c] + eps);
-    for (int r = ty; r < B; r += kColThreadsY) {
+    for (int r = r0 + ty; r < r1; r += kColThreadsY) {
       const float a = fmaxf(z[(int64_t)r * w + c], 0.f);
       h[(int64_t)r * w + c] = g * ((a - m) * inv) + b;
     }
     return;
   }
-  float s = 0.f;
-  if (ok)
-    for (int r = ty; r < B; r += kColThreadsY) s += fmaxf(z[(int64_t)r * w + c], 0.f);
-  const float mean = fold_lanes(sm, s) / (float)B;
-  float s2 = 0.f;
-  if (ok)
-    for (int r = ty; r < B; r += kColThreadsY) {
-      const float d = fmaxf(z[(int64_t)r * w + c], 0.f) - mean;
-      s2 = fmaf(d, d, s2);
-    }
-  const float var = fold_lanes(sm, s2) / (float)B;
-  if (!ok) return;
+  float S1 = 0.f, S2 = 0.f;
+  for (int k = 0; k < R; ++k) {
+    S1 += part[(int64_t)k * w + c];
+    S2 += part[(int64_t)(R + k) * w + c];
+  }
+  const float K = fmaxf(z[c], 0.f);
+  const float d1 = S1 / (float)B;
+  const float mean = K + d1;
+  const float var = fmaxf(S2 / (float)B - d1 * d1, 0.f);
   const float inv = 1.0f / sqrtf(var + eps);
-  for (int r = ty; r < B; r += kColThreadsY) {
+  for (int r = r0 + ty; r < r1; r += kColThreadsY) {
     const int64_t o = (int64_t)r * w + c;
     const float ah = (fmaxf(z[o], 0.f) - mean) * inv;
     ahat[o] = ah;
     h[o] = keep_unit(dp, layer, r, c) ? (g * ah + b) * dp.scale : 0.f;
   }
-  if (ty == 0) {
+  if (rc == 0 && ty == 0) {
     inv_std[c] = inv;
     rmean[c] = (1.f - mom) * rmean[c] + mom * mean;
     rvar[c] = (1.f - mom) * rvar[c] + mom * (var * ((float)B / (float)(B - 1)));
   }
 }
 
-// Hidden-layer epilogue, backward: dy = dh * keep * scale; dgamma = sum dy a_hat,
-// dbeta = sum dy; dz = inv_std (gamma dy - gamma mean(dy) - a_hat gamma mean(dy a_hat)) [z > 0];
-// dbias = sum dz.
-__global__ void __launch_bounds__(512) train_bn_bwd(int B, int w, const float *__restrict__ dh,
-                                                    const float *__restrict__ z, const float *__restrict__ ahat,
-                                                    const float *__restrict__ gamma,
-                                                    const float *__restrict__ inv_std, DropParams dp, int layer,
-                                                    float *__restrict__ dz, float *__restrict__ dgamma,
-                                                    float *__restrict__ dbeta, float *__restrict__ dbias) {
+// Backward statistics per chunk (dy = dh * keep * scale): sum dy, sum dy a_hat,
+// and over the active rows (z > 0): sum dy, sum a_hat, count.  part: [5][R][w].
+__global__ void __launch_bounds__(512) train_bn_bwd_stats(int B, int w, int R, const float *__restrict__ dh,
+                                                          const float *__restrict__ z, const float *__restrict__ ahat,
+                                                          DropParams dp, int layer, float *__restrict__ part) {
   __shared__ float sm[kColThreadsY][kColThreadsX + 1];
-  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y, rc = blockIdx.y;
   const int c = blockIdx.x * kColThreadsX + tx;
   const bool ok = c < w;
-  float sdy = 0.f, sdya = 0.f;
+  int r0, r1;
+  chunk_rows(B, R, rc, r0, r1);
+  float v[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
   if (ok)
-    for (int r = ty; r < B; r += kColThreadsY) {
+    for (int r = r0 + ty; r < r1; r += kColThreadsY) {
       const int64_t o = (int64_t)r * w + c;
       const float dy = keep_unit(dp, layer, r, c) ? dh[o] * dp.scale : 0.f;
-      sdy += dy;
-      sdya = fmaf(dy, ahat[o], sdya);
+      const float ah = ahat[o];
+      v[0] += dy;
+      v[1] = fmaf(dy, ah, v[1]);
+      if (z[o] > 0.f) {
+        v[2] += dy;
+        v[3] += ah;
+        v[4] += 1.f;
+      }
     }
-  sdy = fold_lanes(sm, sdy);
-  sdya = fold_lanes(sm, sdya);
-  float sdz = 0.f;
-  if (ok) {
-    const float g = gamma[c], inv = inv_std[c];
-    const float m1 = g * sdy / (float)B, m2 = g * sdya / (float)B;
-    for (int r = ty; r < B; r += kColThreadsY) {
-      const int64_t o = (int64_t)r * w + c;
-      const float dy = keep_unit(dp, layer, r, c) ? dh[o] * dp.scale : 0.f;
-      const float v = z[o] > 0.f ? inv * (g * dy - m1 - ahat[o] * m2) : 0.f;
-      dz[o] = v;
-      sdz += v;
-    }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) v[k] = fold_lanes(sm, v[k]);
+  if (ok && ty == 0)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) part[(int64_t)(k * R + rc) * w + c] = v[k];
+}
+
+// Hidden-layer epilogue, backward: dgamma = sum dy a_hat, dbeta = sum dy;
+// dz = inv_std (gamma dy - gamma mean(dy) - a_hat gamma mean(dy a_hat)) [z > 0];
+// dbias = sum dz = inv_std (gamma sum_act dy - n_act m1 - m2 sum_act a_hat).
+__global__ void __launch_bounds__(512) train_bn_bwd_apply(int B, int w, int R, const float *__restrict__ dh,
+                                                          const float *__restrict__ z,
+                                                          const float *__restrict__ ahat,
+                                                          const float *__restrict__ part,
+                                                          const float *__restrict__ gamma,
+                                                          const float *__restrict__ inv_std, DropParams dp,
+                                                          int layer, float *__restrict__ dz,
+                                                          float *__restrict__ dgamma, float *__restrict__ dbeta,
+                                                          float *__restrict__ dbias) {
+  const int tx = threadIdx.x, ty = threadIdx.y, rc = blockIdx.y;
+  const int c = blockIdx.x * kColThreadsX + tx;
+  if (c >= w) return;
+  int r0, r1;
+  chunk_rows(B, R, rc, r0, r1);
+  float S[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < R; ++k)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) S[q] += part[(int64_t)(q * R + k) * w + c];
+  const float g = gamma[c], inv = inv_std[c];
+  const float m1 = g * S[0] / (float)B, m2 = g * S[1] / (float)B;
+  for (int r = r0 + ty; r < r1; r += kColThreadsY) {
+    const int64_t o = (int64_t)r * w + c;
+    const float dy = keep_unit(dp, layer, r, c) ? dh[o] * dp.scale : 0.f;
+    dz[o] = z[o] > 0.f ? inv * (g * dy - m1 - ahat[o] * m2) : 0.f;
   }
-  sdz = fold_lanes(sm, sdz);
-  if (ok && ty == 0) {
-    dgamma[c] = sdya;
-    dbeta[c] = sdy;
-    dbias[c] = sdz;
+  if (rc == 0 && ty == 0) {
+    dgamma[c] = S[1];
+    dbeta[c] = S[0];
+    dbias[c] = inv * (g * S[2] - S[4] * m1 - m2 * S[3]);
   }
+}
+
+// Split-K partials of train_sgemm summed in slice order, plus the bias.
+__global__ void train_splitk_reduce(int64_t MN, int N, int S, const float *__restrict__ part,
+                                    const float *__restrict__ bias, float *__restrict__ C) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= MN) return;
+  float v = 0.f;
+  for (int z = 0; z < S; ++z) v += part[(int64_t)z * MN + i];
+  C[i] = v + (bias ? bias[i % N] : 0.f);
 }
 
 // ------------------------------------------------------------------ output layer and loss (T4)
@@ -419,7 +496,10 @@ struct sp_trainer {
   int64_t n_params = 0;
   // offsets into the flat parameter vector: layer l = 0..2 w, b, g, be; then w4, b4
   int64_t ow[4] = {}, ob[4] = {}, og[3] = {}, obe[3] = {};
-  DevBuf params, grads, mom1, mom2, running, norm, act, partial;
+  DevBuf params, grads, mom1, mom2, running, norm, act, partial, scratch;
+  float *bn_part = nullptr;  // BatchNorm chunk partials [5][64][256]
+  float *kpart = nullptr;    // split-K GEMM partials
+  int64_t kpart_cap = 0;     // floats
   size_t partial_cap = 0;
   int B = 0;  // max batch
   float *x = nullptr, *t = nullptr, *z[3] = {}, *ah[3] = {}, *h[3] = {}, *inv[3] = {}, *dz4 = nullptr,
@@ -447,21 +527,49 @@ DropParams drop_params(const sp_trainer *tr, int64_t step) {
   return d;
 }
 
+// C[M][N] = A . B (+ bias) with train_sgemm; GEMMs whose tile grid would not
+// fill the GPU (the dW products: K = batch rows) are split along K into S
+// slices summed in order by train_splitk_reduce.
+void gemm(sp_trainer *tr, int M, int N, int K, const float *A, int64_t sam, int64_t sak, const float *Bm, int64_t sbk,
+          int64_t sbn, const float *bias, float *C, cudaStream_t st, const LaunchHook &hk) {
+  const int gx = (N + kGemmT - 1) / kGemmT, gy = (M + kGemmT - 1) / kGemmT;
+  const int target = 2 * tr->ctx->num_sms;
+  int S = 1;
+  if (gx * gy < target && K >= 4 * kGemmK) {
+    S = std::min((target + gx * gy - 1) / (gx * gy), K / (2 * kGemmK));
+    S = (int)std::min<int64_t>(S, tr->kpart_cap / ((int64_t)M * N));
+    S = std::max(S, 1);
+  }
+  hk.on_begin("train_sgemm", st);
+  train_sgemm<<<dim3(gx, gy, S), 256, 0, st>>>(M, N, K, A, sam, sak, Bm, sbk, sbn, bias, S > 1 ? tr->kpart : C);
+  hk.on_end(st);
+  if (S > 1) {
+    const int64_t MN = (int64_t)M * N;
+    hk.on_begin("train_splitk_reduce", st);
+    train_splitk_reduce<<<(unsigned)((MN + 255) / 256), 256, 0, st>>>(MN, N, S, tr->kpart, bias, C);
+    hk.on_end(st);
+  }
+}
+
 // Forward of rows [0, B) already gathered into tr->x / tr->t.
 void forward(sp_trainer *tr, int B, bool train, const DropParams &dp, cudaStream_t st, const LaunchHook &hk) {
   const float *P = (const float *)tr->params.p;
   const float *hin = tr->x;
   int fan = tr->n_in;
+  const int R = bn_chunks(B);
   for (int l = 0; l < 3; ++l) {
     const int w = kHid[l];
-    dim3 g((w + kGemmT - 1) / kGemmT, (B + kGemmT - 1) / kGemmT);
-    hk.on_begin("train_sgemm", st);
-    train_sgemm<<<g, 256, 0, st>>>(B, w, fan, hin, fan, 1, P + tr->ow[l], 1, fan, P + tr->ob[l], tr->z[l]);
-    hk.on_end(st);
-    hk.on_begin("train_bn_fwd", st);
-    train_bn_fwd<<<(w + 31) / 32, dim3(kColThreadsX, kColThreadsY), 0, st>>>(
-        B, w, tr->z[l], P + tr->og[l], P + tr->obe[l], tr->rm[l], tr->rv[l], tr->ah[l], tr->h[l], tr->inv[l],
-        tr->bn_eps, tr->cfg.bn_momentum, train ? 1 : 0, dp, l);
+    gemm(tr, B, w, fan, hin, fan, 1, P + tr->ow[l], 1, fan, P + tr->ob[l], tr->z[l], st, hk);
+    const dim3 cg((w + kColThreadsX - 1) / kColThreadsX, R), cb(kColThreadsX, kColThreadsY);
+    if (train) {
+      hk.on_begin("train_bn_stats", st);
+      train_bn_stats<<<cg, cb, 0, st>>>(B, w, R, tr->z[l], tr->bn_part);
+      hk.on_end(st);
+    }
+    hk.on_begin("train_bn_apply", st);
+    train_bn_apply<<<cg, cb, 0, st>>>(B, w, R, tr->z[l], tr->bn_part, P + tr->og[l], P + tr->obe[l], tr->rm[l],
+                                      tr->rv[l], tr->ah[l], tr->h[l], tr->inv[l], tr->bn_eps, tr->cfg.bn_momentum,
+                                      train ? 1 : 0, dp, l);
     hk.on_end(st);
     hin = tr->h[l];
     fan = w;
@@ -573,6 +681,16 @@ extern "C" sp_status sp_train_create(sp_ctx *ctx, const sp_mlp_desc *d, const sp
   tr->dh = take(B * 256);
   tr->dzb = take(B * 256);
   tr->loss = take(4);
+  // BatchNorm partials and split-K partials (no allocation inside a step)
+  tr->kpart_cap = (int64_t)32 * 256 * 256;
+  e = cudaMalloc(&tr->scratch.p, ((size_t)5 * 64 * 256 + (size_t)tr->kpart_cap) * sizeof(float));
+  if (e != cudaSuccess) {
+    tr->scratch.p = nullptr;
+    delete tr;
+    return cuda_fail(ctx, e, "sp_train_create: scratch");
+  }
+  tr->bn_part = (float *)tr->scratch.p;
+  tr->kpart = tr->bn_part + (size_t)5 * 64 * 256;
   float *rs = (float *)tr->running.p;
   for (int l = 0, o = 0; l < 3; ++l) {
     tr->rm[l] = rs + o;
@@ -611,26 +729,20 @@ extern "C" sp_status sp_train_step(sp_trainer *tr, const sp_features *in, const 
   train_out_red<<<1, 1024, 0, st>>>(b, tr->h[2], tr->dz4, tr->loss_r, 1, G + tr->ow[3], G + tr->ob[3], tr->loss);
   hk.on_end(st);
   // backward through the hidden layers: dh (layer l's output grad) -> dzb -> dW, dh(l-1)
+  const int R = bn_chunks(b);
   for (int l = 2; l >= 0; --l) {
     const int w = kHid[l], fan = l ? kHid[l - 1] : n_in;
+    const dim3 cg((w + kColThreadsX - 1) / kColThreadsX, R), cb(kColThreadsX, kColThreadsY);
     hk.on_begin("train_bn_bwd", st);
-    train_bn_bwd<<<(w + 31) / 32, dim3(kColThreadsX, kColThreadsY), 0, st>>>(
-        b, w, tr->dh, tr->z[l], tr->ah[l], P + tr->og[l], tr->inv[l], dp, l, tr->dzb, G + tr->og[l],
-        G + tr->obe[l], G + tr->ob[l]);
+    train_bn_bwd_stats<<<cg, cb, 0, st>>>(b, w, R, tr->dh, tr->z[l], tr->ah[l], dp, l, tr->bn_part);
+    train_bn_bwd_apply<<<cg, cb, 0, st>>>(b, w, R, tr->dh, tr->z[l], tr->ah[l], tr->bn_part, P + tr->og[l],
+                                          tr->inv[l], dp, l, tr->dzb, G + tr->og[l], G + tr->obe[l], G + tr->ob[l]);
     hk.on_end(st);
     const float *hprev = l ? tr->h[l - 1] : tr->x;
     // dW[w][fan] = dZ^T H: A(m=unit, k=row) = dzb[row*w + unit], B(k=row, n) = hprev[row*fan + n]
-    hk.on_begin("train_sgemm", st);
-    train_sgemm<<<dim3((fan + kGemmT - 1) / kGemmT, (w + kGemmT - 1) / kGemmT), 256, 0, st>>>(
-        w, fan, b, tr->dzb, 1, w, hprev, fan, 1, nullptr, G + tr->ow[l]);
-    hk.on_end(st);
-    if (l) {
-      // dH[B][fan] = dZ W: A(m=row, k=unit) = dzb[row*w + unit], B(k=unit, n) = W[unit*fan + n]
-      hk.on_begin("train_sgemm", st);
-      train_sgemm<<<dim3((fan + kGemmT - 1) / kGemmT, (b + kGemmT - 1) / kGemmT), 256, 0, st>>>(
-          b, fan, w, tr->dzb, w, 1, P + tr->ow[l], fan, 1, nullptr, tr->dh);
-      hk.on_end(st);
-    }
+    gemm(tr, w, fan, b, tr->dzb, 1, w, hprev, fan, 1, nullptr, G + tr->ow[l], st, hk);
+    // dH[B][fan] = dZ W: A(m=row, k=unit) = dzb[row*w + unit], B(k=unit, n) = W[unit*fan + n]
+    if (l) gemm(tr, b, fan, w, tr->dzb, w, 1, P + tr->ow[l], fan, 1, nullptr, tr->dh, st, hk);
   }
   tr->step += 1;
   const double t = (double)tr->step;
