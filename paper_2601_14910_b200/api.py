@@ -678,9 +678,48 @@ class Context:
         return out_t[:G * C].numpy()
 
     # -- end-to-end: host configs in, host latencies out
+    @staticmethod
+    def _ragged_slices(fam, fh, oh, bounds):
+        """Copy plan for the ragged data of predict_host's slices, from the host
+        arrays at the slice boundaries only: slice i takes [first offset, end of
+        its last config) -- exact when the batch lays its ragged data out config
+        by config, as the generators and any sequential builder do.  The plan is
+        verified on the device (_ragged_guard) and the call is redone with one
+        whole copy if it does not hold.  None: no plan (copy whole)."""
+        if oh is None or fam not in (_abi.SP_ATTENTION, _abi.SP_FUSED_MOE) or len(bounds) < 3:
+            return None
+        row, mult = (0, 2) if fam == _abi.SP_ATTENTION else (1, 1)
+        out, prev = [], 0
+        for a, b in zip(bounds, bounds[1:]):
+            ia = next((k for k in range(a, min(b, a + 64)) if int(oh[k]) >= 0), None)
+            ib = next((k for k in range(b - 1, max(a - 1, b - 65), -1) if int(oh[k]) >= 0), None)
+            if ia is None or ib is None:
+                return None  # long runs of balanced MoE configs: no cheap boundary, copy whole
+            lo, hi = int(oh[ia]), int(oh[ib]) + mult * int(fh[row, ib])
+            if lo < prev or hi < lo:
+                return None
+            out.append((lo, hi))
+            prev = hi
+        return out
+
+    @staticmethod
+    def _ragged_guard(fam, cache, c0, c1, lo, hi, stream):
+        """Device check of slice [c0, c1)'s ragged copy plan: a config whose ragged
+        data is not inside [lo, hi) gets its length field zeroed in the device
+        copy (so it is a cheap SP_PAIR_E_DIM pair instead of reading stale data);
+        returns a device bool, True when the plan held for every config."""
+        row, mult = (0, 2) if fam == _abi.SP_ATTENTION else (1, 1)
+        with torch.cuda.stream(stream):
+            off = cache["roff"][c0:c1]
+            ln = cache["fields"][row, c0:c1]
+            end = off + mult * ln.to(torch.int64)
+            bad = (off >= 0) & ((off < lo) | (end > hi))
+            ln.masked_fill_(bad, 0)
+            return ~bad.any()
+
     def predict_host(self, batch, specs: Specs, model: Model, spec_range=None,
                      out: np.ndarray | torch.Tensor | None = None, chunks: int = 4,
-                     stream=None) -> np.ndarray:
+                     stream=None, _plan: bool = True) -> np.ndarray:
         """The user-facing call.  Host config arrays (numpy or torch; pinned
         memory gives asynchronous copies) -> H2D -> sp_featurize_predict (fused, or sp_featurize -> sp_predict)
         -> D2H of fp32 latencies in spec-major order [spec][config].
@@ -736,12 +775,13 @@ class Context:
         s_h2d, s_d2h = cache["h2d"], cache["d2h"]
         s_h2d.wait_stream(comp)
         out2d = out_t[:n].view(G, C)
+        ranges = None
         if rh is not None and rh.numel() > 0:
-            # the ragged data goes first, in one copy: locating each slice's own
-            # ragged range on the host costs more than the copy it would overlap
-            with torch.cuda.stream(s_h2d):
-                cache["ragged"][:rh.numel()].copy_(rh, non_blocking=True)
-        d2h_done = []
+            ranges = self._ragged_slices(fam, fh, oh, bounds) if _plan else None
+            if ranges is None:  # one copy ahead of the first slice
+                with torch.cuda.stream(s_h2d):
+                    cache["ragged"][:rh.numel()].copy_(rh, non_blocking=True)
+        d2h_done, oks = [], []
         for i, (c0, c1) in enumerate(zip(bounds, bounds[1:])):
             nc = c1 - c0
             with torch.cuda.stream(s_h2d):
@@ -749,9 +789,14 @@ class Context:
                     cache["fields"][fi, c0:c1].copy_(fh[fi, c0:c1], non_blocking=True)
                 if cache["roff"] is not None:
                     cache["roff"][c0:c1].copy_(oh[c0:c1], non_blocking=True)
+                if ranges is not None and ranges[i][1] > ranges[i][0]:  # this slice's own ragged range
+                    lo, hi = ranges[i]
+                    cache["ragged"][lo:hi].copy_(rh[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(s_h2d)
             comp.wait_event(ev)
+            if ranges is not None:
+                oks.append(self._ragged_guard(fam, cache, c0, c1, ranges[i][0], ranges[i][1], comp))
             db = DeviceBatch(fam, cache["fields"][:, c0:c1], cache["ragged"],
                              None if cache["roff"] is None else cache["roff"][c0:c1])
             feats = cache["feats"]
@@ -771,6 +816,8 @@ class Context:
                 d2h_done.append(ev3)
         s_d2h.synchronize()
         comp.wait_stream(s_d2h)
+        if oks and not bool(torch.stack(oks).all().item()):  # the boundary plan missed some ragged data
+            return self.predict_host(batch, specs, model, spec_range, out_t, chunks, stream, _plan=False)
         return out_t[:n].numpy()
 
 

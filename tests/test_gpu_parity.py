@@ -308,6 +308,47 @@ def test_predict_host_equals_device_path(sp, ctx, fam, chunks):
     assert np.array_equal(got, lat.cpu().numpy(), equal_nan=True)
 
 
+@pytest.mark.parametrize("layout", ["reversed", "interior_jump"])
+def test_predict_host_irregular_ragged_layout(sp, ctx, layout):
+    """predict_host copies each slice's ragged range when the layout is config
+    by config; layouts that break that (reversed chunks: caught on the host;
+    an interior config pointing into another slice's range: caught on the
+    device, the call redone with one whole copy) still give exactly the
+    device path's latencies."""
+    b = FAMILY_BATCHES["attention"]()
+    off = b.ragged_off.copy()
+    bs = b.field("BS").astype(np.int64)
+    if layout == "reversed":
+        chunks = [b.ragged[o:o + 2 * n] for o, n in zip(off, bs)][::-1]
+        rag = np.concatenate(chunks).astype(np.int32)
+        lens = (2 * bs)[::-1]
+        starts = np.concatenate([[0], np.cumsum(lens)[:-1]])[::-1]
+        off = starts.astype(np.int64)
+    else:
+        rag = b.ragged.copy()
+        k_src = b.n_configs - 3  # a config in the last slice with the same batch size
+        k = next(k for k in range(5, b.n_configs // 4) if bs[k] == bs[k_src])
+        off[k] = off[k_src]
+    b2 = gen.ConfigBatch(b.family, b.fields.copy(), rag, off)
+    sa = specs.paper_gpu_specs()
+    sh = ctx.load_gpu_specs(sa)
+    m = ctx.load_model(models.random_mlp(b.family, 5), "fp16")
+    f, _ = gpu_features(sp, ctx, b2, sa, specs_handle=sh)
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    ctx.predict(m, f, lat)
+    torch.cuda.synchronize()
+
+    class Host:
+        family = b.family
+
+    h = Host()
+    h.fields = torch.from_numpy(b2.fields).pin_memory()
+    h.ragged = torch.from_numpy(b2.ragged).pin_memory()
+    h.ragged_off = torch.from_numpy(b2.ragged_off).pin_memory()
+    got = ctx.predict_host(h, sh, m, chunks=4)
+    assert np.array_equal(got, lat.cpu().numpy(), equal_nan=True)
+
+
 def test_featurize_deterministic(sp, ctx):
     b = FAMILY_BATCHES["attention"]()
     sa = specs.paper_gpu_specs()
