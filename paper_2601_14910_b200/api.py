@@ -718,14 +718,15 @@ class Context:
             return ~bad.any()
 
     def predict_host(self, batch, specs: Specs, model: Model, spec_range=None,
-                     out: np.ndarray | torch.Tensor | None = None, chunks: int = 4,
+                     out: np.ndarray | torch.Tensor | None = None, chunks=(1, 3, 3, 1),
                      stream=None, _plan: bool = True) -> np.ndarray:
         """The user-facing call.  Host config arrays (numpy or torch; pinned
         memory gives asynchronous copies) -> H2D -> sp_featurize_predict (fused, or sp_featurize -> sp_predict)
         -> D2H of fp32 latencies in spec-major order [spec][config].
 
-        The configs are split into `chunks` slices pipelined over three
-        streams: the H2D of slice i+1 and the D2H of slice i-1 overlap the
+        The configs are split into `chunks` slices (a count, or slice weights:
+        the default (1, 3, 3, 1) keeps the first slice's copy-in and the last
+        slice's copy-out short) pipelined over three streams: the H2D of slice i+1 and the D2H of slice i-1 overlap the
         kernels of slice i (the ragged request / histogram data is copied
         whole, ahead of the first slice).  Device buffers are cached across
         calls."""
@@ -750,11 +751,20 @@ class Context:
             out_t = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
         if n == 0:
             return out_t[:0].numpy()
+        weights = None
+        if not isinstance(chunks, int):  # explicit slice weights, e.g. (1, 3, 3, 1)
+            weights = [float(w) for w in chunks]
+            chunks = len(weights)
         if G >= 64 and G >= 4 * chunks:  # wide spec axis (e.g. config 5): pipeline over specs
             return self._predict_host_by_spec(fam, fh, rh, oh, specs, model, g0, g1, out_t,
                                               max(chunks, 8), stream)
         chunks = max(1, min(chunks, C))
-        bounds = [C * i // chunks for i in range(chunks + 1)]
+        if weights is None or len(weights) != chunks:
+            bounds = [C * i // chunks for i in range(chunks + 1)]
+        else:
+            cum = np.concatenate([[0.0], np.cumsum(weights)]) / sum(weights)
+            bounds = sorted(set([0, C] + [int(C * x) for x in cum]))
+            chunks = len(bounds) - 1
         cmax = max(b1 - b0 for b0, b1 in zip(bounds, bounds[1:]))
         dev = self.torch_device
         key = (fam, nf, C, G, cmax, 0 if rh is None else rh.numel())

@@ -23,7 +23,8 @@ from workloads import models  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="cfg2")
-    ap.add_argument("--chunks", type=int, nargs="+", default=[1, 2, 4, 8])
+    ap.add_argument("--chunks", nargs="+", default=["1", "2", "4", "8"],
+                    help="slice counts, or comma-separated slice weights (e.g. 1,3,3,1)")
     ap.add_argument("--reps", type=int, default=4)
     args = ap.parse_args()
     ctx = sp.Context(0)
@@ -40,7 +41,8 @@ def main():
     hb.ragged_off = None if b.ragged_off is None else torch.from_numpy(b.ragged_off).pin_memory()
     n = (g1 - g0) * b.n_configs
     out = torch.empty(n, dtype=torch.float32).pin_memory()
-    for ch in args.chunks:
+    for spec_ in args.chunks:
+        ch = [float(x) for x in spec_.split(",")] if "," in spec_ else int(spec_)
         for _ in range(2):
             ctx.predict_host(hb, sh, m, (g0, g1), out=out, chunks=ch)
         torch.cuda.synchronize()
@@ -49,7 +51,7 @@ def main():
             ctx.predict_host(hb, sh, m, (g0, g1), out=out, chunks=ch)
         torch.cuda.synchronize()
         ms = (time.perf_counter() - t) / args.reps * 1e3
-        print(json.dumps({"workload": args.workload, "chunks": ch, "ms": ms, "pairs_per_s": n / ms * 1e3}), flush=True)
+        print(json.dumps({"workload": args.workload, "chunks": spec_, "ms": ms, "pairs_per_s": n / ms * 1e3}), flush=True)
 
 
 if __name__ == "__main__":
