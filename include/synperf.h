@@ -621,8 +621,10 @@ void sp_train_destroy(sp_trainer *tr);
  * pair indices into `in`, which must have the model's family; every indexed
  * pair must have status 0 and measured_us > 0).  measured_us: DEVICE fp32
  * [in->n_pairs].  loss_out: DEVICE fp32 [1] receiving the pre-update batch
- * loss, or NULL.  Advances the trainer's step counter (the dropout counter).
- * Asynchronous on `stream`; no allocation.  SP_E_ARG if B < 2 or B > max_batch. */
+ * loss, or NULL.  Advances the trainer's step counter (the dropout counter and
+ * AdamW's t), which lives in device memory: the call can be captured in a CUDA
+ * graph and replayed, each replay taking the next step.  Asynchronous on
+ * `stream`; no allocation.  SP_E_ARG if B < 2 or B > max_batch. */
 sp_status sp_train_step(sp_trainer *tr, const sp_features *in, const float *measured_us,
                         const int64_t *batch_idx, int64_t B, float *loss_out, void *stream);
 

@@ -198,6 +198,19 @@ class Trainer:
                                            int(batch_idx.numel()), self.loss_dev.data_ptr(), _stream_ptr(stream)))
         return self.loss_dev
 
+    def capture(self, feats: "Features", measured_us: torch.Tensor, batch_idx: torch.Tensor) -> "torch.cuda.CUDAGraph":
+        """CUDA graph of one sp_train_step over the fixed device buffer batch_idx
+        (refill it in place between replays).  The step counter, dropout masks and
+        AdamW bias corrections live on the device, so each replay is the next
+        step.  Capture launches nothing; kernel accounting must be off."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fs = feats.c_struct()
+            self._ctx._check(lib.sp_train_step(self._h, C.byref(fs), measured_us.data_ptr(), batch_idx.data_ptr(),
+                                               int(batch_idx.numel()), self.loss_dev.data_ptr(),
+                                               _stream_ptr(torch.cuda.current_stream())))
+        return g
+
     def eval_loss(self, feats: "Features", measured_us: torch.Tensor, idx: torch.Tensor, stream=None) -> torch.Tensor:
         out = torch.empty(1, dtype=torch.float32, device=self._ctx.torch_device)
         fs = feats.c_struct()

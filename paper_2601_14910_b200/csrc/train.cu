@@ -42,13 +42,14 @@ __device__ __forceinline__ uint64_t splitmix_fin(uint64_t z) {
 }
 
 struct DropParams {
-  uint64_t seed, step;
+  uint64_t seed;
+  const int64_t *step;  // DEVICE step counter (so a captured step graph replays correctly)
   uint32_t thr;  // keep iff bits 63..40 >= thr = round(p * 2^24)
   float scale;   // 1 / (1 - p)
 };
 
 __device__ __forceinline__ bool keep_unit(const DropParams &d, int layer, int64_t row, int col) {
-  const uint64_t ctr = ((((d.step * 4u + (uint64_t)layer) << 20) + (uint64_t)row) << 8) + (uint64_t)col;
+  const uint64_t ctr = (((((uint64_t)(*d.step) * 4u + (uint64_t)layer) << 20) + (uint64_t)row) << 8) + (uint64_t)col;
   return (uint32_t)(splitmix_fin(d.seed + ctr * 0x9E3779B97F4A7C15ULL) >> 40) >= d.thr;
 }
 
@@ -420,8 +421,11 @@ __global__ void train_copy_scalar(const float *__restrict__ src, float *__restri
 // ------------------------------------------------------------------ AdamW (T5)
 
 __global__ void train_adamw(int64_t n, float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m,
-                            float *__restrict__ v, float lr, float wd, float b1, float b2, float eps, float bc1,
-                            float bc2) {
+                            float *__restrict__ v, float lr, float wd, float b1, float b2, float eps,
+                            const int64_t *__restrict__ step) {
+  // bias corrections 1 - beta^t in fp64 (t = the step being taken), rounded once
+  const double t = (double)(*step + 1);
+  const float bc1 = (float)(1.0 - pow((double)b1, t)), bc2 = (float)(1.0 - pow((double)b2, t));
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float gi = g[i];
@@ -431,6 +435,10 @@ __global__ void train_adamw(int64_t n, float *__restrict__ p, const float *__res
   v[i] = vi;
   const float mh = mi / bc1, vh = vi / bc2;
   p[i] = p[i] - lr * (wd * p[i] + mh / (sqrtf(vh) + eps));
+}
+
+__global__ void train_step_end(int64_t *step) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *step += 1;
 }
 
 // ------------------------------------------------------------------ normalisation fit (T7)
@@ -498,6 +506,7 @@ struct sp_trainer {
   int64_t ow[4] = {}, ob[4] = {}, og[3] = {}, obe[3] = {};
   DevBuf params, grads, mom1, mom2, running, norm, act, partial, scratch;
   float *bn_part = nullptr;  // BatchNorm chunk partials [5][64][256]
+  int64_t *dstep = nullptr;  // DEVICE step counter (dropout counter, AdamW t - 1)
   float *kpart = nullptr;    // split-K GEMM partials
   int64_t kpart_cap = 0;     // floats
   size_t partial_cap = 0;
@@ -518,10 +527,10 @@ sp_status check_features(sp_trainer *tr, const sp_features *in, const float *mea
   return SP_OK;
 }
 
-DropParams drop_params(const sp_trainer *tr, int64_t step) {
+DropParams drop_params(const sp_trainer *tr) {
   DropParams d;
   d.seed = tr->cfg.seed;
-  d.step = (uint64_t)step;
+  d.step = tr->dstep;
   d.thr = (uint32_t)std::llround((double)tr->cfg.dropout * 16777216.0);
   d.scale = 1.0f / (1.0f - tr->cfg.dropout);
   return d;
@@ -683,13 +692,16 @@ extern "C" sp_status sp_train_create(sp_ctx *ctx, const sp_mlp_desc *d, const sp
   tr->loss = take(4);
   // BatchNorm partials and split-K partials (no allocation inside a step)
   tr->kpart_cap = (int64_t)32 * 256 * 256;
-  e = cudaMalloc(&tr->scratch.p, ((size_t)5 * 64 * 256 + (size_t)tr->kpart_cap) * sizeof(float));
+  const size_t scratch_floats = (size_t)5 * 64 * 256 + (size_t)tr->kpart_cap;  // even: the step counter is 8-aligned
+  e = cudaMalloc(&tr->scratch.p, scratch_floats * sizeof(float) + sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemset(tr->scratch.p, 0, scratch_floats * sizeof(float) + sizeof(int64_t));
   if (e != cudaSuccess) {
     tr->scratch.p = nullptr;
     delete tr;
     return cuda_fail(ctx, e, "sp_train_create: scratch");
   }
   tr->bn_part = (float *)tr->scratch.p;
+  tr->dstep = reinterpret_cast<int64_t *>(tr->bn_part + scratch_floats);
   tr->kpart = tr->bn_part + (size_t)5 * 64 * 256;
   float *rs = (float *)tr->running.p;
   for (int l = 0, o = 0; l < 3; ++l) {
@@ -712,7 +724,7 @@ extern "C" sp_status sp_train_step(sp_trainer *tr, const sp_features *in, const 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const LaunchHook hk = tr->ctx->hook();
   const int b = (int)B, n_in = tr->n_in;
-  const DropParams dp = drop_params(tr, tr->step);
+  const DropParams dp = drop_params(tr);
   float *P = (float *)tr->params.p, *G = (float *)tr->grads.p;
   const float *mu = (const float *)tr->norm.p, *sg = mu + n_in;
 
@@ -745,14 +757,12 @@ extern "C" sp_status sp_train_step(sp_trainer *tr, const sp_features *in, const 
     if (l) gemm(tr, b, fan, w, tr->dzb, w, 1, P + tr->ow[l], fan, 1, nullptr, tr->dh, st, hk);
   }
   tr->step += 1;
-  const double t = (double)tr->step;
-  const float bc1 = (float)(1.0 - std::pow((double)tr->cfg.beta1, t));
-  const float bc2 = (float)(1.0 - std::pow((double)tr->cfg.beta2, t));
   hk.on_begin("train_adamw", st);
   train_adamw<<<(unsigned)((tr->n_params + 255) / 256), 256, 0, st>>>(
       tr->n_params, P, G, (float *)tr->mom1.p, (float *)tr->mom2.p, tr->cfg.lr, tr->cfg.weight_decay,
-      tr->cfg.beta1, tr->cfg.beta2, tr->cfg.adam_eps, bc1, bc2);
+      tr->cfg.beta1, tr->cfg.beta2, tr->cfg.adam_eps, tr->dstep);
   hk.on_end(st);
+  train_step_end<<<1, 32, 0, st>>>(tr->dstep);
   if (loss_out) train_copy_scalar<<<1, 32, 0, st>>>(tr->loss, loss_out);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(tr->ctx, e, "sp_train_step: launch");
@@ -782,7 +792,7 @@ extern "C" sp_status sp_train_eval(sp_trainer *tr, const sp_features *in, const 
   }
   const float *P = (const float *)tr->params.p;
   const float *mu = (const float *)tr->norm.p, *sg = mu + tr->n_in;
-  const DropParams dp = drop_params(tr, 0);
+  const DropParams dp = drop_params(tr);
   for (int64_t c = 0; c < chunks; ++c) {
     const int64_t r0 = c * tr->B, b = std::min<int64_t>(tr->B, n - r0);
     const int64_t ng = b * (tr->n_in + 1);

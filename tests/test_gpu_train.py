@@ -200,3 +200,27 @@ def test_training_reduces_validation_mape(sp, ctx, orc):
     v0 = float(tr.eval_loss(f, m_dev, va_idx).item())
     res = tr.fit(f, m_dev, tr_idx, va_idx, max_epochs=8, patience=3)
     assert res["best_val_loss"] < 0.5 * v0 and res["best_val_loss"] < 0.1, (v0, res["val_history"])
+
+
+def test_captured_step_graph_equals_eager_steps(sp, ctx, orc):
+    """A CUDA graph of sp_train_step replayed three times (the batch buffer refilled
+    in place) gives bitwise the same parameters as three eager steps: the step
+    counter, dropout masks and bias corrections advance on the device."""
+    b, sa, f, o, valid, measured = setup(sp, ctx, orc, family=gen.GEMM, n=150)
+    model = models.random_mlp(b.family, 35)
+    m_dev = dev(measured, np.float32)
+    rng = np.random.default_rng(2)
+    batches = [dev(rng.choice(valid, 128, replace=False), np.int64) for _ in range(3)]
+    eager = ctx.trainer(model, max_batch=128, seed=9)
+    for bi in batches:
+        eager.step(f, m_dev, bi)
+    tr = ctx.trainer(model, max_batch=128, seed=9)
+    buf = torch.empty(128, dtype=torch.int64, device="cuda")
+    g = tr.capture(f, m_dev, buf)
+    for bi in batches:
+        buf.copy_(bi)
+        g.replay()
+    torch.cuda.synchronize()
+    a, c = eager.export(), tr.export()
+    for k in T.PARAM_ORDER + ["m1", "v1", "m2", "v2", "m3", "v3"]:
+        assert np.array_equal(a[k], c[k]), k

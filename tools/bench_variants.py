@@ -111,8 +111,18 @@ def main():
         kst = ctx.profile_read(reset=True)
         ctx.set_profiling(False)
         ms_np = timed(run, args.reps) / len(batches)  # without the per-launch events
+        buf = torch.empty(B, dtype=torch.int64, device="cuda:0")
+        graph = tr.capture(f, meas, buf)
+
+        def run_graph():
+            for bi in batches:
+                buf.copy_(bi)
+                graph.replay()
+
+        ms_graph = timed(run_graph, args.reps) / len(batches)
         print(json.dumps({"variant": "train_step", "workload": "cfg3 features", "batch": B,
                           "ms_per_step": ms_np, "steps_per_s": 1e3 / ms_np, "samples_per_s": B * 1e3 / ms_np,
+                          "graph_ms_per_step": ms_graph, "graph_samples_per_s": B * 1e3 / ms_graph,
                           "tflops": flop * B / (ms_np * 1e-3) / 1e12,
                           "launches_per_step": sum(v[0] for v in kst.values()) / ((args.reps + 2) * len(batches)),
                           "kernels_ms_per_step": {k: v[1] / ((args.reps + 2) * len(batches)) for k, v in kst.items()}}),
