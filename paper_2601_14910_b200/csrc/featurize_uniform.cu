@@ -446,15 +446,14 @@ __global__ void __launch_bounds__(kThreads) uniform_prepass(int fam, ConfigView 
   if (c >= cfg.n_configs) return;
   const UniformCfg u = config_of(fam, cfg, c, fam == SP_FUSED_MOE ? &hist : nullptr);
   uint64_t *o = pre + c;
-  o[0] = (uint64_t)(uint32_t)u.status | ((uint64_t)u.range_bad << 8) | ((uint64_t)(u.tdt + 1) << 16);
-  o[1 * ldc] = (uint64_t)u.T;
+  o[0] = (uint64_t)(uint32_t)u.status | ((uint64_t)u.range_bad << 8) | ((uint64_t)(u.tdt + 1) << 16) |
+         ((uint64_t)(uint32_t)u.T << 32);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    o[(2 + q) * ldc] = (uint64_t)u.task[q];
-    o[(6 + q) * ldc] = (uint64_t)u.tot[q];
-  }
-  o[10 * ldc] = (uint64_t)u.fp.smem;
-  o[11 * ldc] = (uint64_t)(uint32_t)u.fp.warps | ((uint64_t)(uint32_t)u.fp.regs << 32);
+  for (int q = 0; q < 4; ++q) o[(1 + q) * ldc] = (uint64_t)u.task[q];
+  // smem clamped to 32 bits: anything above any SM's capacity gives the same zero quota
+  const uint64_t sm32 = u.fp.smem > 0xffffffffLL ? 0xffffffffull : (uint64_t)u.fp.smem;
+  o[5 * ldc] = sm32 | ((uint64_t)(uint32_t)u.fp.warps << 32);
+  o[6 * ldc] = (uint64_t)(uint32_t)u.fp.regs;
 }
 
 // ------------------------------------------------------------------ clamped edge tiles

@@ -539,12 +539,12 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
 // issuer and epilogue, with 8 producer warps in two groups that take alternate
 // tiles and derive each pair's record from its config pre-pass and spec.
 // Layout: as the kernel above up to H2 (raw staging: 2 groups x kFNR stages of
-// kPreFields u64 per row = the same 48 KB), then the producer -> epilogue side
+// kPreFields u64 per row = 42 KB of the 48 KB), then the producer -> epilogue side
 // ring (t_theory, status per row of kNS tiles) and the barriers.
 constexpr int kFProdWarps = 8;
 constexpr int kFMmaWarp = kEpiWarps + kFProdWarps;
 constexpr int kFThreads = (kFMmaWarp + 1) * 32;
-constexpr int kFNR = 2;
+constexpr int kFNR = 3;
 constexpr uint32_t kFRawBytes = kPreFields * kTile * 8;
 static_assert(2 * kFNR * kFRawBytes <= kNR * kRawBytes, "fused raw staging fits the unfused one");
 constexpr int kNS = 8;  // the producer of tile j + kNS waited for tile j + kNS - kNX's layer-1 MMA,
@@ -755,15 +755,16 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
           side_s = (uint32_t)st;
         } else {
           PairDemand d;
-          d.T = (int64_t)rj[kTile];
+          d.T = (int64_t)(w0 >> 32);
           const int64_t per_sm = (int64_t)(((uint32_t)d.T + (uint32_t)sp.num_sms - 1u) / (uint32_t)sp.num_sms);
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
-            d.tot[qq] = (int64_t)rj[(6 + qq) * kTile];
-            d.mx[qq] = per_sm * (int64_t)rj[(2 + qq) * kTile];
+            const int64_t task = (int64_t)rj[(1 + qq) * kTile];
+            d.tot[qq] = d.T * task;
+            d.mx[qq] = per_sm * task;
           }
-          const uint64_t wr = rj[11 * kTile];
-          const Footprint fp{(int64_t)rj[10 * kTile], (int64_t)(uint32_t)wr, (int64_t)(wr >> 32)};
+          const uint64_t ws = rj[5 * kTile];
+          const Footprint fp{(int64_t)(uint32_t)ws, (int64_t)(ws >> 32), (int64_t)(uint32_t)rj[6 * kTile]};
           float fv[kNumFlts];
           emit_pair(fz.out, p, d, fp, sp, family_pipes(FAM), tdt < 0 ? 0 : tdt, fv);
           side_s = 0;

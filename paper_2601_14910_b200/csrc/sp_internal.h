@@ -69,10 +69,10 @@ struct ConfigView {
 // Fused featurize -> predict (uniform families GEMM, fused MoE, RMSNorm,
 // SiLU&Mul, Scaled MM; SURVEY §8(b) "fused"): the spec-independent part of each
 // config, u64 SoA [kPreFields][ldc]:
-//   0 status | range_bad << 8 | (tensor dtype + 1) << 16    1 T
-//   2..5 per-task Tensor, FMA, XU ops, bytes                6..9 totals
-//   10 smem per task    11 warps | regs << 32
-constexpr int kPreFields = 12;
+//   0 status | range_bad << 8 | (tensor dtype + 1) << 16 | T << 32
+//   1..4 per-task Tensor, FMA, XU ops, bytes (totals = T x these; range-checked here)
+//   5 smem per task (clamped to 32 bits) | warps << 32      6 regs
+constexpr int kPreFields = 7;
 int launch_uniform_prepass(int family, const ConfigView &cfg, uint64_t *pre, int64_t ldc, void *stream);
 
 // Clamped edge tiles (NEXT-4), GEMM and fused MoE; warp per pair.
