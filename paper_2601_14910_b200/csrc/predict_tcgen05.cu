@@ -571,9 +571,10 @@ struct FusedParams {
 // partial tiles; the pre-pass stays in L2 anyway).  Returns false past the end.
 __device__ __forceinline__ bool fused_tile_pair(const FusedIn &fz, int64_t t, uint32_t row, int64_t &p, int64_t &c,
                                                 int &gs) {
-  if (fz.cmajor) {
-    const int64_t cb = t / fz.n_specs;
-    gs = (int)(t - cb * fz.n_specs);
+  if (fz.cmajor) {  // t < n_tiles < 2^31: 32-bit division (the 64-bit one was 5% of the kernel's instructions)
+    const uint32_t ns = (uint32_t)fz.n_specs, cb32 = (uint32_t)t / ns;
+    const int64_t cb = cb32;
+    gs = (int)((uint32_t)t - cb32 * ns);
     c = cb * kTile + row;
     p = (int64_t)gs * fz.C + c;
     return c < fz.C;
