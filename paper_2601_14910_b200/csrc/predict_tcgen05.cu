@@ -100,7 +100,7 @@ constexpr uint32_t kOffBar = kOffZx + 2 * kTile * 4;
 #endif
 // barriers: x_full[kNX] x_empty[kNX] d_full[2] a_ready[2] slot_free[2], then the TMEM base
 constexpr int kBarXFull = 0, kBarXEmpty = kNX, kBarDFull = 2 * kNX, kBarAReady = 2 * kNX + 2,
-              kBarSlotFree = 2 * kNX + 4, kNumBars = 2 * kNX + 6;
+              kBarSlotFree = 2 * kNX + 4, kBarRawFull = 2 * kNX + 6, kNumBars = 2 * kNX + 6 + kNR;
 constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
@@ -163,6 +163,7 @@ constexpr bool kNoMma = false;
 struct Params {
   MlpBf16 m;
   sp_features in;
+  int bulk;  // feature columns 16-byte aligned: full tiles arrive by TMA bulk copies
   float *latency;
   float *eff;
   int64_t n_tiles;
@@ -241,23 +242,50 @@ __device__ __forceinline__ void bias_to_tmem(uint32_t tmem_row, uint32_t c, cons
 
 // ---- producer: features of CTA tile j -> raw stage j % kNR (cp.async; each
 // thread copies, and later reads, only its own row: no barrier needed).
+// Raw stage layout: feature f of row r at byte f * kTile * 8 + r * 8 (int64 slots)
+// or f * kTile * 8 + r * 4 (fp32 slots: a column lands packed).  Full tiles of
+// an aligned record arrive by one TMA bulk copy per feature column (1 KB or
+// 512 B, issued by producer thread 0 on the stage's mbarrier); the tail tile and
+// unaligned records use per-row cp.async.  Returns whether tile j went by bulk.
 template <int FAM>
-__device__ __forceinline__ void produce_issue(const Params &P, int64_t j, int64_t n_local, uint32_t row,
-                                              uint32_t raw_base) {
+__device__ __forceinline__ bool produce_issue(const Params &P, int64_t j, int64_t n_local, uint32_t row,
+                                              uint32_t raw_base, uint32_t bar_raw0) {
+  bool bulk = false;
   if (j < n_local) {
     const int64_t t = blockIdx.x + j * (int64_t)gridDim.x;
-    int64_t p = t * kTile + row;
-    if (p >= P.in.n_pairs) p = 0;  // tail rows: harmless copy, output never stored
+    const int64_t p0 = t * kTile;
     const int64_t ld = P.in.ld;
-    const uint32_t dst = raw_base + (uint32_t)(j % kNR) * kRawBytes + row * 8;
+    const uint32_t stage = raw_base + (uint32_t)(j % kNR) * kRawBytes;
+    bulk = P.bulk && p0 + kTile <= P.in.n_pairs;
+    if (bulk) {
+      // every producer has read this stage's previous tile (consumed last iteration)
+      asm volatile("bar.sync 3, %0;" ::"n"(kProdWarps * 32) : "memory");
+      if (row == 0) {
+        const uint32_t mb = bar_raw0 + 8u * (uint32_t)(j % kNR);
+        uint32_t bytes = 0;
 #pragma unroll
-    for (int f = 0; f < n_in_of(FAM); ++f) {
-      const int sl = in_slot(FAM, f);
-      if (sl >= 16) cp_async4(dst + f * kTile * 8, P.in.flts + (int64_t)(sl - 16) * ld + p);
-      else cp_async8(dst + f * kTile * 8, P.in.ints + (int64_t)sl * ld + p);
+        for (int f = 0; f < n_in_of(FAM); ++f) bytes += in_slot(FAM, f) >= 16 ? kTile * 4 : kTile * 8;
+        tc::mbar_arrive_expect_tx(mb, bytes);
+#pragma unroll
+        for (int f = 0; f < n_in_of(FAM); ++f) {
+          const int sl = in_slot(FAM, f);
+          if (sl >= 16) tc::bulk_g2s(stage + f * kTile * 8, P.in.flts + (int64_t)(sl - 16) * ld + p0, kTile * 4, mb);
+          else tc::bulk_g2s(stage + f * kTile * 8, P.in.ints + (int64_t)sl * ld + p0, kTile * 8, mb);
+        }
+      }
+    } else {
+      int64_t p = p0 + row;
+      if (p >= P.in.n_pairs) p = 0;  // tail rows: harmless copy, output never stored
+#pragma unroll
+      for (int f = 0; f < n_in_of(FAM); ++f) {
+        const int sl = in_slot(FAM, f);
+        if (sl >= 16) cp_async4(stage + f * kTile * 8 + row * 4, P.in.flts + (int64_t)(sl - 16) * ld + p);
+        else cp_async8(stage + f * kTile * 8 + row * 8, P.in.ints + (int64_t)sl * ld + p);
+      }
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per tile
+  return bulk;
 }
 
 template <bool BF16, int FAM>
@@ -288,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       tc::mbar_init(bar(kBarAReady + s), 256);
       tc::mbar_init(bar(kBarSlotFree + s), 256);
     }
+    for (int i = 0; i < kNR; ++i) tc::mbar_init(bar(kBarRawFull + i), 1);
     tc::mbar_init_fence();
   }
   if (warp == kMmaWarp) tc::tmem_alloc<512>(tc::smem_u32(tmem_slot));
@@ -379,13 +408,20 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       na[f] = vec[kVNA + f];
       nc[f] = vec[kVNC + f];
     }
+    const uint32_t bar_raw0 = bar(kBarRawFull);
+    uint32_t bulk_bits = 0;  // bit k: tile j with j % kNR == k went by bulk copy
 #pragma unroll
-    for (int j = 0; j < kNR - 1; ++j) produce_issue<FAM>(P, j, n_local, row, raw_base);
+    for (int j = 0; j < kNR - 1; ++j)
+      bulk_bits |= (uint32_t)produce_issue<FAM>(P, j, n_local, row, raw_base, bar_raw0) << j;
     for (int64_t j = 0; j < n_local; ++j) {
-      produce_issue<FAM>(P, j + kNR - 1, n_local, row, raw_base);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kNR - 1) : "memory");  // tile j's copies landed
+      const int nx = (int)((j + kNR - 1) % kNR);
+      bulk_bits = (bulk_bits & ~(1u << nx)) |
+                  ((uint32_t)produce_issue<FAM>(P, j + kNR - 1, n_local, row, raw_base, bar_raw0) << nx);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kNR - 1) : "memory");  // tile j's cp.async copies landed
+      if (bulk_bits >> (j % kNR) & 1u) tc::mbar_wait(bar_raw0 + 8u * (uint32_t)(j % kNR), (uint32_t)(j / kNR) & 1u);
       // a10: x = (ln(1+v) - mu) / sigma = log2(1+v) * (ln2/sigma) - mu/sigma; x[15] = 1 (bias b1)
       const uint64_t *rj = raw + (size_t)(j % kNR) * (kRawBytes / 8) + row;
+      const float *rjf = reinterpret_cast<const float *>(raw + (size_t)(j % kNR) * (kRawBytes / 8)) + row;
       uint32_t xp[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -396,8 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
           if (f == 15) {
             x2[e] = 1.f;
           } else if (f < n_in_of(FAM)) {
-            const uint64_t u = rj[f * kTile];
-            const float v = in_slot(FAM, f) >= 16 ? __uint_as_float((uint32_t)u) : (float)(int64_t)u;
+            const float v = in_slot(FAM, f) >= 16 ? rjf[f * kTile * 2] : (float)(int64_t)rj[f * kTile];
             x2[e] = fmaf(lg2_ftz(1.f + v), na[f], nc[f]);
           } else {
             x2[e] = 0.f;
@@ -1011,6 +1046,7 @@ int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *laten
   Params P;
   P.m = m;
   P.in = in;
+  P.bulk = in.ld % 4 == 0 && ((uintptr_t)in.ints % 16) == 0 && ((uintptr_t)in.flts % 16) == 0;
   P.latency = latency;
   P.eff = eff;
   P.n_tiles = (in.n_pairs + kTile - 1) / kTile;
