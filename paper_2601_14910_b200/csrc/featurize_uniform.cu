@@ -41,6 +41,12 @@ __device__ __forceinline__ int32_t fld(const ConfigView &v, int k, int64_t c) {
   return __ldg(v.fields + (int64_t)k * v.ld + c);
 }
 
+// ceil(a/b) for 1 <= a, b < 2^31 (config fields and their products checked
+// below 2^31): one 32-bit division instead of the 64-bit software routine.
+__device__ __forceinline__ int64_t cdiv31(int64_t a, int64_t b) {
+  return (int64_t)(((uint32_t)a + (uint32_t)b - 1u) / (uint32_t)b);
+}
+
 __device__ __forceinline__ int64_t sat40(unsigned __int128 x) {
   const unsigned __int128 lim = (unsigned __int128)1 << 40;
   return (int64_t)(x > lim ? lim : x);
@@ -70,11 +76,11 @@ __device__ UniformCfg gemm_cfg(const ConfigView &v, int64_t c) {
   if (tm < 1 || tn < 1 || bk < 1 || stages < 1) { u.status = SP_PAIR_E_TILE; return u; }
   if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return u; }
   if (dt != SP_BF16 && dt != SP_FP16) { u.status = SP_PAIR_E_DTYPE; return u; }
-  const int64_t T = cdiv64(M, tm) * cdiv64(N, tn);
+  const int64_t T = cdiv31(M, tm) * cdiv31(N, tn);
   if (T > kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
   u.T = T;
   u.tdt = (int)dt;
-  const int64_t kpad = cdiv64(K, bk) * bk;
+  const int64_t kpad = cdiv31(K, bk) * bk;
   unsigned __int128 task[4] = {(unsigned __int128)(2 * tm * tn) * kpad, 0, 0,
                                (unsigned __int128)(tm + tn) * kpad * 2};
   finish_totals(u, task);
@@ -172,14 +178,14 @@ __device__ UniformCfg scaled_mm_cfg(const ConfigView &v, int64_t c) {
   if (tm < 1 || tn < 1 || bk < 1 || stages < 1) { u.status = SP_PAIR_E_TILE; return u; }
   if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return u; }
   if (dt != SP_FP8) { u.status = SP_PAIR_E_DTYPE; return u; }
-  const int64_t T = cdiv64(M, tm) * cdiv64(N, tn);
+  const int64_t T = cdiv31(M, tm) * cdiv31(N, tn);
   if (T > kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
   u.T = T;
   u.tdt = 2;
-  const int64_t kpad = cdiv64(K, bk) * bk, kb = cdiv64(K, 128);
+  const int64_t kpad = cdiv31(K, bk) * bk, kb = cdiv31(K, 128);
   unsigned __int128 task[4] = {(unsigned __int128)(2 * tm * tn) * kpad, 0, 0,
                                (unsigned __int128)(tm + tn) * kpad +
-                                   ((unsigned __int128)tm + (unsigned __int128)cdiv64(tn, 128)) * kb * 4};
+                                   ((unsigned __int128)tm + (unsigned __int128)cdiv31(tn, 128)) * kb * 4};
   finish_totals(u, task);
   u.fp.smem = smem > 0 ? smem : sat40((unsigned __int128)stages * (tm + tn) * bk);
   u.fp.warps = warps;
@@ -208,8 +214,8 @@ __device__ SplitKCfg splitk_cfg(const ConfigView &v, int64_t c) {
   if (tm < 1 || tn < 1 || bk < 1 || split < 1 || stages < 1) { u.status = SP_PAIR_E_TILE; return r; }
   if (warps < 1 || regs < 1 || smem < 0) { u.status = SP_PAIR_E_RES; return r; }
   if (dt != SP_BF16 && dt != SP_FP16) { u.status = SP_PAIR_E_DTYPE; return r; }
-  const int64_t kt = cdiv64(K, bk), kps = cdiv64(kt, split), slices = cdiv64(kt, kps);
-  const int64_t tiles = cdiv64(M, tm) * cdiv64(N, tn);  // <= 2^31 * 2^31 / 1: fits in int64
+  const int64_t kt = cdiv31(K, bk), kps = cdiv31(kt, split), slices = cdiv31(kt, kps);
+  const int64_t tiles = cdiv31(M, tm) * cdiv31(N, tn);  // <= 2^31 * 2^31 / 1: fits in int64
   if ((unsigned __int128)tiles * (unsigned __int128)slices > (unsigned __int128)kI32Max) {
     u.status = SP_PAIR_E_RANGE;
     return r;
@@ -268,14 +274,14 @@ __device__ UniformCfg moe_cfg(const ConfigView &v, int64_t c, const MoeHist *his
     if (sum != mt) { u.status = SP_PAIR_E_HIST; return u; }
     for (int64_t e = 0; e < E; ++e) mblocks += cdiv64(__ldg(h + e), bm);
   } else {
-    const int64_t q = mt / E, r = mt % E;
-    mblocks = (unsigned __int128)r * cdiv64(q + 1, bm) + (unsigned __int128)(E - r) * cdiv64(q, bm);
+    const int64_t q = (uint32_t)mt / (uint32_t)E, r = mt - q * E;  // mt < 2^31 (checked above)
+    mblocks = (unsigned __int128)r * cdiv31(q + 1, bm) + (unsigned __int128)(E - r) * cdiv31(q, bm);
   }
-  const unsigned __int128 T = mblocks * (unsigned __int128)cdiv64(N, bn);
+  const unsigned __int128 T = mblocks * (unsigned __int128)cdiv31(N, bn);
   if (T > (unsigned __int128)kI32Max) { u.status = SP_PAIR_E_RANGE; return u; }
   u.T = (int64_t)T;
   u.tdt = (int)dt;
-  const int64_t hpad = cdiv64(H, bk) * bk;
+  const int64_t hpad = cdiv31(H, bk) * bk;
   unsigned __int128 task[4] = {(unsigned __int128)(2 * bm * bn) * hpad, 0, 0,
                                (unsigned __int128)(bm + bn) * hpad * 2};
   finish_totals(u, task);
