@@ -731,15 +731,16 @@ class Context:
             return ~bad.any()
 
     def predict_host(self, batch, specs: Specs, model: Model, spec_range=None,
-                     out: np.ndarray | torch.Tensor | None = None, chunks=(1, 3, 3, 1),
+                     out: np.ndarray | torch.Tensor | None = None, chunks=None,
                      stream=None, _plan: bool = True) -> np.ndarray:
         """The user-facing call.  Host config arrays (numpy or torch; pinned
         memory gives asynchronous copies) -> H2D -> sp_featurize_predict (fused, or sp_featurize -> sp_predict)
         -> D2H of fp32 latencies in spec-major order [spec][config].
 
-        The configs are split into `chunks` slices (a count, or slice weights:
-        the default (1, 3, 3, 1) keeps the first slice's copy-in and the last
-        slice's copy-out short) pipelined over three streams: the H2D of slice i+1 and the D2H of slice i-1 overlap the
+        The configs are split into `chunks` slices (a count, or slice weights;
+        default: (1, 3, 3, 1) for attention, whose kernels outlast the copies --
+        a short first copy-in and last copy-out -- and 4 equal slices for the
+        copy-bound uniform families) pipelined over three streams: the H2D of slice i+1 and the D2H of slice i-1 overlap the
         kernels of slice i (the ragged request / histogram data is copied
         whole, ahead of the first slice).  Device buffers are cached across
         calls."""
@@ -764,6 +765,8 @@ class Context:
             out_t = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
         if n == 0:
             return out_t[:0].numpy()
+        if chunks is None:
+            chunks = (1, 3, 3, 1) if fam == _abi.SP_ATTENTION else 4
         weights = None
         if not isinstance(chunks, int):  # explicit slice weights, e.g. (1, 3, 3, 1)
             weights = [float(w) for w in chunks]

@@ -467,7 +467,8 @@ __global__ void __launch_bounds__(kThreads) uniform_prepass(int fam, ConfigView 
 // SPEC's clamped reading of edge tiles (the alternative to R2's
 // padded tiles): an edge tile computes and loads only its
 // in-range rows/columns, over the exact K (GEMM) or H (fused MoE).  Tasks are no
-// longer uniform, so the busiest SM is not ceil(T/N) tasks.  The task list is a
+// longer uniform, so the busiest SM is not ceil(T/N) tasks.  GEMM has a closed
+// form per SM (clamped_gemm_pair below).  For fused MoE the task list is a
 // sequence of runs of equal tasks (per output-tile row: nt-1 full-width tiles,
 // then the edge tile), and cyclic dealing sends a run [start, start+len) of
 // weight w to SM j  q*w + w*[(j - start) mod N < r]  times (q = len/N, r = len%N).
@@ -506,6 +507,81 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
   return v;
 }
 
+// GEMM clamped, closed form (no task list): with dh = tm - h_last, dw = tn - w_last,
+//   ops(t)   = 2K (tm tn - tm dw [last column] - dh tn [last row] + dh dw [corner])
+//   bytes(t) = K bpe (tm + tn - dw [last column] - dh [last row])
+// so SM s holds  cnt_s, C_s, R_s, K_s  tasks of the four indicator classes:
+//   cnt_s = all tasks (cyclic: q + [s < r]); R_s = the last row, a contiguous run;
+//   K_s = the corner (t = T-1); C_s = the last column, the progression
+//   (nt-1) + i nt, i < mt: with d = gcd(nt, N), P = N/d, residue s is hit iff
+//   d | s - (nt-1), by i = i0 + kP, i0 = ((s - (nt-1))/d) inv(nt/d mod P) mod P,
+//   that is mt/P + [i0 < mt mod P] times.
+// Lanes take SMs; O(N/32) per pair.  Exact (128-bit products).
+__device__ __forceinline__ uint32_t inv_mod(uint32_t a, uint32_t m) {  // gcd(a, m) = 1, m >= 1
+  if (m == 1) return 0;
+  int32_t t = 0, nt = 1;
+  uint32_t r = m, nr = a % m;
+  while (nr != 0) {
+    const uint32_t q = r / nr, r2 = r - q * nr;
+    const int32_t t2 = t - (int32_t)q * nt;
+    t = nt; nt = t2; r = nr; nr = r2;
+  }
+  return t < 0 ? (uint32_t)(t + (int32_t)m) : (uint32_t)t;
+}
+
+__device__ void clamped_gemm_pair(const ConfigView &v, int64_t c, const UniformCfg &u, const DevSpec &s,
+                                  const FeatOut &out, int64_t p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t M = fld(v, 0, c), Nn = fld(v, 1, c), K = fld(v, 2, c), tm = fld(v, 3, c), tn = fld(v, 4, c);
+  const int64_t bpe = bytes_per_elem((int)fld(v, 10, c));
+  const int64_t mt = cdiv31(M, tm), nt = cdiv31(Nn, tn), T = mt * nt;
+  const int64_t dh = tm - (M - (mt - 1) * tm), dw = tn - (Nn - (nt - 1) * tn);
+  typedef __int128 i128;
+  const i128 tot_ops = (i128)2 * K * M * Nn, tot_bytes = (i128)K * bpe * ((i128)nt * M + (i128)mt * Nn);
+  if (tot_ops > (i128)kI64Max || tot_bytes > (i128)kI64Max) {
+    if (lane == 0) emit_error(out, p, SP_PAIR_E_RANGE);
+    return;
+  }
+  // T < 2^31 (validated) and N <= 4096: 32-bit counts
+  const uint32_t N32 = (uint32_t)s.num_sms, T32 = (uint32_t)T, nt32 = (uint32_t)nt, mt32 = (uint32_t)mt;
+  const int64_t q = T32 / N32, r = T32 % N32;
+  const int64_t startR = (T32 - nt32) % N32, qR = nt32 / N32, rR = nt32 % N32;
+  uint32_t d32 = nt32, e32 = N32;  // gcd(nt, N)
+  while (e32 != 0) { const uint32_t t2 = d32 % e32; d32 = e32; e32 = t2; }
+  const uint32_t P32 = N32 / d32, invn = inv_mod((nt32 / d32) % P32, P32);
+  const int64_t a0 = (nt32 - 1u) % N32, qC = mt32 / P32, rC = mt32 % P32;
+  const int64_t sK = (T32 - 1u) % N32;
+  i128 best_o = -1, best_b = -1;
+  // 32-bit residue arithmetic: N <= 4096 (the clamped path's limit), so P^2 < 2^24
+  const uint32_t inv32 = invn;
+  const uint32_t sR = (uint32_t)startR, sA = (uint32_t)a0, rR32 = (uint32_t)rR, rC32 = (uint32_t)rC;
+  for (uint32_t sm = lane; sm < N32; sm += 32) {
+    const int64_t cnt = q + (sm < (uint32_t)r ? 1 : 0);
+    const int64_t Rs = qR + ((sm >= sR ? sm - sR : sm + N32 - sR) < rR32 ? 1 : 0);
+    const uint32_t diff = sm >= sA ? sm - sA : sm + N32 - sA;
+    const uint32_t dq = diff / d32;
+    int64_t Cs = 0;
+    if (dq * d32 == diff) Cs = qC + ((dq * inv32) % P32 < rC32 ? 1 : 0);
+    const int64_t Ks = sm == (uint32_t)sK ? 1 : 0;
+    const i128 o = (i128)2 * K * ((i128)tm * tn * cnt - (i128)tm * dw * Cs - (i128)dh * tn * Rs + (i128)dh * dw * Ks);
+    const i128 b = (i128)K * bpe * ((i128)(tm + tn) * cnt - (i128)dw * Cs - (i128)dh * Rs);
+    best_o = o > best_o ? o : best_o;
+    best_b = b > best_b ? b : best_b;
+  }
+  int64_t mo = (int64_t)best_o, mb = (int64_t)best_b;  // < 2^63: bounded by the totals
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mo = max(mo, (int64_t)__shfl_xor_sync(0xffffffffu, mo, o));
+    mb = max(mb, (int64_t)__shfl_xor_sync(0xffffffffu, mb, o));
+  }
+  if (lane != 0) return;
+  PairDemand dd;
+  dd.T = T;
+  dd.tot[0] = (int64_t)tot_ops; dd.tot[1] = 0; dd.tot[2] = 0; dd.tot[3] = (int64_t)tot_bytes;
+  dd.mx[0] = mo; dd.mx[1] = 0; dd.mx[2] = 0; dd.mx[3] = mb;
+  emit_pair(out, p, dd, u.fp, s, 1, u.tdt);
+}
+
 // One pair, whole warp.  D: this warp's 2*(N_max+1) int64 scratch.
 __device__ void clamped_pair(int fam, const ConfigView &v, int64_t c, const DevSpec &s, const FeatOut &out,
                              int64_t p, int64_t *D) {
@@ -515,20 +591,15 @@ __device__ void clamped_pair(int fam, const ConfigView &v, int64_t c, const DevS
     if (lane == 0) emit_error(out, p, u.status != 0 ? u.status : SP_PAIR_E_DTYPE);
     return;
   }
+  if (fam == SP_GEMM) {
+    clamped_gemm_pair(v, c, u, s, out, p);
+    return;
+  }
   const int N = s.num_sms;
   for (int i = lane; i < 2 * (N + 1); i += 32) D[i] = 0;
   __syncwarp();
   ClampRuns cr;
-  if (fam == SP_GEMM) {
-    const int64_t M = fld(v, 0, c), Nn = fld(v, 1, c), K = fld(v, 2, c), tm = fld(v, 3, c), tn = fld(v, 4, c);
-    const int64_t bpe = bytes_per_elem((int)fld(v, 10, c));
-    const int64_t mt = cdiv64(M, tm), nt = cdiv64(Nn, tn), wl = Nn - (nt - 1) * tn;
-    for (int64_t i = lane; i < mt; i += 32) {
-      const int64_t h = min(tm, M - i * tm), t0 = i * nt;
-      if (nt > 1) add_run(cr, D, N, t0, nt - 1, 2 * h * tn * K, (h + tn) * K * bpe);
-      add_run(cr, D, N, t0 + nt - 1, 1, 2 * h * wl * K, (h + wl) * K * bpe);
-    }
-  } else {  // fused MoE: expert-major, m-block, n-block
+  {  // fused MoE: expert-major, m-block, n-block
     const int64_t M = fld(v, 0, c), E = fld(v, 1, c), topk = fld(v, 2, c), H = fld(v, 3, c), Nn = fld(v, 4, c),
                   bm = fld(v, 5, c), bn = fld(v, 6, c);
     const int64_t bpe = bytes_per_elem((int)fld(v, 13, c));
