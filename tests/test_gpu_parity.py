@@ -480,7 +480,7 @@ def test_featurize_predict_equals_two_calls(sp, ctx, fam, prec):
         assert np.array_equal(e0.view(np.uint32), e1.view(np.uint32)), fam
 
 
-@pytest.mark.parametrize("cfg", ["cfg3", "cfg5"])
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg5", "scaledmm", "splitk"])
 def test_full_size_sampled_fused(sp, ctx, orc, cfg):
     """BASELINE configs 3 (1e6 fused-MoE configs x 11 GPUs) and 5 (1,000 serving
     GEMMs x 100,000 hypothetical specs = 1e8 pairs) at full size through
@@ -489,6 +489,10 @@ def test_full_size_sampled_fused(sp, ctx, orc, cfg):
     (ints bit-exact, floats 1e-5) and fp16 latencies (1e-2)."""
     if cfg == "cfg3":
         b, sa = gen.gen_moe(1_000_000, 1003), specs.paper_gpu_specs()
+    elif cfg == "scaledmm":  # bench --workload scaledmm (fused)
+        b, sa = gen.gen_scaled_mm(1_000_000, 1006), specs.paper_gpu_specs()
+    elif cfg == "splitk":  # bench --workload splitk (the two calls behind the same entry point)
+        b, sa = gen.gen_gemm_splitk(1_000_000, 1007), specs.paper_gpu_specs()
     else:
         b, sa = gen.gen_serving_gemms(1000, 1005), specs.hypothetical_sweep_specs(100_000)
     sh = ctx.load_gpu_specs(sa)
@@ -509,7 +513,7 @@ def test_full_size_sampled_fused(sp, ctx, orc, cfg):
     olat, _, _ = orc.predict(model, o)
     gl = lat[pt].cpu().numpy()
     ok = ~np.isnan(olat)
-    assert ok.mean() > 0.9 and np.array_equal(np.isnan(gl), ~ok)
+    assert ok.mean() > (0.6 if cfg == "scaledmm" else 0.9) and np.array_equal(np.isnan(gl), ~ok)
     np.testing.assert_allclose(gl[ok], olat[ok], rtol=LAT_RTOL_BF16)
     del f, lat
     torch.cuda.empty_cache()
