@@ -153,14 +153,15 @@ def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int =
     g0, g1 = spec_range
     total = (g1 - g0) * batch.n_configs
 
-    def run(n):
+    def run(n, threads=0):
         p = rng.integers(0, total, n)
         ci, si = p % batch.n_configs, g0 + p // batch.n_configs
         t = time.perf_counter()
-        f = O.featurize(batch, spec_arr, cfg_idx=ci, spec_idx=si)
-        O.predict(model, f)
+        f = O.featurize(batch, spec_arr, cfg_idx=ci, spec_idx=si, nthreads=threads)
+        O.predict(model, f, nthreads=threads)
         return time.perf_counter() - t
 
+    threads = O.num_threads()
     n = 256
     dt = run(n)
     while dt < 0.5 and n < 10_000_000:
@@ -168,7 +169,11 @@ def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int =
         dt = run(n)
     n = max(256, int(n * target_s / max(dt, 1e-6)))
     dt = run(n)
-    return n / dt, n, dt, O.num_threads()
+    # one core (SURVEY §8(d) asks for both): a sample sized for ~1/5 of the time budget
+    n1 = max(64, int(n / max(threads, 1) * 0.2))
+    dt1 = run(n1, 1)
+    run(64, threads)  # restore the OpenMP team size
+    return n / dt, n, dt, threads, n1 / dt1
 
 
 def oracle_e2e_rate(traces, sa, mlps, target_s: float, seed: int = 0):
@@ -212,7 +217,7 @@ def run_reference(args, rank, world):
 
     O.build()
     # size one step's sample from a calibration run
-    _, n_cal, dt_cal, threads = oracle_rate(b, sa, rng_, model, target_s=min(2.0, per_step), seed=1)
+    _, n_cal, dt_cal, threads, _ = oracle_rate(b, sa, rng_, model, target_s=min(2.0, per_step), seed=1)
     n_step = max(256, int(n_cal * per_step / max(dt_cal, 1e-6)))
     rng = np.random.default_rng(11)
     g0, g1 = rng_
@@ -415,10 +420,11 @@ def run_gpu(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, dt, thr = oracle_rate(b, sa, (g0, g1), model_d, target_s=args.cpu_seconds)
+        v, n, dt, thr, v1 = oracle_rate(b, sa, (g0, g1), model_d, target_s=args.cpu_seconds)
         line["cpu_baseline"] = {
             "value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
-            "sample": f"{n} random pairs of this workload, fp64 oracle featurize+predict, {dt:.1f} s"}
+            "sample": f"{n} random pairs of this workload, fp64 oracle featurize+predict, {dt:.1f} s",
+            "single_core_value": v1}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
