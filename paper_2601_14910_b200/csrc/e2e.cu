@@ -57,7 +57,7 @@ struct ExpandArgs {
   int32_t nh, nkv, hd, hidden, inter, vocab, qkv_n;
 };
 
-constexpr int kStepsPerWarp = 32;
+constexpr int kStepsPerWarp = 32;  // = lanes: lane j stores step j of the warp's chunk
 
 // E2 + E5: each warp expands kStepsPerWarp consecutive steps (one binary search
 // for the first step's trace, then a walk across trace boundaries).  Lanes hold
@@ -86,6 +86,9 @@ __global__ void __launch_bounds__(256) e2e_expand_kernel(ExpandArgs a) {
       out1 = lane + 32 < nb ? __ldg(a.out_len + b0 + lane + 32) : 0;
     };
     load_trace();
+    int32_t my_bs = 0;
+    bool my_pf = false;
+    int64_t my_roff = 0;
     for (int64_t s = s_first; s < s_last; ++s) {
       while (s >= t_end) {  // next trace (steps of a trace are contiguous; empty traces cannot occur)
         ++r;
@@ -130,26 +133,33 @@ __global__ void __launch_bounds__(256) e2e_expand_kernel(ExpandArgs a) {
         }
         bs = pos;
       }
-      if (lane < SP_NFIELDS_ATTENTION) {
-        const bool pf = k == 0;
-        int32_t v;
-        switch (lane) {
-          case 0: v = bs; break;                                        // BS
-          case 1: v = a.nh; break;                                      // NH
-          case 2: v = a.nkv; break;                                     // NKV
-          case 3: v = a.hd; break;                                      // HD
-          case 4: v = pf ? 128 : 16; break;                             // BQ
-          case 5: v = 64; break;                                        // BKV
-          case 6: v = pf ? 0 : ((int64_t)bs * a.nkv < 128 ? 1024 : 0); break;  // KV_CHUNK
-          case 7: v = pf ? 1 : 0; break;                                // CAUSAL
-          case 8: v = 4; break;                                         // WARPS
-          case 9: v = pf ? 168 : 64; break;                             // REGS
-          case 10: v = 0; break;                                        // SMEM (default footprint)
-          default: v = SP_BF16; break;                                  // DTYPE
-        }
-        a.attn_fields[(int64_t)lane * a.n_steps + s] = v;
+      if (lane == (int)(s - s_first)) {  // lane j keeps step s_first + j's fields for one coalesced store
+        my_bs = bs;
+        my_pf = k == 0;
+        my_roff = roff;
       }
-      if (lane == 0) a.attn_roff[s] = roff;
+    }
+    // the fields and ragged offsets of the warp's steps: row f, columns s_first..s_last-1
+    const int64_t s = s_first + lane;
+    if (s < s_last) {
+      const int32_t bs = my_bs;
+      const bool pf = my_pf;
+      int32_t v[SP_NFIELDS_ATTENTION] = {
+          bs,                                                   // BS
+          a.nh,                                                 // NH
+          a.nkv,                                                // NKV
+          a.hd,                                                 // HD
+          pf ? 128 : 16,                                        // BQ
+          64,                                                   // BKV
+          pf ? 0 : ((int64_t)bs * a.nkv < 128 ? 1024 : 0),      // KV_CHUNK
+          pf ? 1 : 0,                                           // CAUSAL
+          4,                                                    // WARPS
+          pf ? 168 : 64,                                        // REGS
+          0,                                                    // SMEM (default footprint)
+          SP_BF16};                                             // DTYPE
+#pragma unroll
+      for (int f = 0; f < SP_NFIELDS_ATTENTION; ++f) a.attn_fields[(int64_t)f * a.n_steps + s] = v[f];
+      a.attn_roff[s] = my_roff;
     }
   }
 }
