@@ -566,29 +566,55 @@ __device__ __forceinline__ u128 mul_le_i64(u128 a, u128 b, bool &bad) {
 }
 
 // One (config, spec) record from the accumulated per-distinct maxima.
-__device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const AttnCfg &a, int cfg_status,
-                                          int64_t L, uint64_t U, const DistinctMax &m, const DevSpec &s) {
-  if (cfg_status) { emit_error(out, p, cfg_status); return; }
-  const int tdt = (int)a.dt;
-  if (!s.tensor_ok[tdt]) { emit_error(out, p, SP_PAIR_E_DTYPE); return; }
-  const int64_t T = L * a.nkv;
+// Config-level part of a pair's record: T and the GPU totals (exact, 128-bit,
+// with the exact-range rule R22); identical for every spec of the config.
+struct AttnTotals {
+  int status;     // config status
+  int range_bad;  // a total >= 2^63 (reported after the spec's dtype check)
+  int64_t T;
+  int64_t tot[4];
+};
+
+__device__ __forceinline__ AttnTotals attn_totals(const AttnCfg &a, int cfg_status, int64_t L, uint64_t U) {
+  AttnTotals t{};
+  t.status = cfg_status;
+  if (cfg_status) return t;
+  t.T = L * a.nkv;
   const u128 Ua = (u128)U * (u128)a.nkv;  // < 2^63 (U < 2^32, nkv < 2^31)
   bool bad = false;
   const u128 totT = mul_le_i64((u128)4 * (u128)a.bq * (u128)a.hd * (u128)a.bkv, Ua, bad);
   const u128 totX = mul_le_i64((u128)a.bq * ((u128)a.bkv + 1), Ua, bad);
-  const u128 totB = mul_le_i64((u128)2 * (u128)a.hd, (u128)a.bq * (u128)T + (u128)2 * (u128)a.bkv * Ua, bad);
-  if (bad || totT > kI64Max || totX > kI64Max || totB > kI64Max) { emit_error(out, p, SP_PAIR_E_RANGE); return; }
+  const u128 totB = mul_le_i64((u128)2 * (u128)a.hd, (u128)a.bq * (u128)t.T + (u128)2 * (u128)a.bkv * Ua, bad);
+  t.range_bad = bad || totT > kI64Max || totX > kI64Max || totB > kI64Max;
+  t.tot[0] = (int64_t)totT;
+  t.tot[1] = 0;
+  t.tot[2] = (int64_t)totX;
+  t.tot[3] = (int64_t)totB;
+  return t;
+}
+
+// One pair: the spec-dependent checks in the oracle's order, the busiest-SM
+// demands from the distinct-N maxima, and the record.
+__device__ __forceinline__ void attn_emit_pair(const FeatOut &out, int64_t p, const AttnCfg &a, const AttnTotals &t,
+                                               const DistinctMax &m, const DevSpec &s) {
+  if (t.status) { emit_error(out, p, t.status); return; }
+  const int tdt = (int)a.dt;
+  if (!s.tensor_ok[tdt]) { emit_error(out, p, SP_PAIR_E_DTYPE); return; }
+  if (t.range_bad) { emit_error(out, p, SP_PAIR_E_RANGE); return; }
   PairDemand d;
-  d.T = T;
-  d.tot[0] = (int64_t)totT;
-  d.tot[1] = 0;
-  d.tot[2] = (int64_t)totX;
-  d.tot[3] = (int64_t)totB;
+  d.T = t.T;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) d.tot[q] = t.tot[q];
   d.mx[0] = (int64_t)4 * a.bq * a.hd * a.bkv * m.maxS;  // <= totT (maxS <= U*nkv)
   d.mx[1] = 0;
   d.mx[2] = (int64_t)a.bq * ((int64_t)a.bkv + 1) * m.maxS;
   d.mx[3] = (int64_t)2 * a.hd * m.maxB;
   emit_pair(out, p, d, a.fp, s, 5, tdt);
+}
+
+__device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const AttnCfg &a, int cfg_status,
+                                          int64_t L, uint64_t U, const DistinctMax &m, const DevSpec &s) {
+  attn_emit_pair(out, p, a, attn_totals(a, cfg_status, L, U), m, s);
 }
 
 // Whole per-config pipeline for one distinct set; per-distinct maxima go to
@@ -712,21 +738,38 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) attn_schedule_cross
 
 // Emit kernel (cross mode): thread per config, specs of the range in turn;
 // consecutive threads write consecutive records of one spec (full sectors).
+constexpr int kEmitSpecTile = 16;
+
+// Record writer of the cross path: thread per config, grid y over tiles of 16
+// specs staged in shared memory (with their distinct-N slots).  The config-level
+// totals are computed once per config; each spec then costs its dtype check, the
+// busiest-SM demands and the record store (pair p = j * C + c: a warp's stores
+// to every SoA row are 32 consecutive elements).
 __global__ void __launch_bounds__(256) attn_emit_cross(ConfigView cfg, const DevSpec *__restrict__ specs, int g0,
                                                        int n_specs, const int32_t *__restrict__ spec_slot,
                                                        AttnResults res, FeatOut out) {
+  __shared__ DevSpec s_spec[kEmitSpecTile];
+  __shared__ int32_t s_slot[kEmitSpecTile];
+  const int j0 = blockIdx.y * kEmitSpecTile, j1 = min(n_specs, j0 + kEmitSpecTile);
+  {
+    const int n_words = (j1 - j0) * (int)(sizeof(DevSpec) / 16);
+    const int4 *src = reinterpret_cast<const int4 *>(specs + g0 + j0);
+    int4 *dst = reinterpret_cast<int4 *>(s_spec);
+    for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = __ldg(src + i);
+    if (threadIdx.x < j1 - j0) s_slot[threadIdx.x] = __ldg(spec_slot + j0 + threadIdx.x);
+  }
+  __syncthreads();
   const int64_t C = cfg.n_configs;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const int st = __ldg(res.st + c);
   const AttnCfg al = st ? AttnCfg{} : load_cfg_lane(cfg, c);
-  const int64_t L = __ldg(res.L + c);
-  const uint64_t U = __ldg(res.U + c);
-  for (int j = 0; j < n_specs; ++j) {
-    const int64_t slot = __ldg(spec_slot + j);
+  const AttnTotals tt = attn_totals(al, st, st ? 0 : __ldg(res.L + c), st ? 0 : __ldg(res.U + c));
+  for (int j = j0; j < j1; ++j) {
+    const int64_t slot = s_slot[j - j0];
     DistinctMax m{0, 0};
     if (!st) m = DistinctMax{__ldg(res.mS + slot * res.ld + c), __ldg(res.mB + slot * res.ld + c)};
-    attn_emit(out, (int64_t)j * C + c, al, st, L, U, m, specs[g0 + j]);
+    attn_emit_pair(out, (int64_t)j * C + c, al, tt, m, s_spec[j - j0]);
   }
 }
 
@@ -1078,7 +1121,8 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
       if (e) return e;
       y = y1;
     }
-    const unsigned blocks = (unsigned)((cfg.n_configs + 255) / 256);
+    const dim3 blocks((unsigned)((cfg.n_configs + 255) / 256),
+                      (unsigned)((spec_end - spec_begin + kEmitSpecTile - 1) / kEmitSpecTile));
     hook.on_begin("attn_emit_cross", st);
     attn_emit_cross<<<blocks, 256, 0, st>>>(cfg, specs, spec_begin, spec_end - spec_begin, plan.spec_slot, res,
                                             out);
