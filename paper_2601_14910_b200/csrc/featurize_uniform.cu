@@ -140,12 +140,14 @@ __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c,
     for (int q = 0; q < 4; ++q) {
       if (jj[q] < 0) break;  // warp-uniform
       const uint32_t bmj = (uint32_t)__shfl_sync(0xffffffffu, bm, jj[q]);
+      FastDiv fbm;  // ceil(t_e / BM) by multiply-high: one division per config, not per count
+      fbm.init(bmj);
       int64_t sum = 0, mb = 0;
       int neg = 0;
       auto take = [&](int32_t te) {
         neg |= te < 0;
         sum += te;
-        mb += te > 0 ? ((uint32_t)te + bmj - 1u) / bmj : 0u;
+        mb += te > 0 ? fbm.div((uint32_t)te + bmj - 1u) : 0u;  // te, BM < 2^31: the sum fits 32 bits
       };
 #pragma unroll
       for (int r = 0; r < 4; ++r) take(t[q][r]);
