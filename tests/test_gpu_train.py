@@ -224,3 +224,27 @@ def test_captured_step_graph_equals_eager_steps(sp, ctx, orc):
     a, c = eager.export(), tr.export()
     for k in T.PARAM_ORDER + ["m1", "v1", "m2", "v2", "m3", "v3"]:
         assert np.array_equal(a[k], c[k]), k
+
+
+def test_training_argument_errors(sp, ctx, orc):
+    """The C-ABI refuses bad training arguments with SP_E_ARG / SP_E_DATA and
+    leaves the trainer usable."""
+    b, sa, f, o, valid, measured = setup(sp, ctx, orc, family=gen.GEMM, n=60)
+    model = models.random_mlp(b.family, 36)
+    with pytest.raises(sp.SynPerfError):
+        ctx.trainer(model, max_batch=1)                      # max_batch < 2
+    with pytest.raises(sp.SynPerfError):
+        ctx.trainer(model, loss="pinball", quantile=1.5)     # q outside (0, 1)
+    with pytest.raises(sp.SynPerfError):
+        ctx.trainer(dict(model, n_in=15))                    # Table IV width of another family
+    tr = ctx.trainer(model, max_batch=64)
+    m_dev = dev(measured, np.float32)
+    with pytest.raises(sp.SynPerfError):
+        tr.step(f, m_dev, dev(valid[:65], np.int64))         # B > max_batch
+    with pytest.raises(sp.SynPerfError):
+        tr.step(f, m_dev, dev(valid[:1], np.int64))          # B < 2
+    other = sp.Features.empty(gen.ATTENTION, f.n_pairs, ctx.torch_device)
+    with pytest.raises(sp.SynPerfError):
+        tr.step(other, m_dev, dev(valid[:8], np.int64))      # family mismatch
+    loss = float(tr.step(f, m_dev, dev(valid[:64], np.int64)).item())
+    assert np.isfinite(loss)
