@@ -818,11 +818,11 @@ class Context:
                 if ranges is not None and ranges[i][1] > ranges[i][0]:  # this slice's own ragged range
                     lo, hi = ranges[i]
                     cache["ragged"][lo:hi].copy_(rh[lo:hi], non_blocking=True)
+                if ranges is not None:  # on the copy stream: off the kernels' critical path
+                    oks.append(self._ragged_guard(fam, cache, c0, c1, ranges[i][0], ranges[i][1], s_h2d))
                 ev = torch.cuda.Event()
                 ev.record(s_h2d)
             comp.wait_event(ev)
-            if ranges is not None:
-                oks.append(self._ragged_guard(fam, cache, c0, c1, ranges[i][0], ranges[i][1], comp))
             db = DeviceBatch(fam, cache["fields"][:, c0:c1], cache["ragged"],
                              None if cache["roff"] is None else cache["roff"][c0:c1])
             feats = cache["feats"]
