@@ -202,5 +202,36 @@ def mlp_input(model: dict, ints_col: np.ndarray, flts_col: np.ndarray) -> np.nda
     return out[:n]
 
 
+def _round16(a: np.ndarray, kind: str) -> np.ndarray:
+    """Round fp64 values to bf16 or fp16, round-to-nearest-even, back to fp64."""
+    if kind == "fp16":
+        return np.asarray(a, np.float64).astype(np.float16).astype(np.float64)
+    u = np.asarray(a, np.float64).astype(np.float32).view(np.uint32)  # fp64 -> fp32 (RNE), then fp32 -> bf16 (RNE)
+    r = (u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) & np.uint32(0xFFFF0000)
+    return r.view(np.float32).astype(np.float64)
+
+
+def predict_emulated(model: dict, feats: OracleFeatures, kind: str = "bf16", idx=None):
+    """O12 --emulate-bf16: the O10-O11 MLP with every weight matrix
+    and each layer's input rounded to 16 bits (bf16 or fp16, RNE), accumulation
+    and BatchNorm in fp64.  Isolates operand rounding from accumulation order when
+    diagnosing the 16-bit GPU predictor.  Returns latency_us for pairs idx
+    (default all); NaN for pairs with status != 0."""
+    idx = np.arange(feats.status.shape[0]) if idx is None else np.asarray(idx)
+    x = np.stack([mlp_input(model, feats.ints[:, p], feats.flts[:, p]) for p in idx])
+    eps = float(model.get("bn_eps", 1e-5))
+    h = _round16(x, kind)
+    for l in (1, 2, 3):
+        a = h @ _round16(np.asarray(model[f"w{l}"], np.float64), kind).T + np.asarray(model[f"b{l}"], np.float64)
+        r = np.maximum(a, 0.0)
+        y = (np.asarray(model[f"g{l}"], np.float64) * (r - np.asarray(model[f"m{l}"], np.float64))
+             / np.sqrt(np.asarray(model[f"v{l}"], np.float64) + eps) + np.asarray(model[f"be{l}"], np.float64))
+        h = _round16(y, kind) if l < 3 else y  # layer 3 feeds the fp32 output layer
+    z = h @ np.asarray(model["w4"], np.float64) + float(model["b4"])
+    e = 1.0 / (1.0 + np.exp(-z))
+    lat = feats.flts[11][idx] / e
+    return np.where(feats.status[idx] == 0, lat, np.nan)
+
+
 def num_threads() -> int:
     return int(lib().orc_num_threads())

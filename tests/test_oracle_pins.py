@@ -641,3 +641,38 @@ def test_clamped_totals_are_exact_element_counts(orc):
     ok = o.status == 0
     M, tk, N, H = (mo.field(n).astype(np.int64) for n in ("M", "TOPK", "N", "H"))
     assert ok.any() and (o.ints[orc.INT_NAMES.index("tot_T")][ok] == (2 * M * tk * N * H)[ok]).all()
+
+
+def test_emulated_16bit_mlp(orc):
+    """O12 --emulate-bf16: the bf16 rounding helper rounds to
+    nearest even (1 + 2^-8 ties to 1, 1 + 3*2^-8 to 1 + 2^-6); the emulation
+    stays within a 16-bit envelope of the fp64 oracle; fp16 (10-bit mantissa)
+    lands closer than bf16 (7-bit); with weights already in bf16 and identity
+    BatchNorm only the layer-input rounding remains."""
+    from oracle.oracle import _round16
+    assert _round16(np.array([1 + 2.0 ** -8]), "bf16")[0] == 1.0
+    assert _round16(np.array([1 + 3 * 2.0 ** -8]), "bf16")[0] == 1 + 2.0 ** -6
+    b = gen.gen_gemm(40, 21)
+    o = orc.featurize(b, A100)
+    model = models.random_mlp(b.family, 4)
+    lat, _, _ = orc.predict(model, o)
+    em = orc.predict_emulated(model, o, "bf16")
+    ok = o.status == 0
+    rel = np.abs(em[ok] / lat[ok] - 1)
+    assert rel.max() < 0.1 and rel.max() > 0  # rounding visible, bounded
+    em16 = orc.predict_emulated(model, o, "fp16")
+    rel16 = np.abs(em16[ok] / lat[ok] - 1)
+    assert rel16.mean() < rel.mean()  # 10-bit mantissa beats 7-bit
+    # weights already bf16, BN identity, a single config whose inputs are exact: emulation == fp64 oracle
+    m2 = {k: (orc._round16(np.asarray(v, np.float64), "bf16").astype(np.float32) if k.startswith("w") else v)
+          for k, v in model.items()}
+    for l, w in zip((1, 2, 3), (256, 128, 64)):
+        m2[f"g{l}"] = np.ones(w, np.float32)
+        m2[f"be{l}"] = np.zeros(w, np.float32)
+        m2[f"m{l}"] = np.zeros(w, np.float32)
+        m2[f"v{l}"] = np.full(w, 1 - 1e-5, np.float32)
+    m2["bn_eps"] = np.float32(1e-5)
+    lat2, _, _ = orc.predict(m2, o)
+    em2 = orc.predict_emulated(m2, o, "bf16")
+    # only the layer inputs are rounded now: small, but not zero, deviation
+    assert np.nanmax(np.abs(em2[ok] / lat2[ok] - 1)) < 0.1
