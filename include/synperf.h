@@ -23,7 +23,8 @@
  *    the last warning) of a context.  There is no CPU fallback: without a
  *    usable sm_100 device, sp_create fails.
  *  - Readings of passages where the paper is silent or ambiguous are listed
- *    as R1..R22 in DESIGN.md §3 and cited below as such.
+ *    as R1..R25 (feature stage), E1..E9 (end-to-end composition) and T1..T9
+ *    (estimator training) in DESIGN.md §3, §3b and §3c, and cited below as such.
  */
 #ifndef SYNPERF_H_
 #define SYNPERF_H_
