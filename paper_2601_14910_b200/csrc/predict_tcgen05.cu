@@ -577,6 +577,11 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
 // kPreFields u64 per row = 42 KB of the 48 KB), then the producer -> epilogue side
 // ring (t_theory, status per row of kNS tiles) and the barriers.
 constexpr int kFProdWarps = 8;
+// Two producer groups take tiles j = gid (mod 2).  The X-ring parity wait of tile
+// j (phase of tile j - kNX) is unambiguous only if the same group produced tile
+// j - kNX (which itself waited for tile j - 2 kNX), so kNX must be a multiple of
+// the group count: a 3-group variant broke exactly this (a tile of stale X rows).
+static_assert(kNX % (kFProdWarps / 4) == 0, "X ring depth must be a multiple of the producer group count");
 constexpr int kFMmaWarp = kEpiWarps + kFProdWarps;
 constexpr int kFThreads = (kFMmaWarp + 1) * 32;
 constexpr int kFNR = 3;
