@@ -346,10 +346,14 @@ sp_status sp_featurize_sched(sp_ctx *ctx, const sp_config_batch *cfg, const sp_s
  *                    to the padded reading R2: an edge tile of a GEMM (fused
  *                    MoE) computes and loads only its in-range rows and columns,
  *                    ma x na over the exact K (H): Tensor 2*ma*na*K, bytes
- *                    (ma+na)*K*bpe.  Tasks are then non-uniform; the busiest SM
- *                    is found exactly (cyclic dealing of runs of equal tasks,
- *                    one warp per pair).  GEMM and fused MoE with SP_SCHED_RR
- *                    only (SP_E_UNSUPPORTED otherwise); <= 4096 SMs per spec.
+ *                    (ma+na)*K*bpe; an attention task only its qr in-range
+ *                    query rows over its exact kv length len: Tensor 4*qr*len*hd,
+ *                    XU qr*len + qr*ceil(len/BKV), bytes (qr + 2*len)*hd*bpe.
+ *                    Tasks are then non-uniform; the busiest SM is found exactly
+ *                    (GEMM: closed form per SM; MoE: runs of equal tasks;
+ *                    attention: every task walked; one warp per pair).  GEMM,
+ *                    fused MoE and attention with SP_SCHED_RR only
+ *                    (SP_E_UNSUPPORTED otherwise); <= 4096 SMs per spec.
  */
 #define SP_FEAT_CLAMPED 1u
 

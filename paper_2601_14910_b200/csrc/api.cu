@@ -350,17 +350,23 @@ extern "C" sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, co
   const DevSpec *ds = (const DevSpec *)specs->dev.p;
   int e;
   if (flags & SP_FEAT_CLAMPED) {
-    if (fam != SP_GEMM && fam != SP_FUSED_MOE)
-      return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_ex: clamped edge tiles are implemented for GEMM and fused MoE");
+    if (fam != SP_GEMM && fam != SP_FUSED_MOE && fam != SP_ATTENTION)
+      return fail(ctx, SP_E_UNSUPPORTED,
+                  "sp_featurize_ex: clamped edge tiles are implemented for GEMM, fused MoE and attention");
     if (scheduler != SP_SCHED_RR)
       return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_ex: clamped edge tiles use the cyclic (RR) scheduler");
     if (specs->max_sms > 4096) return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_ex: clamped mode supports <= 4096 SMs");
     const bool cross = pairs->kind == SP_PAIRS_CROSS;
     const LaunchHook h = ctx->hook();
-    h.on_begin("featurize_clamped", stream);
-    e = launch_featurize_clamped(fam, cv, ds, cross ? pairs->spec_begin : 0, specs->n, n_pairs,
-                                 cross ? nullptr : pairs->cfg_idx, cross ? nullptr : pairs->spec_idx, specs->max_sms,
-                                 fo, ctx->num_sms, stream);
+    h.on_begin(fam == SP_ATTENTION ? "attn_clamped" : "featurize_clamped", stream);
+    if (fam == SP_ATTENTION)
+      e = launch_attention_clamped(cv, ds, cross ? pairs->spec_begin : 0, specs->n, n_pairs,
+                                   cross ? nullptr : pairs->cfg_idx, cross ? nullptr : pairs->spec_idx,
+                                   specs->max_sms, fo, ctx->num_sms, stream);
+    else
+      e = launch_featurize_clamped(fam, cv, ds, cross ? pairs->spec_begin : 0, specs->n, n_pairs,
+                                   cross ? nullptr : pairs->cfg_idx, cross ? nullptr : pairs->spec_idx,
+                                   specs->max_sms, fo, ctx->num_sms, stream);
     h.on_end(stream);
   } else if (fam == SP_ATTENTION && scheduler != SP_SCHED_RR) {
     // sequential scheduler simulation: per-warp shared memory for the largest target set

@@ -1072,6 +1072,128 @@ int launch_nd(int nd, const ConfigView &cfg, const AttnPlan &plan, const AttnRes
   }
 }
 
+// ------------------------------------------------------------------ clamped edge tiles (attention)
+
+// SPEC's clamped reading applied to FA2 tasks (NEXT-4): a task
+// computes only its in-range query rows qr = min(BQ, rows - i BQ) over its
+// exact kv length len (no BKV padding): Tensor 4 qr len hd, XU qr len + qr
+// ceil(len/BKV), bytes (qr hd + 2 len hd) bpe.  Demands are no longer affine
+// in one unit count, so the head-rotation identity of the cross kernel does not
+// apply: a warp per pair walks every task (all kv-heads, in task order, lanes
+// over 32 q-blocks with a scan of their chunk counts for the task index) and
+// adds its demands to three per-SM arrays in shared memory (64-bit atomics:
+// exact in any order), then takes the totals and the per-quantity maxima.
+// O(T/32) per pair: a modelling variant.
+__device__ void attn_clamped_pair(const ConfigView &cfg, int64_t c, const DevSpec &sp, int64_t p,
+                                  unsigned long long *S, int lane, const FeatOut &out) {
+  AttnCfg a = load_cfg(cfg, c, lane);
+  if (a.status) {
+    if (lane == 0) emit_error(out, p, a.status);
+    return;
+  }
+  if (a.chunk == -1) a.chunk = plan_chunk(a, sp, lane);
+  const FastDiv fg = make_fd((uint32_t)a.g);
+  const int64_t L = count_tasks(a, lane, fg);
+  if (L > kI32Max || L * a.nkv > kI32Max) {
+    if (lane == 0) emit_error(out, p, SP_PAIR_E_RANGE);
+    return;
+  }
+  const int N = sp.num_sms;
+  const FastDiv fN = make_fd((uint32_t)N);
+  for (int i = lane; i < 3 * N; i += 32) S[i] = 0ull;
+  __syncwarp();
+  u128 tot[3] = {0, 0, 0};
+  uint64_t U = 0;
+  const uint64_t hd = (uint64_t)a.hd, bq = (uint64_t)a.bq, bkv = (uint64_t)a.bkv, bpe = 2;  // bf16/fp16 (validated)
+  uint32_t base = 0;  // index of the next task (< 2^31)
+  for (int32_t h = 0; h < a.nkv; ++h) {
+    for (int64_t b = 0; b < a.bs; ++b) {
+      const uint32_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
+      const uint64_t rows = (uint64_t)q * a.g, nqb = (rows + bq - 1) / bq;
+      for (uint64_t i0 = 0; i0 < nqb; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const bool act = i < nqb;
+        const uint32_t need = act ? kv_need(i, bq, rows, q, kv, a.causal != 0, fg) : 0u;
+        const uint32_t nch = !act ? 0u : (a.chunk > 0 ? (need + (uint32_t)a.chunk - 1u) / (uint32_t)a.chunk : 1u);
+        uint32_t incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t start = base + incl - nch;
+        base += __shfl_sync(0xffffffffu, incl, 31);
+        const uint64_t qr = act ? min(bq, rows - i * bq) : 0;
+        for (uint32_t cc = 0; cc < nch; ++cc) {
+          const uint64_t len = a.chunk > 0 ? min((uint64_t)a.chunk, (uint64_t)need - (uint64_t)cc * a.chunk) : need;
+          const uint64_t units = (len + bkv - 1) / bkv;
+          const uint64_t w[3] = {4 * qr * len * hd, qr * len + qr * units, (qr * hd + 2 * len * hd) * bpe};
+          const uint32_t j = fN.mod(start + cc);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            atomicAdd(S + k * N + j, (unsigned long long)w[k]);
+            tot[k] += w[k];
+          }
+          if (h == 0) U += units;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  U = warp_sum_u64(U);
+  int bad = 0;
+  int64_t T64[3], mx[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned long long lo = (unsigned long long)tot[k], hi = (unsigned long long)(tot[k] >> 64);
+    u128 t = 0;
+    for (int l = 0; l < 32; ++l)
+      t += ((u128)__shfl_sync(0xffffffffu, hi, l) << 64) | __shfl_sync(0xffffffffu, lo, l);
+    bad |= t > kI64Max;
+    T64[k] = (int64_t)t;
+    unsigned long long m = 0;
+    for (int jj = lane; jj < N; jj += 32) m = max(m, S[k * N + jj]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    mx[k] = (int64_t)m;
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  if (U > (uint64_t)kU32Max) { emit_error(out, p, SP_PAIR_E_RANGE); return; }  // validation order: before dtype
+  if (!sp.tensor_ok[a.dt]) { emit_error(out, p, SP_PAIR_E_DTYPE); return; }
+  if (bad) { emit_error(out, p, SP_PAIR_E_RANGE); return; }
+  PairDemand d;
+  d.T = L * a.nkv;
+  d.tot[0] = T64[0]; d.tot[1] = 0; d.tot[2] = T64[1]; d.tot[3] = T64[2];
+  d.mx[0] = mx[0]; d.mx[1] = 0; d.mx[2] = mx[1]; d.mx[3] = mx[2];
+  emit_pair(out, p, d, a.fp, sp, 5, a.dt);
+}
+
+__global__ void attn_clamped_kernel(ConfigView cfg, const DevSpec *__restrict__ specs, int g0, int n_specs,
+                                    int64_t n_pairs, const int64_t *__restrict__ cfg_idx,
+                                    const int32_t *__restrict__ spec_idx, int max_sms, FeatOut out) {
+  extern __shared__ unsigned long long s_acc[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  unsigned long long *S = s_acc + (size_t)warp * 3 * max_sms;
+  for (int64_t p = (int64_t)blockIdx.x * nw + warp; p < n_pairs; p += (int64_t)gridDim.x * nw) {
+    int64_t c;
+    int g;
+    if (cfg_idx) {
+      c = __ldg(cfg_idx + p);
+      g = __ldg(spec_idx + p);
+      if (c < 0 || c >= cfg.n_configs || g < 0 || g >= n_specs) {
+        if (lane == 0) emit_error(out, p, SP_PAIR_E_INDEX);
+        continue;
+      }
+    } else {
+      g = g0 + (int)(p / cfg.n_configs);
+      c = p - (int64_t)(g - g0) * cfg.n_configs;
+    }
+    attn_clamped_pair(cfg, c, specs[g], p, S, lane, out);
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 int launch_attention_sim(int mode, const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
@@ -1154,6 +1276,23 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
   featurize_attention_list<<<(unsigned)(want < cap ? want : cap), kWarps * 32, smem, st>>>(
       cfg, specs, n_specs, words, n_pairs, cfg_idx, spec_idx, out);
   hook.on_end(st);
+  return (int)cudaGetLastError();
+}
+
+int launch_attention_clamped(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
+                             int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx, int max_sms,
+                             const FeatOut &out, int num_device_sms, void *stream) {
+  if (n_pairs == 0) return 0;
+  const size_t per_warp = (size_t)3 * max_sms * sizeof(unsigned long long);
+  const int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp));
+  const size_t smem = per_warp * warps;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(attn_clamped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const int64_t blocks = std::min<int64_t>((n_pairs + warps - 1) / warps, (int64_t)num_device_sms * 16);
+  attn_clamped_kernel<<<(unsigned)blocks, 32 * warps, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      cfg, specs, spec_begin, n_specs, n_pairs, cfg_idx, spec_idx, max_sms, out);
   return (int)cudaGetLastError();
 }
 

@@ -76,6 +76,10 @@ constexpr int kPreFields = 7;
 int launch_uniform_prepass(int family, const ConfigView &cfg, uint64_t *pre, int64_t ldc, void *stream);
 
 // Clamped edge tiles (NEXT-4), GEMM and fused MoE; warp per pair.
+// Clamped edge tiles for attention (NEXT-4): warp per pair, every task walked.
+int launch_attention_clamped(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
+                             int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx, int max_sms,
+                             const FeatOut &out, int num_device_sms, void *stream);
 int launch_featurize_clamped(int family, const ConfigView &cfg, const DevSpec *specs, int spec_begin, int n_specs,
                              int64_t n_pairs, const int64_t *cfg_idx, const int32_t *spec_idx, int max_sms,
                              const FeatOut &out, int num_device_sms, void *stream);

@@ -376,7 +376,7 @@ def test_predict_host_wide_spec_axis(sp, ctx, fam):
 
 # ------------------------------------------------------------- clamped edge tiles (SP_FEAT_CLAMPED, NEXT-4)
 
-@pytest.mark.parametrize("fam", ["gemm", "moe"])
+@pytest.mark.parametrize("fam", ["gemm", "moe", "attention"])
 def test_clamped_parity(sp, ctx, orc, fam):
     """Clamped edge tiles vs the oracle's CLAMPED flag: CROSS over Table VI and
     the odd SM counts, and a LIST with out-of-range indices."""
@@ -403,8 +403,8 @@ def test_clamped_parity(sp, ctx, orc, fam):
 
 def test_clamped_edge_cases(sp, ctx, orc):
     """Single tile, exact multiples (clamped = padded when K is a multiple of BK),
-    one row of tiles, huge M (many rows), and the golden MoE case; unsupported
-    families / schedulers are refused."""
+    one row of tiles, huge M (many rows), and the golden MoE case; row-wise
+    families and non-RR schedulers are refused."""
     cols = {k: [] for k in gen.FIELDS[gen.GEMM]}
 
     def add(**kw):
@@ -436,10 +436,10 @@ def test_clamped_edge_cases(sp, ctx, orc):
     ctx.featurize(sp.DeviceBatch.from_host(mb, ctx.torch_device), ctx.load_gpu_specs(s3), f, clamped=True)
     gi, _, gs = sp.features_to_host(f)
     assert gs[0] == 0 and (gi[6, 0], gi[10, 0], gi[3, 0], gi[9, 0]) == (g["max_T"], g["bytes_max"], g["tot_T"], g["bytes"])
-    att = FAMILY_BATCHES["attention"]()
-    fa = sp.Features.empty(att.family, len(sa) * att.n_configs, ctx.torch_device)
-    with pytest.raises(sp.SynPerfError):
-        ctx.featurize(sp.DeviceBatch.from_host(att, ctx.torch_device), sh, fa, clamped=True)
+    rms = FAMILY_BATCHES["rmsnorm"]()
+    fr = sp.Features.empty(rms.family, len(sa) * rms.n_configs, ctx.torch_device)
+    with pytest.raises(sp.SynPerfError):  # row-wise kernels have no edge tiles
+        ctx.featurize(sp.DeviceBatch.from_host(rms, ctx.torch_device), sh, fr, clamped=True)
     f = sp.Features.empty(b.family, len(sa) * b.n_configs, ctx.torch_device)
     with pytest.raises(sp.SynPerfError):
         ctx.featurize(db, sh, f, clamped=True, scheduler="greedy")
@@ -517,3 +517,36 @@ def test_full_size_sampled_fused(sp, ctx, orc, cfg):
     np.testing.assert_allclose(gl[ok], olat[ok], rtol=LAT_RTOL_BF16)
     del f, lat
     torch.cuda.empty_cache()
+
+
+def test_clamped_attention_edge_cases(sp, ctx, orc):
+    """Clamped attention: partial last q-blocks, causal + split-KV, the split-KV
+    planner (-1), decode, GQA packing, kv shorter than BKV, and domain errors."""
+    cols = {k: [] for k in gen.FIELDS[gen.ATTENTION]}
+    rag, off = [], []
+
+    def add(reqs, **kw):
+        d = dict(NH=8, NKV=2, HD=128, BQ=64, BKV=64, KV_CHUNK=0, CAUSAL=1, WARPS=4, REGS=128, SMEM=0, DTYPE=0)
+        d.update(kw)
+        d["BS"] = len(reqs)
+        for k in cols:
+            cols[k].append(d[k])
+        off.append(len(rag))
+        for q, kv in reqs:
+            rag.extend([q, kv])
+
+    add([(100, 100)])                                   # partial q-blocks, causal
+    add([(300, 5000), (77, 2000)], KV_CHUNK=512)        # causal + split-KV
+    add([(1, 4000), (1, 300)], BQ=16, CAUSAL=0, KV_CHUNK=-1)   # planner
+    add([(1, 20)] * 9, BQ=16, CAUSAL=0)                 # decode, kv < BKV
+    add([(33, 40)], NH=32, NKV=2)                       # GQA group 16
+    add([(5, 3)])                                       # causal with kv < q: status 5
+    b = gen.make_batch(gen.ATTENTION, cols, rag, off)
+    sa = np.concatenate([odd_specs(), specs.paper_gpu_specs()])
+    sh = ctx.load_gpu_specs(sa)
+    f = sp.Features.empty(b.family, len(sa) * b.n_configs, ctx.torch_device)
+    ctx.featurize(sp.DeviceBatch.from_host(b, ctx.torch_device), sh, f, clamped=True)
+    torch.cuda.synchronize()
+    o = orc.featurize(b, sa, flags=orc.CLAMPED)
+    assert (o.status == 0).sum() > 0 and (o.status == 5).any()
+    assert_feature_parity(sp.features_to_host(f), o, "clamped attention edges")

@@ -1,8 +1,8 @@
 """Throughput of the §8(f) variants on one B200 (one JSON line each):
   * sp_featurize_sched GREEDY / MINHEAP on a slice of BASELINE config 2
     (attention x 11 GPUs; sequential scheduler simulation, warp per pair);
-  * sp_featurize_ex SP_FEAT_CLAMPED (clamped edge tiles) vs the padded closed
-    form, GEMM and fused MoE x 11 GPUs;
+  * sp_featurize_ex SP_FEAT_CLAMPED (clamped edge tiles) vs the padded path,
+    GEMM, fused MoE and attention x 11 GPUs;
   * sp_perf_gap (P80 gap diagnosis) over BASELINE config 3 (fused MoE x 11,
     the paper applies it to its fused-MoE dataset);
   * sp_train_step (on-GPU estimator training, NEXT-4) on config-3 features at
@@ -61,7 +61,8 @@ def main():
                           "ms": ms, "pairs_per_s": n / (ms * 1e-3)}), flush=True)
     # ---- clamped edge tiles (SP_FEAT_CLAMPED): GEMM (config-1 shapes) and fused MoE (config 3), x 11 GPUs
     from workloads import gen, specs as wspecs
-    for name, bb in (("gemm 1e5 x 11", gen.gen_gemm(100_000, 1001)), ("cfg3 x0.1", bench.build_workload("cfg3", 0, 1, 0.1)[0])):
+    for name, bb in (("gemm 1e5 x 11", gen.gen_gemm(100_000, 1001)), ("cfg3 x0.1", bench.build_workload("cfg3", 0, 1, 0.1)[0]),
+                     ("cfg2 x0.02", bench.build_workload("cfg2", 0, 1, 0.02)[0])):
         sa2 = wspecs.paper_gpu_specs()
         sh2 = ctx.load_gpu_specs(sa2)
         db2 = sp.DeviceBatch.from_host(bb, "cuda:0")
