@@ -327,8 +327,9 @@ sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *
  *                    task goes to the worker with the least accumulated busy time.
  * Busy time of a task = max over the family's pipes of ops_p / Th_p;
  * ties go to the lowest SM / worker index.  For the uniform-task
- * families (GEMM, fused MoE, RMSNorm, SiLU&Mul) all three give the cyclic
- * partition, so they share the closed form.  Attention under GREEDY / MINHEAP
+ * families (GEMM, fused MoE, RMSNorm, SiLU&Mul, Scaled MM) all three give the
+ * cyclic partition, so they share the closed form.  Split-K GEMM (two task
+ * sizes, R25) supports SP_SCHED_RR only (SP_E_UNSUPPORTED otherwise).  Attention under GREEDY / MINHEAP
  * is simulated task by task (one warp per pair): exact, but ~100x slower than
  * SP_SCHED_RR; SP_E_UNSUPPORTED if the scheduler state of the spec range
  * (N_SM, or N_SM x max CTAs/SM, 12 bytes each) exceeds a warp's shared memory.

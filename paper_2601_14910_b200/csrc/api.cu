@@ -368,6 +368,9 @@ extern "C" sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, co
                                    cross ? nullptr : pairs->cfg_idx, cross ? nullptr : pairs->spec_idx,
                                    specs->max_sms, fo, ctx->num_sms, stream);
     h.on_end(stream);
+  } else if (fam == SP_GEMM_SPLITK && scheduler != SP_SCHED_RR) {
+    // split-K tasks come in two sizes (R25): GREEDY / MINHEAP would not reduce to the cyclic closed form
+    return fail(ctx, SP_E_UNSUPPORTED, "sp_featurize_sched: split-K GEMM supports the cyclic (RR) scheduler only");
   } else if (fam == SP_ATTENTION && scheduler != SP_SCHED_RR) {
     // sequential scheduler simulation: per-warp shared memory for the largest target set
     const bool cross = pairs->kind == SP_PAIRS_CROSS;

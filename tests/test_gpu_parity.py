@@ -156,6 +156,19 @@ def test_attention_edge_cases(sp, ctx, orc):
     assert_feature_parity(g, o, "attention edges")
 
 
+def test_splitk_refuses_non_cyclic_schedulers(sp, ctx):
+    """Split-K tasks come in two sizes, so GREEDY / MINHEAP do not reduce to the
+    cyclic closed form: the call is refused rather than answered with RR."""
+    b = FAMILY_BATCHES["gemm_splitk"]().subset(np.arange(50))
+    sa = specs.paper_gpu_specs()
+    sh = ctx.load_gpu_specs(sa)
+    db = sp.DeviceBatch.from_host(b, ctx.torch_device)
+    f = sp.Features.empty(b.family, len(sa) * b.n_configs, ctx.torch_device)
+    for sched in ("greedy", "minheap"):
+        with pytest.raises(sp.SynPerfError):
+            ctx.featurize(db, sh, f, scheduler=sched)
+
+
 def test_splitk_edge_cases(sp, ctx, orc):
     """Split-K: the hand-derived golden cases (wrapping / disjoint task classes,
     empty slices), SPLIT_K far above the k-tile count, a single k-tile, one
