@@ -59,8 +59,10 @@ typedef enum sp_pair_status {
   SP_PAIR_E_CAUSAL = 5,  /* causal attention request with kvlen < qlen */
   SP_PAIR_E_RES = 6,     /* warps < 1, regs < 1 or smem < 0 */
   SP_PAIR_E_DTYPE = 7,   /* dtype not supported by the family, or spec lacks that tensor rate */
-  SP_PAIR_E_RANGE = 8,   /* outside the exact range: T >= 2^31, a total >= 2^63, per-kv-head
-                            sum kv_eff/BKV >= 2^32, M*topk >= 2^31 or qlen*g >= 2^31 (R22) */
+  SP_PAIR_E_RANGE = 8,   /* a total >= 2^63 (does not fit the int64 record, R22), or past the
+                            kernels' 32-bit working range: T >= 2^31, per-kv-head sum
+                            kv_eff/BKV >= 2^32, M*topk >= 2^31 or qlen*g >= 2^31 (an
+                            implementation limit, not the paper's: the oracle answers there) */
   SP_PAIR_E_INDEX = 9    /* SP_PAIRS_LIST entry with a config or spec index out of range */
 } sp_pair_status;
 

@@ -65,6 +65,9 @@ def lib():
                                            C.c_void_p]
         L.orc_mlp_input.restype = C.c_int
         L.orc_mlp_input.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_count.restype = C.c_int
+        L.orc_count.argtypes = [C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                C.c_void_p]
         L.orc_num_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -126,6 +129,20 @@ def task_list(batch, c: int = 0, flags: int = 0, cap: int = 1 << 20) -> np.ndarr
     if n < 0:
         raise ValueError(f"config rejected with status {-n}")
     return out[:n].copy()
+
+
+def count(batch, c: int = 0) -> tuple[int, int, int]:
+    """(status, T, U) of config c: its task count and, for attention, the
+    per-kv-head sum of kv_eff/BKV, as the oracle's domain check counts them
+    (no 32-bit limit; saturated counts read as 2^63 - 1)."""
+    fields = np.ascontiguousarray(batch.fields, dtype=np.int32)
+    rag = None
+    if batch.ragged_off is not None and batch.ragged_off[c] >= 0:
+        rag = np.ascontiguousarray(batch.ragged[batch.ragged_off[c]:], dtype=np.int32)
+    T = C.c_int64(0)
+    U = C.c_int64(0)
+    st = lib().orc_count(batch.family, _ptr(fields), fields.shape[1], c, _ptr(rag), C.byref(T), C.byref(U))
+    return int(st), int(T.value), int(U.value)
 
 
 def schedule_rr(n_tasks: int, n_sm: int) -> np.ndarray:

@@ -97,8 +97,6 @@ enum { I_NTASKS, I_OCC, I_WAVES, I_TOT_T, I_TOT_F, I_TOT_X, I_MAX_T, I_MAX_F, I_
 enum { F_CG_T, F_CG_F, F_CG_X, F_CS_T, F_CS_F, F_CS_X, F_GLOB_G, F_L2_G, F_GLOB_S, F_L2_S,
        F_SMEM_S, F_TTHEORY, N_F };
 
-#define INT32_LIM 2147483647LL
-#define UINT32_LIM 4294967295LL
 #define INT64_LIM 9223372036854775807LL
 
 /* Demands are accumulated in 128-bit integers so that the exact-range rule
@@ -304,30 +302,25 @@ static int is_tensor_family(int fam) {
   return fam == FAM_GEMM || fam == FAM_ATTENTION || fam == FAM_MOE || fam == FAM_SCALED || fam == FAM_SPLITK;
 }
 
-/* Validates one config; also computes its task count T (int64) and, for
- * attention, the per-kv-head kv-unit sum, to enforce the documented exact
- * range (T < 2^31, per-head sum of kv_eff/BKV < 2^32).  Returns a status. */
-static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_out) {
+/* Validates one config against the paper's domain (every dimension >= 1,
+ * heads divisible, causal kv >= q, a histogram summing to M*topk, ...) and
+ * counts its tasks T and, for attention, the per-kv-head kv-unit sum
+ * U = sum of kv_eff/BKV over one head's tasks (tests compare them with the
+ * GPU's exact-range limits).  The oracle itself has no 32-bit limit: it
+ * enumerates whatever the config defines (R22: only a count that does not fit
+ * the int64 record is out of range, decided after the enumeration).
+ * Counts saturate at SAT128.  Returns a status. */
+static int validate(int fam, const int64_t *x, const int32_t *rag, i128 *T_out, i128 *U_out) {
   *T_out = 0;
+  *U_out = 0;
   switch (fam) {
-    case FAM_SCALED: {
+    case FAM_SCALED: case FAM_GEMM: {
       if (x[G_M] < 1 || x[G_N] < 1 || x[G_K] < 1) return ST_DIM;
       if (x[G_TM] < 1 || x[G_TN] < 1 || x[G_BK] < 1 || x[G_STAGES] < 1) return ST_TILE;
       if (x[G_WARPS] < 1 || x[G_REGS] < 1 || x[G_SMEM] < 0) return ST_RES;
-      if (x[G_DTYPE] != DT_FP8) return ST_DTYPE;
-      int64_t T = cdiv(x[G_M], x[G_TM]) * cdiv(x[G_N], x[G_TN]);
-      if (T > INT32_LIM) return ST_RANGE;
-      *T_out = T;
-      return ST_OK;
-    }
-    case FAM_GEMM: {
-      if (x[G_M] < 1 || x[G_N] < 1 || x[G_K] < 1) return ST_DIM;
-      if (x[G_TM] < 1 || x[G_TN] < 1 || x[G_BK] < 1 || x[G_STAGES] < 1) return ST_TILE;
-      if (x[G_WARPS] < 1 || x[G_REGS] < 1 || x[G_SMEM] < 0) return ST_RES;
-      if (x[G_DTYPE] != DT_BF16 && x[G_DTYPE] != DT_FP16) return ST_DTYPE;
-      int64_t T = cdiv(x[G_M], x[G_TM]) * cdiv(x[G_N], x[G_TN]);
-      if (T > INT32_LIM) return ST_RANGE;
-      *T_out = T;
+      if (fam == FAM_SCALED ? x[G_DTYPE] != DT_FP8 : (x[G_DTYPE] != DT_BF16 && x[G_DTYPE] != DT_FP16))
+        return ST_DTYPE;
+      *T_out = (i128)cdiv(x[G_M], x[G_TM]) * cdiv(x[G_N], x[G_TN]);
       return ST_OK;
     }
     case FAM_SPLITK: {
@@ -336,9 +329,7 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
       if (x[K_WARPS] < 1 || x[K_REGS] < 1 || x[K_SMEM] < 0) return ST_RES;
       if (x[K_DTYPE] != DT_BF16 && x[K_DTYPE] != DT_FP16) return ST_DTYPE;
       int64_t kt = cdiv(x[K_K], x[K_BK]), slices = cdiv(kt, cdiv(kt, x[K_SPLIT]));
-      i128 T = (i128)slices * cdiv(x[K_M], x[K_TM]) * cdiv(x[K_N], x[K_TN]);
-      if (T > INT32_LIM) return ST_RANGE;
-      *T_out = (int64_t)T;
+      *T_out = (i128)slices * cdiv(x[K_M], x[K_TM]) * cdiv(x[K_N], x[K_TN]);
       return ST_OK;
     }
     case FAM_MOE: {
@@ -347,7 +338,6 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
       if (x[E_WARPS] < 1 || x[E_REGS] < 1 || x[E_SMEM] < 0) return ST_RES;
       if (x[E_DTYPE] != DT_BF16 && x[E_DTYPE] != DT_FP16) return ST_DTYPE;
       int64_t mt = x[E_M] * x[E_TOPK];
-      if (mt > INT32_LIM) return ST_RANGE;
       i128 T = 0;
       if (rag) {
         int64_t sum = 0;
@@ -361,9 +351,7 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
         int64_t q = mt / x[E_E], r = mt % x[E_E];
         T = (i128)r * cdiv(q + 1, x[E_BM]) + (i128)(x[E_E] - r) * cdiv(q, x[E_BM]);
       }
-      T *= cdiv(x[E_N], x[E_BN]);
-      if (T > INT32_LIM) return ST_RANGE;
-      *T_out = (int64_t)T;
+      *T_out = T * cdiv(x[E_N], x[E_BN]);
       return ST_OK;
     }
     case FAM_RMSNORM: case FAM_SILU: {
@@ -384,13 +372,12 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
         int64_t qlen = rag[2 * b], kvlen = rag[2 * b + 1];
         if (qlen < 1 || kvlen < 1) return ST_DIM;
         if (x[A_CAUSAL] && kvlen < qlen) return ST_CAUSAL;
-        if (qlen * g > INT32_LIM) return ST_RANGE;
       }
       /* per-head task count L and kv-unit sum U, counted item by item */
-      int64_t L = 0, U = 0;
+      i128 L = 0, U = 0;
       for (int64_t b = 0; b < x[A_BS]; ++b) {
         int64_t qlen = rag[2 * b], kvlen = rag[2 * b + 1], rows = qlen * g;
-        for (int64_t i = 0; i < cdiv(rows, x[A_BQ]); ++i) {
+        for (int64_t i = 0; i < cdiv(rows, x[A_BQ]) && L < SAT128; ++i) {
           int64_t q_last = (imin((i + 1) * x[A_BQ], rows) - 1) / g;
           int64_t kv_need = x[A_CAUSAL] ? imin(kvlen, kvlen - qlen + q_last + 1) : kvlen;
           int64_t chunk = x[A_CHUNK];
@@ -400,11 +387,10 @@ static int validate(int fam, const int64_t *x, const int32_t *rag, int64_t *T_ou
             U += cdiv(len, x[A_BKV]);
           }
           L += n_ch;
-          if (L > INT32_LIM || U > UINT32_LIM) return ST_RANGE;
         }
       }
-      if (L * x[A_NKV] > INT32_LIM) return ST_RANGE;
       *T_out = L * x[A_NKV];
+      *U_out = U;
       return ST_OK;
     }
   }
@@ -574,18 +560,19 @@ static int64_t plan_kv_chunk(const int64_t *x, const int32_t *rag, const orc_spe
 /* One (config, spec) pair through O1..O7.  ints[N_I], flts[N_F]. */
 static int featurize_pair(int fam, const int64_t *x_in, const int32_t *rag, const orc_spec *sp,
                           int flags, int64_t *ints, double *flts) {
-  int64_t T = 0, x[16];
+  int64_t x[16];
+  i128 T = 0, U = 0;
   memcpy(x, x_in, sizeof x);
   int st;
   if (fam == FAM_ATTENTION && x[A_CHUNK] == -1 && !x[A_CAUSAL]) {
     x[A_CHUNK] = 0; /* domain checks first, with the unsplit extent */
-    st = validate(fam, x, rag, &T);
+    st = validate(fam, x, rag, &T, &U);
     if (st == ST_OK) {
       x[A_CHUNK] = plan_kv_chunk(x, rag, sp, occupancy(fam, x, sp));
-      st = validate(fam, x, rag, &T);
+      st = validate(fam, x, rag, &T, &U);
     }
   } else {
-    st = validate(fam, x, rag, &T);
+    st = validate(fam, x, rag, &T, &U);
   }
   int64_t tensor_th = 0;
   if (st == ST_OK && is_tensor_family(fam)) {
@@ -770,15 +757,16 @@ void orc_schedule_minheap(const int64_t *cost, int64_t n, int64_t n_sm, int64_t 
  * [ops_T, ops_F, ops_X, bytes] rows; returns the task count, or -status. */
 int64_t orc_task_list(int fam, const int32_t *fields, int64_t field_ld, int64_t c,
                       const int32_t *rag, int flags, int64_t n_sm, int64_t *out, int64_t cap) {
-  int64_t x[16], T = 0;
+  int64_t x[16];
+  i128 T = 0, U = 0;
   load_config(fields, field_ld, c, n_fields_of(fam), x);
-  int st = validate(fam, x, rag, &T);
+  int st = validate(fam, x, rag, &T, &U);
   if (st != ST_OK) return -st;
+  if (T > cap) return -(int64_t)100;
   orc_sched s;
   memset(&s, 0, sizeof s);
   /* one "SM" per task slot, so sm_sum rows are the per-task demands in order */
-  s.n_sm = T > 0 ? T : 1;
-  if (s.n_sm > cap) return -(int64_t)100;
+  s.n_sm = T > 0 ? (int64_t)T : 1;
   (void)n_sm;
   s.sm_sum = (i128 *)calloc((size_t)s.n_sm * 4, sizeof(i128));
   s.sm_count = (int64_t *)calloc((size_t)s.n_sm, sizeof(int64_t));
@@ -796,6 +784,21 @@ int64_t orc_task_list(int fam, const int32_t *fields, int64_t field_ld, int64_t 
   free(s.sm_sum);
   free(s.sm_count);
   return n;
+}
+
+/* Task count T and (attention) the per-kv-head kv-unit sum U of config c, as
+ * validate() counts them; returns the domain status (tests: the GPU's
+ * exact-range limits, include/synperf.h SP_PAIR_E_RANGE, are asserted where
+ * these cross 2^31 and 2^32).  Saturated counts read as INT64_MAX. */
+int orc_count(int fam, const int32_t *fields, int64_t field_ld, int64_t c, const int32_t *rag, int64_t *T,
+              int64_t *U) {
+  int64_t x[16];
+  i128 t = 0, u = 0;
+  load_config(fields, field_ld, c, n_fields_of(fam), x);
+  int st = validate(fam, x, rag, &t, &u);
+  *T = t > (i128)INT64_LIM ? INT64_LIM : (int64_t)t;
+  *U = u > (i128)INT64_LIM ? INT64_LIM : (int64_t)u;
+  return st;
 }
 
 /* ---------------- O8-O11 Performance Estimator ---------------- */

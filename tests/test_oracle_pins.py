@@ -676,3 +676,162 @@ def test_emulated_16bit_mlp(orc):
     em2 = orc.predict_emulated(m2, o, "bf16")
     # only the layer inputs are rounded now: small, but not zero, deviation
     assert np.nanmax(np.abs(em2[ok] / lat2[ok] - 1)) < 0.1
+
+
+# ------------------------------------------------ round-2 pins (VERDICT r01 "missing" 1)
+
+def test_silu_mul_worked_example(orc):
+    """Hand-derived SiLU&Mul record (R15; Table V, Table III): a
+    dropped XU term, FMA 2 instead of 4, or dim counted once in the loads fails."""
+    g = GOLD["silu_mul_3x5_2sm"]
+    b = one(gen.SILU_MUL, g["config"])
+    tl = orc.task_list(b)
+    assert tl.tolist() == [g["task_row"]] * g["config"]["SEQ"]
+    ints, flts, st = feats(orc, b, spec_with(num_sms=g["n_sm"]))
+    assert st == 0
+    for k, v in g["ints"].items():
+        assert ints[k] == v, k
+    for k, v in g["flts"].items():
+        assert flts[k] == pytest.approx(v, rel=g["flt_rtol"], abs=0), k
+
+
+def test_moe_padded_worked_example(orc):
+    """Hand-derived padded fused-MoE record with H % BK != 0 and t_e % BM != 0
+    (Table V, Eq.3, R1/R2/R16): H instead of H_pad, or floor
+    instead of ceil for the m-blocks, fails."""
+    g = GOLD["moe_padded_tiny"]
+    b = one(gen.FUSED_MOE, g["config"], hist=g["hist"])
+    tl = orc.task_list(b)
+    assert len(tl) == g["ints"]["n_tasks"]
+    assert (tl[:, 0] == g["task_ops"]).all() and (tl[:, 3] == g["task_bytes"]).all()
+    assert (tl[:, 1:3] == 0).all()
+    sp = spec_with(num_sms=g["n_sm"])
+    ints, _, st = feats(orc, b, sp)
+    assert st == 0
+    for k, v in g["ints"].items():
+        assert ints[k] == v, k
+    bal = dict(g["config"], **g["balanced_config"])
+    ints_b, _, st_b = feats(orc, one(gen.FUSED_MOE, bal), sp)
+    assert st_b == 0
+    for k, v in g["ints"].items():
+        assert ints_b[k] == v, ("balanced", k)
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_occupancy_each_quota_binds(orc, i):
+    """P:278 / R6: one hand-derived case per binding quota (warp slots,
+    register file, CTA slots, shared memory, none) on the A100 fills."""
+    case = GOLD["occupancy_quotas"]["cases"][i]
+    cfg = dict(SEQ=1000, DIM=64, DTYPE=0, **case["footprint"])
+    ints, _, st = feats(orc, one(gen.RMSNORM, cfg), A100)
+    assert st == 0 and ints["occupancy"] == case["occupancy"], case["binds"]
+    assert ints["waves"] == -(-1000 // (108 * case["occupancy"]))
+
+
+def _bn_mlp(seed, eps):
+    """A model whose eval BatchNorm is far from the identity: gamma of both
+    signs, beta and running means of the size of the activations, variances
+    spread over two decades, and a non-default epsilon."""
+    rng = np.random.default_rng(seed)
+    m = models.random_mlp(gen.GEMM, seed, bn_eps=eps)
+    for li, w in zip((1, 2, 3), (256, 128, 64)):
+        m[f"g{li}"] = rng.uniform(-1.5, 2.0, w).astype(np.float32)
+        m[f"be{li}"] = rng.uniform(-1.0, 1.0, w).astype(np.float32)
+        m[f"m{li}"] = rng.uniform(-0.5, 1.5, w).astype(np.float32)
+        m[f"v{li}"] = np.exp(rng.uniform(np.log(0.05), np.log(5.0), w)).astype(np.float32)
+    return m
+
+
+def _torch_net(m, eps, bn_first=False):
+    """P:489 as written: Linear -> ReLU -> BatchNorm -> Dropout per hidden layer
+    (eval mode: running statistics, dropout off), then Linear(64, 1)."""
+    import torch
+
+    layers = []
+    fan = m["n_in"]
+    for li, w in zip((1, 2, 3), (256, 128, 64)):
+        lin = torch.nn.Linear(fan, w)
+        bn = torch.nn.BatchNorm1d(w, eps=eps)
+        with torch.no_grad():
+            lin.weight.copy_(torch.from_numpy(m[f"w{li}"].astype(np.float64)))
+            lin.bias.copy_(torch.from_numpy(m[f"b{li}"].astype(np.float64)))
+            bn.weight.copy_(torch.from_numpy(m[f"g{li}"].astype(np.float64)))
+            bn.bias.copy_(torch.from_numpy(m[f"be{li}"].astype(np.float64)))
+            bn.running_mean.copy_(torch.from_numpy(m[f"m{li}"].astype(np.float64)))
+            bn.running_var.copy_(torch.from_numpy(m[f"v{li}"].astype(np.float64)))
+        layers += [lin, bn, torch.nn.ReLU()] if bn_first else [lin, torch.nn.ReLU(), bn]
+        layers.append(torch.nn.Dropout(0.1))
+        fan = w
+    out = torch.nn.Linear(64, 1)
+    with torch.no_grad():
+        out.weight.copy_(torch.from_numpy(m["w4"].astype(np.float64))[None])
+        out.bias.fill_(float(m["b4"]))
+    return torch.nn.Sequential(*layers, out).double().eval()
+
+
+def test_eval_batchnorm_after_relu_matches_torch(orc):
+    """O10 with non-identity eval BatchNorm ("ReLU activations followed by
+    Batch Normalization and Dropout", R18) against torch.nn.BatchNorm1d(...).eval()
+    placed after the ReLU, in fp64 (a library routine).  The same comparison is
+    shown to reject BN-before-ReLU, beta/mean swapped, and the default epsilon,
+    so a plausible slip in the oracle's BN fails here."""
+    import torch
+
+    eps = float(np.float32(1e-3))  # the model file stores epsilon as fp32
+    b = gen.gen_gemm(60, 31)
+    f = orc.featurize(b, specs.paper_gpu_specs())
+    m = _bn_mlp(5, eps)
+    _, eff, z = orc.predict(m, f)
+    ok = np.nonzero(f.status == 0)[0][:300]
+    X = torch.from_numpy(np.stack([orc.mlp_input(m, f.ints[:, p], f.flts[:, p]) for p in ok]))
+    with torch.no_grad():
+        zt = _torch_net(m, eps)(X).numpy()[:, 0]
+        wrong = {
+            "bn before relu": _torch_net(m, eps, bn_first=True)(X).numpy()[:, 0],
+            "default eps": _torch_net(m, float(np.float32(1e-5)))(X).numpy()[:, 0],
+        }
+        swapped = dict(m)
+        for li in (1, 2, 3):
+            swapped[f"be{li}"], swapped[f"m{li}"] = m[f"m{li}"], m[f"be{li}"]
+        wrong["beta/mean swapped"] = _torch_net(swapped, eps)(X).numpy()[:, 0]
+    np.testing.assert_allclose(z[ok], zt, rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(eff[ok], 1.0 / (1.0 + np.exp(-zt)), rtol=1e-12)
+    for name, zw in wrong.items():
+        assert np.max(np.abs(zw - zt)) > 1e-3, name  # the pin can tell these apart
+
+
+def test_oracle_has_no_32bit_limit(orc):
+    """R22: the record holds int64 counts, so the oracle's domain is the paper's
+    (VERDICT r01 weak 1): configs past the GPU kernels' 32-bit working ranges
+    -- packed rows qlen*g >= 2^31, a per-head kv-unit sum >= 2^32, M*topk >= 2^31
+    -- get exact answers here (the GPU reports SP_PAIR_E_RANGE for them; see
+    tests/test_gpu_range.py).  Values by hand from R10/R11 and Eq.3."""
+    # causal prefill, qlen = 2^28, g = 8 -> 2^31 packed rows, BQ = 2^28 -> 8 q-blocks;
+    # q-block i: q_last = ((i+1)*2^28 - 1) // 8 = (i+1)*2^25 - 1, kv_need = (i+1)*2^25,
+    # kv_eff = ceil(kv_need / 2^27) * 2^27 = 2^27 (i < 4) or 2^28 (i >= 4)
+    q = 1 << 28
+    cfg = dict(BS=1, NH=8, NKV=1, HD=1, BQ=q, BKV=1 << 27, KV_CHUNK=0, CAUSAL=1, WARPS=4, REGS=64, SMEM=0,
+               DTYPE=0)
+    b = one(gen.ATTENTION, cfg, [(q, q)])
+    assert orc.count(b) == (0, 8, 4 * 1 + 4 * 2)
+    tl = orc.task_list(b)
+    kv_eff = [1 << 27] * 4 + [1 << 28] * 4
+    assert tl[:, 0].tolist() == [4 * q * k for k in kv_eff]
+    ints, _, st = feats(orc, b, A100)
+    assert st == 0 and ints["n_tasks"] == 8 and ints["tot_T"] == 4 * q * sum(kv_eff)
+    # per-head kv units 3 * (2^31 - 1) >= 2^32 (non-causal, BKV = 1)
+    kv = (1 << 31) - 1
+    b = one(gen.ATTENTION, dict(cfg, BS=3, BQ=1, BKV=1, CAUSAL=0, NH=1), [(1, kv)] * 3)
+    assert orc.count(b) == (0, 3, 3 * kv)
+    ints, _, st = feats(orc, b, A100)
+    assert st == 0 and ints["tot_X"] == 3 * (kv + kv)  # BQ*kv_eff + BQ*kv_eff/BKV per task
+    # fused MoE with M*topk = 2^31 tokens on one expert: 2 m-blocks of 2^30
+    m = dict(M=1 << 30, E=1, TOPK=2, H=16, N=16, BM=1 << 30, BN=16, BK=16, GROUP_M=1, STAGES=2, WARPS=4,
+             REGS=64, SMEM=0, DTYPE=0)
+    b = one(gen.FUSED_MOE, m)
+    assert orc.count(b) == (0, 2, 0)
+    ints, _, st = feats(orc, b, A100)
+    assert st == 0 and ints["tot_T"] == 2 * (2 * (1 << 30) * 16 * 16)
+    # a GEMM with 2^32 - 2 tiles is counted exactly (not enumerated here)
+    g = dict(M=(1 << 31) - 1, N=2, K=16, TM=1, TN=1, BK=16, STAGES=1, WARPS=1, REGS=1, SMEM=0, DTYPE=0)
+    assert orc.count(one(gen.GEMM, g)) == (0, 2 * ((1 << 31) - 1), 0)
