@@ -700,7 +700,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--scale", type=float, default=1.0, help="workload size multiplier (testing)")
-    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"])
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "fp32"])
     ap.add_argument("--scheduler", default="rr", choices=["rr", "greedy", "minheap"],
                     help="Scheduling Simulator variant (sp_featurize_sched; default cyclic RR)")
     ap.add_argument("--fused", default="auto", choices=["auto", "on", "off"],

@@ -211,9 +211,11 @@ typedef struct sp_features {
 
 typedef enum sp_precision {
   SP_MLP_FP32 = 0,  /* CUDA-core fp32 path: parity within 1e-5 relative of the fp64 oracle */
-  SP_MLP_BF16 = 1,  /* tcgen05/TMEM path, bf16 operands, fp32 accumulate: parity within 1e-2 */
+  SP_MLP_BF16 = 1,  /* REFUSED by sp_load_model (SP_E_UNSUPPORTED): bf16 operands (8-bit
+                       mantissa) measured 3e-2 max latency error vs the fp64 oracle, outside
+                       north_star's 1e-2 bar for a 16-bit MLP */
   SP_MLP_FP16 = 2   /* tcgen05/TMEM path, fp16 operands, fp32 accumulate: parity within 1e-2
-                       (typically ~4x tighter than bf16: 10-bit mantissa); same tensor rate */
+                       (measured max 5e-3); same dense tensor rate as bf16 */
 } sp_precision;
 
 /*
@@ -287,9 +289,10 @@ int32_t sp_specs_count(const sp_specs *specs);
  * Estimator load.  Copies the HOST description, checks
  * n_in == 4*pipes(family)+7 and that every value is finite and sigma, var,
  * bn_eps are sane (SP_E_DATA otherwise), and builds device layouts:
- * SP_MLP_FP32 keeps fp32 weights with BN as a per-unit affine; SP_MLP_BF16 / _FP16
- * fold each BN affine into the next layer (algebraically exact, R18) and
- * packs bf16 weights in the tcgen05 UMMA shared-memory layout.
+ * SP_MLP_FP32 keeps fp32 weights with BN as a per-unit affine; SP_MLP_FP16
+ * folds each BN affine into the next layer (algebraically exact, R18) and
+ * packs fp16 weights in the tcgen05 UMMA shared-memory layout.  SP_MLP_BF16
+ * returns SP_E_UNSUPPORTED (see sp_precision).
  */
 sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *desc, sp_model **out);
 void sp_free_model(sp_model *model);

@@ -447,7 +447,8 @@ class Context:
         return mu, sg
 
     def load_model(self, model: dict, precision: str = "fp16") -> Model:
-        """precision: "fp16" / "bf16" (tcgen05 tensor-core path) or "fp32" (CUDA cores)."""
+        """precision: "fp16" (tcgen05 tensor-core path) or "fp32" (CUDA cores); "bf16" is
+        refused by the library (SP_E_UNSUPPORTED: it misses the 1e-2 latency bar)."""
         d = _abi.sp_mlp_desc()
         d.family = int(model["family"])
         d.n_in = int(model["n_in"])

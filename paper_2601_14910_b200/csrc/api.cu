@@ -536,6 +536,11 @@ extern "C" sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *d, sp_model *
     return fail(ctx, SP_E_DATA, "sp_load_model: n_in does not match the family's Table IV layout");
   if (d->precision != SP_MLP_FP32 && d->precision != SP_MLP_BF16 && d->precision != SP_MLP_FP16)
     return fail(ctx, SP_E_ARG, "sp_load_model: unknown precision");
+  // bf16 operands (8-bit mantissa) measured a 3e-2 max latency error against the fp64
+  // oracle with seeded weights, outside north_star's 1e-2 for a 16-bit MLP: refused.
+  if (d->precision == SP_MLP_BF16)
+    return fail(ctx, SP_E_UNSUPPORTED,
+                "sp_load_model: SP_MLP_BF16 misses the 1e-2 latency bar (measured 3e-2); use SP_MLP_FP16");
   const float *arrs[] = {d->mu, d->sigma, d->w1, d->b1, d->g1, d->be1, d->m1, d->v1, d->w2, d->b2, d->g2,
                          d->be2, d->m2, d->v2, d->w3, d->b3, d->g3, d->be3, d->m3, d->v3, d->w4};
   const size_t lens[] = {(size_t)n_in, (size_t)n_in, 256u * n_in, 256, 256, 256, 256, 256, 128 * 256, 128,
@@ -610,14 +615,13 @@ extern "C" sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *d, sp_model *
     q.n_in = n_in;
     q.family = d->family;
   }
-  if (d->precision == SP_MLP_BF16 || d->precision == SP_MLP_FP16) {
+  if (d->precision == SP_MLP_FP16) {
     std::vector<uint16_t> wpack;
     std::vector<float> vecs;
     float b4 = 0.f;
-    const bool bf16 = d->precision == SP_MLP_BF16;
-    m->m16.bf16 = bf16 ? 1 : 0;
-    if (!pack_mlp_16bit(*d, s, t, bf16, wpack, vecs, b4))
-      return fail(ctx, SP_E_UNSUPPORTED, "sp_load_model: bf16 tcgen05 path unavailable in this build");
+    m->m16.bf16 = 0;
+    if (!pack_mlp_16bit(*d, s, t, false, wpack, vecs, b4))
+      return fail(ctx, SP_E_UNSUPPORTED, "sp_load_model: tcgen05 path unavailable in this build");
     cudaError_t e = m->bf16w.alloc_copy(wpack.data(), wpack.size() * 2);
     if (e == cudaSuccess) e = m->bf16v.alloc_copy(vecs.data(), vecs.size() * 4);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "sp_load_model: bf16 upload");
@@ -648,7 +652,7 @@ extern "C" sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_fea
   cudaSetDevice(ctx->device);
   int e;
   const LaunchHook h = ctx->hook();
-  if (model->precision == SP_MLP_BF16 || model->precision == SP_MLP_FP16) {
+  if (model->precision == SP_MLP_FP16) {
     h.on_begin("predict_tcgen05", stream);
     e = launch_predict_tcgen05(model->m16, *in, latency_us, efficiency, ctx->num_sms, stream);
   } else {

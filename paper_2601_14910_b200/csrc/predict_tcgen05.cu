@@ -1057,8 +1057,7 @@ int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *laten
   P.n_tiles = (in.n_pairs + kTile - 1) / kTile;
   const int64_t grid = P.n_tiles < num_device_sms ? P.n_tiles : num_device_sms;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return (int)(m.bf16 ? launch_fam<true>(m.family, P, (unsigned)grid, st)
-                      : launch_fam<false>(m.family, P, (unsigned)grid, st));
+  return (int)launch_fam<false>(m.family, P, (unsigned)grid, st);  // fp16 operands (bf16 is refused at load)
 }
 
 template <bool BF16>
@@ -1090,8 +1089,7 @@ int launch_predict_tcgen05_fused(const MlpBf16 &m, const FusedIn &fi, float *lat
   P.n_tiles = fi.cmajor ? fi.n_specs * ((fi.C + kTile - 1) / kTile) : (fi.n_pairs + kTile - 1) / kTile;
   const int64_t grid = P.n_tiles < num_device_sms ? P.n_tiles : num_device_sms;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return (int)(m.bf16 ? launch_fused<true>(m.family, P, (unsigned)grid, st)
-                      : launch_fused<false>(m.family, P, (unsigned)grid, st));
+  return (int)launch_fused<false>(m.family, P, (unsigned)grid, st);
 }
 
 }  // namespace sp

@@ -171,12 +171,15 @@ def test_compose_parity_small(sp, ctx, orc, precision, tp, pp):
     np.testing.assert_allclose(cat.sum(axis=2), tot, rtol=1e-12)  # additivity
 
 
-def test_compose_full_size_sampled(sp, ctx, orc):
-    """BASELINE config 4 at full size (Llama-3-8B, 256 traces, launch config of
-    bench.py): sampled steps recomputed literally by the oracle; the per-trace
+@pytest.mark.parametrize("name", ["llama3-8b", "qwen2.5-14b"])
+def test_compose_full_size_sampled(sp, ctx, orc, name):
+    """BASELINE config 4 at full size (256 traces, launch config of bench.py)
+    for both serving models -- Qwen2.5-14B's 40/8 heads give GQA group 5,
+    which does not divide BQ, so its causal prefill runs the general q_last
+    path: sampled steps recomputed literally by the oracle; the per-trace
     totals equal the sum of the step latencies (a property at any size)."""
     tr = gen.gen_serving_traces(256, 1004)
-    model = gen.serving_model("llama3-8b")
+    model = gen.serving_model(name)
     sa = specs.paper_gpu_specs()
     plan, res, mdl = run_both(sp, ctx, model, tr, "fp16", sa)
     inf = plan.info()

@@ -2,7 +2,7 @@
 
 Bar (BASELINE.json north_star): every integer slot and status bit-exact;
 fp32 float features within 1e-5 relative of the fp64 oracle; latency within
-1e-5 relative for the fp32 MLP and 1e-2 for the bf16 tcgen05 MLP.
+1e-5 relative for the fp32 MLP and 1e-2 for the 16-bit (fp16) tcgen05 MLP.
 """
 import numpy as np
 import pytest
@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 FEAT_RTOL = 1e-5
 LAT_RTOL_FP32 = 1e-5
-LAT_RTOL_BF16 = 1e-2
+LAT_RTOL_16 = 1e-2
 
 
 @pytest.fixture(scope="module")
@@ -64,6 +64,9 @@ def assert_feature_parity(g, o, where=""):
 FAMILY_BATCHES = {
     "gemm": lambda: gen.gen_gemm(700, 1001),
     "attention": lambda: gen.gen_attention(150, 150, 1002, max_bs=6, qlen_max=4000, kvlen_max=6000),
+    # GQA groups that do not divide BQ (Qwen2.5-14B: 40/8 = 5): the general causal q_last path
+    "attention_gqa": lambda: gen.gen_attention(200, 100, 1012, max_bs=6, qlen_max=4000, kvlen_max=6000,
+                                               groups=(3, 5, 6, 12)),
     "moe": lambda: gen.gen_moe(600, 1003),
     "rmsnorm": lambda: gen.gen_rowwise(gen.RMSNORM, 500, 1004),
     "silu": lambda: gen.gen_rowwise(gen.SILU_MUL, 500, 1005),
@@ -224,18 +227,29 @@ def test_uniform_edge_cases(sp, ctx, orc):
 
 def test_full_size_sampled_cfg2(sp, ctx, orc):
     """BASELINE config 2 at full size (1e6 configs x 11 specs), in the launch
-    configuration bench.py times; 3000 sampled pairs checked one by one."""
+    configuration bench.py times (sp_featurize, then the fp16 tcgen05 sp_predict
+    over all 1.1e7 pairs: ~580 tiles per CTA); 3000 sampled pairs checked one by
+    one -- features bit-exact / 1e-5, latencies at north_star's 1e-2."""
     b = gen.gen_attention(500_000, 500_000, 1002)
     b, _ = gen.shuffle(b, 7)
     sa = specs.paper_gpu_specs()
     f, _ = gpu_features(sp, ctx, b, sa)
+    model = models.random_mlp(b.family, 5)
+    mh = ctx.load_model(model, "fp16")
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    ctx.predict(mh, f, lat)
+    torch.cuda.synchronize()
     rng = np.random.default_rng(3)
-    p = rng.integers(0, f.n_pairs, 3000)
+    p = np.concatenate([rng.integers(0, f.n_pairs, 2990), np.arange(5), f.n_pairs - 1 - np.arange(5)])
     ci, si = p % b.n_configs, p // b.n_configs
     o = orc.featurize(b, sa, cfg_idx=ci, spec_idx=si)
     pt = torch.from_numpy(p).cuda()
     g = (f.ints[:, pt].cpu().numpy(), f.flts[:, pt].cpu().numpy(), f.status[pt].cpu().numpy())
     assert_feature_parity(g, o, "cfg2 full-size sample")
+    olat, _, _ = orc.predict(model, o)
+    glat = lat[pt].cpu().numpy().astype(np.float64)
+    assert (o.status == 0).all()
+    np.testing.assert_allclose(glat, olat, rtol=LAT_RTOL_16, atol=0, err_msg="cfg2 full-size fp16 latency")
 
 
 def _predict_both(sp, ctx, orc, batch, sa, precision, seed=5):
@@ -263,23 +277,48 @@ def test_predict_fp32_parity(sp, ctx, orc, fam):
 
 
 @pytest.mark.parametrize("fam", list(FAMILY_BATCHES))
-@pytest.mark.parametrize("prec", ["fp16", "bf16"])
-def test_predict_tcgen05_parity(sp, ctx, orc, fam, prec):
+def test_predict_tcgen05_parity(sp, ctx, orc, fam):
     b = FAMILY_BATCHES[fam]().subset(np.arange(300))
     sa = specs.paper_gpu_specs()
-    lat, eff, olat, oeff = _predict_both(sp, ctx, orc, b, sa, prec)
+    lat, eff, olat, oeff = _predict_both(sp, ctx, orc, b, sa, "fp16")
     ok = ~np.isnan(olat)
     assert np.array_equal(np.isnan(lat), ~ok)
     rel = np.abs(lat[ok] / olat[ok] - 1)
-    print(f"{prec} {fam}: max rel {rel.max():.2e} p99 {np.quantile(rel, 0.99):.2e} mean {rel.mean():.2e}")
-    if prec == "fp16":
-        # the product path: north_star's 16-bit bar, every element
-        np.testing.assert_allclose(lat[ok], olat[ok], rtol=LAT_RTOL_BF16)
-    else:
-        # bf16 operands (8-bit mantissa) do NOT meet 1e-2 on every element with
-        # these weights (max ~2.5e-2 measured); its envelope is
-        # pinned here so a regression shows, and fp16 is the default.
-        assert np.quantile(rel, 0.99) < 2e-2 and rel.max() < 4e-2
+    print(f"fp16 {fam}: max rel {rel.max():.2e} p99 {np.quantile(rel, 0.99):.2e} mean {rel.mean():.2e}")
+    np.testing.assert_allclose(lat[ok], olat[ok], rtol=LAT_RTOL_16)  # every element
+
+
+def test_bf16_predictor_refused(sp, ctx):
+    """bf16 operands miss north_star's 1e-2 (measured 3e-2 in r01): refused at
+    load rather than served with a looser envelope."""
+    with pytest.raises(sp.SynPerfError, match="SP_E_UNSUPPORTED"):
+        ctx.load_model(models.random_mlp(gen.GEMM, 5), "bf16")
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+@pytest.mark.parametrize("fam", ["gemm", "attention"])
+def test_predict_non_identity_batchnorm(sp, ctx, orc, fam, prec):
+    """Eval BatchNorm far from the identity (gamma of both signs, variances over
+    two decades, eps 1e-3), folded into the next layer on the GPU (R18): the
+    fold must reproduce the oracle's unfused Linear -> ReLU -> BN."""
+    b = FAMILY_BATCHES[fam]().subset(np.arange(300))
+    sa = specs.paper_gpu_specs()
+    rng = np.random.default_rng(17)
+    model = models.random_mlp(b.family, 17, bn_eps=1e-3)
+    for li, w in zip((1, 2, 3), (256, 128, 64)):
+        model[f"g{li}"] = rng.uniform(-1.5, 2.0, w).astype(np.float32)
+        model[f"be{li}"] = rng.uniform(-1.0, 1.0, w).astype(np.float32)
+        model[f"m{li}"] = rng.uniform(-0.5, 1.5, w).astype(np.float32)
+        model[f"v{li}"] = np.exp(rng.uniform(np.log(0.05), np.log(5.0), w)).astype(np.float32)
+    f, _ = gpu_features(sp, ctx, b, sa)
+    mh = ctx.load_model(model, prec)
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    ctx.predict(mh, f, lat)
+    torch.cuda.synchronize()
+    o = orc.featurize(b, sa)
+    olat, _, _ = orc.predict(model, o)
+    ok = o.status == 0
+    np.testing.assert_allclose(lat.cpu().numpy()[ok], olat[ok], rtol=LAT_RTOL_FP32 if prec == "fp32" else LAT_RTOL_16)
 
 
 def test_predict_zero_output_layer_exact(sp, ctx, orc):
@@ -287,7 +326,7 @@ def test_predict_zero_output_layer_exact(sp, ctx, orc):
     b = gen.gen_gemm(200, 9)
     sa = specs.paper_gpu_specs()
     f, (gi, gf, gs) = gpu_features(sp, ctx, b, sa)
-    for prec in ("fp32", "bf16", "fp16"):
+    for prec in ("fp32", "fp16"):
         mh = ctx.load_model(models.zero_output_mlp(gen.GEMM, 1), prec)
         lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
         ctx.predict(mh, f, lat)
@@ -388,7 +427,7 @@ def test_predict_host_wide_spec_axis(sp, ctx, fam):
 
 # ------------------------------------------------------------- clamped edge tiles (SP_FEAT_CLAMPED, NEXT-4)
 
-@pytest.mark.parametrize("fam", ["gemm", "moe", "attention"])
+@pytest.mark.parametrize("fam", ["gemm", "moe", "attention", "attention_gqa"])
 def test_clamped_parity(sp, ctx, orc, fam):
     """Clamped edge tiles vs the oracle's CLAMPED flag: CROSS over Table VI and
     the odd SM counts, and a LIST with out-of-range indices."""
@@ -460,7 +499,7 @@ def test_clamped_edge_cases(sp, ctx, orc):
 # ------------------------------------------------------------- fused featurize -> predict (sp_featurize_predict)
 
 @pytest.mark.parametrize("fam", ["gemm", "moe", "rmsnorm", "silu", "scaled_mm", "attention", "gemm_splitk"])
-@pytest.mark.parametrize("prec", ["fp16", "bf16"])
+@pytest.mark.parametrize("prec", ["fp16", "fp32"])
 def test_featurize_predict_equals_two_calls(sp, ctx, fam, prec):
     """The fused call writes the same records, bit for bit, and the same latencies
     and efficiencies as sp_featurize + sp_predict (full and partial spec ranges,
@@ -526,7 +565,7 @@ def test_full_size_sampled_fused(sp, ctx, orc, cfg):
     gl = lat[pt].cpu().numpy()
     ok = ~np.isnan(olat)
     assert ok.mean() > (0.6 if cfg == "scaledmm" else 0.9) and np.array_equal(np.isnan(gl), ~ok)
-    np.testing.assert_allclose(gl[ok], olat[ok], rtol=LAT_RTOL_BF16)
+    np.testing.assert_allclose(gl[ok], olat[ok], rtol=LAT_RTOL_16)
     del f, lat
     torch.cuda.empty_cache()
 

@@ -123,7 +123,7 @@ def gen_gemm(n: int, seed: int, m_range=(2, 131072), n_range=(384, 152064),
 
 
 def gen_attention(n_prefill: int, n_decode: int, seed: int, max_bs=16,
-                  qlen_max=20097, kvlen_max=20481) -> ConfigBatch:
+                  qlen_max=20097, kvlen_max=20481, groups=(1, 2, 4, 8, 16)) -> ConfigBatch:
     """BASELINE config 2 recipe, ranges of §V-B.
 
     bs ~ U{1..16}; nkv in {1,2,4,8}; group g in {1,2,4,8,16}, nh = nkv*g in [2,128];
@@ -132,15 +132,18 @@ def gen_attention(n_prefill: int, n_decode: int, seed: int, max_bs=16,
     BQ in {64,128}, BKV in {32,64}, unsplit.  Decode: qlen = 1,
     kvlen ~ logU[4, 20481], BQ = 16, BKV in {32,64}, kv_chunk in {0,256,...,2048}.
     Configs are prefill first, then decode (callers shuffle before sharding).
+    `groups` replaces the GQA group menu (tests: groups that do not divide BQ,
+    e.g. Qwen2.5-14B's 40/8 = 5).
     """
     rng = np.random.default_rng(seed)
     n = n_prefill + n_decode
     bs = rng.integers(1, max_bs + 1, n)
     nkv = rng.choice([1, 2, 4, 8], n)
-    g = rng.choice([1, 2, 4, 8, 16], n)
+    groups = list(groups)
+    g = rng.choice(groups, n)
     bad = (nkv * g) < 2
     while bad.any():
-        g[bad] = rng.choice([1, 2, 4, 8, 16], int(bad.sum()))
+        g[bad] = rng.choice(groups, int(bad.sum()))
         bad = (nkv * g) < 2
     nh = nkv * g
     hd = rng.choice([64, 128], n)
