@@ -143,9 +143,11 @@ class ClockSampler:
 
 # ----------------------------------------------------------- reference (oracle)
 
-def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int = 0):
+def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int = 0, keep: dict | None = None):
     """Times the fp64 oracle (as it stands) on a bounded random sample of the
-    workload's pairs: featurize + predict.  Returns (pairs/s, n_sample, secs, threads)."""
+    workload's pairs: featurize + predict.  Returns (pairs/s, n_sample, secs,
+    threads, single-core pairs/s).  keep: receives the main sample's local pair
+    indices and the oracle's features and latencies (the bench's parity check)."""
     from oracle import oracle as O
 
     O.build()
@@ -153,13 +155,16 @@ def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int =
     g0, g1 = spec_range
     total = (g1 - g0) * batch.n_configs
 
-    def run(n, threads=0):
+    def run(n, threads=0, store=False):
         p = rng.integers(0, total, n)
         ci, si = p % batch.n_configs, g0 + p // batch.n_configs
         t = time.perf_counter()
         f = O.featurize(batch, spec_arr, cfg_idx=ci, spec_idx=si, nthreads=threads)
-        O.predict(model, f, nthreads=threads)
-        return time.perf_counter() - t
+        lat, _, _ = O.predict(model, f, nthreads=threads)
+        dt = time.perf_counter() - t
+        if store and keep is not None:
+            keep.update(pairs=p, feats=f, latency=lat)
+        return dt
 
     threads = O.num_threads()
     n = 256
@@ -168,7 +173,7 @@ def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int =
         n *= 4
         dt = run(n)
     n = max(256, int(n * target_s / max(dt, 1e-6)))
-    dt = run(n)
+    dt = run(n, store=True)
     # one core (SURVEY §8(d) asks for both): a sample sized for ~1/5 of the time budget
     n1 = max(64, int(n / max(threads, 1) * 0.2))
     dt1 = run(n1, 1)
@@ -176,10 +181,11 @@ def oracle_rate(batch, spec_arr, spec_range, model, target_s: float, seed: int =
     return n / dt, n, dt, threads, n1 / dt1
 
 
-def oracle_e2e_rate(traces, sa, mlps, target_s: float, seed: int = 0):
+def oracle_e2e_rate(traces, sa, mlps, target_s: float, seed: int = 0, keep: list | None = None):
     """Times the literal E2E oracle (oracle/e2e.py) on random serving steps:
     every invocation of the sampled steps featurised + predicted on every spec
-    and summed.  Returns (step-spec predictions/s, pairs/s, n_steps, secs, threads)."""
+    and summed.  Returns (step-spec predictions/s, pairs/s, n_steps, secs, threads).
+    keep: receives (model, trace, step, oracle step latency per spec) per sample."""
     from oracle import e2e as E
     from oracle import oracle as O
 
@@ -195,9 +201,12 @@ def oracle_e2e_rate(traces, sa, mlps, target_s: float, seed: int = 0):
         r = int(rng.integers(0, traces.n_traces))
         ins, outs = traces.trace(r)
         st = E.steps_of_trace(ins, outs)
-        pf, req = st[int(rng.integers(0, len(st)))]
+        k = int(rng.integers(0, len(st)))
+        pf, req = st[k]
         invs = E.forward_pass(m, req, pf)
-        E.predict_e2e([invs], len(sa), kf, None)
+        o_steps, _, _ = E.predict_e2e([invs], len(sa), kf, None)
+        if keep is not None:
+            keep.append((name, r, k, o_steps[:, 0]))
         n_pairs += len(invs) * len(sa)
         steps.append((name, r))
     dt = time.perf_counter() - t0
@@ -396,6 +405,8 @@ def run_gpu(args, rank, world, local_rank):
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json")) or {}
     feat_ms, pred_ms = float(t_feat.mean()), float(t_pred.mean())
     roof = roofline(args, b, n_pairs, n_in, precision, kst, peaks, prof, tot_ms)
+    if b.family == gen.ATTENTION and roof["kernel"] == "attn_schedule_cross":
+        roof["algorithmic"] = attention_work(b, sa, (g0, g1), feats, roof["avg_launch_ms"])
 
     line = {
         "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -420,15 +431,49 @@ def run_gpu(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, dt, thr, v1 = oracle_rate(b, sa, (g0, g1), model_d, target_s=args.cpu_seconds)
+        keep = {}
+        v, n, dt, thr, v1 = oracle_rate(b, sa, (g0, g1), model_d, target_s=args.cpu_seconds, keep=keep)
         line["cpu_baseline"] = {
             "value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
             "sample": f"{n} random pairs of this workload, fp64 oracle featurize+predict, {dt:.1f} s",
             "single_core_value": v1}
+        line["parity"] = parity_stats(keep, feats, lat, precision)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def parity_stats(keep, feats, lat, precision):
+    """north_star's bar on this run's own output: the GPU records and latencies
+    of the last timed step at the cpu_baseline sample's pairs, against the
+    oracle's values for the same pairs (computed by the timed oracle run)."""
+    import torch
+
+    p = keep["pairs"]
+    o = keep["feats"]
+    idx = torch.from_numpy(p).to(feats.status.device)
+    gs = feats.status[idx].cpu().numpy()
+    gi = feats.ints[:, idx].cpu().numpy()
+    gf = feats.flts[:, idx].cpu().numpy().astype(np.float64)
+    gl = lat[idx].cpu().numpy().astype(np.float64)
+    ok = o.status == 0
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rf = np.abs(gf[:, ok] / o.flts[:, ok] - 1.0)
+        rf = np.where(o.flts[:, ok] == 0, np.abs(gf[:, ok]), rf)
+        rl = np.abs(gl[ok] / keep["latency"][ok] - 1.0)
+    bar = 1e-5 if precision == "fp32" else 1e-2
+    max_f = float(rf.max()) if rf.size else 0.0
+    max_l = float(rl.max()) if rl.size else 0.0
+    res = {"pairs": int(len(p)), "valid_pairs": int(ok.sum()),
+           "status_mismatches": int((gs != o.status).sum()),
+           "int_mismatches": int((gi != o.ints).any(axis=0).sum()),
+           "max_rel_float": max_f, "max_rel_latency": max_l,
+           "float_bar": 1e-5, "latency_bar": bar,
+           "sample": "the cpu_baseline sample's pairs; GPU output of the last timed step"}
+    res["pass"] = bool(res["status_mismatches"] == 0 and res["int_mismatches"] == 0 and max_f <= 1e-5
+                       and max_l <= bar)
+    return res
 
 
 def run_gpu_e2e(args, rank, world, local_rank):
@@ -469,12 +514,15 @@ def run_gpu_e2e(args, rank, world, local_rank):
     gathered = torch.empty(world * tot_all.numel(), dtype=torch.float64, device=dev) if dist else None
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
+    results = [None] * len(plans)
+
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
         for i, p in enumerate(plans):
             p.expand(stream)
             r = ctx.predict_e2e(p, specs_h, mdl, None, (0, G), step_latencies=True, stream=stream)
+            results[i] = r
             tot_all[i].copy_(r.trace_us)
         if gathered is not None:
             dist.all_gather_into_tensor(gathered, tot_all.view(-1))
@@ -500,6 +548,8 @@ def run_gpu_e2e(args, rank, world, local_rank):
         torch.cuda.synchronize()
     ctx.set_profiling(False)
     kst = ctx.profile_read(reset=True)
+    # the last timed step's composed step latencies (the parity check below; host API calls reuse buffers)
+    steps_gpu = {name: results[i].step_us.cpu().numpy() for i, name in enumerate(E2E_MODELS)}
     if dist is not None:
         dist.barrier()
     t_step = np.array([e[0].elapsed_time(e[1]) for e in evs])
@@ -561,12 +611,24 @@ def run_gpu_e2e(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sps, pps, n, dt, thr = oracle_e2e_rate(traces, sa, mlps, args.cpu_seconds)
+        keep = []
+        sps, pps, n, dt, thr = oracle_e2e_rate(traces, sa, mlps, args.cpu_seconds, keep=keep)
         line["cpu_baseline"] = {
             "value": pps, "unit": UNIT, "cores": thr, "kind": "oracle",
             "step_predictions_per_s": sps,
             "sample": f"{n} random serving steps, every invocation featurised + predicted literally "
                       f"on 11 specs (fp64 oracle), {dt:.1f} s"}
+        # parity: the GPU's composed step latencies of the last timed step at the sampled steps
+        step_off = np.concatenate([[0], np.cumsum([int(traces.trace(r)[1].max()) for r in range(n_tr)])])
+        rel = [np.abs(steps_gpu[name][:, step_off[r] + k].astype(np.float64) / o - 1.0).max()
+               for name, r, k, o in keep]
+        bar = 1e-5 if args.precision == "fp32" else 1e-2
+        line["parity"] = {"steps": len(keep), "step_spec_values": len(keep) * G,
+                          "max_rel_step_latency": float(max(rel)), "latency_bar": bar,
+                          "pass": bool(max(rel) <= bar),
+                          "sample": "the cpu_baseline sample's serving steps (literal oracle: every "
+                                    "invocation of the step featurised + predicted); GPU step latencies "
+                                    "of the last timed step"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -645,6 +707,27 @@ def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling,
             "d2h_bytes_per_step": int(d2h), "steps": steps,
             "api": "Context.predict_host (pinned host configs -> H2D -> sp_featurize -> "
                    "sp_predict -> D2H latencies)"}
+
+
+def attention_work(b, sa, spec_range, feats, ms):
+    """Algorithmic work of one attn_schedule_cross launch, counted from its own
+    output: head-0 tasks (a config's task count T / nkv, the record's first
+    slot) x the distinct SM counts of the spec range (the kernel
+    accumulates one residue table per distinct N), and the (pair, task) units
+    the records describe (sum of T over all pairs)."""
+    import torch
+
+    g0, g1 = spec_range
+    C = b.n_configs
+    T0 = feats.ints[0, :C].clamp(min=0)  # spec g0's records: pair p = c
+    nkv = torch.from_numpy(b.field("NKV").astype(np.int64)).to(T0.device)
+    head0 = int((T0 // nkv).sum().item())
+    distinct = int(len(np.unique(sa["num_sms"][g0:g1])))
+    pair_tasks = int(feats.ints[0, :(g1 - g0) * C].clamp(min=0).sum().item())
+    units = head0 * distinct
+    return {"units_per_launch": units, "unit": "head-0 task x distinct SM count",
+            "units_per_s": units / (ms * 1e-3), "head0_tasks": head0, "distinct_sm_counts": distinct,
+            "pair_tasks_per_launch": pair_tasks, "pair_tasks_per_s": pair_tasks / (ms * 1e-3)}
 
 
 def roofline(args, b, n_pairs, n_in, precision, kst, peaks, prof, tot_ms):
