@@ -292,7 +292,12 @@ int32_t sp_specs_count(const sp_specs *specs);
  * SP_MLP_FP32 keeps fp32 weights with BN as a per-unit affine; SP_MLP_FP16
  * folds each BN affine into the next layer (algebraically exact, R18) and
  * packs fp16 weights in the tcgen05 UMMA shared-memory layout.  SP_MLP_BF16
- * returns SP_E_UNSUPPORTED (see sp_precision).
+ * returns SP_E_UNSUPPORTED (see sp_precision).  SP_MLP_FP16 returns
+ * SP_E_DATA when a folded weight W*diag(gamma/sqrt(var+eps)) or the layer-1
+ * bias rounds past the fp16 range (|v| > 65504, e.g. a tiny BN variance);
+ * SP_MLP_FP32 accepts such a model.  At predict time the fp16 path converts
+ * activations with saturation (cvt.rn.satfinite): an activation past 65504 is
+ * clamped to it, never inf/NaN.
  */
 sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *desc, sp_model **out);
 void sp_free_model(sp_model *model);

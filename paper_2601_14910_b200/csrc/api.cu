@@ -620,8 +620,11 @@ extern "C" sp_status sp_load_model(sp_ctx *ctx, const sp_mlp_desc *d, sp_model *
     std::vector<float> vecs;
     float b4 = 0.f;
     m->m16.bf16 = 0;
-    if (!pack_mlp_16bit(*d, s, t, false, wpack, vecs, b4))
-      return fail(ctx, SP_E_UNSUPPORTED, "sp_load_model: tcgen05 path unavailable in this build");
+    const int pk = pack_mlp_16bit(*d, s, t, false, wpack, vecs, b4);
+    if (pk == 1) return fail(ctx, SP_E_UNSUPPORTED, "sp_load_model: tcgen05 path unavailable in this build");
+    if (pk == 2)  // W' = W diag(gamma/sqrt(var+eps)) past +-65504 (e.g. a tiny BN variance)
+      return fail(ctx, SP_E_DATA,
+                  "sp_load_model: a BN-folded weight or bias exceeds the fp16 range (|v| > 65504); use SP_MLP_FP32");
     cudaError_t e = m->bf16w.alloc_copy(wpack.data(), wpack.size() * 2);
     if (e == cudaSuccess) e = m->bf16v.alloc_copy(vecs.data(), vecs.size() * 4);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "sp_load_model: bf16 upload");

@@ -11,7 +11,7 @@
 // accumulate onto them; the last BN goes into the output layer (w4' = w4 s3,
 // b4' = b4 + w4.t3).  The activations H1, H2 never touch shared memory: each
 // epilogue reads D from TMEM, applies ReLU + 16-bit packing (one
-// cvt.rn.relu.f16x2 per two values) and writes the packed rows back into TMEM,
+// cvt.rn.satfinite.relu.f16x2 per two values) and writes the packed rows back into TMEM,
 // where the next layer reads them as its A operand ("TS" MMA); only the
 // weights (B) stream from shared memory.  The final 64 -> 1 layer is 64 FMAs
 // per row.
@@ -975,13 +975,16 @@ static uint16_t to_bits16(double v, bool bf16) {
   return u;
 }
 
-bool pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const std::vector<double> *t, bool bf16,
-                    std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4) {
+int pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const std::vector<double> *t, bool bf16,
+                   std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4) {
   const int n_in = d.n_in;
-  if (n_in > kK1 - 1) return false;  // column 15 carries the bias
+  if (n_in > kK1 - 1) return 1;  // column 15 carries the bias
   wpack.assign(kWBytes / 2, 0);
+  bool overflow = false;  // a folded weight that rounds to +-inf in the 16-bit format
   auto put = [&](uint32_t base, uint32_t r, uint32_t k, uint32_t K, double v) {
-    wpack[(base + op_off(r, k, K)) / 2] = to_bits16(v, bf16);
+    const uint16_t u = to_bits16(v, bf16);
+    overflow |= bf16 ? (u & 0x7f80u) == 0x7f80u : (u & 0x7c00u) == 0x7c00u;
+    wpack[(base + op_off(r, k, K)) / 2] = u;
   };
   for (int n = 0; n < 256; ++n) {
     for (int k = 0; k < n_in; ++k) put(kOffW1, n, k, kK1, d.w1[n * n_in + k]);
@@ -1015,7 +1018,10 @@ bool pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const st
     vecs[kVNC + k] = (float)(-(double)d.mu[k] / sg);
   }
   b4 = (float)bb;
-  return true;
+  for (float v : vecs)  // fp32 presets / output layer / normalisation coefficients
+    overflow |= !std::isfinite(v);
+  overflow |= !std::isfinite(b4);
+  return overflow ? 2 : 0;
 }
 
 template <bool BF16>

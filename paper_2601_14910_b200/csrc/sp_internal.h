@@ -175,9 +175,10 @@ struct MlpBf16 {  // tcgen05 path, 16-bit operands (bf16 or fp16)
 };
 // Host: BN-folded bf16 weights in the kernel's shared-memory image, plus fp32
 // vectors.  s[l], t[l]: BN(eval) affine of hidden layer l (fp64).  Returns
-// false if the tcgen05 path is not available.
-bool pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const std::vector<double> *t, bool bf16,
-                    std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4);
+// 0 on success, 1 if the tcgen05 path is not available (n_in), 2 if a folded
+// weight rounds to +-inf in the 16-bit format or an fp32 vector is not finite.
+int pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const std::vector<double> *t, bool bf16,
+                   std::vector<uint16_t> &wpack, std::vector<float> &vecs, float &b4);
 int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *latency, float *eff,
                            int num_device_sms, void *stream);
 // The fused kernel: producers derive each pair's record from the pre-pass and

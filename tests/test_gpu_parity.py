@@ -295,6 +295,36 @@ def test_bf16_predictor_refused(sp, ctx):
         ctx.load_model(models.random_mlp(gen.GEMM, 5), "bf16")
 
 
+def test_fp16_range_checked_at_load(sp, ctx):
+    """A BN variance of 1e-12 folds W2' = W2 * gamma / sqrt(var + eps) past
+    fp16's 65504: the fp16 load refuses it (SP_E_DATA) instead of packing
+    infinities; the fp32 path, which keeps BN unfolded, accepts it."""
+    model = models.random_mlp(gen.GEMM, 5, bn_eps=1e-12)
+    model["v1"] = np.full(256, 1e-12, np.float32)
+    model["g1"] = np.full(256, 10.0, np.float32)
+    with pytest.raises(sp.SynPerfError, match="SP_E_DATA"):
+        ctx.load_model(model, "fp16")
+    ctx.load_model(model, "fp32")
+
+
+def test_fp16_activations_saturate(sp, ctx):
+    """Layer-1 pre-activations far past 65504 (weights 4000 on every input):
+    the epilogue's cvt.rn.satfinite clamps them, so no latency is NaN (cvt.rn
+    would give inf activations, then inf - inf = NaN in the next layer; the
+    sigmoid may still legitimately underflow the efficiency to 0 -> inf)."""
+    b = gen.gen_gemm(300, 31)
+    sa = specs.paper_gpu_specs()
+    model = models.random_mlp(gen.GEMM, 6)
+    model["w1"] = np.full_like(model["w1"], 4000.0)
+    f, (gi, gf, gs) = gpu_features(sp, ctx, b, sa)
+    mh = ctx.load_model(model, "fp16")
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda")
+    ctx.predict(mh, f, lat)
+    torch.cuda.synchronize()
+    ok = gs == 0
+    assert not np.isnan(lat.cpu().numpy()[ok]).any()
+
+
 @pytest.mark.parametrize("prec", ["fp32", "fp16"])
 @pytest.mark.parametrize("fam", ["gemm", "attention"])
 def test_predict_non_identity_batchnorm(sp, ctx, orc, fam, prec):

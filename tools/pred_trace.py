@@ -62,3 +62,6 @@ print("per-warp (rows: warp = slot*8 + half*4 + quadrant), cycles from t0:")
 print("      " + " ".join(f"{n[:10]:>10}" for n in names))
 for w in range(16):
     print(f"w{w:2d}   " + " ".join(f"{wbuf[w, it, i] - t0:10d}" for i in range(8)))
+out = os.environ.get("PRED_TRACE_OUT")
+if out:  # raw stamps for offline analysis
+    np.savez(out, buf=buf, wbuf=wbuf)
