@@ -705,8 +705,8 @@ def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling,
     pairs_all = n_pairs * world if scaling == "weak" else n_specs * b.n_configs
     return {"value": pairs_all * steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "api": "Context.predict_host (pinned host configs -> H2D -> sp_featurize -> "
-                   "sp_predict -> D2H latencies)"}
+            "api": "sp_predict_host via Context.predict_host (pinned host configs -> pipelined H2D -> "
+                   "sp_featurize_predict -> D2H latencies, all inside libsynperf)"}
 
 
 def attention_work(b, sa, spec_range, feats, ms):

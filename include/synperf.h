@@ -16,8 +16,19 @@
  *    memory of the context's device (e.g. torch tensors' data_ptr()); HOST
  *    pointers are ordinary host memory and are only read during the call.
  *  - `stream` arguments are cudaStream_t passed as void* (NULL = legacy
- *    default stream).  sp_featurize / sp_predict are asynchronous on that
- *    stream: no allocation, no host synchronisation inside.
+ *    default stream).  sp_featurize / sp_predict / sp_featurize_predict are
+ *    asynchronous on that stream.  They use CONTEXT-OWNED device scratch --
+ *    the attention schedule plan of a spec range (built and uploaded with a
+ *    synchronous copy the first time the range is seen), the attention
+ *    per-config results and the fused pass's config pre-pass (grow-only:
+ *    a call with more configs than any before reallocates).  Hence:
+ *      * calls on one context must be serialized on one stream (two streams
+ *        sharing a context would race on that scratch; use one context per
+ *        stream for concurrency);
+ *      * a call that builds a plan or grows scratch allocates and
+ *        synchronizes: call sp_prepare first (or make one warm-up call at
+ *        the largest size) to make the following calls allocation-free and
+ *        safe to capture in a CUDA graph.
  *  - No exception crosses the ABI and the library never aborts.  Every call
  *    returns an sp_status; sp_last_error() describes the last failure (or
  *    the last warning) of a context.  There is no CPU fallback: without a
@@ -322,6 +333,18 @@ sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *
                        const sp_pairing *pairs, const sp_features *out, void *stream);
 
 /*
+ * Reserve the context-owned scratch (see Conventions) for calls of `family`
+ * with up to `n_configs` configs over specs [spec_begin, spec_end) (CROSS):
+ * builds and uploads the attention schedule plan of that range and grows the
+ * attention result / fused pre-pass scratch.  After it, sp_featurize,
+ * sp_predict and sp_featurize_predict at those sizes neither allocate nor
+ * synchronize (CUDA-graph capturable).  Synchronous.  Errors: SP_E_ARG,
+ * SP_E_UNSUPPORTED (as sp_featurize), SP_E_INTERNAL (allocation).
+ */
+sp_status sp_prepare(sp_ctx *ctx, int32_t family, int64_t n_configs, const sp_specs *specs, int32_t spec_begin,
+                     int32_t spec_end);
+
+/*
  * Scheduling Simulator variants ("supporting the two main scheduling
  * paradigms").  sp_featurize uses SP_SCHED_RR.
  *   SP_SCHED_RR      hardware round-robin as cyclic dealing, task t -> SM
@@ -390,14 +413,44 @@ sp_status sp_predict(sp_ctx *ctx, const sp_model *model, const sp_features *in, 
  * cores run the MLP instead of in a separate HBM-bound pass.  Applies to the
  * uniform-task families (GEMM, fused MoE, RMSNorm, SiLU&Mul, Scaled MM) with
  * SP_PAIRS_CROSS and a 16-bit (tcgen05) model; anything else runs the two
- * calls in sequence.  A small per-config pre-pass (96 B per config, in a
+ * calls in sequence.  A small per-config pre-pass (56 B per config, in a
  * context-owned grow-only scratch: the first call with more configs than
- * before allocates) runs first.  Asynchronous on `stream`; errors as
+ * before allocates; see sp_prepare) runs first.  Asynchronous on `stream`; errors as
  * sp_featurize and sp_predict.
  */
 sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs,
                                const sp_pairing *pairs, const sp_model *model, const sp_features *out,
                                float *latency_us, float *efficiency, void *stream);
+
+/*
+ * Host-buffer end-to-end prediction: SPEC's predict_latency batched
+ * over the CROSS pairing of specs [spec_begin, spec_end) x all configs --
+ * the call a user makes with configs in host memory.
+ *   host_cfg:     as sp_config_batch, but fields / ragged / ragged_off are
+ *                 HOST pointers (pinned memory gives asynchronous copies;
+ *                 pageable memory works, with staged copies)
+ *   host_latency: HOST fp32 [spec_end - spec_begin][n_configs], spec-major as
+ *                 sp_featurize numbers pairs; NaN for pairs with status != 0
+ *   slice_weights / n_slices: the configs are cut into slices pipelined over
+ *                 three streams (H2D of slice i+1 and D2H of slice i-1 overlap
+ *                 the kernels of slice i).  NULL weights: n_slices equal
+ *                 slices (0: the default, 4; attention also defaults to the
+ *                 weights (1, 3, 3, 1)); otherwise n_slices relative weights.
+ *                 A wide spec axis (>= 64 specs and >= 4 slices per spec)
+ *                 is sliced by spec instead (configs uploaded once).
+ *   stream:       the kernels run on it; the copies on two library streams
+ *                 ordered after the work already on `stream`.
+ * Each slice copies only its own range of the ragged data, planned from the
+ * host offsets at the slice boundaries and checked on the device; a batch
+ * whose ragged data is not laid out config by config is redone with one whole
+ * copy (same result).  Blocks until host_latency is written.  Uses context-
+ * owned grow-only device staging (the first call at a new size allocates):
+ * calls on one context must not run concurrently.  Errors: SP_E_ARG (NULL,
+ * sizes, range), then as sp_featurize_predict; SP_E_INTERNAL on a CUDA error.
+ */
+sp_status sp_predict_host(sp_ctx *ctx, const sp_config_batch *host_cfg, const sp_specs *specs,
+                          int32_t spec_begin, int32_t spec_end, const sp_model *model, float *host_latency,
+                          const float *slice_weights, int32_t n_slices, void *stream);
 
 /*
  * Performance-gap diagnosis (PAPER §VII).  A

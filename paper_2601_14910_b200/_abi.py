@@ -145,6 +145,8 @@ def _load():
         "sp_featurize_ex": (C.c_int, [vp, vp, vp, vp, i32, u32, vp, vp]),
         "sp_predict": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "sp_featurize_predict": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "sp_prepare": (C.c_int, [vp, i32, i64, vp, i32, i32]),
+        "sp_predict_host": (C.c_int, [vp, C.POINTER(sp_config_batch), vp, i32, i32, vp, vp, vp, i32, vp]),
         "sp_perf_gap": (C.c_int, [vp, vp, vp, vp, vp, i64, i32, i32, C.c_float, C.c_float, vp, vp, vp, vp]),
         "sp_set_profiling": (C.c_int, [vp, i32]),
         "sp_profile_read": (i32, [vp, C.POINTER(sp_kernel_stat), i32, i32]),
@@ -177,7 +179,7 @@ lib = _load()
 
 EXPORTED = ["sp_create", "sp_destroy", "sp_last_error", "sp_version", "sp_device_sms",
             "sp_load_gpu_specs", "sp_free_specs", "sp_specs_count", "sp_load_model",
-            "sp_free_model", "sp_featurize", "sp_featurize_sched", "sp_featurize_ex", "sp_predict", "sp_featurize_predict", "sp_perf_gap", "sp_set_profiling", "sp_profile_read",
+            "sp_free_model", "sp_featurize", "sp_featurize_sched", "sp_featurize_ex", "sp_predict", "sp_featurize_predict", "sp_predict_host", "sp_prepare", "sp_perf_gap", "sp_set_profiling", "sp_profile_read",
             "sp_e2e_plan_create", "sp_e2e_plan_update", "sp_e2e_plan_expand", "sp_free_e2e_plan", "sp_e2e_plan_info",
             "sp_e2e_plan_batch", "sp_load_comm_model", "sp_free_comm_model", "sp_e2e_compose",
             "sp_train_create", "sp_train_destroy", "sp_train_step", "sp_train_eval", "sp_train_export_count",

@@ -641,210 +641,60 @@ class Context:
         (stream or torch.cuda.current_stream(self.torch_device)).synchronize()
         return tot.numpy(), cat.numpy()
 
-    def _predict_host_by_spec(self, fam, fh, rh, oh, specs, model, g0, g1, out_t, chunks, stream):
-        """predict_host for a wide spec range: the configs go H2D once, then
-        spec slices [ga, gb) are featurised + predicted while the previous
-        slice's latencies -- a contiguous run of the spec-major output -- go D2H."""
-        G, C = g1 - g0, int(fh.shape[1])
-        bounds = [g0 + G * i // chunks for i in range(chunks + 1)]
-        gmax = max(b - a for a, b in zip(bounds, bounds[1:]))
-        dev = self.torch_device
-        key = ("spec", fam, tuple(fh.shape), C, gmax, 0 if rh is None else rh.numel())
-        cache = getattr(self, "_host_cache", None)
-        if cache is None or cache["key"] != key:
-            cache = {
-                "key": key,
-                "fields": torch.empty(tuple(fh.shape), dtype=torch.int32, device=dev),
-                "ragged": None if rh is None else torch.empty(max(rh.numel(), 1), dtype=torch.int32, device=dev),
-                "roff": None if oh is None else torch.empty(C, dtype=torch.int64, device=dev),
-                "feats": Features.empty(fam, gmax * C, dev),
-                "lat": [torch.empty(gmax * C, dtype=torch.float32, device=dev) for _ in range(2)],
-                "d2h": torch.cuda.Stream(dev),
-            }
-            self._host_cache = cache
-        comp = stream or torch.cuda.current_stream(dev)
-        s_d2h = cache["d2h"]
-        cache["fields"].copy_(fh, non_blocking=True)
-        if rh is not None:
-            cache["ragged"][:rh.numel()].copy_(rh, non_blocking=True)
-        if oh is not None:
-            cache["roff"].copy_(oh, non_blocking=True)
-        db = DeviceBatch(fam, cache["fields"], cache["ragged"], cache["roff"])
-        feats = cache["feats"]
-        done = []
-        for i, (ga, gb) in enumerate(zip(bounds, bounds[1:])):
-            n = (gb - ga) * C
-            lat = cache["lat"][i % 2]
-            if i >= 2:
-                comp.wait_event(done[i - 2])
-            feats.n_pairs = n
-            self.featurize_predict(db, specs, model, feats, lat, None, cross(ga, gb), comp)
-            ev = torch.cuda.Event()
-            ev.record(comp)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev)
-                out_t[(ga - g0) * C:(gb - g0) * C].copy_(lat[:n], non_blocking=True)
-                ev2 = torch.cuda.Event()
-                ev2.record(s_d2h)
-                done.append(ev2)
-        s_d2h.synchronize()
-        comp.wait_stream(s_d2h)
-        return out_t[:G * C].numpy()
+    def prepare(self, family: int, n_configs: int, specs: Specs, spec_range=None) -> None:
+        """sp_prepare: build the attention plan of the spec range and grow the
+        context scratch, so later calls at these sizes neither allocate nor
+        synchronize (and can be captured in a CUDA graph)."""
+        g0, g1 = spec_range if spec_range is not None else (0, len(specs))
+        self._check(lib.sp_prepare(self._h, int(family), int(n_configs), specs.handle, g0, g1))
 
     # -- end-to-end: host configs in, host latencies out
-    @staticmethod
-    def _ragged_slices(fam, fh, oh, bounds):
-        """Copy plan for the ragged data of predict_host's slices, from the host
-        arrays at the slice boundaries only: slice i takes [first offset, end of
-        its last config) -- exact when the batch lays its ragged data out config
-        by config, as the generators and any sequential builder do.  The plan is
-        verified on the device (_ragged_guard) and the call is redone with one
-        whole copy if it does not hold.  None: no plan (copy whole)."""
-        if oh is None or fam not in (_abi.SP_ATTENTION, _abi.SP_FUSED_MOE) or len(bounds) < 3:
-            return None
-        row, mult = (0, 2) if fam == _abi.SP_ATTENTION else (1, 1)
-        out, prev = [], 0
-        for a, b in zip(bounds, bounds[1:]):
-            ia = next((k for k in range(a, min(b, a + 64)) if int(oh[k]) >= 0), None)
-            ib = next((k for k in range(b - 1, max(a - 1, b - 65), -1) if int(oh[k]) >= 0), None)
-            if ia is None or ib is None:
-                return None  # long runs of balanced MoE configs: no cheap boundary, copy whole
-            lo, hi = int(oh[ia]), int(oh[ib]) + mult * int(fh[row, ib])
-            if lo < prev or hi < lo:
-                return None
-            out.append((lo, hi))
-            prev = hi
-        return out
-
-    @staticmethod
-    def _ragged_guard(fam, cache, c0, c1, lo, hi, stream):
-        """Device check of slice [c0, c1)'s ragged copy plan: a config whose ragged
-        data is not inside [lo, hi) gets its length field zeroed in the device
-        copy (so it is a cheap SP_PAIR_E_DIM pair instead of reading stale data);
-        returns a device bool, True when the plan held for every config."""
-        row, mult = (0, 2) if fam == _abi.SP_ATTENTION else (1, 1)
-        with torch.cuda.stream(stream):
-            off = cache["roff"][c0:c1]
-            ln = cache["fields"][row, c0:c1]
-            end = off + mult * ln.to(torch.int64)
-            bad = (off >= 0) & ((off < lo) | (end > hi))
-            ln.masked_fill_(bad, 0)
-            return ~bad.any()
-
     def predict_host(self, batch, specs: Specs, model: Model, spec_range=None,
                      out: np.ndarray | torch.Tensor | None = None, chunks=None,
-                     stream=None, _plan: bool = True) -> np.ndarray:
-        """The user-facing call.  Host config arrays (numpy or torch; pinned
-        memory gives asynchronous copies) -> H2D -> sp_featurize_predict (fused, or sp_featurize -> sp_predict)
-        -> D2H of fp32 latencies in spec-major order [spec][config].
-
-        The configs are split into `chunks` slices (a count, or slice weights;
-        default: (1, 3, 3, 1) for attention, whose kernels outlast the copies --
-        a short first copy-in and last copy-out -- and 4 equal slices for the
-        copy-bound uniform families) pipelined over three streams: the H2D of slice i+1 and the D2H of slice i-1 overlap the
-        kernels of slice i (the ragged request / histogram data is copied
-        whole, ahead of the first slice).  Device buffers are cached across
-        calls."""
+                     stream=None) -> np.ndarray:
+        """The user-facing call, sp_predict_host: host config arrays (numpy or
+        torch; pinned memory gives asynchronous copies) -> pipelined H2D /
+        featurize + predict / D2H inside the library -> fp32 latencies in
+        spec-major order [spec][config] (a numpy view of `out`, pinned by
+        default).  `chunks`: a slice count, or relative slice weights such as
+        (1, 3, 3, 1); None = the library default."""
         g0, g1 = spec_range if spec_range is not None else (0, len(specs))
-        G = g1 - g0
         fam = int(batch.family)
 
         def host_t(a, dt):
             if a is None:
                 return None
             t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
-            return t if t.dtype == dt else t.to(dt)
+            t = t if t.dtype == dt else t.to(dt)
+            assert t.device.type == "cpu", "predict_host takes host arrays"
+            return t.contiguous()
 
         fh = host_t(batch.fields, torch.int32)
         rh = host_t(batch.ragged, torch.int32)
         oh = host_t(batch.ragged_off, torch.int64)
-        nf, C = int(fh.shape[0]), int(fh.shape[1])
-        n = G * C
+        nf, C_ = int(fh.shape[0]), int(fh.shape[1])
+        n = (g1 - g0) * C_
         if out is None:
             out_t = torch.empty(max(n, 1), dtype=torch.float32, pin_memory=True)
         else:
             out_t = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+        assert out_t.dtype == torch.float32 and out_t.is_contiguous() and out_t.numel() >= n
         if n == 0:
             return out_t[:0].numpy()
-        if chunks is None:
-            chunks = (1, 3, 3, 1) if fam == _abi.SP_ATTENTION else 4
-        weights = None
-        if not isinstance(chunks, int):  # explicit slice weights, e.g. (1, 3, 3, 1)
-            weights = [float(w) for w in chunks]
-            chunks = len(weights)
-        if G >= 64 and G >= 4 * chunks:  # wide spec axis (e.g. config 5): pipeline over specs
-            return self._predict_host_by_spec(fam, fh, rh, oh, specs, model, g0, g1, out_t,
-                                              max(chunks, 8), stream)
-        chunks = max(1, min(chunks, C))
-        if weights is None or len(weights) != chunks:
-            bounds = [C * i // chunks for i in range(chunks + 1)]
-        else:
-            cum = np.concatenate([[0.0], np.cumsum(weights)]) / sum(weights)
-            bounds = sorted(set([0, C] + [int(C * x) for x in cum]))
-            chunks = len(bounds) - 1
-        cmax = max(b1 - b0 for b0, b1 in zip(bounds, bounds[1:]))
-        dev = self.torch_device
-        key = (fam, nf, C, G, cmax, 0 if rh is None else rh.numel())
-        cache = getattr(self, "_host_cache", None)
-        if cache is None or cache["key"] != key:
-            cache = {
-                "key": key,
-                "fields": torch.empty((nf, C), dtype=torch.int32, device=dev),
-                "ragged": None if rh is None else torch.empty(max(rh.numel(), 1), dtype=torch.int32, device=dev),
-                "roff": None if oh is None else torch.empty(C, dtype=torch.int64, device=dev),
-                "feats": Features.empty(fam, G * cmax, dev),
-                "lat": [torch.empty(G * cmax, dtype=torch.float32, device=dev) for _ in range(2)],
-                "h2d": torch.cuda.Stream(dev),
-                "d2h": torch.cuda.Stream(dev),
-            }
-            self._host_cache = cache
-        comp = stream or torch.cuda.current_stream(dev)
-        s_h2d, s_d2h = cache["h2d"], cache["d2h"]
-        s_h2d.wait_stream(comp)
-        out2d = out_t[:n].view(G, C)
-        ranges = None
-        if rh is not None and rh.numel() > 0:
-            ranges = self._ragged_slices(fam, fh, oh, bounds) if _plan else None
-            if ranges is None:  # one copy ahead of the first slice
-                with torch.cuda.stream(s_h2d):
-                    cache["ragged"][:rh.numel()].copy_(rh, non_blocking=True)
-        d2h_done, oks = [], []
-        for i, (c0, c1) in enumerate(zip(bounds, bounds[1:])):
-            nc = c1 - c0
-            with torch.cuda.stream(s_h2d):
-                for fi in range(nf):  # contiguous row pieces: async DMA from pinned memory
-                    cache["fields"][fi, c0:c1].copy_(fh[fi, c0:c1], non_blocking=True)
-                if cache["roff"] is not None:
-                    cache["roff"][c0:c1].copy_(oh[c0:c1], non_blocking=True)
-                if ranges is not None and ranges[i][1] > ranges[i][0]:  # this slice's own ragged range
-                    lo, hi = ranges[i]
-                    cache["ragged"][lo:hi].copy_(rh[lo:hi], non_blocking=True)
-                if ranges is not None:  # on the copy stream: off the kernels' critical path
-                    oks.append(self._ragged_guard(fam, cache, c0, c1, ranges[i][0], ranges[i][1], s_h2d))
-                ev = torch.cuda.Event()
-                ev.record(s_h2d)
-            comp.wait_event(ev)
-            db = DeviceBatch(fam, cache["fields"][:, c0:c1], cache["ragged"],
-                             None if cache["roff"] is None else cache["roff"][c0:c1])
-            feats = cache["feats"]
-            feats.n_pairs = G * nc
-            lat = cache["lat"][i % 2]
-            if i >= 2:  # the D2H that read this buffer two slices ago must be done
-                comp.wait_event(d2h_done[i - 2])
-            self.featurize_predict(db, specs, model, feats, lat, None, cross(g0, g1), comp)
-            ev2 = torch.cuda.Event()
-            ev2.record(comp)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev2)
-                for g in range(G):  # contiguous row pieces: async DMA into pinned memory
-                    out2d[g, c0:c1].copy_(lat[g * nc:(g + 1) * nc], non_blocking=True)
-                ev3 = torch.cuda.Event()
-                ev3.record(s_d2h)
-                d2h_done.append(ev3)
-        s_d2h.synchronize()
-        comp.wait_stream(s_d2h)
-        if oks and not bool(torch.stack(oks).all().item()):  # the boundary plan missed some ragged data
-            return self.predict_host(batch, specs, model, spec_range, out_t, chunks, stream, _plan=False)
+        cb = _abi.sp_config_batch(fam, nf, C_, C_, fh.data_ptr(),
+                                  rh.data_ptr() if rh is not None and rh.numel() else None,
+                                  oh.data_ptr() if oh is not None else None,
+                                  rh.numel() if rh is not None else 0)
+        w = None
+        ns = 0
+        if chunks is not None:
+            if isinstance(chunks, int):
+                ns = int(chunks)
+            else:
+                w = (C.c_float * len(chunks))(*[float(x) for x in chunks])
+                ns = len(chunks)
+        self._check(lib.sp_predict_host(self._h, C.byref(cb), specs.handle, g0, g1, model.handle,
+                                        out_t.data_ptr(), w, ns, _stream_ptr(stream)))
         return out_t[:n].numpy()
 
 

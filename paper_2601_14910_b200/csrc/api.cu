@@ -291,6 +291,51 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
   return SP_OK;
 }
 
+// Context scratch, grow-only (include/synperf.h Conventions; sp_prepare).
+static sp_status grow_buf(sp_ctx *ctx, void *&p, size_t &bytes, size_t need, const char *what) {
+  if (need <= bytes) return SP_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  cudaError_t me = cudaMalloc(&p, need);
+  if (me != cudaSuccess) {
+    p = nullptr;
+    return cuda_fail(ctx, me, what);
+  }
+  bytes = need;
+  return SP_OK;
+}
+// attention per-config results of the schedule kernel: st (4 B), L, U, and maxS/maxB per slot (8 B each)
+static sp_status grow_attn_res(sp_ctx *ctx, int64_t C, int n_slots) {
+  const int64_t ld = (C + 31) & ~(int64_t)31;
+  return grow_buf(ctx, ctx->attn_res, ctx->attn_res_bytes, (size_t)ld * (4 + 8 + 8 + 16 * (size_t)n_slots),
+                  "attention result scratch");
+}
+static sp_status grow_pre(sp_ctx *ctx, int64_t C) {
+  const int64_t ldc = (C + 31) & ~(int64_t)31;
+  return grow_buf(ctx, ctx->pre, ctx->pre_bytes, (size_t)ldc * kPreFields * sizeof(uint64_t),
+                  "fused pre-pass scratch");
+}
+
+extern "C" sp_status sp_prepare(sp_ctx *ctx, int32_t family, int64_t n_configs, const sp_specs *specs_c,
+                                int32_t spec_begin, int32_t spec_end) {
+  if (!ctx) return fail(nullptr, SP_E_ARG, "sp_prepare: ctx is NULL");
+  if (!specs_c || nfields_of(family) < 0 || n_configs < 0) return fail(ctx, SP_E_ARG, "sp_prepare: bad argument");
+  sp_specs *specs = const_cast<sp_specs *>(specs_c);
+  if (spec_begin < 0 || spec_end > specs->n || spec_begin > spec_end)
+    return fail(ctx, SP_E_ARG, "sp_prepare: spec range out of bounds");
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  if (family == SP_ATTENTION) {
+    const AttnPlan *plan = nullptr;
+    sp_status st = attn_plan(ctx, specs, spec_begin, spec_end, &plan);
+    if (st != SP_OK) return st;
+    return grow_attn_res(ctx, n_configs, plan->n_slots);
+  }
+  if (family != SP_GEMM_SPLITK) return grow_pre(ctx, n_configs);
+  return SP_OK;
+}
+
 // --------------------------------------------------------------- featurize
 
 extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs_c,
@@ -395,18 +440,8 @@ extern "C" sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, co
       run.counters = ctx->counters;
       // per-config results of the schedule kernel: st (4 B), L, U, and maxS/maxB per slot (8 B each)
       const int64_t C = cfg->n_configs, ld = (C + 31) & ~(int64_t)31;
-      const size_t need = (size_t)ld * (4 + 8 + 8 + 16 * (size_t)run.n_slots);
-      if (need > ctx->attn_res_bytes) {
-        if (ctx->attn_res) cudaFree(ctx->attn_res);
-        ctx->attn_res = nullptr;
-        ctx->attn_res_bytes = 0;
-        cudaError_t me = cudaMalloc(&ctx->attn_res, need);
-        if (me != cudaSuccess) {
-          ctx->attn_res = nullptr;
-          return cuda_fail(ctx, me, "sp_featurize: attention result scratch");
-        }
-        ctx->attn_res_bytes = need;
-      }
+      st = grow_attn_res(ctx, C, run.n_slots);
+      if (st != SP_OK) return st;
       char *base = (char *)ctx->attn_res;
       AttnResults res;
       res.ld = ld;
@@ -481,17 +516,8 @@ extern "C" sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cf
   cudaSetDevice(ctx->device);
   const int64_t C = cfg->n_configs, ldc = (C + 31) & ~(int64_t)31;
   const size_t need = (size_t)ldc * kPreFields * sizeof(uint64_t);
-  if (need > ctx->pre_bytes) {
-    if (ctx->pre) cudaFree(ctx->pre);
-    ctx->pre = nullptr;
-    ctx->pre_bytes = 0;
-    cudaError_t me = cudaMalloc(&ctx->pre, need);
-    if (me != cudaSuccess) {
-      ctx->pre = nullptr;
-      return cuda_fail(ctx, me, "sp_featurize_predict: pre-pass scratch");
-    }
-    ctx->pre_bytes = need;
-  }
+  sp_status gst = grow_pre(ctx, C);
+  if (gst != SP_OK) return gst;
   ConfigView cv{cfg->fields, cfg->ragged, cfg->ragged_off, cfg->n_configs, cfg->field_ld};
   const LaunchHook h = ctx->hook();
   h.on_begin("uniform_prepass", stream);

@@ -24,6 +24,27 @@ struct sp_ctx {
   void *pre = nullptr;  // DEVICE config pre-pass of the fused path (kPreFields u64 per config), grow-only
   size_t pre_bytes = 0;
   std::string err;
+  // sp_predict_host (host.cu): grow-only device staging, two copy streams, events
+  struct HostBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    cudaError_t need(size_t n) {
+      if (n <= bytes) return cudaSuccess;
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      cudaError_t e = cudaMalloc(&p, n);
+      if (e == cudaSuccess) bytes = n;
+      else p = nullptr;
+      return e;
+    }
+    ~HostBuf() {
+      if (p) cudaFree(p);
+    }
+  };
+  HostBuf h_fields, h_ragged, h_roff, h_feats, h_lat[2], h_flag;
+  cudaStream_t h_h2d = nullptr, h_d2h = nullptr;
+  std::vector<cudaEvent_t> h_events;  // sync-only events, reused across calls
   // kernel accounting (sp_set_profiling / sp_profile_read)
   struct KStat {
     int64_t launches = 0;
@@ -42,6 +63,9 @@ struct sp_ctx {
   const char *open_kernel = nullptr;
   cudaEvent_t open_ev = nullptr;
   ~sp_ctx() {
+    if (h_h2d) cudaStreamDestroy(h_h2d);
+    if (h_d2h) cudaStreamDestroy(h_d2h);
+    for (auto e : h_events) cudaEventDestroy(e);
     if (counters) cudaFree(counters);
     if (attn_res) cudaFree(attn_res);
     if (pre) cudaFree(pre);

@@ -433,6 +433,68 @@ def test_predict_host_irregular_ragged_layout(sp, ctx, layout):
     assert np.array_equal(got, lat.cpu().numpy(), equal_nan=True)
 
 
+@pytest.mark.parametrize("fam", ["attention", "moe"])
+def test_predict_host_pageable_weights_subrange(sp, ctx, fam):
+    """sp_predict_host from pageable numpy arrays, explicit slice weights, a
+    spec sub-range: the device path's latencies for those specs, bit for bit."""
+    b = FAMILY_BATCHES[fam]()
+    sa = specs.paper_gpu_specs()
+    sh = ctx.load_gpu_specs(sa)
+    m = ctx.load_model(models.random_mlp(b.family, 5), "fp16")
+    db = sp.DeviceBatch.from_host(b, ctx.torch_device)
+    n = 5 * b.n_configs
+    f = sp.Features.empty(b.family, n, ctx.torch_device)
+    lat = torch.empty(n, dtype=torch.float32, device="cuda")
+    ctx.featurize(db, sh, f, sp.cross(2, 7))
+    ctx.predict(m, f, lat)
+    torch.cuda.synchronize()
+    got = ctx.predict_host(b, sh, m, spec_range=(2, 7), chunks=(1, 3, 3, 1))
+    assert np.array_equal(got, lat.cpu().numpy(), equal_nan=True)
+    got2 = ctx.predict_host(b, sh, m, spec_range=(2, 7), chunks=7)  # reuses the grown staging
+    assert np.array_equal(got2, got, equal_nan=True)
+
+
+def test_predict_host_argument_errors(sp, ctx):
+    b = FAMILY_BATCHES["gemm"]()
+    sa = specs.paper_gpu_specs()
+    sh = ctx.load_gpu_specs(sa)
+    m = ctx.load_model(models.random_mlp(b.family, 5), "fp16")
+    with pytest.raises(sp.SynPerfError, match="SP_E_ARG"):
+        ctx.predict_host(b, sh, m, spec_range=(3, 40))
+    mm = ctx.load_model(models.random_mlp(gen.ATTENTION, 5), "fp16")
+    with pytest.raises(sp.SynPerfError, match="SP_E_ARG"):  # family mismatch, from sp_featurize_predict
+        ctx.predict_host(b, sh, mm)
+
+
+@pytest.mark.parametrize("fam", ["attention", "gemm"])
+def test_prepare_then_graph_capture(sp, ctx, fam):
+    """After sp_prepare the hot calls neither allocate nor synchronize: a fresh
+    context captures featurize_predict in a CUDA graph, and replays equal the
+    eager result."""
+    b = FAMILY_BATCHES[fam]()
+    sa = specs.paper_gpu_specs()
+    c2 = sp.Context(0)
+    sh = c2.load_gpu_specs(sa)
+    m = c2.load_model(models.random_mlp(b.family, 5), "fp16")
+    db = sp.DeviceBatch.from_host(b, c2.torch_device)
+    n = len(sa) * b.n_configs
+    f = sp.Features.empty(b.family, n, c2.torch_device)
+    lat = torch.empty(n, dtype=torch.float32, device="cuda")
+    c2.prepare(b.family, b.n_configs, sh)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        c2.featurize_predict(db, sh, m, f, lat, stream=s)
+    lat.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    got = lat.cpu().numpy().copy()
+    lat2 = torch.empty_like(lat)
+    c2.featurize_predict(db, sh, m, f, lat2)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, lat2.cpu().numpy(), equal_nan=True)
+
+
 def test_featurize_deterministic(sp, ctx):
     b = FAMILY_BATCHES["attention"]()
     sa = specs.paper_gpu_specs()
