@@ -51,34 +51,66 @@ E2E_MODELS = ("llama3-8b", "qwen2.5-14b")
 E2E_FAMILIES = (gen.GEMM, gen.ATTENTION, gen.RMSNORM, gen.SILU_MUL)
 
 
-def build_workload(name: str, rank: int, world: int, scale: float = 1.0):
-    """Returns (batch, spec_array, (g0, g1), scaling) for this rank."""
+def build_workload(name: str, rank: int, world: int, scale: float = 1.0, scaling: str | None = None):
+    """Returns (batch, spec_array, (g0, g1), scaling).  Strong scaling (the
+    default): the same global workload on every rank, which
+    run_gpu shards with dist.Sharder (see SHARDING); weak: rank r's own
+    full-size workload (seeded by r) over all specs."""
+    weak = scaling == "weak"
+    r = rank if weak else 0
+    scaling = "weak" if weak else "strong"
     if name == "cfg1":
-        return gen.gen_gemm(1000, 1001), specs.spec_by_name("A100"), (0, 1), "weak"
+        return gen.gen_gemm(1000, 1001 + 7919 * r), specs.spec_by_name("A100"), (0, 1), scaling
     if name == "cfg2":
         n = int(500_000 * scale)
-        b = gen.gen_attention(n, n, 1002 + 7919 * rank)
-        b, _ = gen.shuffle(b, 7 + rank)  # mix prefill/decode cost for balance (SURVEY §8(e))
+        b = gen.gen_attention(n, n, 1002 + 7919 * r)
         sa = specs.paper_gpu_specs()
-        return b, sa, (0, len(sa)), "weak"
+        return b, sa, (0, len(sa)), scaling
     if name == "cfg3":
-        b = gen.gen_moe(int(1_000_000 * scale), 1003 + 7919 * rank)
+        b = gen.gen_moe(int(1_000_000 * scale), 1003 + 7919 * r)
         sa = specs.paper_gpu_specs()
-        return b, sa, (0, len(sa)), "weak"
+        return b, sa, (0, len(sa)), scaling
     if name == "scaledmm":
-        b = gen.gen_scaled_mm(int(1_000_000 * scale), 1006 + 7919 * rank)
+        b = gen.gen_scaled_mm(int(1_000_000 * scale), 1006 + 7919 * r)
         sa = specs.paper_gpu_specs()
-        return b, sa, (0, len(sa)), "weak"
+        return b, sa, (0, len(sa)), scaling
     if name == "splitk":
-        b = gen.gen_gemm_splitk(int(1_000_000 * scale), 1007 + 7919 * rank)
+        b = gen.gen_gemm_splitk(int(1_000_000 * scale), 1007 + 7919 * r)
         sa = specs.paper_gpu_specs()
-        return b, sa, (0, len(sa)), "weak"
+        return b, sa, (0, len(sa)), scaling
     if name == "cfg5":
         b = gen.gen_serving_gemms(1000, 1005)
         sa = specs.hypothetical_sweep_specs(int(100_000 * scale))
-        G = len(sa)
-        return b, sa, (rank * G // world, (rank + 1) * G // world), "strong"
+        return b, sa, (0, len(sa)), "strong"  # the 10^8-pair sweep is one workload, sharded by spec
     raise SystemExit(f"unknown workload {name}")
+
+
+# How the bench shards each workload across ranks (dist.Sharder): the config
+# axis after a seeded shuffle (cost balance: attention configs range over five
+# orders of magnitude of tasks; at N = 1 the shuffle is the cfg2 order the
+# tests use, gen.shuffle(b, 7)), or the spec axis for the 10^5-spec sweep.
+SHARDING = {"cfg5": ("spec", None)}
+DEFAULT_SHARDING = ("config", 7)
+
+
+def sharder_for(name: str, b, sa, rank: int, world: int, scaling: str, chunks: int):
+    from paper_2601_14910_b200.dist import Sharder
+
+    axis, seed = SHARDING.get(name, DEFAULT_SHARDING)
+    if scaling == "weak":  # the rank's own workload, unsharded
+        return Sharder(b.n_configs, len(sa), 1, 0, axis, seed, chunks)
+    return Sharder(b.n_configs, len(sa), world, rank, axis, seed, chunks)
+
+
+def local_workload(name: str, scale: float = 1.0):
+    """The single-GPU bench workload as run_gpu computes it (the shard of rank 0
+    of 1: the global batch in the sharder's order) -- for the tools."""
+    b, sa, rng, scaling = build_workload(name, 0, 1, scale)
+    sh = sharder_for(name, b, sa, 0, 1, scaling, 1)
+    cfg = sh.configs
+    if len(cfg) != b.n_configs or not np.array_equal(cfg, np.arange(len(cfg))):
+        b = b.subset(cfg)
+    return b, sa, rng, scaling
 
 
 # -------------------------------------------------------------------- clocks
@@ -302,6 +334,7 @@ def run_gpu(args, rank, world, local_rank):
     import torch
 
     import paper_2601_14910_b200 as sp
+    from paper_2601_14910_b200.dist import ShardedPredictor
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -311,58 +344,57 @@ def run_gpu(args, rank, world, local_rank):
 
         dist.init_process_group("nccl", device_id=dev)
     ctx = sp.Context(local_rank)
-    b, sa, (g0, g1), scaling = build_workload(args.workload, rank, world, args.scale)
+    b, sa, (g0, g1), scaling = build_workload(args.workload, rank, world, args.scale, args.scaling)
+    # the all-gather of chunk k overlaps chunk k+1's compute; each extra chunk costs a launch tail
+    # (measured at N = 1: 4 chunks +16% on cfg2, +7% on cfg3), so N > 1 defaults to 2
+    chunks = args.chunks if args.chunks > 0 else (1 if world == 1 else 2)
+    sharder = sharder_for(args.workload, b, sa, rank, world, scaling, chunks)
     specs_h = ctx.load_gpu_specs(sa)
     model_d = models.random_mlp(b.family, 42)
     precision = args.precision
     model = ctx.load_model(model_d, precision)
     n_in = int(model_d["n_in"])
-    db = sp.DeviceBatch.from_host(b, dev)
-    n_pairs = (g1 - g0) * b.n_configs
-    feats = sp.Features.empty(b.family, n_pairs, dev)
-    # predictions padded to the all-gather's equal per-rank count (dist.Sharder)
-    from paper_2601_14910_b200.dist import Sharder
-
-    if scaling == "strong":
-        padded = Sharder(b.n_configs, len(sa), world, rank, "spec").padded_pairs
-    else:
-        padded = n_pairs  # weak scaling: every rank has a same-sized workload of its own
-    lat = torch.full((max(padded, 1),), float("nan"), dtype=torch.float32, device=dev)
-    pairs = sp.cross(g0, g1)
+    # this rank's shard: configs sharder.configs x specs sharder.spec_range, uploaded once
+    pred = ShardedPredictor(ctx, b, sa, model, sharder, specs=specs_h)
+    g0, g1 = sharder.spec_range
+    n_pairs = sharder.local_pairs
     stream = torch.cuda.current_stream()
-    gathered = None
-    if dist is not None and not args.no_gather:
-        gathered = torch.empty(world * padded, dtype=torch.float32, device=dev)
+    gather = world > 1 and not args.no_gather
+    gathered_weak = None
+    if gather and scaling == "weak":  # every rank's own full workload: one all-gather of it
+        gathered_weak = torch.empty(world * sharder.padded_pairs, dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    if args.scheduler != "rr" or (args.fused == "off" and b.family in FUSABLE) or precision == "fp32":
+        # variants outside the fused pass: sp_featurize_sched + sp_predict (unsharded, rank-local)
+        feats_v = sp.Features.empty(b.family, n_pairs, dev)
+        lat_v = torch.empty(max(n_pairs, 1), dtype=torch.float32, device=dev)
 
-    # fused feature + predictor pass (sp_featurize_predict) for the uniform families
-    fused = (args.fused == "on" or (args.fused == "auto" and b.family in FUSABLE)) and \
-        args.scheduler == "rr" and precision != "fp32"
+        def compute():
+            ctx.featurize(pred.db, specs_h, feats_v, sp.cross(g0, g1), stream, scheduler=args.scheduler)
+            ctx.predict(model, feats_v, lat_v, None, stream)
+    else:
+        feats_v = lat_v = None
+
+        def compute():
+            if scaling == "strong" and gather:
+                pred.run()  # chunk by chunk, the all-gather of chunk k overlapping chunk k+1
+            else:
+                pred.run(gather=False)
+                if gathered_weak is not None:
+                    dist.all_gather_into_tensor(gathered_weak, pred.local)
 
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        if fused:
-            ctx.featurize_predict(db, specs_h, model, feats, lat, None, pairs, stream)
-            if ev is not None:
-                ev[1].record(stream)
-        else:
-            ctx.featurize(db, specs_h, feats, pairs, stream, scheduler=args.scheduler)
-            if ev is not None:
-                ev[1].record(stream)
-            ctx.predict(model, feats, lat, None, stream)
+        compute()
         if ev is not None:
-            ev[2].record(stream)
-        if gathered is not None:  # the single exchange: ncclAllGather of fp32 predictions
-            dist.all_gather_into_tensor(gathered, lat[:padded])
-        if ev is not None:
-            ev[3].record(stream)
+            ev[1].record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -377,36 +409,43 @@ def run_gpu(args, rank, world, local_rank):
     kst = ctx.profile_read(reset=True)  # {kernel: (launches, device ms)} of the timed region
     if dist is not None:
         dist.barrier()
-    t_feat = np.array([e[0].elapsed_time(e[1]) for e in evs])
-    t_pred = np.array([e[1].elapsed_time(e[2]) for e in evs])
-    t_step = np.array([e[0].elapsed_time(e[3]) for e in evs])
+    t_step = np.array([e[0].elapsed_time(e[1]) for e in evs])
     tot_ms = float(t_step.sum())
     if dist is not None:
         t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    pairs_all = n_pairs * (world if scaling == "weak" else 1)
-    if scaling == "strong":
-        pairs_all = len(sa) * b.n_configs
+    pairs_all = n_pairs * world if scaling == "weak" else len(sa) * b.n_configs
     value = pairs_all * args.steps / (tot_ms * 1e-3)
 
-    # ---- parity spot-check of this run's output (sampled, oracle) is done in tests;
-    # here only sanity: no NaN outside error pairs.
-    st = feats.status[:n_pairs]
-    bad = int(((st == 0) & torch.isnan(lat[:n_pairs])).sum().item())
-    if bad:
-        raise SystemExit(f"{bad} valid pairs produced NaN latency")
+    # the last step's records and latencies in this rank's local order (one chunk: all of them)
+    one_pass = feats_v is not None or len(sharder.chunk_bounds()) == 1
+    feats = feats_v if feats_v is not None else pred.feats
+    lat = lat_v if lat_v is not None else pred.last
+    if one_pass:  # sanity: no NaN outside error pairs
+        st = feats.status[:n_pairs]
+        bad = int(((st == 0) & torch.isnan(lat[:n_pairs])).sum().item())
+        if bad:
+            raise SystemExit(f"{bad} valid pairs produced NaN latency")
 
-    # ---- e2e through the public API with host buffers (rank-local)
-    e2e = run_e2e(args, ctx, specs_h, model, b, (g0, g1), dev, dist, world, scaling, len(sa))
+    # ---- e2e through the public API with host buffers (this rank's shard)
+    local_b = b if (sharder.axis == "spec" or np.array_equal(sharder.configs, np.arange(b.n_configs))) \
+        else b.subset(sharder.configs)
+    e2e = run_e2e(args, ctx, specs_h, model, local_b, (g0, g1), dev, dist, world, scaling, len(sa),
+                  pairs_all)
 
     # ---- roofline of the dominant kernel
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json")) or {}
-    feat_ms, pred_ms = float(t_feat.mean()), float(t_pred.mean())
-    roof = roofline(args, b, n_pairs, n_in, precision, kst, peaks, prof, tot_ms)
-    if b.family == gen.ATTENTION and roof["kernel"] == "attn_schedule_cross":
-        roof["algorithmic"] = attention_work(b, sa, (g0, g1), feats, roof["avg_launch_ms"])
+    n_chunks = 1 if feats_v is not None else len(sharder.chunk_bounds())
+    roof = roofline(args, local_b, n_pairs / n_chunks, n_in, precision, kst, peaks, prof, tot_ms)
+    if b.family == gen.ATTENTION and roof["kernel"] == "attn_schedule_cross" and one_pass:
+        roof["algorithmic"] = attention_work(local_b, sa, (g0, g1), feats, roof["avg_launch_ms"])
+    stage = {}
+    for k, (n, t) in kst.items():
+        key = "predict" if k.startswith("predict") else "featurize"
+        stage[key] = stage.get(key, 0.0) + t / args.steps
+    stage["other (copies, all-gather wait)"] = max(0.0, tot_ms / args.steps - sum(stage.values()))
 
     line = {
         "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -419,11 +458,14 @@ def run_gpu(args, rank, world, local_rank):
             "pairs_per_gpu": n_pairs, "configs_per_gpu": b.n_configs, "specs": g1 - g0,
             "family": gen.FAMILY_NAMES[b.family], "mlp_precision": precision,
             "scheduler": args.scheduler,
-            "parallelism": f"dp{world}" + ("+allgather" if gathered is not None else ""),
+            "parallelism": f"dp{world}" + ("+allgather" if gather else ""),
+            "sharding": {"axis": sharder.axis, "seeded_shuffle": sharder.axis == "config" and
+                         SHARDING.get(args.workload, DEFAULT_SHARDING)[1] is not None,
+                         "allgather_chunks": n_chunks if gather else 0,
+                         "pairs_this_rank": n_pairs, "pairs_total": pairs_all},
             "l2": "flushed between timed steps (256 MiB write, outside the events)",
         },
-        "stage_ms": {("featurize+predict (fused)" if fused else "featurize"): feat_ms, "predict": pred_ms,
-                     "allgather": float((t_step - t_feat - t_pred).mean())},
+        "stage_ms": stage,
         "roofline": roof,
         "kernels": {k: {"launches": n, "avg_ms": t / max(n, 1)} for k, (n, t) in sorted(kst.items())},
         "e2e": e2e,
@@ -437,22 +479,29 @@ def run_gpu(args, rank, world, local_rank):
             "value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
             "sample": f"{n} random pairs of this workload, fp64 oracle featurize+predict, {dt:.1f} s",
             "single_core_value": v1}
-        line["parity"] = parity_stats(keep, feats, lat, precision)
+        if one_pass:
+            line["parity"] = parity_stats(keep, feats, lat, precision, sharder)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
 
-def parity_stats(keep, feats, lat, precision):
+def parity_stats(keep, feats, lat, precision, sharder):
     """north_star's bar on this run's own output: the GPU records and latencies
     of the last timed step at the cpu_baseline sample's pairs, against the
-    oracle's values for the same pairs (computed by the timed oracle run)."""
+    oracle's values for the same pairs (computed by the timed oracle run).
+    The sample's pairs are global (g * C + c); the run's buffers are in the
+    shard's local order [g][position of c in sharder.configs] (N = 1)."""
     import torch
 
     p = keep["pairs"]
     o = keep["feats"]
-    idx = torch.from_numpy(p).to(feats.status.device)
+    C = sharder.n_configs
+    inv = np.empty(C, dtype=np.int64)
+    inv[sharder.configs] = np.arange(C)
+    local = (p // C) * C + inv[p % C]
+    idx = torch.from_numpy(local).to(feats.status.device)
     gs = feats.status[idx].cpu().numpy()
     gi = feats.ints[:, idx].cpu().numpy()
     gf = feats.flts[:, idx].cpu().numpy().astype(np.float64)
@@ -667,7 +716,7 @@ def roofline_e2e(infos, G, kst, peaks, prof, tot_ms, args):
             "launches": launches, "per_unit": per_unit, "peak_source": src}
 
 
-def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling, n_specs):
+def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling, n_specs, pairs_all):
     """Same metric through Context.predict_host with pinned host buffers: every
     step copies the configs H2D and the fp32 latencies D2H."""
     import torch
@@ -702,7 +751,6 @@ def run_e2e(args, ctx, specs_h, model, b, spec_range, dev, dist, world, scaling,
         tt = torch.tensor([el], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         el = float(tt.item())
-    pairs_all = n_pairs * world if scaling == "weak" else n_specs * b.n_configs
     return {"value": pairs_all * steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
             "api": "sp_predict_host via Context.predict_host (pinned host configs -> pipelined H2D -> "
@@ -789,6 +837,11 @@ def main():
     ap.add_argument("--fused", default="auto", choices=["auto", "on", "off"],
                     help="sp_featurize_predict for the uniform families (auto) or never (off)")
     ap.add_argument("--no-gather", action="store_true")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="strong (default): one global workload sharded across ranks; weak: every rank "
+                         "its own full-size workload (cfg5 is always strong)")
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="all-gather chunks overlapped with compute (0: 1 at N=1, 2 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=5)

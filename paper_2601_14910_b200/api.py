@@ -61,6 +61,12 @@ class DeviceBatch:
         return DeviceBatch(int(batch.family), up(batch.fields, torch.int32),
                            up(batch.ragged, torch.int32), up(batch.ragged_off, torch.int64))
 
+    def slice(self, c0: int, c1: int) -> "DeviceBatch":
+        """Configs [c0, c1) as a view (field rows keep their stride; the ragged
+        data is shared, its offsets are absolute)."""
+        return DeviceBatch(self.family, self.fields[:, c0:c1], self.ragged,
+                           None if self.ragged_off is None else self.ragged_off[c0:c1])
+
     def c_struct(self) -> _abi.sp_config_batch:
         s = _abi.sp_config_batch()
         s.family = self.family

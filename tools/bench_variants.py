@@ -50,7 +50,7 @@ def main():
     args = ap.parse_args()
     ctx = sp.Context(0)
     # ---- scheduler variants on a config-2 slice
-    b, sa, (g0, g1), _ = bench.build_workload("cfg2", 0, 1, args.scale)
+    b, sa, (g0, g1), _ = bench.local_workload("cfg2", args.scale)
     sh = ctx.load_gpu_specs(sa)
     db = sp.DeviceBatch.from_host(b, "cuda:0")
     n = (g1 - g0) * b.n_configs
@@ -61,8 +61,8 @@ def main():
                           "ms": ms, "pairs_per_s": n / (ms * 1e-3)}), flush=True)
     # ---- clamped edge tiles (SP_FEAT_CLAMPED): GEMM (config-1 shapes) and fused MoE (config 3), x 11 GPUs
     from workloads import gen, specs as wspecs
-    for name, bb in (("gemm 1e5 x 11", gen.gen_gemm(100_000, 1001)), ("cfg3 x0.1", bench.build_workload("cfg3", 0, 1, 0.1)[0]),
-                     ("cfg2 x0.02", bench.build_workload("cfg2", 0, 1, 0.02)[0])):
+    for name, bb in (("gemm 1e5 x 11", gen.gen_gemm(100_000, 1001)), ("cfg3 x0.1", bench.local_workload("cfg3", 0.1)[0]),
+                     ("cfg2 x0.02", bench.local_workload("cfg2", 0.02)[0])):
         sa2 = wspecs.paper_gpu_specs()
         sh2 = ctx.load_gpu_specs(sa2)
         db2 = sp.DeviceBatch.from_host(bb, "cuda:0")
@@ -73,7 +73,7 @@ def main():
             print(json.dumps({"variant": "featurize_clamped" if clamped else "featurize_padded", "workload": name,
                               "pairs": n2, "ms": ms, "pairs_per_s": n2 / (ms * 1e-3)}), flush=True)
     # ---- gap diagnosis over config 3
-    b, sa, (g0, g1), _ = bench.build_workload("cfg3", 0, 1, 1.0)
+    b, sa, (g0, g1), _ = bench.local_workload("cfg3", 1.0)
     sh = ctx.load_gpu_specs(sa)
     db = sp.DeviceBatch.from_host(b, "cuda:0")
     n = (g1 - g0) * b.n_configs

@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=4)
     args = ap.parse_args()
     ctx = sp.Context(0)
-    b, sa, (g0, g1), _ = bench.build_workload(args.workload, 0, 1, 1.0)
+    b, sa, (g0, g1), _ = bench.local_workload(args.workload, 1.0)
     sh = ctx.load_gpu_specs(sa)
     m = ctx.load_model(models.random_mlp(b.family, 42), "fp16")
 

@@ -5,7 +5,7 @@ import bench, paper_2601_14910_b200 as sp
 from workloads import models
 ctx = sp.Context(0)
 for w in ("cfg3", "cfg2"):
-    b, sa, (g0, g1), _ = bench.build_workload(w, 0, 1, 1.0)
+    b, sa, (g0, g1), _ = bench.local_workload(w, 1.0)
     sh = ctx.load_gpu_specs(sa)
     m = ctx.load_model(models.random_mlp(b.family, 42), "fp16")
     class H: pass

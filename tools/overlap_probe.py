@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--chunk-specs", type=int, default=1)
     args = ap.parse_args()
     ctx = sp.Context(0)
-    b, sa, (g0, g1), _ = bench.build_workload(args.workload, 0, 1, 1.0)
+    b, sa, (g0, g1), _ = bench.local_workload(args.workload, 1.0)
     sh = ctx.load_gpu_specs(sa)
     db = sp.DeviceBatch.from_host(b, "cuda:0")
     C = b.n_configs

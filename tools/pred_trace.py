@@ -21,7 +21,7 @@ from paper_2601_14910_b200 import _abi  # noqa: E402
 from workloads import models  # noqa: E402
 
 ctx = sp.Context(0)
-b, sa, (g0, g1), _ = bench.build_workload("cfg2", 0, 1, 0.25)
+b, sa, (g0, g1), _ = bench.local_workload("cfg2", 0.25)
 sh = ctx.load_gpu_specs(sa)
 m = ctx.load_model(models.random_mlp(b.family, 42), "fp16")
 db = sp.DeviceBatch.from_host(b, "cuda:0")

@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--precision", default="fp16")
     args = ap.parse_args()
     ctx = sp.Context(0)
-    b, sa, (g0, g1), _ = bench.build_workload(args.workload, 0, 1, args.scale)
+    b, sa, (g0, g1), _ = bench.local_workload(args.workload, args.scale)
     sh = ctx.load_gpu_specs(sa)
     md = models.random_mlp(b.family, 42)
     m = ctx.load_model(md, args.precision)
