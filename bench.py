@@ -330,19 +330,28 @@ def load_json(path):
         return None
 
 
+def device_of(local_rank: int, args) -> int:
+    """The rank's GPU: LOCAL_RANK, or all ranks on GPU 0 for the gloo functional check."""
+    return local_rank if args.dist_backend == "nccl" else 0
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
 
     import paper_2601_14910_b200 as sp
     from paper_2601_14910_b200.dist import ShardedPredictor
 
+    local_rank = device_of(local_rank, args)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # functional check of the N > 1 path on a single GPU (timings meaningless)
+            dist.init_process_group("gloo")
     ctx = sp.Context(local_rank)
     b, sa, (g0, g1), scaling = build_workload(args.workload, rank, world, args.scale, args.scaling)
     # the all-gather of chunk k overlaps chunk k+1's compute; each extra chunk costs a launch tail
@@ -535,13 +544,17 @@ def run_gpu_e2e(args, rank, world, local_rank):
 
     import paper_2601_14910_b200 as sp
 
+    local_rank = device_of(local_rank, args)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # functional check of the N > 1 path on a single GPU (timings meaningless)
+            dist.init_process_group("gloo")
     ctx = sp.Context(local_rank)
     n_tr = max(1, int(256 * args.scale))
     traces = gen.gen_serving_traces(n_tr, 1004 + 7919 * rank)
@@ -840,6 +853,9 @@ def main():
     ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
                     help="strong (default): one global workload sharded across ranks; weak: every rank "
                          "its own full-size workload (cfg5 is always strong)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: every rank on GPU 0 over gloo -- a functional check of the N>1 path on a "
+                         "one-GPU box, not a measurement")
     ap.add_argument("--chunks", type=int, default=0,
                     help="all-gather chunks overlapped with compute (0: 1 at N=1, 2 at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -323,6 +323,13 @@ void sp_free_model(sp_model *model);
  *   pairs: CROSS (n_pairs = (spec_end-spec_begin)*n_configs) or LIST.
  *   out:   caller-owned DEVICE SoA; out->family must equal cfg->family and
  *          out->n_pairs the pairing's pair count.
+ * EDGE TILES ARE PADDED (reading R2): a partial output tile
+ * counts its full tile_M x tile_N x ceil(K/BK)*BK MMA work and loads, as the
+ * MMA units execute them (Table VII's 0.01% total-op error vs NCU, P:529-530,
+ * is only plausible for executed, i.e. padded, tiles).  This DIFFERS from
+ * SPEC's default, which clamps edge tiles to their in-range extent (S:124,
+ * S:155): that reading is sp_featurize_ex(.., SP_FEAT_CLAMPED, ..) (GEMM,
+ * fused MoE, attention; Scaled MM and split-K GEMM are padded only).
  * Integer slots are exact (bit-identical to the fp64 oracle); float slots are
  * computed in fp64 from the exact integers and rounded once to fp32 (R20).
  * Synchronous errors: SP_E_ARG (NULL, sizes, family/field-count mismatch,

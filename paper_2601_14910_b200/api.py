@@ -475,7 +475,7 @@ class Context:
     def featurize(self, batch: DeviceBatch, specs: Specs, out: Features, pairs=None,
                   stream=None, scheduler: str = "rr", clamped: bool = False) -> Features:
         """sp_featurize (scheduler "rr"), sp_featurize_sched ("greedy", "minheap"), or
-        sp_featurize_ex with SP_FEAT_CLAMPED (clamped edge tiles, GEMM / fused MoE)."""
+        sp_featurize_ex with SP_FEAT_CLAMPED (clamped edge tiles: GEMM, fused MoE, attention)."""
         if pairs is None:
             pairs = cross(0, len(specs))
         cb = batch.c_struct()

@@ -519,6 +519,10 @@ __device__ DistinctMax fold(const AttnCfg &a, uint32_t *A, int32_t N, const Fast
   const uint32_t qn = fdN.div(T), rn = T - qn * (uint32_t)N;
   SumT m_lo = 0, m_hi = 0;
   if (sizeof(SumT) == 4 && N <= kFoldDupMax) {
+    // the duplicate overwrites memory other lanes read in the previous region's
+    // fold (regions fold last-first): order those reads first (the REDUX maxima in
+    // between synchronize the lanes but do not order shared memory)
+    __syncwarp();
     for (int32_t x = lane; x < N; x += 32) A[N + x] = A[x];
     __syncwarp();
     switch ((N + 31) >> 5) {
