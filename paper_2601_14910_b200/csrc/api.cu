@@ -278,6 +278,7 @@ static sp_status attn_plan(sp_ctx *ctx, sp_specs *sp, int b, int e, const AttnPl
   pd->view.distinct_off = (const int32_t *)pd->distinct_off.p;
   pd->view.spec_slot = (const int32_t *)pd->spec_slot.p;
   pd->view.n_slots = (int32_t)dn.size();
+  pd->view.min_n = dn.empty() ? 0 : dn.front();  // Ns ascending
   pd->view.n_groups = (int32_t)groups.size();
   pd->view.words_per_warp = words_max + kAttnScratchWords;  // accumulators + request scratch
   for (const AttnGroup &gr : groups) {
@@ -308,7 +309,8 @@ static sp_status grow_buf(sp_ctx *ctx, void *&p, size_t &bytes, size_t need, con
 // attention per-config results of the schedule kernel: st (4 B), L, U, and maxS/maxB per slot (8 B each)
 static sp_status grow_attn_res(sp_ctx *ctx, int64_t C, int n_slots) {
   const int64_t ld = (C + 31) & ~(int64_t)31;
-  return grow_buf(ctx, ctx->attn_res, ctx->attn_res_bytes, (size_t)ld * (4 + 8 + 8 + 16 * (size_t)n_slots),
+  return grow_buf(ctx, ctx->attn_res, ctx->attn_res_bytes,
+                  (size_t)ld * (4 + 8 + 8 + 16 * (size_t)n_slots + 4 * (size_t)kAttnPreWords),
                   "attention result scratch");
 }
 static sp_status grow_pre(sp_ctx *ctx, int64_t C) {
@@ -450,6 +452,7 @@ extern "C" sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, co
       res.mS = (int64_t *)(base + 16 * ld);
       res.mB = res.mS + (size_t)run.n_slots * ld;
       res.st = (int32_t *)(res.mB + (size_t)run.n_slots * ld);
+      res.pre = (uint32_t *)(res.st + ld);
       e = launch_featurize_attention(cv, ds, pairs->spec_begin, pairs->spec_end, specs->n, run, res, n_pairs,
                                      nullptr, nullptr, specs->max_sms, fo, ctx->num_sms, stream, ctx->hook());
     } else {

@@ -79,6 +79,21 @@ struct AttnCfg {
   Footprint fp;
 };
 
+// Divisors of a config's hot arithmetic (FastDiv: multiply-high + shift).
+// make_fd costs a 64-bit division; the cross path gets them from attn_prepass
+// (thread per config) instead of recomputing them warp-uniformly.
+struct AttnDivs {
+  FastDiv g, bkv, bq, chunk;
+};
+__device__ __forceinline__ AttnDivs make_divs(const AttnCfg &a) {
+  AttnDivs d;
+  d.g = make_fd((uint32_t)a.g);
+  d.bkv = make_fd((uint32_t)a.bkv);
+  d.bq = make_fd((uint32_t)a.bq);
+  d.chunk = a.chunk > 0 ? make_fd((uint32_t)a.chunk) : FastDiv{1u, 1u, 0u};
+  return d;
+}
+
 // PLANNER: accept kv_chunk = -1 (non-causal) for the split-KV planner (R24).
 // The cross schedule kernel uses PLANNER = false and reports such configs as
 // SP_PAIR_E_TILE; attn_planner_cross then rewrites their records (keeping the
@@ -186,18 +201,20 @@ __device__ int32_t plan_chunk(const AttnCfg &a, const DevSpec &sp, int lane) {
 
 // Pre-pass: per-head task count L (lanes over requests; causal split-KV walks
 // the request's q-blocks).  Saturates at 2^40 (anything above 2^31 is RANGE).
-__device__ int64_t count_tasks(const AttnCfg &a, int lane, const FastDiv &fg) {
+// 32-bit operands throughout: q*g < 2^31, BQ, BKV, chunk, kv < 2^31 (validated),
+// so every "x + d - 1" below is < 2^32 (FastDiv::div takes any 32-bit n).
+__device__ int64_t count_tasks(const AttnCfg &a, int lane, const AttnDivs &dv) {
   uint64_t part = 0;
   for (int64_t b = lane; b < a.bs; b += 32) {
     const uint32_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
-    const uint64_t rows = (uint64_t)q * a.g, nqb = (rows + a.bq - 1) / a.bq;
+    const uint32_t rows = q * (uint32_t)a.g, nqb = dv.bq.div(rows + (uint32_t)a.bq - 1u);
     if (a.chunk == 0) {
       part = sat_add(part, nqb);
     } else if (!a.causal) {
-      part = sat_add(part, nqb * ((kv + a.chunk - 1) / a.chunk));
+      part = sat_add(part, (uint64_t)nqb * dv.chunk.div(kv + (uint32_t)a.chunk - 1u));
     } else {
-      for (uint64_t i = 0; i < nqb && part < (1ull << 40); ++i)
-        part = sat_add(part, (kv_need(i, a.bq, rows, q, kv, true, fg) + a.chunk - 1) / a.chunk);
+      for (uint32_t i = 0; i < nqb && part < (1ull << 40); ++i)
+        part = sat_add(part, dv.chunk.div(kv_need(i, a.bq, rows, q, kv, true, dv.g) + (uint32_t)a.chunk - 1u));
     }
   }
   return (int64_t)min(warp_sum_u64(part), (uint64_t)(1ull << 40));
@@ -205,23 +222,24 @@ __device__ int64_t count_tasks(const AttnCfg &a, int lane, const FastDiv &fg) {
 
 // Sparse path (T <= min N): every SM holds at most one task, so only the unit
 // sum U and the largest unit umax are needed.  Lanes over requests.
-__device__ void sparse_units(const AttnCfg &a, int lane, const FastDiv &fg, uint64_t &U, uint32_t &umax) {
+__device__ void sparse_units(const AttnCfg &a, int lane, const AttnDivs &dv, uint64_t &U, uint32_t &umax) {
   uint64_t us = 0;
   uint32_t um = 0;
   for (int64_t b = lane; b < a.bs; b += 32) {
     const uint32_t q = __ldg(a.req + 2 * b), kv = __ldg(a.req + 2 * b + 1);
-    const uint64_t rows = (uint64_t)q * a.g, nqb = (rows + a.bq - 1) / a.bq;
-    for (uint64_t i = 0; i < nqb; ++i) {
-      const uint32_t need = kv_need(i, a.bq, rows, q, kv, a.causal, fg);
+    const uint32_t rows = q * (uint32_t)a.g, nqb = dv.bq.div(rows + (uint32_t)a.bq - 1u);
+    for (uint32_t i = 0; i < nqb; ++i) {
+      const uint32_t need = kv_need(i, a.bq, rows, q, kv, a.causal, dv.g);
       if (a.chunk == 0) {
-        const uint32_t u = (uint32_t)((need + a.bkv - 1) / a.bkv);
+        const uint32_t u = dv.bkv.div(need + (uint32_t)a.bkv - 1u);
         us += u;
         um = max(um, u);
       } else {
-        for (uint64_t c0 = 0; c0 < need; c0 += a.chunk) {
-          const uint32_t u = (uint32_t)((min((uint64_t)a.chunk, need - c0) + a.bkv - 1) / a.bkv);
+        for (uint32_t c0 = 0; c0 < need; c0 += (uint32_t)a.chunk) {
+          const uint32_t u = dv.bkv.div(min((uint32_t)a.chunk, need - c0) + (uint32_t)a.bkv - 1u);
           us += u;
           um = max(um, u);
+          if (need - c0 <= (uint32_t)a.chunk) break;  // (c0 + chunk may wrap 32 bits)
         }
       }
     }
@@ -292,21 +310,21 @@ __device__ uint64_t accumulate_causal_split(const AttnCfg &a, uint32_t *acc, con
 // request from a boundary bitmask (one warp OR-reduction per step).
 template <int ND, bool SMALL>
 __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint32_t *scr, const int32_t (&N)[ND],
-                               const int32_t (&off)[ND], const FastDiv *fdN, int lane, const FastDiv &fg) {
+                               const int32_t (&off)[ND], const FastDiv *fdN, int lane, const AttnDivs &dv) {
   for (int w = lane * 4; w < words; w += 128) *reinterpret_cast<uint4 *>(acc + w) = make_uint4(0, 0, 0, 0);
   __syncwarp();
-  const FastDiv fbkv = make_fd((uint32_t)a.bkv);
+  const FastDiv &fg = dv.g, &fbkv = dv.bkv;
   const bool split = a.chunk > 0;
   if (split && a.causal) {
     const uint64_t us = accumulate_causal_split<ND>(a, acc, off, fdN, lane, fg, fbkv);
     __syncwarp();
     return warp_sum_u64(us);
   }
-  const FastDiv fbq = make_fd((uint32_t)a.bq);
+  const FastDiv &fbq = dv.bq;
   // causal without split-KV and g | BQ: kv_need is affine in the q-block index
   const uint32_t a_per = (uint32_t)(a.bq / a.g);
   const bool lin = !split && a.causal && a.bq % a.g == 0 && (int64_t)a.bq * 33 < (1ll << 30);
-  const FastDiv fchunk = split ? make_fd((uint32_t)a.chunk) : FastDiv{1u, 1u, 0u};
+  const FastDiv &fchunk = dv.chunk;
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);  // shared-window byte address
   const uint32_t lm_le = lanemask_le();
   uint32_t *s_start = scr, *s_a1 = scr + 32, *s_a2 = scr + 64, *s_a3 = scr + 96, *s_uf = scr + 128,
@@ -623,17 +641,17 @@ __device__ __forceinline__ void attn_emit(const FeatOut &out, int64_t p, const A
 
 // Whole per-config pipeline for one distinct set; per-distinct maxima go to
 // mS[d * ms], mB[d * ms] (written by lane 0).
+// Lpre >= 0: the task count L from attn_prepass (else counted here).
 template <int ND, bool SMALL>
-__device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, uint32_t *scr, const int32_t (&N)[ND],
-                           const int32_t (&off)[ND], const FastDiv *fdN, int32_t minN, int lane, int64_t &L,
-                           uint64_t &U, int64_t *mS, int64_t *mB, int64_t ms) {
-  const FastDiv fg = make_fd((uint32_t)a.g);
-  L = count_tasks(a, lane, fg);
+__device__ int attn_config(const AttnCfg &a, const AttnDivs &dv, int64_t Lpre, uint32_t *acc, int words,
+                           uint32_t *scr, const int32_t (&N)[ND], const int32_t (&off)[ND], const FastDiv *fdN,
+                           int32_t minN, int lane, int64_t &L, uint64_t &U, int64_t *mS, int64_t *mB, int64_t ms) {
+  L = Lpre >= 0 ? Lpre : count_tasks(a, lane, dv);
   if (L > kI32Max || L * a.nkv > kI32Max) return SP_PAIR_E_RANGE;
   const int64_t T = L * a.nkv;
   if (T <= minN) {
     uint32_t umax;
-    sparse_units(a, lane, fg, U, umax);
+    sparse_units(a, lane, dv, U, umax);
     if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
     if (lane == 0)
       for (int d = 0; d < ND; ++d) {
@@ -643,7 +661,7 @@ __device__ int attn_config(const AttnCfg &a, uint32_t *acc, int words, uint32_t 
     __syncwarp();
     return 0;
   }
-  U = accumulate<ND, SMALL>(a, acc, words, scr, N, off, fdN, lane, fg);
+  U = accumulate<ND, SMALL>(a, acc, words, scr, N, off, fdN, lane, dv);
   if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
   const bool s32 = U * (uint64_t)a.nkv < (1ull << 32);
   // last region first: fold() duplicates region d into [off_d + N_d, off_d + 2 N_d),
@@ -680,6 +698,151 @@ __device__ __forceinline__ AttnCfg load_cfg_lane(const ConfigView &v, int64_t c)
 // Per-warp shared-memory region: [stash of 32 configs | request scratch | accumulators].
 // fold()'s duplicate of the last region (N <= kFoldDupMax, reads to 2N + 31) must fit in the request scratch
 static_assert(kAttnScratchWords >= kFoldDupMax + 32, "fold duplicate overruns the warp region");
+
+// ---- cross-mode pre-pass (thread per config).  Everything about a config that
+// does not need its task stream is scalar work: validation (in the oracle's
+// order, as load_cfg), g, the task count L (count_tasks), the range rule on L,
+// and the FastDiv constants of g, BKV, BQ and the kv chunk (a 64-bit division
+// each).  A warp per config did it warp-uniformly, 32x the instructions.
+// Configs whose whole record follows from it are finished here: invalid
+// configs, and sparse ones (T <= the smallest SM count of the range: every SM
+// holds at most one task, so max_j S_j = the largest task's u for every
+// distinct N).  The rest are flagged for attn_schedule_cross, which reads L
+// and the divisors from the record.  Causal + split-KV configs (a chunk count
+// per q-block) leave L to the warp.
+enum : uint32_t { kPreWarp = 1u, kPreWarpCounts = 2u };
+
+__global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults res, int32_t min_n, int32_t n_slots) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= v.n_configs) return;
+  int32_t f[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) f[k] = __ldg(v.fields + (int64_t)k * v.ld + c);
+  const int32_t bs = f[BS], nh = f[NH], nkv = f[NKV], hd = f[HD], bq = f[BQ], bkv = f[BKV], chunk = f[CHUNK],
+                causal = f[CAUSAL], dt = f[DTYPE];
+  const int64_t off = v.ragged_off ? __ldg(v.ragged_off + c) : -1;
+  int st = 0;
+  int32_t g = 0;
+  // validation, in load_cfg's (the oracle's) order
+  if (off < 0 || bs < 1 || nh < 1 || nkv < 1 || hd < 1) st = SP_PAIR_E_DIM;
+  else if (bq < 1 || bkv < 1 || chunk < 0) st = SP_PAIR_E_TILE;  // kv_chunk -1: attn_planner_cross
+  else if (f[WARPS] < 1 || f[REGS] < 1 || f[SMEM] < 0) st = SP_PAIR_E_RES;
+  else if (dt != SP_BF16 && dt != SP_FP16) st = SP_PAIR_E_DTYPE;
+  else if (nh % nkv != 0) st = SP_PAIR_E_HEADS;
+  const int32_t *req = st ? nullptr : v.ragged + off;
+  if (!st) {
+    g = nh / nkv;
+    for (int32_t b = 0; b < bs; ++b) {  // the first failing request decides
+      const int64_t q = __ldg(req + 2 * b), kv = __ldg(req + 2 * b + 1);
+      if (q < 1 || kv < 1) st = SP_PAIR_E_DIM;
+      else if (causal && kv < q) st = SP_PAIR_E_CAUSAL;
+      else if (q * g > kI32Max) st = SP_PAIR_E_RANGE;
+      if (st) break;
+    }
+  }
+  uint32_t flags = 0;
+  int64_t L = 0;
+  uint64_t U = 0;
+  AttnDivs dv{};
+  if (!st) {
+    dv.g = make_fd((uint32_t)g);
+    dv.bkv = make_fd((uint32_t)bkv);
+    dv.bq = make_fd((uint32_t)bq);
+    dv.chunk = chunk > 0 ? make_fd((uint32_t)chunk) : FastDiv{1u, 1u, 0u};
+    if (chunk > 0 && causal) {
+      flags = kPreWarp | kPreWarpCounts;
+    } else {
+      uint64_t part = 0;  // count_tasks, saturating at 2^40
+      for (int32_t b = 0; b < bs; ++b) {
+        const uint32_t q = __ldg(req + 2 * b), kv = __ldg(req + 2 * b + 1);
+        const uint32_t nqb = dv.bq.div(q * (uint32_t)g + (uint32_t)bq - 1u);
+        part = sat_add(part, chunk == 0 ? (uint64_t)nqb : (uint64_t)nqb * dv.chunk.div(kv + (uint32_t)chunk - 1u));
+      }
+      L = (int64_t)part;
+      if (L > kI32Max || L * nkv > kI32Max) {
+        st = SP_PAIR_E_RANGE;
+        L = 0;
+      } else if (L * nkv > min_n) {
+        flags = kPreWarp;
+      } else {  // sparse: U and the largest unit (sparse_units)
+        uint32_t um = 0;
+        for (int32_t b = 0; b < bs; ++b) {
+          const uint32_t q = __ldg(req + 2 * b), kv = __ldg(req + 2 * b + 1);
+          const uint32_t rows = q * (uint32_t)g, nqb = dv.bq.div(rows + (uint32_t)bq - 1u);
+          for (uint32_t i = 0; i < nqb; ++i) {
+            const uint32_t need = kv_need(i, bq, rows, q, kv, causal, dv.g);
+            if (chunk == 0) {
+              const uint32_t u = dv.bkv.div(need + (uint32_t)bkv - 1u);
+              U += u;
+              um = max(um, u);
+            } else {
+              for (uint32_t c0 = 0; c0 < need; c0 += (uint32_t)chunk) {
+                const uint32_t u = dv.bkv.div(min((uint32_t)chunk, need - c0) + (uint32_t)bkv - 1u);
+                U += u;
+                um = max(um, u);
+                if (need - c0 <= (uint32_t)chunk) break;
+              }
+            }
+          }
+        }
+        if (U > (uint64_t)kU32Max) {
+          st = SP_PAIR_E_RANGE;
+          L = 0;
+          U = 0;
+        } else {
+          for (int32_t d = 0; d < n_slots; ++d) {
+            res.mS[(int64_t)d * res.ld + c] = (int64_t)um;
+            res.mB[(int64_t)d * res.ld + c] = (int64_t)bq + 2 * (int64_t)bkv * um;
+          }
+        }
+      }
+    }
+  }
+  res.st[c] = st;
+  res.L[c] = L;
+  res.U[c] = U;
+  uint32_t *pr = res.pre + c;
+  const int64_t ld = res.ld;
+  pr[0] = flags;
+  if (flags) {
+    pr[1 * ld] = (uint32_t)g;
+    pr[2 * ld] = dv.g.m;
+    pr[3 * ld] = dv.g.s;
+    pr[4 * ld] = dv.bkv.m;
+    pr[5 * ld] = dv.bkv.s;
+    pr[6 * ld] = dv.bq.m;
+    pr[7 * ld] = dv.bq.s;
+    pr[8 * ld] = dv.chunk.m;
+    pr[9 * ld] = dv.chunk.s;
+  }
+}
+
+// A flagged config for the warp: its fields (lanes 0..11, one load each) and the
+// pre-pass record (lanes 0..9), broadcast by shuffles.  Valid by construction.
+__device__ __forceinline__ AttnCfg load_cfg_pre(const ConfigView &v, const AttnResults &res, int64_t c, int lane,
+                                                AttnDivs &dv, uint32_t &flags) {
+  AttnCfg a{};
+  const int32_t f = lane < 12 ? __ldg(v.fields + (int64_t)lane * v.ld + c) : 0;
+  const uint32_t r = lane < kAttnPreWords ? __ldg(res.pre + (int64_t)lane * res.ld + c) : 0u;
+  a.bs = __shfl_sync(0xffffffffu, f, BS);
+  a.nh = __shfl_sync(0xffffffffu, f, NH);
+  a.nkv = __shfl_sync(0xffffffffu, f, NKV);
+  a.hd = __shfl_sync(0xffffffffu, f, HD);
+  a.bq = __shfl_sync(0xffffffffu, f, BQ);
+  a.bkv = __shfl_sync(0xffffffffu, f, BKV);
+  a.chunk = __shfl_sync(0xffffffffu, f, CHUNK);
+  a.causal = __shfl_sync(0xffffffffu, f, CAUSAL);
+  a.dt = __shfl_sync(0xffffffffu, f, DTYPE);
+  flags = __shfl_sync(0xffffffffu, r, 0);
+  a.g = (int32_t)__shfl_sync(0xffffffffu, r, 1);
+  dv.g = FastDiv{(uint32_t)a.g, __shfl_sync(0xffffffffu, r, 2), __shfl_sync(0xffffffffu, r, 3)};
+  dv.bkv = FastDiv{(uint32_t)a.bkv, __shfl_sync(0xffffffffu, r, 4), __shfl_sync(0xffffffffu, r, 5)};
+  dv.bq = FastDiv{(uint32_t)a.bq, __shfl_sync(0xffffffffu, r, 6), __shfl_sync(0xffffffffu, r, 7)};
+  dv.chunk = FastDiv{a.chunk > 0 ? (uint32_t)a.chunk : 1u, __shfl_sync(0xffffffffu, r, 8),
+                     __shfl_sync(0xffffffffu, r, 9)};
+  a.req = v.ragged + __ldg(v.ragged_off + c);
+  return a;
+}
 
 // CROSS mode.  Warps take chunks of 32 consecutive configs from a per-group
 // Schedule kernel (cross mode): warps pull chunks of 32 configs; per config
@@ -721,15 +884,21 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) attn_schedule_cross
     chunk = __shfl_sync(0xffffffffu, chunk, 0);
     if (chunk >= n_chunks) break;
     const int64_t c0 = chunk * 32;
-    const int nc = (int)min((int64_t)32, C - c0);
-    for (int j = 0; j < nc; ++j) {
+    // configs the pre-pass left to the warps (invalid and sparse ones are done)
+    const bool mine = c0 + lane < C && (__ldg(res.pre + c0 + lane) & kPreWarp);
+    uint32_t todo = __ballot_sync(0xffffffffu, mine);
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
       const int64_t c = c0 + j;
-      const AttnCfg a = load_cfg<false>(cfg, c, lane);
-      int st = a.status;
+      AttnDivs dv;
+      uint32_t flags;
+      const AttnCfg a = load_cfg_pre(cfg, res, c, lane, dv, flags);
       int64_t L = 0;
       uint64_t U = 0;
-      if (st == 0)
-        st = attn_config<ND, SMALL>(a, acc, words, scr, N, off, s_fd, minN, lane, L, U, mS + c, mB + c, res.ld);
+      const int64_t Lpre = (flags & kPreWarpCounts) ? -1 : __ldg(res.L + c);
+      const int st = attn_config<ND, SMALL>(a, dv, Lpre, acc, words, scr, N, off, s_fd, minN, lane, L, U, mS + c,
+                                            mB + c, res.ld);
       // the per-config fields do not depend on the group: group 0 writes them
       if (lane == 0 && blockIdx.y == 0) {
         res.st[c] = st;
@@ -792,10 +961,11 @@ __device__ void attn_one_pair(const ConfigView &cfg, int64_t c, const DevSpec &s
   const int words = (N[0] + kAttnSlack + 3) & ~3;
   if (st == 0) {
     if (a.chunk == -1) a.chunk = plan_chunk(a, sp, lane);
+    const AttnDivs dv = make_divs(a);
     if (N[0] >= kAttnLazyMinN)
-      st = attn_config<1, false>(a, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
+      st = attn_config<1, false>(a, dv, -1, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
     else
-      st = attn_config<1, true>(a, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
+      st = attn_config<1, true>(a, dv, -1, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
   }
   if (lane == 0) attn_emit(out, p, a, st, L, U, DistinctMax{sm[0], sm[1]}, sp);
   __syncwarp();
@@ -902,7 +1072,7 @@ template <int MODE>  // 1 GREEDY, 2 MINHEAP
 __device__ void attn_sim_pair(const AttnCfg &a, const SimRegion &r, uint32_t N, uint32_t occ, int lane, int64_t &L,
                               uint64_t &U, DistinctMax &m, int &st) {
   const FastDiv fg = make_fd((uint32_t)a.g);
-  L = count_tasks(a, lane, fg);
+  L = count_tasks(a, lane, make_divs(a));
   if (L > kI32Max || L * a.nkv > kI32Max) { st = SP_PAIR_E_RANGE; return; }
   const uint32_t T = (uint32_t)(L * a.nkv);
   const uint64_t slots = (uint64_t)N * occ;
@@ -1097,7 +1267,7 @@ __device__ void attn_clamped_pair(const ConfigView &cfg, int64_t c, const DevSpe
   }
   if (a.chunk == -1) a.chunk = plan_chunk(a, sp, lane);
   const FastDiv fg = make_fd((uint32_t)a.g);
-  const int64_t L = count_tasks(a, lane, fg);
+  const int64_t L = count_tasks(a, lane, make_divs(a));
   if (L > kI32Max || L * a.nkv > kI32Max) {
     if (lane == 0) emit_error(out, p, SP_PAIR_E_RANGE);
     return;
@@ -1236,6 +1406,11 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
     if (cfg.n_configs == 0 || plan.n_groups == 0) return 0;
     // one launch per run of groups with the same (distinct count, small-N) shape
     cudaError_t me = cudaMemsetAsync(plan.counters, 0, (size_t)plan.n_groups * sizeof(int), st);
+    if (me != cudaSuccess) return (int)me;
+    hook.on_begin("attn_prepass", st);
+    attn_prepass<<<(unsigned)((cfg.n_configs + 255) / 256), 256, 0, st>>>(cfg, res, plan.min_n, plan.n_slots);
+    hook.on_end(st);
+    me = cudaGetLastError();
     if (me != cudaSuccess) return (int)me;
     for (int y = 0; y < plan.n_groups;) {
       const int nd = plan.host_nd[y];

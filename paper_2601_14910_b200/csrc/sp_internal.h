@@ -115,6 +115,7 @@ struct AttnPlan {
   int *counters;               // DEVICE [n_groups] work counters (context scratch, zeroed per launch)
   const int32_t *spec_slot;    // DEVICE, per spec of the range: its distinct slot (absolute)
   int32_t n_slots;             // distinct slots over all groups
+  int32_t min_n;               // smallest SM count of the range (attn_prepass's sparse rule)
 };
 // Per-config results of the schedule kernel (context scratch, cross mode):
 // st/L/U [C], mS/mB [n_slots][ld].
@@ -124,7 +125,9 @@ struct AttnResults {
   uint64_t *U;
   int64_t *mS, *mB;
   int64_t ld;
+  uint32_t *pre;  // attn_prepass record [kAttnPreWords][ld]: flags, g, FastDiv (m, s) of g, BKV, BQ, chunk
 };
+constexpr int kAttnPreWords = 10;
 // Optional per-launch hook (kernel accounting, sp_set_profiling): begin/end
 // bracket one kernel launch on the launch stream.
 struct LaunchHook {
