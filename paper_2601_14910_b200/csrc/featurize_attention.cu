@@ -415,10 +415,16 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       // __syncwarp after it orders them for the fold); the atomic path may diverge
       if (SMALL) __syncwarp();
     };
+    uint32_t span[ND];  // region length in bytes
+#pragma unroll
+    for (int d = 0; d < ND; ++d) span[d] = 4u * (uint32_t)N[d];
     auto wrap = [&]() {
       if (!SMALL) {
+        // compare + predicated subtract: 2 instructions per region (the C form compiled to 4)
 #pragma unroll
-        for (int d = 0; d < ND; ++d) p[d] = p[d] >= hi[d] ? p[d] - 4u * (uint32_t)N[d] : p[d];
+        for (int d = 0; d < ND; ++d)
+          asm("{\n.reg .pred w;\nsetp.ge.u32 w, %0, %1;\n@w sub.u32 %0, %0, %2;\n}" : "+r"(p[d]) : "r"(hi[d]),
+              "r"(span[d]));
       }
     };
     uint32_t bcur = 0;  // chunk-local request holding task k0
@@ -505,20 +511,34 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
 constexpr int kFoldDupMax = SP_FOLD_DUP_MAX;
 
 template <typename SumT, int R>
-__device__ __forceinline__ void fold_rows(const uint32_t *A, int32_t N, uint32_t Lm, int32_t nkv, uint32_t rn,
-                                          int lane, SumT &m_lo, SumT &m_hi) {
+__device__ __forceinline__ void fold_rows(uint32_t *A, int32_t N, uint32_t Lm, int32_t nkv, uint32_t rn, int lane,
+                                          SumT &m_lo, SumT &m_hi) {
   SumT S[R];
+  if (nkv == 1) {  // one head: no rotation, S_j = A[j]
 #pragma unroll
-  for (int i = 0; i < R; ++i) S[i] = 0;
-  const uint32_t *b0 = A + N + lane;
-  uint32_t o = 0;  // h * L mod N
+    for (int i = 0; i < R; ++i) S[i] = (uint32_t)(lane + 32 * i) < (uint32_t)N ? A[lane + 32 * i] : 0u;
+  } else {
+    // the duplicate overwrites memory other lanes read in the previous region's
+    // fold (regions fold last-first): order those reads first (the REDUX maxima in
+    // between synchronize the lanes but do not order shared memory)
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (lane + 32 * i < N) A[N + lane + 32 * i] = A[lane + 32 * i];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < R; ++i) S[i] = 0;
+    const uint32_t *b0 = A + N + lane;
+    uint32_t o = 0;  // h * L mod N
 #pragma unroll 1  // code size: the kernel is instruction-cache sensitive
-  for (int32_t h = 0; h < nkv; ++h) {
-    const uint32_t *b = b0 - o;
+    for (int32_t h = 0; h < nkv; ++h) {
+      const uint32_t *b = b0 - o;
 #pragma unroll
-    for (int i = 0; i < R; ++i) S[i] += b[32 * i];
-    o += Lm;
-    o = o >= (uint32_t)N ? o - (uint32_t)N : o;
+      for (int i = 0; i < R; ++i) S[i] += b[32 * i];
+      asm("{\n.reg .pred w;\nadd.u32 %0, %0, %1;\nsetp.ge.u32 w, %0, %2;\n@w sub.u32 %0, %0, %2;\n}"
+          : "+r"(o)
+          : "r"(Lm), "r"((uint32_t)N));
+    }
   }
 #pragma unroll
   for (int i = 0; i < R; ++i) {
@@ -530,19 +550,21 @@ __device__ __forceinline__ void fold_rows(const uint32_t *A, int32_t N, uint32_t
   }
 }
 
+// Per distinct N: the maxima of S_j over the two task-count classes, SMs
+// j < rn (qn + 1 tasks) and j >= rn (qn tasks), with T = qn N + rn.  The
+// record's max_j S_j and max_j (BQ n_j + 2 BKV S_j) follow from (lo, hi) by
+// finish_max, in the (thread-per-config) emit kernel.
+struct DistinctLoHi {
+  int64_t lo, hi;
+};
+
 template <typename SumT>
-__device__ DistinctMax fold(const AttnCfg &a, uint32_t *A, int32_t N, const FastDiv &fdN, uint32_t L, uint32_t T,
-                            int lane) {
+__device__ DistinctLoHi fold(const AttnCfg &a, uint32_t *A, int32_t N, const FastDiv &fdN, uint32_t L, uint32_t T,
+                             int lane) {
   const uint32_t Lm = fdN.mod(L);
-  const uint32_t qn = fdN.div(T), rn = T - qn * (uint32_t)N;
+  const uint32_t rn = T - fdN.div(T) * (uint32_t)N;
   SumT m_lo = 0, m_hi = 0;
   if (sizeof(SumT) == 4 && N <= kFoldDupMax) {
-    // the duplicate overwrites memory other lanes read in the previous region's
-    // fold (regions fold last-first): order those reads first (the REDUX maxima in
-    // between synchronize the lanes but do not order shared memory)
-    __syncwarp();
-    for (int32_t x = lane; x < N; x += 32) A[N + x] = A[x];
-    __syncwarp();
     switch ((N + 31) >> 5) {
       case 1: fold_rows<SumT, 1>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
       case 2: fold_rows<SumT, 2>(A, N, Lm, a.nkv, rn, lane, m_lo, m_hi); break;
@@ -566,17 +588,23 @@ __device__ DistinctMax fold(const AttnCfg &a, uint32_t *A, int32_t N, const Fast
       else m_hi = max(m_hi, S);
     }
   }
-  int64_t lo, hi;
-  if (sizeof(SumT) == 4) {  // one REDUX each instead of a 5-step 64-bit shuffle tree
-    lo = (int64_t)__reduce_max_sync(0xffffffffu, (uint32_t)m_lo);
-    hi = (int64_t)__reduce_max_sync(0xffffffffu, (uint32_t)m_hi);
-  } else {
-    lo = warp_max64((int64_t)m_lo);
-    hi = warp_max64((int64_t)m_hi);
-  }
+  if (sizeof(SumT) == 4)  // one REDUX each instead of a 5-step 64-bit shuffle tree
+    return DistinctLoHi{(int64_t)__reduce_max_sync(0xffffffffu, (uint32_t)m_lo),
+                        (int64_t)__reduce_max_sync(0xffffffffu, (uint32_t)m_hi)};
+  return DistinctLoHi{warp_max64((int64_t)m_lo), warp_max64((int64_t)m_hi)};
+}
+
+// max_j S_j and max_j (BQ n_j + 2 BKV S_j) of a distinct N from the class maxima
+// (lo over the rn SMs with qn + 1 tasks, hi over the others; T = qn N + rn).
+// Sparse configs (T <= N, at most one task per SM) pass (umax, umax): for T < N
+// the hi term 2 BKV umax (qn = 0) never exceeds the lo term BQ + 2 BKV umax, and
+// for T = N (rn = 0, every SM one task) the hi term is the answer.
+__device__ __forceinline__ DistinctMax finish_max(int64_t lo, int64_t hi, int64_t T, int32_t N, int64_t bq,
+                                                  int64_t bkv) {
+  const int64_t qn = T / N, rn = T - qn * N;
   int64_t mB = 0;
-  if (rn > 0) mB = (int64_t)a.bq * (qn + 1) + 2 * (int64_t)a.bkv * lo;
-  if (rn < (uint32_t)N) mB = max(mB, (int64_t)a.bq * qn + 2 * (int64_t)a.bkv * hi);
+  if (rn > 0) mB = bq * (qn + 1) + 2 * bkv * lo;
+  if (rn < N) mB = max(mB, bq * qn + 2 * bkv * hi);
   return DistinctMax{max(lo, hi), mB};
 }
 
@@ -653,10 +681,10 @@ __device__ int attn_config(const AttnCfg &a, const AttnDivs &dv, int64_t Lpre, u
     uint32_t umax;
     sparse_units(a, lane, dv, U, umax);
     if (U > (uint64_t)kU32Max) return SP_PAIR_E_RANGE;
-    if (lane == 0)
+    if (lane == 0)  // every SM holds at most one task: (lo, hi) = (umax, umax), see sparse_lohi
       for (int d = 0; d < ND; ++d) {
         mS[d * ms] = (int64_t)umax;
-        mB[d * ms] = (int64_t)a.bq + 2 * (int64_t)a.bkv * umax;
+        mB[d * ms] = (int64_t)umax;
       }
     __syncwarp();
     return 0;
@@ -668,11 +696,11 @@ __device__ int attn_config(const AttnCfg &a, const AttnDivs &dv, int64_t Lpre, u
   // over regions already folded and the (dead) request scratch that follows them
 #pragma unroll 1
   for (int d = ND - 1; d >= 0; --d) {
-    const DistinctMax m = s32 ? fold<uint32_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane)
-                              : fold<uint64_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
-    if (lane == 0) {
-      mS[d * ms] = m.maxS;
-      mB[d * ms] = m.maxB;
+    const DistinctLoHi m = s32 ? fold<uint32_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane)
+                               : fold<uint64_t>(a, acc + off[d], N[d], fdN[d], (uint32_t)L, (uint32_t)T, lane);
+    if (lane == 0) {  // (lo, hi): finish_max makes the record's maxima
+      mS[d * ms] = m.lo;
+      mB[d * ms] = m.hi;
     }
   }
   __syncwarp();
@@ -791,8 +819,8 @@ __global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults re
           U = 0;
         } else {
           for (int32_t d = 0; d < n_slots; ++d) {
-            res.mS[(int64_t)d * res.ld + c] = (int64_t)um;
-            res.mB[(int64_t)d * res.ld + c] = (int64_t)bq + 2 * (int64_t)bkv * um;
+            res.mS[(int64_t)d * res.ld + c] = (int64_t)um;  // (lo, hi) = (umax, umax): see finish_max
+            res.mB[(int64_t)d * res.ld + c] = (int64_t)um;
           }
         }
       }
@@ -941,7 +969,9 @@ __global__ void __launch_bounds__(256) attn_emit_cross(ConfigView cfg, const Dev
   for (int j = j0; j < j1; ++j) {
     const int64_t slot = s_slot[j - j0];
     DistinctMax m{0, 0};
-    if (!st) m = DistinctMax{__ldg(res.mS + slot * res.ld + c), __ldg(res.mB + slot * res.ld + c)};
+    if (!st)
+      m = finish_max(__ldg(res.mS + slot * res.ld + c), __ldg(res.mB + slot * res.ld + c), tt.T,
+                     s_spec[j - j0].num_sms, al.bq, al.bkv);
     attn_emit_pair(out, (int64_t)j * C + c, al, tt, m, s_spec[j - j0]);
   }
 }
@@ -967,7 +997,9 @@ __device__ void attn_one_pair(const ConfigView &cfg, int64_t c, const DevSpec &s
     else
       st = attn_config<1, true>(a, dv, -1, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
   }
-  if (lane == 0) attn_emit(out, p, a, st, L, U, DistinctMax{sm[0], sm[1]}, sp);
+  if (lane == 0)
+    attn_emit(out, p, a, st, L, U, st ? DistinctMax{0, 0} : finish_max(sm[0], sm[1], L * a.nkv, N[0], a.bq, a.bkv),
+              sp);
   __syncwarp();
 }
 
