@@ -415,16 +415,16 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       // __syncwarp after it orders them for the fold); the atomic path may diverge
       if (SMALL) __syncwarp();
     };
-    uint32_t span[ND];  // region length in bytes
+    uint32_t nspan[ND];  // minus the region length in bytes (uniform: a UR operand of the add)
 #pragma unroll
-    for (int d = 0; d < ND; ++d) span[d] = 4u * (uint32_t)N[d];
+    for (int d = 0; d < ND; ++d) nspan[d] = 0u - 4u * (uint32_t)N[d];
     auto wrap = [&]() {
       if (!SMALL) {
-        // compare + predicated subtract: 2 instructions per region (the C form compiled to 4)
+        // compare + predicated add: 2 instructions per region (the C form compiled to 4)
 #pragma unroll
         for (int d = 0; d < ND; ++d)
-          asm("{\n.reg .pred w;\nsetp.ge.u32 w, %0, %1;\n@w sub.u32 %0, %0, %2;\n}" : "+r"(p[d]) : "r"(hi[d]),
-              "r"(span[d]));
+          asm("{\n.reg .pred w;\nsetp.ge.u32 w, %0, %1;\n@w add.u32 %0, %0, %2;\n}" : "+r"(p[d]) : "r"(hi[d]),
+              "r"(nspan[d]));
       }
     };
     uint32_t bcur = 0;  // chunk-local request holding task k0
@@ -599,9 +599,10 @@ __device__ DistinctLoHi fold(const AttnCfg &a, uint32_t *A, int32_t N, const Fas
 // Sparse configs (T <= N, at most one task per SM) pass (umax, umax): for T < N
 // the hi term 2 BKV umax (qn = 0) never exceeds the lo term BQ + 2 BKV umax, and
 // for T = N (rn = 0, every SM one task) the hi term is the answer.
-__device__ __forceinline__ DistinctMax finish_max(int64_t lo, int64_t hi, int64_t T, int32_t N, int64_t bq,
+__device__ __forceinline__ DistinctMax finish_max(int64_t lo, int64_t hi, int64_t T, const FastDiv &fN, int64_t bq,
                                                   int64_t bkv) {
-  const int64_t qn = T / N, rn = T - qn * N;
+  const int32_t N = (int32_t)fN.d;
+  const int64_t qn = fN.div((uint32_t)T), rn = T - qn * N;  // T < 2^31 (range rule)
   int64_t mB = 0;
   if (rn > 0) mB = bq * (qn + 1) + 2 * bkv * lo;
   if (rn < N) mB = max(mB, bq * qn + 2 * bkv * hi);
@@ -758,66 +759,65 @@ __global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults re
   else if (dt != SP_BF16 && dt != SP_FP16) st = SP_PAIR_E_DTYPE;
   else if (nh % nkv != 0) st = SP_PAIR_E_HEADS;
   const int32_t *req = st ? nullptr : v.ragged + off;
-  if (!st) {
-    g = nh / nkv;
-    for (int32_t b = 0; b < bs; ++b) {  // the first failing request decides
-      const int64_t q = __ldg(req + 2 * b), kv = __ldg(req + 2 * b + 1);
-      if (q < 1 || kv < 1) st = SP_PAIR_E_DIM;
-      else if (causal && kv < q) st = SP_PAIR_E_CAUSAL;
-      else if (q * g > kI32Max) st = SP_PAIR_E_RANGE;
-      if (st) break;
-    }
-  }
   uint32_t flags = 0;
   int64_t L = 0;
   uint64_t U = 0;
   AttnDivs dv{};
   if (!st) {
+    g = nh / nkv;
     dv.g = make_fd((uint32_t)g);
     dv.bkv = make_fd((uint32_t)bkv);
     dv.bq = make_fd((uint32_t)bq);
     dv.chunk = chunk > 0 ? make_fd((uint32_t)chunk) : FastDiv{1u, 1u, 0u};
-    if (chunk > 0 && causal) {
-      flags = kPreWarp | kPreWarpCounts;
-    } else {
-      uint64_t part = 0;  // count_tasks, saturating at 2^40
-      for (int32_t b = 0; b < bs; ++b) {
-        const uint32_t q = __ldg(req + 2 * b), kv = __ldg(req + 2 * b + 1);
-        const uint32_t nqb = dv.bq.div(q * (uint32_t)g + (uint32_t)bq - 1u);
-        part = sat_add(part, chunk == 0 ? (uint64_t)nqb : (uint64_t)nqb * dv.chunk.div(kv + (uint32_t)chunk - 1u));
-      }
-      L = (int64_t)part;
-      if (L > kI32Max || L * nkv > kI32Max) {
-        st = SP_PAIR_E_RANGE;
-        L = 0;
-      } else if (L * nkv > min_n) {
-        flags = kPreWarp;
-      } else {  // sparse: U and the largest unit (sparse_units)
-        uint32_t um = 0;
-        for (int32_t b = 0; b < bs; ++b) {
-          const uint32_t q = __ldg(req + 2 * b), kv = __ldg(req + 2 * b + 1);
-          const uint32_t rows = q * (uint32_t)g, nqb = dv.bq.div(rows + (uint32_t)bq - 1u);
-          for (uint32_t i = 0; i < nqb; ++i) {
-            const uint32_t need = kv_need(i, bq, rows, q, kv, causal, dv.g);
-            if (chunk == 0) {
-              const uint32_t u = dv.bkv.div(need + (uint32_t)bkv - 1u);
-              U += u;
-              um = max(um, u);
-            } else {
-              for (uint32_t c0 = 0; c0 < need; c0 += (uint32_t)chunk) {
-                const uint32_t u = dv.bkv.div(min((uint32_t)chunk, need - c0) + (uint32_t)bkv - 1u);
-                U += u;
-                um = max(um, u);
-                if (need - c0 <= (uint32_t)chunk) break;
-              }
-            }
+    const bool csplit = chunk > 0 && causal;  // a chunk count per q-block: the warp counts L
+    // one pass over the requests: validation (the first failing request decides),
+    // the task count (count_tasks, saturating at 2^40) and, while the running
+    // count can still be sparse (T <= min_n), the units (sparse_units)
+    uint64_t part = 0;
+    uint32_t um = 0;
+    bool sparse = !csplit;
+    for (int32_t b = 0; b < bs; ++b) {
+      const int64_t q = __ldg(req + 2 * b), kv = __ldg(req + 2 * b + 1);
+      if (q < 1 || kv < 1) st = SP_PAIR_E_DIM;
+      else if (causal && kv < q) st = SP_PAIR_E_CAUSAL;
+      else if (q * g > kI32Max) st = SP_PAIR_E_RANGE;
+      if (st) break;
+      if (csplit) continue;
+      const uint32_t rows = (uint32_t)q * (uint32_t)g, nqb = dv.bq.div(rows + (uint32_t)bq - 1u);
+      part = sat_add(part, chunk == 0 ? (uint64_t)nqb
+                                      : (uint64_t)nqb * dv.chunk.div((uint32_t)kv + (uint32_t)chunk - 1u));
+      sparse = sparse && part * (uint64_t)nkv <= (uint64_t)min_n;
+      if (!sparse) continue;
+      for (uint32_t i = 0; i < nqb; ++i) {  // <= min_n tasks in all
+        const uint32_t need = kv_need(i, bq, rows, (uint32_t)q, (uint32_t)kv, causal, dv.g);
+        if (chunk == 0) {
+          const uint32_t u = dv.bkv.div(need + (uint32_t)bkv - 1u);
+          U += u;
+          um = max(um, u);
+        } else {
+          for (uint32_t c0 = 0; c0 < need; c0 += (uint32_t)chunk) {
+            const uint32_t u = dv.bkv.div(min((uint32_t)chunk, need - c0) + (uint32_t)bkv - 1u);
+            U += u;
+            um = max(um, u);
+            if (need - c0 <= (uint32_t)chunk) break;
           }
         }
-        if (U > (uint64_t)kU32Max) {
+      }
+    }
+    if (!st) {
+      if (csplit) {
+        flags = kPreWarp | kPreWarpCounts;
+      } else {
+        L = (int64_t)part;
+        if (L > kI32Max || L * nkv > kI32Max) {
           st = SP_PAIR_E_RANGE;
           L = 0;
-          U = 0;
-        } else {
+        } else if (!sparse) {
+          flags = kPreWarp;
+        } else if (U > (uint64_t)kU32Max) {
+          st = SP_PAIR_E_RANGE;
+          L = 0;
+        } else {  // sparse: every SM holds at most one task
           for (int32_t d = 0; d < n_slots; ++d) {
             res.mS[(int64_t)d * res.ld + c] = (int64_t)um;  // (lo, hi) = (umax, umax): see finish_max
             res.mB[(int64_t)d * res.ld + c] = (int64_t)um;
@@ -825,6 +825,7 @@ __global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults re
         }
       }
     }
+    if (st || flags) U = 0;  // res.U is final for finished (sparse) configs only
   }
   res.st[c] = st;
   res.L[c] = L;
@@ -951,13 +952,17 @@ __global__ void __launch_bounds__(256) attn_emit_cross(ConfigView cfg, const Dev
                                                        AttnResults res, FeatOut out) {
   __shared__ DevSpec s_spec[kEmitSpecTile];
   __shared__ int32_t s_slot[kEmitSpecTile];
+  __shared__ FastDiv s_fn[kEmitSpecTile];
   const int j0 = blockIdx.y * kEmitSpecTile, j1 = min(n_specs, j0 + kEmitSpecTile);
   {
     const int n_words = (j1 - j0) * (int)(sizeof(DevSpec) / 16);
     const int4 *src = reinterpret_cast<const int4 *>(specs + g0 + j0);
     int4 *dst = reinterpret_cast<int4 *>(s_spec);
     for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = __ldg(src + i);
-    if (threadIdx.x < j1 - j0) s_slot[threadIdx.x] = __ldg(spec_slot + j0 + threadIdx.x);
+    if (threadIdx.x < j1 - j0) {
+      s_slot[threadIdx.x] = __ldg(spec_slot + j0 + threadIdx.x);
+      s_fn[threadIdx.x] = make_fd((uint32_t)__ldg(&specs[g0 + j0 + threadIdx.x].num_sms));
+    }
   }
   __syncthreads();
   const int64_t C = cfg.n_configs;
@@ -970,8 +975,8 @@ __global__ void __launch_bounds__(256) attn_emit_cross(ConfigView cfg, const Dev
     const int64_t slot = s_slot[j - j0];
     DistinctMax m{0, 0};
     if (!st)
-      m = finish_max(__ldg(res.mS + slot * res.ld + c), __ldg(res.mB + slot * res.ld + c), tt.T,
-                     s_spec[j - j0].num_sms, al.bq, al.bkv);
+      m = finish_max(__ldg(res.mS + slot * res.ld + c), __ldg(res.mB + slot * res.ld + c), tt.T, s_fn[j - j0],
+                     al.bq, al.bkv);
     attn_emit_pair(out, (int64_t)j * C + c, al, tt, m, s_spec[j - j0]);
   }
 }
@@ -998,7 +1003,7 @@ __device__ void attn_one_pair(const ConfigView &cfg, int64_t c, const DevSpec &s
       st = attn_config<1, true>(a, dv, -1, acc, words, scr, N, off, fd, N[0], lane, L, U, sm, sm + 1, 1);
   }
   if (lane == 0)
-    attn_emit(out, p, a, st, L, U, st ? DistinctMax{0, 0} : finish_max(sm[0], sm[1], L * a.nkv, N[0], a.bq, a.bkv),
+    attn_emit(out, p, a, st, L, U, st ? DistinctMax{0, 0} : finish_max(sm[0], sm[1], L * a.nkv, *fd, a.bq, a.bkv),
               sp);
   __syncwarp();
 }

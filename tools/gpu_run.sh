@@ -1,3 +1,3 @@
-mkdir -p gpurun_out/r02q
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/r02q/pytest.txt 2>&1; tail -n 4 gpurun_out/r02q/pytest.txt
-timeout 300 python tools/time_stages.py --reps 10 > gpurun_out/r02q/stages.txt 2>&1; cat gpurun_out/r02q/stages.txt
+mkdir -p gpurun_out/r02s
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_range.py tests/test_gpu_sched.py -q -x > gpurun_out/r02s/pytest.txt 2>&1; tail -n 2 gpurun_out/r02s/pytest.txt
+bash tools/gpu_ab.sh gpurun_out/r02s cfg2 prev faA faB default prev default
