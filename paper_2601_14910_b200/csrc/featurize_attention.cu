@@ -947,7 +947,10 @@ constexpr int kEmitSpecTile = 16;
 // totals are computed once per config; each spec then costs its dtype check, the
 // busiest-SM demands and the record store (pair p = j * C + c: a warp's stores
 // to every SoA row are 32 consecutive elements).
-__global__ void __launch_bounds__(256) attn_emit_cross(ConfigView cfg, const DevSpec *__restrict__ specs, int g0,
+#ifndef SP_EMIT_MINB
+#define SP_EMIT_MINB 3  // 80 registers, 3 blocks/SM: measured best of 1, 3, 4 on cfg2 (128 registers left it at 23% warps)
+#endif
+__global__ void __launch_bounds__(256, SP_EMIT_MINB) attn_emit_cross(ConfigView cfg, const DevSpec *__restrict__ specs, int g0,
                                                        int n_specs, const int32_t *__restrict__ spec_slot,
                                                        AttnResults res, FeatOut out) {
   __shared__ DevSpec s_spec[kEmitSpecTile];
