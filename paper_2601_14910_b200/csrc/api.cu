@@ -332,13 +332,46 @@ extern "C" sp_status sp_prepare(sp_ctx *ctx, int32_t family, int64_t n_configs, 
     const AttnPlan *plan = nullptr;
     sp_status st = attn_plan(ctx, specs, spec_begin, spec_end, &plan);
     if (st != SP_OK) return st;
-    return grow_attn_res(ctx, n_configs, plan->n_slots);
+    st = grow_attn_res(ctx, n_configs, plan->n_slots);
+    if (st != SP_OK) return st;
+    return grow_pre(ctx, n_configs);  // the fused path's per-config record
   }
   if (family != SP_GEMM_SPLITK) return grow_pre(ctx, n_configs);
   return SP_OK;
 }
 
 // --------------------------------------------------------------- featurize
+
+// Attention, CROSS: plan + scratch, then the pre-pass, schedule, (emit) and planner
+// kernels.  emit = false for the fused path (the fused kernel writes the records).
+static sp_status attn_cross(sp_ctx *ctx, sp_specs *specs, const sp_pairing *pairs, const ConfigView &cv,
+                            const FeatOut &fo, int64_t n_pairs, void *stream, bool emit, AttnPlan &run,
+                            AttnResults &res) {
+  const AttnPlan *plan = nullptr;
+  sp_status st = attn_plan(ctx, specs, pairs->spec_begin, pairs->spec_end, &plan);
+  if (st != SP_OK) return st;
+  if (plan->n_groups > kAttnMaxGroups)
+    return fail(ctx, SP_E_UNSUPPORTED, "attention featurization: too many distinct SM-count groups");
+  run = *plan;
+  run.counters = ctx->counters;
+  // per-config results of the schedule kernel: st (4 B), L, U, (lo, hi) per slot (8 B each), pre-pass record
+  const int64_t C = cv.n_configs, ld = (C + 31) & ~(int64_t)31;
+  st = grow_attn_res(ctx, C, run.n_slots);
+  if (st != SP_OK) return st;
+  char *base = (char *)ctx->attn_res;
+  res.ld = ld;
+  res.L = (int64_t *)base;
+  res.U = (uint64_t *)(base + 8 * ld);
+  res.mS = (int64_t *)(base + 16 * ld);
+  res.mB = res.mS + (size_t)run.n_slots * ld;
+  res.st = (int32_t *)(res.mB + (size_t)run.n_slots * ld);
+  res.pre = (uint32_t *)(res.st + ld);
+  const int e = launch_featurize_attention(cv, (const DevSpec *)specs->dev.p, pairs->spec_begin, pairs->spec_end,
+                                           specs->n, run, res, n_pairs, nullptr, nullptr, specs->max_sms, fo,
+                                           ctx->num_sms, stream, ctx->hook(), emit);
+  if (e) return cuda_fail(ctx, e, "sp_featurize: attention launch");
+  return SP_OK;
+}
 
 extern "C" sp_status sp_featurize(sp_ctx *ctx, const sp_config_batch *cfg, const sp_specs *specs_c,
                                   const sp_pairing *pairs, const sp_features *out, void *stream) {
@@ -433,28 +466,11 @@ extern "C" sp_status sp_featurize_ex(sp_ctx *ctx, const sp_config_batch *cfg, co
                              cross ? nullptr : pairs->spec_idx, max_targets, fo, ctx->num_sms, stream, ctx->hook());
   } else if (fam == SP_ATTENTION) {
     if (pairs->kind == SP_PAIRS_CROSS) {
-      const AttnPlan *plan = nullptr;
-      sp_status st = attn_plan(ctx, specs, pairs->spec_begin, pairs->spec_end, &plan);
-      if (st != SP_OK) return st;
-      if (plan->n_groups > kAttnMaxGroups)
-        return fail(ctx, SP_E_UNSUPPORTED, "attention featurization: too many distinct SM-count groups");
-      AttnPlan run = *plan;
-      run.counters = ctx->counters;
-      // per-config results of the schedule kernel: st (4 B), L, U, and maxS/maxB per slot (8 B each)
-      const int64_t C = cfg->n_configs, ld = (C + 31) & ~(int64_t)31;
-      st = grow_attn_res(ctx, C, run.n_slots);
-      if (st != SP_OK) return st;
-      char *base = (char *)ctx->attn_res;
+      AttnPlan run;
       AttnResults res;
-      res.ld = ld;
-      res.L = (int64_t *)base;
-      res.U = (uint64_t *)(base + 8 * ld);
-      res.mS = (int64_t *)(base + 16 * ld);
-      res.mB = res.mS + (size_t)run.n_slots * ld;
-      res.st = (int32_t *)(res.mB + (size_t)run.n_slots * ld);
-      res.pre = (uint32_t *)(res.st + ld);
-      e = launch_featurize_attention(cv, ds, pairs->spec_begin, pairs->spec_end, specs->n, run, res, n_pairs,
-                                     nullptr, nullptr, specs->max_sms, fo, ctx->num_sms, stream, ctx->hook());
+      sp_status st = attn_cross(ctx, specs, pairs, cv, fo, n_pairs, stream, true, run, res);
+      if (st != SP_OK) return st;
+      e = 0;
     } else {
       if (specs->max_sms > kAttnMaxSms)
         return fail(ctx, SP_E_UNSUPPORTED, "attention featurization supports at most 4096 SMs per spec");
@@ -490,7 +506,7 @@ extern "C" sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cf
   if (model->family != cfg->family) return fail(ctx, SP_E_ARG, "sp_featurize_predict: config/model family mismatch");
   const int fam = cfg->family;
   const bool fusable = (fam == SP_GEMM || fam == SP_FUSED_MOE || fam == SP_RMSNORM || fam == SP_SILU_MUL ||
-                        fam == SP_SCALED_MM) &&
+                        fam == SP_SCALED_MM || fam == SP_ATTENTION) &&
                        pairs->kind == SP_PAIRS_CROSS &&
                        (model->precision == SP_MLP_BF16 || model->precision == SP_MLP_FP16);
   if (!fusable) {  // the two-kernel path (attention, split-K, pair lists, the fp32 predictor)
@@ -506,6 +522,8 @@ extern "C" sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cf
   if (cfg->n_configs > 0 && !cfg->fields) return fail(ctx, SP_E_ARG, "sp_featurize_predict: fields is NULL");
   if (fam == SP_FUSED_MOE && cfg->ragged_off && !cfg->ragged)
     return fail(ctx, SP_E_ARG, "sp_featurize_predict: MoE ragged_off without ragged");
+  if (fam == SP_ATTENTION && cfg->n_configs > 0 && (!cfg->ragged || !cfg->ragged_off))
+    return fail(ctx, SP_E_ARG, "sp_featurize_predict: attention needs ragged (qlen, kvlen) data");
   if (out->family != fam) return fail(ctx, SP_E_ARG, "sp_featurize_predict: out->family != cfg->family");
   if (pairs->spec_begin < 0 || pairs->spec_end > specs->n || pairs->spec_begin > pairs->spec_end)
     return fail(ctx, SP_E_ARG, "sp_featurize_predict: spec range out of bounds");
@@ -523,11 +541,29 @@ extern "C" sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cf
   if (gst != SP_OK) return gst;
   ConfigView cv{cfg->fields, cfg->ragged, cfg->ragged_off, cfg->n_configs, cfg->field_ld};
   const LaunchHook h = ctx->hook();
-  h.on_begin("uniform_prepass", stream);
-  int e = launch_uniform_prepass(fam, cv, (uint64_t *)ctx->pre, ldc, stream);
-  h.on_end(stream);
-  if (e) return cuda_fail(ctx, e, "sp_featurize_predict: pre-pass launch");
-  FusedIn fi;
+  FusedIn fi{};
+  int e;
+  if (fam == SP_ATTENTION) {
+    // schedule (+ the planner's pairs, written to `out`), then the per-config record
+    AttnPlan run;
+    AttnResults res;
+    sp_status st = attn_cross(ctx, const_cast<sp_specs *>(specs), pairs, cv,
+                              FeatOut{out->ints, out->flts, out->status, out->ld}, n_pairs, stream, false, run, res);
+    if (st != SP_OK) return st;
+    h.on_begin("attn_fuse_prep", stream);
+    e = launch_attn_fuse_prep(cv, res, (uint64_t *)ctx->pre, ldc, stream);
+    h.on_end(stream);
+    if (e) return cuda_fail(ctx, e, "sp_featurize_predict: attention pre-pass launch");
+    fi.slot = run.spec_slot;
+    fi.lo = res.mS;
+    fi.hi = res.mB;
+    fi.lohi_ld = res.ld;
+  } else {
+    h.on_begin("uniform_prepass", stream);
+    e = launch_uniform_prepass(fam, cv, (uint64_t *)ctx->pre, ldc, stream);
+    h.on_end(stream);
+    if (e) return cuda_fail(ctx, e, "sp_featurize_predict: pre-pass launch");
+  }
   fi.pre = (const uint64_t *)ctx->pre;
   fi.ldc = ldc;
   fi.C = C;

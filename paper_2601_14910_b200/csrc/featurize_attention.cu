@@ -1437,10 +1437,40 @@ int launch_attention_sim(int mode, const ConfigView &cfg, const DevSpec *specs, 
 // shared memory one warp of the simulation kernel needs (<= 227 KB or unsupported)
 int64_t attention_sim_smem_bytes(int64_t max_targets) { return sim_words(max_targets) * 8; }
 
+// Per-config record of the fused attention path (layout in sp_internal.h): what
+// attn_emit_cross computes once per config before its spec loop -- status, T
+// and the exact GPU totals (attn_totals) -- for the fused kernel's producers,
+// which finish each pair from it, its spec and the slot's (lo, hi).
+__global__ void __launch_bounds__(256) attn_fuse_prep(ConfigView cfg, AttnResults res, uint64_t *__restrict__ pre,
+                                                      int64_t ldc) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cfg.n_configs) return;
+  const int st = __ldg(res.st + c);
+  const bool planner = __ldg(cfg.fields + (int64_t)CHUNK * cfg.ld + c) == -1;
+  const AttnCfg al = st ? AttnCfg{} : load_cfg_lane(cfg, c);
+  const AttnTotals tt = attn_totals(al, st, st ? 0 : __ldg(res.L + c), st ? 0 : __ldg(res.U + c));
+  pre[c] = (uint64_t)(uint32_t)tt.status | (uint64_t)(tt.range_bad ? 1u : 0u) << 8 | (uint64_t)(planner ? 1u : 0u) << 9 |
+           (uint64_t)(uint32_t)(st ? 0 : al.dt + 1) << 16 | (uint64_t)(uint32_t)tt.T << 32;
+  pre[1 * ldc + c] = (uint64_t)tt.tot[0];
+  pre[2 * ldc + c] = (uint64_t)tt.tot[2];
+  pre[3 * ldc + c] = (uint64_t)tt.tot[3];
+  pre[4 * ldc + c] = (uint64_t)(uint32_t)al.bq | (uint64_t)(uint32_t)al.bkv << 32;
+  pre[5 * ldc + c] = (uint64_t)(uint32_t)min(al.fp.smem, (int64_t)0xffffffffLL) | (uint64_t)(uint32_t)al.fp.warps << 32;
+  pre[6 * ldc + c] = (uint64_t)(uint32_t)al.fp.regs | (uint64_t)(uint32_t)al.hd << 32;
+}
+
+int launch_attn_fuse_prep(const ConfigView &cfg, const AttnResults &res, uint64_t *pre, int64_t ldc, void *stream) {
+  if (cfg.n_configs == 0) return 0;
+  attn_fuse_prep<<<(unsigned)((cfg.n_configs + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      cfg, res, pre, ldc);
+  return (int)cudaGetLastError();
+}
+
 int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
                                int n_specs, const AttnPlan &plan, const AttnResults &res, int64_t n_pairs,
                                const int64_t *cfg_idx, const int32_t *spec_idx, int32_t max_sms,
-                               const FeatOut &out, int num_device_sms, void *stream, const LaunchHook &hook) {
+                               const FeatOut &out, int num_device_sms, void *stream, const LaunchHook &hook,
+                               bool emit) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (cfg_idx == nullptr) {
     if (cfg.n_configs == 0 || plan.n_groups == 0) return 0;
@@ -1462,14 +1492,17 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
       if (e) return e;
       y = y1;
     }
-    const dim3 blocks((unsigned)((cfg.n_configs + 255) / 256),
-                      (unsigned)((spec_end - spec_begin + kEmitSpecTile - 1) / kEmitSpecTile));
-    hook.on_begin("attn_emit_cross", st);
-    attn_emit_cross<<<blocks, 256, 0, st>>>(cfg, specs, spec_begin, spec_end - spec_begin, plan.spec_slot, res,
-                                            out);
-    hook.on_end(st);
-    cudaError_t le = cudaGetLastError();
-    if (le != cudaSuccess) return (int)le;
+    cudaError_t le;
+    if (emit) {
+      const dim3 blocks((unsigned)((cfg.n_configs + 255) / 256),
+                        (unsigned)((spec_end - spec_begin + kEmitSpecTile - 1) / kEmitSpecTile));
+      hook.on_begin("attn_emit_cross", st);
+      attn_emit_cross<<<blocks, 256, 0, st>>>(cfg, specs, spec_begin, spec_end - spec_begin, plan.spec_slot, res,
+                                              out);
+      hook.on_end(st);
+      le = cudaGetLastError();
+      if (le != cudaSuccess) return (int)le;
+    }
     // planner configs (kv_chunk = -1): per pair, after the cross kernels skipped them
     const int pw = ((max_sms + kAttnSlack + 3) & ~3) + kAttnScratchWords;
     const size_t psmem = (size_t)kWarps * pw * 4;

@@ -154,6 +154,10 @@ __device__ long long g_pred_wtrace[16][64][16];  // every epilogue warp (lane 0)
 #define EPI_WAIT(b, ph) tc::mbar_wait_sleep(b, ph)
 #endif
 
+#ifndef SP_STAGGER
+#define SP_STAGGER 0
+#endif
+constexpr bool kStagger = SP_STAGGER;
 #ifdef SP_EXP_NOMMA
 constexpr bool kNoMma = true;
 #else
@@ -346,6 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
           if (j >= n_local) continue;
           const uint32_t B = tmem + (uint32_t)(s * 256);
           if (layer[s] == 0) {
+            // stagger: no layer 1 while the other slot's layer-1 epilogue runs (both epilogues at
+            // once leave the tensor pipe idle and lock the slots in phase)
+            if (kStagger && js[s ^ 1] < n_local && layer[s ^ 1] == 1) continue;
             const int xi = (int)(j % kNX);
             if (!tc::mbar_test(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u)) continue;
             if (j >= 2 && !tc::mbar_test(bar(kBarSlotFree + s), pf[s])) continue;
@@ -691,6 +698,9 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
           if (j >= n_local) continue;
           const uint32_t B = tmem + (uint32_t)(s * 256);
           if (layer[s] == 0) {
+            // stagger: no layer 1 while the other slot's layer-1 epilogue runs (both epilogues at
+            // once leave the tensor pipe idle and lock the slots in phase)
+            if (kStagger && js[s ^ 1] < n_local && layer[s ^ 1] == 1) continue;
             const int xi = (int)(j % kNX);
             if (!tc::mbar_test(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u)) continue;
             if (j >= 2 && !tc::mbar_test(bar(kBarSlotFree + s), pf[s])) continue;
@@ -784,8 +794,22 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       for (int f = 0; f < 16; ++f) xv[f] = 0.f;
       float side_t = 0.f;
       uint32_t side_s = 1;
-      if (live) {
-        const uint64_t w0 = rj[0];
+      const uint64_t w0 = live ? rj[0] : 0;
+      if (FAM == SP_ATTENTION && live && ((w0 >> 9) & 1)) {
+        // planner config (kv_chunk -1): attn_planner_cross wrote its record; read it back
+        const int64_t ld = fz.out.ld;
+        const uint32_t st = fz.out.status[p];
+        side_s = st;
+        if (st == 0) {
+          side_t = fz.out.flts[(int64_t)F_TTHEORY * ld + p];
+#pragma unroll
+          for (int f = 0; f < n_in_of(FAM); ++f) {
+            const int sl = in_slot(FAM, f);
+            const float v = sl >= 16 ? fz.out.flts[(int64_t)(sl - 16) * ld + p] : (float)fz.out.ints[(int64_t)sl * ld + p];
+            xv[f] = fmaf(lg2_ftz(1.f + v), na[f], nc[f]);
+          }
+        }
+      } else if (live) {
         int st = (int)(w0 & 0xff);
         const int tdt = (int)((w0 >> 16) & 0xff) - 1;
         const DevSpec &sp = fz.specs[fz.g0 + gs];
@@ -797,12 +821,34 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
         } else {
           PairDemand d;
           d.T = (int64_t)(w0 >> 32);
-          const int64_t per_sm = (int64_t)(((uint32_t)d.T + (uint32_t)sp.num_sms - 1u) / (uint32_t)sp.num_sms);
+          if (FAM == SP_ATTENTION) {
+            // totals from the record; busiest SM from the slot's class maxima (finish_max):
+            // T = qn N + rn, lo over the rn SMs with qn + 1 tasks, hi over the rest
+            const int64_t slot = fz.slot[gs];
+            const int64_t lo = fz.lo[slot * fz.lohi_ld + c], hi = fz.hi[slot * fz.lohi_ld + c];
+            const uint64_t w4 = rj[4 * kTile];
+            const int64_t bq = (uint32_t)w4, bkv = (uint32_t)(w4 >> 32), hd = (uint32_t)(rj[6 * kTile] >> 32);
+            const int64_t N = sp.num_sms, qn = (int64_t)((uint32_t)d.T / (uint32_t)N), rn = d.T - qn * N;
+            int64_t mB = 0;
+            if (rn > 0) mB = bq * (qn + 1) + 2 * bkv * lo;
+            if (rn < N) mB = max(mB, bq * qn + 2 * bkv * hi);
+            const int64_t mS = max(lo, hi);
+            d.tot[0] = (int64_t)rj[1 * kTile];
+            d.tot[1] = 0;
+            d.tot[2] = (int64_t)rj[2 * kTile];
+            d.tot[3] = (int64_t)rj[3 * kTile];
+            d.mx[0] = 4 * bq * hd * bkv * mS;  // <= totT (mS <= U nkv)
+            d.mx[1] = 0;
+            d.mx[2] = bq * (bkv + 1) * mS;
+            d.mx[3] = 2 * hd * mB;
+          } else {
+            const int64_t per_sm = (int64_t)(((uint32_t)d.T + (uint32_t)sp.num_sms - 1u) / (uint32_t)sp.num_sms);
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int64_t task = (int64_t)rj[(1 + qq) * kTile];
-            d.tot[qq] = d.T * task;
-            d.mx[qq] = per_sm * task;
+            for (int qq = 0; qq < 4; ++qq) {
+              const int64_t task = (int64_t)rj[(1 + qq) * kTile];
+              d.tot[qq] = d.T * task;
+              d.mx[qq] = per_sm * task;
+            }
           }
           const uint64_t ws = rj[5 * kTile];
           const Footprint fp{(int64_t)(uint32_t)ws, (int64_t)(ws >> 32), (int64_t)(uint32_t)rj[6 * kTile]};
@@ -1075,6 +1121,7 @@ static cudaError_t launch_fused(int fam, const FusedParams &P, unsigned grid, cu
     case SP_FUSED_MOE: kern = predict_tcgen05_fused_kernel<BF16, SP_FUSED_MOE>; break;
     case SP_RMSNORM: kern = predict_tcgen05_fused_kernel<BF16, SP_RMSNORM>; break;
     case SP_SILU_MUL: kern = predict_tcgen05_fused_kernel<BF16, SP_SILU_MUL>; break;
+    case SP_ATTENTION: kern = predict_tcgen05_fused_kernel<BF16, SP_ATTENTION>; break;
     default: return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmemBytes);

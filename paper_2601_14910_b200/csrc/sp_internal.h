@@ -137,10 +137,12 @@ struct LaunchHook {
   void on_begin(const char *k, void *st) const { if (begin) begin(self, k, st); }
   void on_end(void *st) const { if (end) end(self, st); }
 };
+// emit = false (cross mode, the fused path): no attn_emit_cross; the planner's pairs are still written.
 int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int spec_begin, int spec_end,
                                int n_specs, const AttnPlan &plan, const AttnResults &res, int64_t n_pairs,
                                const int64_t *cfg_idx, const int32_t *spec_idx, int32_t max_sms,
-                               const FeatOut &out, int num_device_sms, void *stream, const LaunchHook &hook);
+                               const FeatOut &out, int num_device_sms, void *stream, const LaunchHook &hook,
+                               bool emit = true);
 
 // Attention under SP_SCHED_GREEDY / SP_SCHED_MINHEAP: warp per pair, sequential
 // scheduler simulation (CROSS when cfg_idx == nullptr, else LIST).  max_targets =
@@ -198,7 +200,19 @@ struct FusedIn {
   const DevSpec *specs;
   FeatOut out;
   int64_t n_pairs;
+  // attention (FAM = SP_ATTENTION): per spec of the range its distinct slot, and the
+  // schedule kernel's per-(slot, config) class maxima (lo, hi) [n_slots][lohi_ld]
+  const int32_t *slot;
+  const int64_t *lo, *hi;
+  int64_t lohi_ld;
 };
+// Attention pre-pass of the fused path (thread per config; after attn_schedule_cross
+// and attn_planner_cross), u64 SoA [kPreFields][ldc]:
+//   0 status | range_bad << 8 | planner << 9 | (tensor dtype + 1) << 16 | T << 32
+//   1 total Tensor ops  2 total XU ops  3 total load bytes
+//   4 BQ | BKV << 32    5 smem per task | warps << 32    6 regs | head dim << 32
+// planner = kv_chunk -1: its records are attn_planner_cross's, read back.
+int launch_attn_fuse_prep(const ConfigView &cfg, const AttnResults &res, uint64_t *pre, int64_t ldc, void *stream);
 int launch_predict_tcgen05_fused(const MlpBf16 &m, const FusedIn &fi, float *latency, float *eff,
                                  int num_device_sms, void *stream);
 

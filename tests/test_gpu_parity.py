@@ -626,6 +626,43 @@ def test_featurize_predict_equals_two_calls(sp, ctx, fam, prec):
         assert np.array_equal(e0.view(np.uint32), e1.view(np.uint32)), fam
 
 
+def test_featurize_predict_attention_planner_and_errors(sp, ctx, orc):
+    """The fused attention path with split-KV planner configs (kv_chunk -1: the
+    planner kernel's records are read back by the producers), domain errors
+    (zero batch, GQA mismatch, causal kv < q) and both causal paths: records
+    and latencies bit-identical to the two calls, and the oracle's ints."""
+    b = gen.gen_attention(120, 120, 77, max_bs=6, qlen_max=3000, kvlen_max=6000, groups=(1, 3, 4, 5))
+    ch = b.fields[gen.FIELDS[gen.ATTENTION].index("KV_CHUNK")]
+    causal = b.fields[gen.FIELDS[gen.ATTENTION].index("CAUSAL")]
+    ch[(np.arange(b.n_configs) % 4 == 1) & (causal == 0)] = -1
+    nh = b.fields[gen.FIELDS[gen.ATTENTION].index("NH")]
+    nh[7] += 1  # nh % nkv != 0 -> SP_PAIR_E_HEADS (unless nkv = 1)
+    sa = specs.paper_gpu_specs()
+    sh = ctx.load_gpu_specs(sa)
+    m = ctx.load_model(models.random_mlp(b.family, 12), "fp16")
+    db = sp.DeviceBatch.from_host(b, ctx.torch_device)
+    n = len(sa) * b.n_configs
+    outs = []
+    for fused in (False, True):
+        f = sp.Features.empty(b.family, n, ctx.torch_device)
+        lat = torch.full((n,), -1.0, dtype=torch.float32, device="cuda")
+        if fused:
+            ctx.featurize_predict(db, sh, m, f, lat)
+        else:
+            ctx.featurize(db, sh, f)
+            ctx.predict(m, f, lat)
+        torch.cuda.synchronize()
+        outs.append((sp.features_to_host(f), lat.cpu().numpy()))
+    (gi0, gf0, gs0), l0 = outs[0]
+    (gi1, gf1, gs1), l1 = outs[1]
+    assert (ch == -1).sum() > 10
+    assert np.array_equal(gs0, gs1) and np.array_equal(gi0, gi1)
+    assert np.array_equal(gf0.view(np.uint32), gf1.view(np.uint32))
+    assert np.array_equal(l0.view(np.uint32), l1.view(np.uint32))
+    o = orc.featurize(b, sa)
+    assert np.array_equal(gs1, o.status) and np.array_equal(gi1, o.ints)
+
+
 @pytest.mark.parametrize("cfg", ["cfg3", "cfg5", "scaledmm", "splitk"])
 def test_full_size_sampled_fused(sp, ctx, orc, cfg):
     """BASELINE configs 3 (1e6 fused-MoE configs x 11 GPUs) and 5 (1,000 serving
