@@ -613,7 +613,11 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
 // Layout: as the kernel above up to H2 (raw staging: 2 groups x kFNR stages of
 // kPreFields u64 per row = 42 KB of the 48 KB), then the producer -> epilogue side
 // ring (t_theory, status per row of kNS tiles) and the barriers.
-constexpr int kFProdWarps = 8;
+#ifndef SP_FPROD_WARPS
+#define SP_FPROD_WARPS 8
+#endif
+constexpr int kFProdWarps = SP_FPROD_WARPS;
+constexpr int kFGroups = kFProdWarps / 4;  // producer groups, taking tiles j = gid (mod kFGroups)
 // Two producer groups take tiles j = gid (mod 2).  The X-ring parity wait of tile
 // j (phase of tile j - kNX) is unambiguous only if the same group produced tile
 // j - kNX (which itself waited for tile j - 2 kNX), so kNX must be a multiple of
@@ -621,9 +625,9 @@ constexpr int kFProdWarps = 8;
 static_assert(kNX % (kFProdWarps / 4) == 0, "X ring depth must be a multiple of the producer group count");
 constexpr int kFMmaWarp = kEpiWarps + kFProdWarps;
 constexpr int kFThreads = (kFMmaWarp + 1) * 32;
-constexpr int kFNR = 2;
+constexpr int kFNR = 4 / kFGroups;  // raw stages per producer group
 constexpr uint32_t kFRawBytes = kPreFields * kTile * 8;
-static_assert(2 * kFNR * kFRawBytes <= kNR * kRawBytes, "fused raw staging fits the unfused one");
+static_assert(kFGroups * kFNR * kFRawBytes <= kNR * kRawBytes, "fused raw staging fits the unfused one");
 constexpr int kNS = 8;  // the producer of tile j + kNS waited for tile j + kNS - kNX's layer-1 MMA,
                         // which needed tile j's slot freed: the ring never overruns
 constexpr uint32_t kFOffSide = kOffBar;
@@ -648,8 +652,8 @@ struct FusedParams {
 // partial tiles; the pre-pass stays in L2 anyway).  Returns false past the end.
 __device__ __forceinline__ bool fused_tile_pair(const FusedIn &fz, int64_t t, uint32_t row, int64_t &p, int64_t &c,
                                                 int &gs) {
-  if (fz.cmajor) {  // t < n_tiles < 2^31: 32-bit division (the 64-bit one was 5% of the kernel's instructions)
-    const uint32_t ns = (uint32_t)fz.n_specs, cb32 = (uint32_t)t / ns;
+  if (fz.cmajor) {  // t < n_tiles < 2^31: FastDiv (a plain 32-bit division was 3.4% of the kernel's instructions)
+    const uint32_t ns = (uint32_t)fz.n_specs, cb32 = FastDiv{ns, fz.ns_m, fz.ns_s}.div((uint32_t)t);
     const int64_t cb = cb32;
     gs = (int)((uint32_t)t - cb32 * ns);
     c = cb * kTile + row;
@@ -808,18 +812,18 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
         int64_t p, c;
         int gs;
         if (!fused_tile_pair(fz, blockIdx.x + j * G, row, p, c, gs)) c = 0;  // tail rows: harmless copy
-        const uint32_t dst = raw_base + (uint32_t)((j >> 1) % kFNR) * kFRawBytes + row * 8;
+        const uint32_t dst = raw_base + (uint32_t)((j / kFGroups) % kFNR) * kFRawBytes + row * 8;
 #pragma unroll
         for (int f = 0; f < kPreFields; ++f) cp_async8(dst + f * kTile * 8, fz.pre + (int64_t)f * fz.ldc + c);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll
-    for (int jj = 0; jj < kFNR - 1; ++jj) issue(gid + 2 * jj);
-    for (int64_t j = gid; j < n_local; j += 2) {
-      issue(j + 2 * (kFNR - 1));
+    for (int jj = 0; jj < kFNR - 1; ++jj) issue(gid + kFGroups * jj);
+    for (int64_t j = gid; j < n_local; j += kFGroups) {
+      issue(j + kFGroups * (kFNR - 1));
       asm volatile("cp.async.wait_group %0;" ::"n"(kFNR - 1) : "memory");
-      const uint64_t *rj = raw + (size_t)((j >> 1) % kFNR) * (kFRawBytes / 8) + row;
+      const uint64_t *rj = raw + (size_t)((j / kFGroups) % kFNR) * (kFRawBytes / 8) + row;
       int64_t p, c;
       int gs;
       const bool live = fused_tile_pair(fz, blockIdx.x + j * G, row, p, c, gs);
@@ -1175,6 +1179,13 @@ int launch_predict_tcgen05_fused(const MlpBf16 &m, const FusedIn &fi, float *lat
   P.latency = latency;
   P.eff = eff;
   P.fz.inv_c = 1.0 / (double)fi.C;
+  {  // FastDiv of n_specs (host): s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1
+    const uint64_t d = (uint64_t)(fi.n_specs > 0 ? fi.n_specs : 1);
+    uint32_t sh = 0;
+    while ((1ull << sh) < d) ++sh;
+    P.fz.ns_s = sh;
+    P.fz.ns_m = (uint32_t)((((1ull << sh) - d) << 32) / d + 1);
+  }
   P.n_tiles = fi.cmajor ? fi.n_specs * ((fi.C + kTile - 1) / kTile) : (fi.n_pairs + kTile - 1) / kTile;
   const int64_t grid = P.n_tiles < num_device_sms ? P.n_tiles : num_device_sms;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

@@ -195,6 +195,7 @@ struct FusedIn {
   int64_t C;
   int64_t n_specs;  // spec_end - spec_begin
   double inv_c;     // 1 / C (set by the launcher)
+  uint32_t ns_m, ns_s;  // FastDiv constants of n_specs (set by the launcher)
   int cmajor;       // config-major tile order (large pre-pass, see predict_tcgen05.cu)
   int g0;
   const DevSpec *specs;

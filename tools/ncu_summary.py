@@ -92,7 +92,7 @@ def main():
         lines.append(f"| {k} | {n} | {t*1e3:.3f} | {t/tot:.1%} |")
     traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    tw = traffic.setdefault(w, {})
+    tw = traffic[w] = {}  # one capture per workload: no keys left over from an earlier one
     for tag in ("featurize", "predict"):
         rep = os.path.join(d, f"{tag}.ncu-rep")
         if not os.path.exists(rep):

@@ -16,7 +16,7 @@ FEAT=attn_schedule_cross
 SKIP=3; COUNT=1; PSKIP=3
 case "$W" in
   cfg2) ;;
-  cfg4) SKIP=6; COUNT=2; PSKIP=25 ;;  # a step: 2 attention launches; predict 25 = 1st timed step's Llama attention
+  cfg4) SKIP=6; COUNT=2; PSKIP=20 ;;  # a step: 2 attention launches (one per serving model)
   splitk) FEAT=featurize_splitk_cross ;;
   *) FEAT=uniform_prepass ;;  # uniform families run the fused pass: pre-pass + predict_tcgen05_fused
 esac
