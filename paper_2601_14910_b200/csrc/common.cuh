@@ -48,38 +48,59 @@ struct PairDemand {
   int64_t mx[4];    // max over SMs per quantity (R7)
 };
 
+// floor(a / b), b >= 1, exact: for a < 2^24 an fp32 reciprocal estimate
+// corrected by one either way (the integer division is ~20 instructions);
+// larger a take the integer division.
+__device__ __forceinline__ uint32_t udiv_q(uint32_t a, uint32_t b) {
+  if (a >= (1u << 24)) return a / b;
+  uint32_t q = (uint32_t)__fmul_rz((float)a, __frcp_rn((float)b));  // within one of floor(a/b)
+  if (q * b > a) --q;                                                 // (q + 1) b <= a + b < 2^25
+  else if ((q + 1) * b <= a) ++q;
+  return q;
+}
+
+template <bool FAST>
+__device__ __forceinline__ uint32_t udiv(uint32_t a, uint32_t b) {
+  return FAST ? udiv_q(a, b) : a / b;
+}
+
 // a4: occ = max(1, min(smem quota, RF quota, warp quota, CTA limit)) (R6).
+template <bool FAST = false>
 __device__ __forceinline__ int64_t occupancy(const Footprint &fp, const DevSpec &s) {
   int64_t occ = s.max_ctas;
-  if (fp.smem > 0) occ = min(occ, fp.smem > s.smem_per_sm ? 0 : (int64_t)((uint32_t)s.smem_per_sm / (uint32_t)fp.smem));
+  if (fp.smem > 0) occ = min(occ, fp.smem > s.smem_per_sm ? 0 : (int64_t)udiv<FAST>((uint32_t)s.smem_per_sm, (uint32_t)fp.smem));
   int64_t rden = fp.regs * 32 * fp.warps;
-  occ = min(occ, rden > s.regs_per_sm ? 0 : (int64_t)((uint32_t)s.regs_per_sm / (uint32_t)rden));
-  occ = min(occ, fp.warps > s.max_warps ? 0 : (int64_t)((uint32_t)s.max_warps / (uint32_t)fp.warps));
+  occ = min(occ, rden > s.regs_per_sm ? 0 : (int64_t)udiv<FAST>((uint32_t)s.regs_per_sm, (uint32_t)rden));
+  occ = min(occ, fp.warps > s.max_warps ? 0 : (int64_t)udiv<FAST>((uint32_t)s.max_warps, (uint32_t)fp.warps));
   return occ < 1 ? 1 : occ;
 }
 
 // waves = ceil(T / (N_SM * occ)) with T < 2^31.
+template <bool FAST = false>
 __device__ __forceinline__ int64_t waves_of(int64_t T, int64_t nsm, int64_t occ) {
   int64_t den = nsm * occ;
   if (T == 0) return 0;
   if (den >= T) return 1;
-  return (int64_t)(((uint32_t)T + (uint32_t)den - 1u) / (uint32_t)den);
+  return (int64_t)udiv<FAST>((uint32_t)T + (uint32_t)den - 1u, (uint32_t)den);
 }
 
 // a7-a9: cycles from the exact integers in fp64, one rounding to fp32 (R20),
 // and the record store.  tdt = tensor dtype index (0 bf16, 1 fp16, 2 fp8).
 // fv (optional): receives the 12 float slots as stored (the fused predictor
 // normalises them without reading the record back).
+// FAST: fp32-reciprocal quotients (udiv_q) -- measured per kernel: it sped up
+// the fused attention kernel and slowed the fused MoE kernel (register allocation).
+template <bool FAST = false>
 __device__ __forceinline__ void emit_pair(const FeatOut &o, int64_t p, const PairDemand &d,
                                           const Footprint &fp, const DevSpec &s, int pipes,
                                           int tdt, float *fv = nullptr) {
   const int64_t ld = o.ld;
-  int64_t occ = occupancy(fp, s);
+  int64_t occ = occupancy<FAST>(fp, s);
   int64_t *I = o.ints + p;
   float *F = o.flts + p;
   I[I_NTASKS * ld] = d.T;
   I[I_OCC * ld] = occ;
-  I[I_WAVES * ld] = waves_of(d.T, s.num_sms, occ);
+  I[I_WAVES * ld] = waves_of<FAST>(d.T, s.num_sms, occ);
   I[I_TOT_T * ld] = d.tot[0];
   I[I_TOT_F * ld] = d.tot[1];
   I[I_TOT_X * ld] = d.tot[2];

@@ -114,6 +114,10 @@ __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c,
     bm = fld(v, 5, c);
   }
   MoeHist mine;
+  // FastDiv of this lane's own BM, once per lane (its init is a 64-bit division;
+  // done warp-uniformly per config it was most of the pre-pass's instructions)
+  FastDiv my_fbm{1u, 1u, 0u};
+  if (off >= 0 && E >= 1 && bm >= 1) my_fbm.init((uint32_t)bm);
   unsigned need = __ballot_sync(0xffffffffu, off >= 0 && E >= 1 && bm >= 1);
   while (need) {
     int jj[4];
@@ -140,8 +144,8 @@ __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c,
     for (int q = 0; q < 4; ++q) {
       if (jj[q] < 0) break;  // warp-uniform
       const uint32_t bmj = (uint32_t)__shfl_sync(0xffffffffu, bm, jj[q]);
-      FastDiv fbm;  // ceil(t_e / BM) by multiply-high: one division per config, not per count
-      fbm.init(bmj);
+      // ceil(t_e / BM) by multiply-high
+      const FastDiv fbm{bmj, __shfl_sync(0xffffffffu, my_fbm.m, jj[q]), __shfl_sync(0xffffffffu, my_fbm.s, jj[q])};
       int64_t sum = 0, mb = 0;
       int neg = 0;
       auto take = [&](int32_t te) {

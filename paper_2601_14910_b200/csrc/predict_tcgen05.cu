@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
             const int64_t lo = fz.lo[slot * fz.lohi_ld + c], hi = fz.hi[slot * fz.lohi_ld + c];
             const uint64_t w4 = rj[4 * kTile];
             const int64_t bq = (uint32_t)w4, bkv = (uint32_t)(w4 >> 32), hd = (uint32_t)(rj[6 * kTile] >> 32);
-            const int64_t N = sp.num_sms, qn = (int64_t)((uint32_t)d.T / (uint32_t)N), rn = d.T - qn * N;
+            const int64_t N = sp.num_sms, qn = (int64_t)udiv_q((uint32_t)d.T, (uint32_t)N), rn = d.T - qn * N;
             int64_t mB = 0;
             if (rn > 0) mB = bq * (qn + 1) + 2 * bkv * lo;
             if (rn < N) mB = max(mB, bq * qn + 2 * bkv * hi);
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
           const uint64_t ws = rj[5 * kTile];
           const Footprint fp{(int64_t)(uint32_t)ws, (int64_t)(ws >> 32), (int64_t)(uint32_t)rj[6 * kTile]};
           float fv[kNumFlts];
-          emit_pair(fz.out, p, d, fp, sp, family_pipes(FAM), tdt < 0 ? 0 : tdt, fv);
+          emit_pair<FAM == SP_ATTENTION>(fz.out, p, d, fp, sp, family_pipes(FAM), tdt < 0 ? 0 : tdt, fv);
           side_s = 0;
           side_t = fv[F_TTHEORY];
 #pragma unroll

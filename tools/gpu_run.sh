@@ -1,3 +1,3 @@
-mkdir -p gpurun_out/r02z
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:predict_tcgen05_fused -s 3 -c 1 -o gpurun_out/r02z/fused python bench.py --workload cfg3 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/r02z/ncu.log 2>&1
-ls gpurun_out/r02z
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > /tmp/pt.txt 2>&1; tail -n 2 /tmp/pt.txt
+for v in default default; do for w in cfg3 cfg2; do timeout 300 python bench.py --workload $w --steps 10 --no-cpu-baseline --e2e-steps 1 > /tmp/b.json 2>/dev/null; python -c "
+import json; d=json.loads(open('/tmp/b.json').read().strip().splitlines()[-1]); print('$v $w', d['ms_per_step'], {k:round(v['avg_ms'],4) for k,v in d['kernels'].items()})"; done; done
