@@ -18,13 +18,25 @@ __device__ __forceinline__ int bytes_per_elem(int dtype) {
 // Unsigned 32-bit division by a runtime-invariant divisor d >= 1 via a
 // multiply-high (round-up method): q = (umulhi(n, m) + n) >> s, computed in
 // 64 bits so it is exact for every n < 2^32.
+// Magic multiplier of d (not a power of two), s = ceil(log2 d):
+// m = floor(2^(32+s) / d) - 2^32 + 1.  The quotient comes from an fp64 division
+// (within one of the exact value) corrected by a 64-bit multiply check: a few
+// instructions instead of the ~100 of the 64-bit integer division subroutine.
+__device__ __forceinline__ uint32_t fastdiv_magic(uint32_t d, uint32_t s) {
+  if (s >= 32) return (uint32_t)((((1ull << s) - d) << 32) / d + 1);  // d > 2^31: integer path
+  const uint64_t num = 1ull << (32 + s);
+  uint64_t q = (uint64_t)__ddiv_rz((double)num, (double)d);
+  if (q * d > num) --q;                // q < 2^33, d < 2^32: no overflow
+  else if ((q + 1) * d <= num) ++q;
+  return (uint32_t)(q - (1ull << 32) + 1);
+}
+
 struct FastDiv {
   uint32_t d, m, s;
   __device__ __forceinline__ void init(uint32_t div) {
     d = div;
-    s = 0;
-    while ((1ull << s) < div) ++s;
-    m = (uint32_t)((((1ull << s) - div) << 32) / div + 1);
+    s = div <= 1 ? 0 : 32 - __clz(div - 1);
+    m = (div & (div - 1)) ? fastdiv_magic(div, s) : 1u;
   }
   __device__ __forceinline__ uint32_t div(uint32_t n) const {
     uint64_t t = (uint64_t)__umulhi(n, m) + n;

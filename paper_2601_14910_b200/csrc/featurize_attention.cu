@@ -67,7 +67,7 @@ __device__ __forceinline__ FastDiv make_fd(uint32_t d) {
   FastDiv f;
   f.d = d;
   f.s = d <= 1 ? 0 : 32 - __clz(d - 1);
-  f.m = (d & (d - 1)) ? (uint32_t)((((1ull << f.s) - d) << 32) / d + 1) : 1u;
+  f.m = (d & (d - 1)) ? fastdiv_magic(d, f.s) : 1u;
   return f;
 }
 
@@ -788,19 +788,30 @@ __global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults re
                                       : (uint64_t)nqb * dv.chunk.div((uint32_t)kv + (uint32_t)chunk - 1u));
       sparse = sparse && part * (uint64_t)nkv <= (uint64_t)min_n;
       if (!sparse) continue;
-      for (uint32_t i = 0; i < nqb; ++i) {  // <= min_n tasks in all
-        const uint32_t need = kv_need(i, bq, rows, (uint32_t)q, (uint32_t)kv, causal, dv.g);
+      // units of one q-block of kv extent `need`: unsplit, one task of ceil(need/BKV);
+      // split, n - 1 full chunks of ceil(chunk/BKV) and a last one (closed form)
+      auto units = [&](uint32_t need, uint64_t &su, uint32_t &mu) {
         if (chunk == 0) {
-          const uint32_t u = dv.bkv.div(need + (uint32_t)bkv - 1u);
-          U += u;
-          um = max(um, u);
+          su = mu = dv.bkv.div(need + (uint32_t)bkv - 1u);
         } else {
-          for (uint32_t c0 = 0; c0 < need; c0 += (uint32_t)chunk) {
-            const uint32_t u = dv.bkv.div(min((uint32_t)chunk, need - c0) + (uint32_t)bkv - 1u);
-            U += u;
-            um = max(um, u);
-            if (need - c0 <= (uint32_t)chunk) break;
-          }
+          const uint32_t n = dv.chunk.div(need + (uint32_t)chunk - 1u);
+          const uint32_t ul = dv.bkv.div(need - (n - 1u) * (uint32_t)chunk + (uint32_t)bkv - 1u);
+          const uint32_t uf = n > 1 ? dv.bkv.div((uint32_t)chunk + (uint32_t)bkv - 1u) : 0u;
+          su = (uint64_t)(n - 1u) * uf + ul;
+          mu = max(uf, ul);
+        }
+      };
+      uint64_t su;
+      uint32_t mu;
+      if (!causal) {  // every q-block has kv_need = kvlen
+        units((uint32_t)kv, su, mu);
+        U += (uint64_t)nqb * su;
+        um = max(um, mu);
+      } else {
+        for (uint32_t i = 0; i < nqb; ++i) {  // <= min_n tasks in all
+          units(kv_need(i, bq, rows, (uint32_t)q, (uint32_t)kv, true, dv.g), su, mu);
+          U += su;
+          um = max(um, mu);
         }
       }
     }
