@@ -160,6 +160,10 @@ __device__ long long g_pred_wtrace[16][64][16];  // every epilogue warp (lane 0)
 #define EPI_WAIT(b, ph) tc::mbar_wait_sleep(b, ph)
 #endif
 
+#ifndef SP_ISSUER_BACKOFF
+#define SP_ISSUER_BACKOFF 0
+#endif
+constexpr int kIssuerBackoff = SP_ISSUER_BACKOFF;  // ns of sleep per polling round of the MMA issuer
 #ifndef SP_STAGGER
 #define SP_STAGGER 0
 #endif
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       int layer[2] = {0, 0};
       uint32_t pa[2] = {0, 0}, pf[2] = {0, 0};
       while (js[0] < n_local || js[1] < n_local) {
+        if (kIssuerBackoff > 0) __nanosleep(kIssuerBackoff);  // off the epilogue warps' issue slots
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int64_t j = js[s];
@@ -726,6 +731,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       int layer[2] = {0, 0};
       uint32_t pa[2] = {0, 0}, pf[2] = {0, 0};
       while (js[0] < n_local || js[1] < n_local) {
+        if (kIssuerBackoff > 0) __nanosleep(kIssuerBackoff);  // off the epilogue warps' issue slots
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int64_t j = js[s];
