@@ -441,7 +441,7 @@ sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cfg, const sp
  *   slice_weights / n_slices: the configs are cut into slices pipelined over
  *                 three streams (H2D of slice i+1 and D2H of slice i-1 overlap
  *                 the kernels of slice i).  NULL weights: n_slices equal
- *                 slices (0: the default, 4; attention also defaults to the
+ *                 slices (0: the default, 8; attention defaults to the
  *                 weights (1, 3, 3, 1)); otherwise n_slices relative weights.
  *                 A wide spec axis (>= 64 specs and >= 4 slices per spec)
  *                 is sliced by spec instead (configs uploaded once).

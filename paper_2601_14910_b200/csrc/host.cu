@@ -7,7 +7,7 @@
 //
 //  * Config slices (the default): slice weights, e.g. (1, 3, 3, 1) for
 //    attention, whose kernels outlast the copies (a short first copy-in and
-//    last copy-out), and 4 equal slices for the copy-bound uniform families.
+//    last copy-out), and 8 equal slices for the copy-bound uniform families.
 //    Each slice copies only its own range of the ragged data (attention
 //    (qlen, kvlen) pairs, MoE histograms), planned from the host offsets at
 //    the slice boundaries.  The plan is exact when the ragged data is laid out
@@ -196,7 +196,8 @@ sp_status run(sp_ctx *ctx, const sp_config_batch *h, const sp_specs *specs, int3
       }
       if (b.back() != C) b.push_back(C);
     } else {
-      const int64_t k = std::max<int64_t>(1, std::min<int64_t>(n_slices > 0 ? n_slices : 4, C));
+      // default 8 equal slices (copy-bound uniform families: measured 3.13e9 vs 2.99e9 pairs/s with 4 on cfg3)
+      const int64_t k = std::max<int64_t>(1, std::min<int64_t>(n_slices > 0 ? n_slices : 8, C));
       for (int64_t i = 1; i <= k; ++i) b.push_back(C * i / k);
     }
     const int64_t ns = (int64_t)b.size() - 1;
