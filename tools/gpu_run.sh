@@ -1,2 +1,4 @@
-timeout 600 python tools/e2e_chunks.py --workload cfg2 --chunks 1,3,3,1 4 6 1,2,3,3,2,1 1,4,4,1 1,2,2,2,2,1 8 1,3,3,3,1
-timeout 600 python tools/e2e_chunks.py --workload cfg3 --chunks 4 8 2 1,3,3,1
+export SYNPERF_LIB=variants/lib_pf.so
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_range.py -q -x -k "attention or range" > /tmp/pt.txt 2>&1; tail -n 2 /tmp/pt.txt
+unset SYNPERF_LIB
+bash tools/gpu_ab.sh gpurun_out/r02aj cfg2 cur pf cur pf
