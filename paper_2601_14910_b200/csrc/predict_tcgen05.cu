@@ -83,27 +83,12 @@ constexpr uint32_t kOffX = kWBytes;
 constexpr uint32_t kOffRaw = kOffX + kNX * kXBytes;
 constexpr uint32_t kOffVec = kOffRaw + kNR * kRawBytes;
 constexpr uint32_t kOffZx = kOffVec + kVecBytes;  // [2][128] fp32 partial logits
-// Default: H2 goes to shared memory and L3 runs as an SS MMA (2.7% faster than
-// reading it from TMEM: the kernel is bound by TMEM reads).
-// -DSP_L3_TS restores the TS form; -DSP_L2H_SS (half of H1 in shared memory)
-// measured 26% slower (shared-memory bound).
-#if !defined(SP_L3_TS) && !defined(SP_L2H_SS) && !defined(SP_L3_SS)
-#define SP_L3_SS 1
-#endif
-#if defined(SP_L3_SS) && defined(SP_L2H_SS)
-#error "SP_L3_SS and SP_L2H_SS need the same shared memory"
-#endif
-#if defined(SP_L3_SS) || defined(SP_L2H_SS)
-#define SP_ACT_SMEM 1
-#endif
-#ifdef SP_ACT_SMEM
-// H2 (SP_L3_SS) or H1 K 0..127 (SP_L2H_SS) per TMEM slot in shared memory (L3 as an SS MMA): [128 rows][128 K] 16-bit, K-major
+// H2 per TMEM slot in shared memory (layer 3 as an SS MMA): [128 rows][128 K]
+// 16-bit, K-major.  Measured 2.7% faster than reading it from TMEM (TS); half
+// of H1 in shared memory measured 26% slower (shared-memory bound).
 constexpr uint32_t kH2Bytes = kTile * 128 * 2;  // 32 KB
 constexpr uint32_t kOffH2 = kOffZx + 2 * kTile * 4;
 constexpr uint32_t kOffBar = kOffH2 + 2 * kH2Bytes;
-#else
-constexpr uint32_t kOffBar = kOffZx + 2 * kTile * 4;
-#endif
 // barriers: x_full[kNX] x_empty[kNX] d_full[2] a_ready[2] slot_free[2], then the TMEM base
 constexpr int kBarXFull = 0, kBarXEmpty = kNX, kBarDFull = 2 * kNX, kBarAReady = 2 * kNX + 2,
               kBarSlotFree = 2 * kNX + 4, kBarRawFull = 2 * kNX + 6, kNumBars = 2 * kNX + 6 + kNR;
@@ -154,20 +139,8 @@ __device__ long long g_pred_wtrace[16][64][16];  // every epilogue warp (lane 0)
 #define PTRACE(role, it, idx)
 #endif
 
-#ifdef SP_EPI_SPIN
-#define EPI_WAIT(b, ph) tc::mbar_wait(b, ph)
-#else
 #define EPI_WAIT(b, ph) tc::mbar_wait_sleep(b, ph)
-#endif
 
-#ifndef SP_ISSUER_BACKOFF
-#define SP_ISSUER_BACKOFF 0
-#endif
-constexpr int kIssuerBackoff = SP_ISSUER_BACKOFF;  // ns of sleep per polling round of the MMA issuer
-#ifndef SP_STAGGER
-#define SP_STAGGER 0
-#endif
-constexpr bool kStagger = SP_STAGGER;
 #ifdef SP_EXP_NOMMA
 constexpr bool kNoMma = true;
 #else
@@ -234,7 +207,6 @@ __device__ __forceinline__ void epi_hidden_tmem(uint32_t tmem_row, uint32_t src,
   }
 }
 
-#ifdef SP_ACT_SMEM
 // Hidden epilogue to shared memory: fp32 TMEM columns [src, src + 64) of this
 // lane's row -> ReLU -> 16-bit -> K columns [k0, k0 + 64) of the row in the
 // UMMA K-major layout (K = 128): eight 16-byte core-matrix rows.
@@ -252,7 +224,6 @@ __device__ __forceinline__ void epi_hidden_smem64(uint32_t tmem_row, uint32_t sr
   for (int c = 0; c < 8; ++c)
     tc::st_shared_v4(hbuf + op_off(row, k0 + 8 * c, 128), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
 }
-#endif
 
 // Write a bias vector (broadcast over rows) into TMEM columns [c, c + NC).
 template <int NC>
@@ -372,16 +343,12 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       int layer[2] = {0, 0};
       uint32_t pa[2] = {0, 0}, pf[2] = {0, 0};
       while (js[0] < n_local || js[1] < n_local) {
-        if (kIssuerBackoff > 0) __nanosleep(kIssuerBackoff);  // off the epilogue warps' issue slots
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int64_t j = js[s];
           if (j >= n_local) continue;
           const uint32_t B = tmem + (uint32_t)(s * 256);
           if (layer[s] == 0) {
-            // stagger: no layer 1 while the other slot's layer-1 epilogue runs (both epilogues at
-            // once leave the tensor pipe idle and lock the slots in phase)
-            if (kStagger && js[s ^ 1] < n_local && layer[s ^ 1] == 1) continue;
             const int xi = (int)(j % kNX);
             if (!tc::mbar_test(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u)) continue;
             if (j >= 2 && !tc::mbar_test(bar(kBarSlotFree + s), pf[s])) continue;
@@ -403,28 +370,15 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
 #pragma unroll
               for (int ks = 0; ks < 16; ++ks) {
                 const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
-#ifdef SP_L2H_SS
-                if (ks < 8) {  // K 0..127 from shared memory
-                  if (!kNoMma)
-                    tc::mma_f16kind(B + 64, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
-                                    tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
-                  continue;
-                }
-#endif
                 if (!kNoMma)
                   tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
-            } else {  // H2 from TMEM (or shared memory with SP_L3_SS); D3 preset to b3'
+            } else {  // H2 from shared memory; D3 preset to b3'
 #pragma unroll
               for (int ks = 0; ks < 8; ++ks) {
-#ifdef SP_L3_SS
                 if (!kNoMma)
                   tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
                                   tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64, 1);
-#else
-                if (!kNoMma) tc::mma_f16kind_ts(B + 192, B + 8 * ks, tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64,
-                                   1);
-#endif
               }
             }
           }
@@ -522,24 +476,10 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       EPT(2);
       pd ^= 1;
       tc::fence_after();
-#ifndef SP_EXP_NOEPI
-#ifdef SP_L2H_SS
-      if (h == 0) {
-        epi_hidden_smem64<BF16>(tmem_row, 0, sbase + kOffH2 + s * kH2Bytes, row, 0);
-        epi_hidden_smem64<BF16>(tmem_row, 64, sbase + kOffH2 + s * kH2Bytes, row, 64);
-      }
-#else
       if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
-#endif
       else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
-#endif
-#ifndef SP_EXP_NOBIAS
       bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
-#endif
       tc::tmem_wait_st();
-#ifdef SP_L2H_SS
-      tc::fence_proxy_async();  // generic-proxy H1 writes -> visible to the tensor core
-#endif
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
@@ -549,20 +489,10 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       EPT(4);
       pd ^= 1;
       tc::fence_after();
-#ifndef SP_EXP_NOEPI
-#ifdef SP_L3_SS
       epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
-#else
-      epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
-#endif
-#endif
-#ifndef SP_EXP_NOBIAS
       bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
-#endif
       tc::tmem_wait_st();
-#ifdef SP_L3_SS
       tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
-#endif
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(5);
@@ -731,16 +661,12 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       int layer[2] = {0, 0};
       uint32_t pa[2] = {0, 0}, pf[2] = {0, 0};
       while (js[0] < n_local || js[1] < n_local) {
-        if (kIssuerBackoff > 0) __nanosleep(kIssuerBackoff);  // off the epilogue warps' issue slots
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int64_t j = js[s];
           if (j >= n_local) continue;
           const uint32_t B = tmem + (uint32_t)(s * 256);
           if (layer[s] == 0) {
-            // stagger: no layer 1 while the other slot's layer-1 epilogue runs (both epilogues at
-            // once leave the tensor pipe idle and lock the slots in phase)
-            if (kStagger && js[s ^ 1] < n_local && layer[s ^ 1] == 1) continue;
             const int xi = (int)(j % kNX);
             if (!tc::mbar_test(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u)) continue;
             if (j >= 2 && !tc::mbar_test(bar(kBarSlotFree + s), pf[s])) continue;
@@ -762,28 +688,15 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
 #pragma unroll
               for (int ks = 0; ks < 16; ++ks) {
                 const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
-#ifdef SP_L2H_SS
-                if (ks < 8) {  // K 0..127 from shared memory
-                  if (!kNoMma)
-                    tc::mma_f16kind(B + 64, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
-                                    tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
-                  continue;
-                }
-#endif
                 if (!kNoMma)
                   tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
-            } else {  // H2 from TMEM (or shared memory with SP_L3_SS); D3 preset to b3'
+            } else {  // H2 from shared memory; D3 preset to b3'
 #pragma unroll
               for (int ks = 0; ks < 8; ++ks) {
-#ifdef SP_L3_SS
                 if (!kNoMma)
                   tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
                                   tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64, 1);
-#else
-                if (!kNoMma) tc::mma_f16kind_ts(B + 192, B + 8 * ks, tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64,
-                                   1);
-#endif
               }
             }
           }
@@ -960,24 +873,10 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       EPT(2);
       pd ^= 1;
       tc::fence_after();
-#ifndef SP_EXP_NOEPI
-#ifdef SP_L2H_SS
-      if (h == 0) {
-        epi_hidden_smem64<BF16>(tmem_row, 0, sbase + kOffH2 + s * kH2Bytes, row, 0);
-        epi_hidden_smem64<BF16>(tmem_row, 64, sbase + kOffH2 + s * kH2Bytes, row, 64);
-      }
-#else
       if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
-#endif
       else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
-#endif
-#ifndef SP_EXP_NOBIAS
       bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
-#endif
       tc::tmem_wait_st();
-#ifdef SP_L2H_SS
-      tc::fence_proxy_async();  // generic-proxy H1 writes -> visible to the tensor core
-#endif
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
@@ -987,20 +886,10 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       EPT(4);
       pd ^= 1;
       tc::fence_after();
-#ifndef SP_EXP_NOEPI
-#ifdef SP_L3_SS
       epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
-#else
-      epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
-#endif
-#endif
-#ifndef SP_EXP_NOBIAS
       bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
-#endif
       tc::tmem_wait_st();
-#ifdef SP_L3_SS
       tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
-#endif
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(5);
