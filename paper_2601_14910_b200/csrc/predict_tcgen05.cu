@@ -7,8 +7,9 @@
 //   D3[128x64]  = H2[128x128] . W3'^T  (W3' = W3 diag(s2))
 // issued by one thread as tcgen05.mma (M = 128, 16-bit in, fp32 accumulate).
 // The folded BatchNorm shifts become biases (b2' = b2 + W2 t1, ...) that the
-// epilogue presets into the D2/D3 accumulators (tcgen05.st) before the MMAs
-// accumulate onto them; the last BN goes into the output layer (w4' = w4 s3,
+// first MMA of each layer writes into the D2/D3 accumulators (constant bias
+// tiles, accumulate = 0) before the weight MMAs accumulate onto them; the
+// last BN goes into the output layer (w4' = w4 s3,
 // b4' = b4 + w4.t3).  The activations H1, H2 never touch shared memory: each
 // epilogue reads D from TMEM, applies ReLU + 16-bit packing (one
 // cvt.rn.satfinite.relu.f16x2 per two values) and writes the packed rows back into TMEM,
@@ -66,7 +67,19 @@ constexpr int kNR = 2;   // raw feature staging depth (tiles in flight per produ
 constexpr uint32_t kW1Bytes = 256 * kK1 * 2;   //  8 KB
 constexpr uint32_t kW2Bytes = 128 * 256 * 2;   // 64 KB
 constexpr uint32_t kW3Bytes = 64 * 128 * 2;    // 16 KB
-constexpr uint32_t kWBytes = kW1Bytes + kW2Bytes + kW3Bytes;
+// Bias tiles: b2', b3' enter D2, D3 through the first MMA of their layer
+// (accumulate = 0): D[m][n] = sum_k ONE[m][k] BB[n][k] = hi(b'[n]) + lo(b'[n]),
+// with ONE[m] = (1, 1, 0, ..., 0) and BB[n] = (hi, lo, 0, ...) as 16-bit pairs
+// (hi + lo carries the fp32 bias to ~22 bits, summed in the fp32 accumulator).
+// This replaces the epilogue's TMEM presets (96 KB of tcgen05.st per tile, on the
+// layer-to-layer critical path) with two K = 16 MMAs.  The tiles alias in shared
+// memory: ONE is one 8-row group read with SBO = 0 (every row group the same)
+// and its second K core matrix is zero; BB's two K core matrices alias (LBO = 0),
+// the second multiplied by ONE's zeros.
+constexpr uint32_t kOnesBytes = 2 * 128;      // [8 rows][16 K]
+constexpr uint32_t kB2bBytes = 128 * 8 * 2;   // [128 N][8 K]
+constexpr uint32_t kB3bBytes = 64 * 8 * 2;    // [64 N][8 K]
+constexpr uint32_t kWBytes = kW1Bytes + kW2Bytes + kW3Bytes + kOnesBytes + kB2bBytes + kB3bBytes;
 // X stage: the normalised inputs as two 16-bit tiles, hi = fp16(x) and lo =
 // fp16(x - hi), each [128 x 16] (4 KB): layer 1 runs D1 = X_hi.W1^T + X_lo.W1^T
 // (two K = 16 MMAs on the same W1), so x enters at ~22 bits instead of 11.
@@ -79,6 +92,7 @@ constexpr uint32_t kRawBytes = 16 * kTile * 8; // 16 KB per raw stage: [feature]
 constexpr int kVB2 = 0, kVB3 = 128, kVW4 = 192, kVNA = 256, kVNC = 272, kVecFloats = 288;
 constexpr uint32_t kVecBytes = kVecFloats * 4;
 constexpr uint32_t kOffW1 = 0, kOffW2 = kW1Bytes, kOffW3 = kW1Bytes + kW2Bytes;
+constexpr uint32_t kOffOnes = kOffW3 + kW3Bytes, kOffB2b = kOffOnes + kOnesBytes, kOffB3b = kOffB2b + kB2bBytes;
 constexpr uint32_t kOffX = kWBytes;
 constexpr uint32_t kOffRaw = kOffX + kNX * kXBytes;
 constexpr uint32_t kOffVec = kOffRaw + kNR * kRawBytes;
@@ -225,24 +239,6 @@ __device__ __forceinline__ void epi_hidden_smem64(uint32_t tmem_row, uint32_t sr
     tc::st_shared_v4(hbuf + op_off(row, k0 + 8 * c, 128), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
 }
 
-// Write a bias vector (broadcast over rows) into TMEM columns [c, c + NC).
-template <int NC>
-__device__ __forceinline__ void bias_to_tmem(uint32_t tmem_row, uint32_t c, const float *bias) {
-#pragma unroll 1
-  for (int c0 = 0; c0 < NC; c0 += 32) {
-    uint32_t v[32];
-#pragma unroll
-    for (int j = 0; j < 32; j += 4) {
-      const float4 b = *reinterpret_cast<const float4 *>(bias + c0 + j);
-      v[j] = __float_as_uint(b.x);
-      v[j + 1] = __float_as_uint(b.y);
-      v[j + 2] = __float_as_uint(b.z);
-      v[j + 3] = __float_as_uint(b.w);
-    }
-    tc::tmem_st32(tmem_row + c + c0, v);
-  }
-}
-
 // ---- producer: features of CTA tile j -> raw stage j % kNR (cp.async; each
 // thread copies, and later reads, only its own row: no barrier needed).
 // Raw stage layout: feature f of row r at byte f * kTile * 8 + r * 8 (int64 slots)
@@ -366,14 +362,20 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
             if (!tc::mbar_test(bar(kBarAReady + s), pa[s])) continue;
             pa[s] ^= 1;
             tc::fence_after();
-            if (layer[s] == 1) {  // H1 from TMEM; D2 preset to b2'
+            if (layer[s] == 1) {  // D2 = b2' (bias tiles), += H1 (TMEM) . W2'^T
+              if (!kNoMma)
+                tc::mma_f16kind(B + 64, tc::smem_desc(sbase + kOffOnes, 128, 0), tc::smem_desc(sbase + kOffB2b, 0, 128),
+                                i128, 0);
 #pragma unroll
               for (int ks = 0; ks < 16; ++ks) {
                 const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
                 if (!kNoMma)
                   tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
-            } else {  // H2 from shared memory; D3 preset to b3'
+            } else {  // D3 = b3' (bias tiles), += H2 (shared memory) . W3'^T
+              if (!kNoMma)
+                tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffOnes, 128, 0), tc::smem_desc(sbase + kOffB3b, 0, 128),
+                                i64, 0);
 #pragma unroll
               for (int ks = 0; ks < 8; ++ks) {
                 if (!kNoMma)
@@ -470,28 +472,23 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
         t_theory = __ldg(P.in.flts + (int64_t)F_TTHEORY * P.in.ld + p);
         stbyte = __ldg(P.in.status + p);
       }
-      // layer 1: D1 half h -> H1 (half 0 -> [0, 64), half 1 -> [192, 256));
-      // preset D2 columns 64h..64h+63 (TMEM [64+64h, 128+64h), read by this half) = b2'[64h..]
+      // layer 1: D1 half h -> H1 (half 0 -> [0, 64), half 1 -> [192, 256))
       EPI_WAIT(bar_d, pd);
       EPT(2);
       pd ^= 1;
       tc::fence_after();
       if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
       else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
-      bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
       tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
-      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 packed in [32h, 32h+32) (H1 is retired);
-      // preset D3 columns 32h.. [192+32h, 224+32h) = b3'[32h..]
+      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 (shared memory, K 64h..64h+63)
       EPI_WAIT(bar_d, pd);
       EPT(4);
       pd ^= 1;
       tc::fence_after();
       epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
-      bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
-      tc::tmem_wait_st();
       tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
       tc::fence_before();
       tc::mbar_arrive(bar_a);
@@ -684,14 +681,20 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
             if (!tc::mbar_test(bar(kBarAReady + s), pa[s])) continue;
             pa[s] ^= 1;
             tc::fence_after();
-            if (layer[s] == 1) {  // H1 from TMEM; D2 preset to b2'
+            if (layer[s] == 1) {  // D2 = b2' (bias tiles), += H1 (TMEM) . W2'^T
+              if (!kNoMma)
+                tc::mma_f16kind(B + 64, tc::smem_desc(sbase + kOffOnes, 128, 0), tc::smem_desc(sbase + kOffB2b, 0, 128),
+                                i128, 0);
 #pragma unroll
               for (int ks = 0; ks < 16; ++ks) {
                 const uint32_t a = B + (ks < 8 ? 8 * ks : 192 + 8 * (ks - 8));
                 if (!kNoMma)
                   tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
-            } else {  // H2 from shared memory; D3 preset to b3'
+            } else {  // D3 = b3' (bias tiles), += H2 (shared memory) . W3'^T
+              if (!kNoMma)
+                tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffOnes, 128, 0), tc::smem_desc(sbase + kOffB3b, 0, 128),
+                                i64, 0);
 #pragma unroll
               for (int ks = 0; ks < 8; ++ks) {
                 if (!kNoMma)
@@ -867,28 +870,23 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
         t_theory = reinterpret_cast<const float *>(smem + kFOffSide)[si * kTile + row];
         stbyte = (smem + kFOffSide + kNS * kTile * 4)[si * kTile + row];
       }
-      // layer 1: D1 half h -> H1 (half 0 -> [0, 64), half 1 -> [192, 256));
-      // preset D2 columns 64h..64h+63 (TMEM [64+64h, 128+64h), read by this half) = b2'[64h..]
+      // layer 1: D1 half h -> H1 (half 0 -> [0, 64), half 1 -> [192, 256))
       EPI_WAIT(bar_d, pd);
       EPT(2);
       pd ^= 1;
       tc::fence_after();
       if (h == 0) epi_hidden_tmem<128, BF16>(tmem_row, 0, 0);
       else epi_hidden_tmem<128, BF16, true>(tmem_row, 128, 192);
-      bias_to_tmem<64>(tmem_row, 64 + 64 * h, vec + kVB2 + 64 * h);
       tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
-      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 packed in [32h, 32h+32) (H1 is retired);
-      // preset D3 columns 32h.. [192+32h, 224+32h) = b3'[32h..]
+      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 (shared memory, K 64h..64h+63)
       EPI_WAIT(bar_d, pd);
       EPT(4);
       pd ^= 1;
       tc::fence_after();
       epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
-      bias_to_tmem<32>(tmem_row, 192 + 32 * h, vec + kVB3 + 32 * h);
-      tc::tmem_wait_st();
       tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
       tc::fence_before();
       tc::mbar_arrive(bar_a);
@@ -987,6 +985,27 @@ int pack_mlp_16bit(const sp_mlp_desc &d, const std::vector<double> *s, const std
     for (int k = 0; k < 128; ++k) acc += (double)d.w3[n * 128 + k] * t[1][k];
     vecs[kVB3 + n] = (float)acc;
   }
+  // bias tiles (see kOnesBytes): ONE rows (1, 1, 0 ...), second K core matrix 0;
+  // BB[n] = (hi, lo) of the fp32 bias, hi = 16-bit(b), lo = 16-bit(b - hi)
+  for (int r = 0; r < 8; ++r)
+    for (int k = 0; k < 2; ++k) put(kOffOnes, r, k, 8, 1.0);
+  auto put_bias = [&](uint32_t base, int n, float b) {
+    const uint16_t hb = to_bits16((double)b, bf16);
+    double hv;
+    if (bf16) {
+      __nv_bfloat16 h;
+      std::memcpy(&h, &hb, 2);
+      hv = (double)__bfloat162float(h);
+    } else {
+      __half h;
+      std::memcpy(&h, &hb, 2);
+      hv = (double)__half2float(h);
+    }
+    put(base, n, 0, 8, (double)b);
+    put(base, n, 1, 8, (double)b - hv);
+  };
+  for (int n = 0; n < 128; ++n) put_bias(kOffB2b, n, vecs[kVB2 + n]);
+  for (int n = 0; n < 64; ++n) put_bias(kOffB3b, n, vecs[kVB3 + n]);
   double bb = d.b4;
   for (int k = 0; k < 64; ++k) {
     vecs[kVW4 + k] = (float)((double)d.w4[k] * s[2][k]);
