@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--precision", default="fp16")
+    ap.add_argument("--fused", action="store_true", help="also time sp_featurize_predict (the bench step)")
     args = ap.parse_args()
     ctx = sp.Context(0)
     b, sa, (g0, g1), _ = bench.local_workload(args.workload, args.scale)
@@ -47,8 +48,20 @@ def main():
     torch.cuda.synchronize()
     tf = sorted(e[0].elapsed_time(e[1]) for e in ev)
     tp = sorted(e[1].elapsed_time(e[2]) for e in ev)
+    fused = ""
+    if args.fused:
+        for _ in range(3):
+            ctx.featurize_predict(db, sh, m, f, lat, pairs=pr)
+        ef = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.reps)]
+        for e in ef:
+            e[0].record()
+            ctx.featurize_predict(db, sh, m, f, lat, pairs=pr)
+            e[1].record()
+        torch.cuda.synchronize()
+        tz = sorted(e[0].elapsed_time(e[1]) for e in ef)
+        fused = f"  fused {tz[len(tz)//2]:.3f} ms (min {tz[0]:.3f})"
     print(f"{os.environ.get('SYNPERF_LIB', 'default')}: featurize {tf[len(tf)//2]:.3f} ms (min {tf[0]:.3f})  "
-          f"predict {tp[len(tp)//2]:.3f} ms (min {tp[0]:.3f})  pairs {n}")
+          f"predict {tp[len(tp)//2]:.3f} ms (min {tp[0]:.3f}){fused}  pairs {n}")
 
 
 if __name__ == "__main__":
