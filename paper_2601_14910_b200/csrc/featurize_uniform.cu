@@ -102,8 +102,10 @@ struct MoeHist {
 // holding config c0 + j: the warp takes its configs four at a time, its lanes
 // reading 32 consecutive counts per config (coalesced; the first 128 counts of
 // all four configs are loaded before any is reduced, so four histograms are in
-// flight instead of one), and reduces with shuffles.  Lane j receives config
-// j's result.  All 32 lanes must call it.
+// flight instead of one), and reduces with REDUX (32-bit partials; see take()).
+// A saturated or negative partial marks the histogram invalid (`neg`: moe_cfg
+// reports SP_PAIR_E_HIST, as for a sum that differs from M topk).  Lane j
+// receives config j's result.  All 32 lanes must call it.
 __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c, bool valid) {
   const int lane = threadIdx.x & 31;
   int64_t off = -1;
@@ -144,27 +146,29 @@ __device__ __forceinline__ MoeHist moe_hist_warp(const ConfigView &v, int64_t c,
     for (int q = 0; q < 4; ++q) {
       if (jj[q] < 0) break;  // warp-uniform
       const uint32_t bmj = (uint32_t)__shfl_sync(0xffffffffu, bm, jj[q]);
-      // ceil(t_e / BM) by multiply-high
+      // ceil(t_e / BM) = (max(t_e, 1) - 1) / BM + [t_e > 0] by multiply-high (operand < 2^31)
       const FastDiv fbm{bmj, __shfl_sync(0xffffffffu, my_fbm.m, jj[q]), __shfl_sync(0xffffffffu, my_fbm.s, jj[q])};
-      int64_t sum = 0, mb = 0;
-      int neg = 0;
+      // 32-bit lane partials: `ors` collects the sign bits (a negative count), `sum`
+      // saturates at 2^31 (a valid histogram sums to M topk < 2^31, so a saturated
+      // partial is an invalid one either way), `mb` is exact whenever the
+      // histogram is valid (sum_e ceil(t_e/BM) <= sum_e t_e < 2^31)
+      uint32_t ors = 0, sum = 0, mb = 0;
       auto take = [&](int32_t te) {
-        neg |= te < 0;
-        sum += te;
-        mb += te > 0 ? fbm.div((uint32_t)te + bmj - 1u) : 0u;  // te, BM < 2^31: the sum fits 32 bits
+        ors |= (uint32_t)te;
+        sum = min(sum + (uint32_t)te, 1u << 31);  // sum <= 2^31, te < 2^31 when ors keeps bit 31 clear
+        mb += fbm.div31((uint32_t)max(te, 1) - 1u) + (te > 0 ? 1u : 0u);
       };
 #pragma unroll
-      for (int r = 0; r < 4; ++r) take(t[q][r]);
+      for (int r = 0; r < 4; ++r)
+        if (32 * r < Ej[q]) take(t[q][r]);  // warp-uniform: rows past E hold no counts
       for (int32_t e = lane + 128; e < Ej[q]; e += 32) take(__ldg(v.ragged + oj[q] + e));  // E > 128
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        mb += __shfl_xor_sync(0xffffffffu, mb, o);
-      }
-      neg = __any_sync(0xffffffffu, neg);
+      // warp totals by REDUX: the sum as two 16-bit halves (each total < 2^21), exact
+      const int neg = __any_sync(0xffffffffu, (ors >> 31) != 0 || sum >= (1u << 31));
+      const uint32_t s_hi = __reduce_add_sync(0xffffffffu, sum >> 16), s_lo = __reduce_add_sync(0xffffffffu, sum & 0xffffu);
+      const uint32_t mbt = __reduce_add_sync(0xffffffffu, mb);
       if (lane == jj[q]) {
-        mine.sum = sum;
-        mine.mblocks = mb;
+        mine.sum = ((int64_t)s_hi << 16) + (int64_t)s_lo;
+        mine.mblocks = mbt;
         mine.neg = neg;
       }
     }

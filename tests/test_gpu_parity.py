@@ -225,6 +225,48 @@ def test_uniform_edge_cases(sp, ctx, orc):
     assert_feature_parity(g, o, "moe edges")
 
 
+def test_moe_histogram_edge_cases(sp, ctx, orc):
+    """Fused-MoE histograms the warp pass reduces in 32-bit partials (R16, status 4
+    = SP_PAIR_E_HIST): a negative count, counts whose exact sum is 2^32 + M topk
+    (a wrapping 32-bit sum would accept it), one expert holding M topk ~ 1.9e9
+    tokens, E > 128 (the tail loop), E = 1, and E = 33 (a partial second row);
+    every record against the oracle, bit-exact."""
+    big = 2 ** 31 - 1
+    hists = [
+        [5, -1, 4],                   # negative count, sum = M topk
+        [big, big, 10],               # exact sum 2^32 + 8: invalid
+        [1879048192],                 # M topk = 2^28 * 7, one expert
+        list(range(1, 201)),          # E = 200: sum 20100
+        list(range(1, 201)),          # E = 200, wrong sum
+        [6],                          # E = 1
+        [1] * 32 + [7],               # E = 33
+        [0, 0, 8],                    # zero-token experts
+    ]
+    mt = [8, 8, 1879048192, 20100, 20100, 6, 39, 8]
+    topk = [2, 2, 7, 4, 4, 1, 3, 2]
+    n = len(hists)
+    M = [m // k for m, k in zip(mt, topk)]
+    M[4] += 1  # config 4: the histogram sums to 20100, M topk = 20104
+    off = np.cumsum([0] + [len(h) for h in hists[:-1]]).tolist()
+    cols = dict(M=M, E=[len(h) for h in hists], TOPK=topk, H=[1024] * n, N=[512] * n,
+                BM=[16, 16, 64, 32, 32, 16, 16, 16], BN=[64] * n, BK=[32] * n, GROUP_M=[1] * n,
+                STAGES=[3] * n, WARPS=[4] * n, REGS=[128] * n, SMEM=[0] * n, DTYPE=[0] * n)
+    b = gen.make_batch(gen.FUSED_MOE, cols, sum(hists, []), off)
+    sa = np.concatenate([specs.paper_gpu_specs(), odd_specs()])
+    _, g = gpu_features(sp, ctx, b, sa)
+    o = orc.featurize(b, sa)
+    st = o.status.reshape(len(sa), n)[0]
+    assert st.tolist() == [4, 4, 0, 0, 4, 0, 0, 0], st
+    assert_feature_parity(g, o, "moe histograms")
+    # the fused pass (pre-pass + producers) reads the same histogram results
+    f = sp.Features.empty(b.family, len(sa) * n, "cuda:0")
+    lat = torch.empty(f.n_pairs, dtype=torch.float32, device="cuda:0")
+    ctx.featurize_predict(sp.DeviceBatch.from_host(b, "cuda:0"), ctx.load_gpu_specs(sa),
+                          ctx.load_model(models.random_mlp(b.family, 8), "fp16"), f, lat)
+    torch.cuda.synchronize()
+    assert_feature_parity(sp.features_to_host(f), o, "moe histograms (fused)")
+
+
 def test_full_size_sampled_cfg2(sp, ctx, orc):
     """BASELINE config 2 at full size (1e6 configs x 11 specs), in the launch
     configuration bench.py times (sp_featurize, then the fp16 tcgen05 sp_predict
