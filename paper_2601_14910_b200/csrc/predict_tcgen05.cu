@@ -59,10 +59,10 @@ constexpr int kProdWarps = 4;
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 // MMA issue (bare predictor): one thread per TMEM slot, each in its own warp
 // (kIssuers = 2), or (SP_ONE_ISSUER) one thread polling both slots.  With a thread per slot each
-// issuer sleeps in try_wait on its own slot's next barrier, and the two issue
+// issuer waits in try_wait on its own slot's next barrier, and the two issue
 // streams interleave in the tensor pipe's queue: a slot's short layer (L1, L3)
 // no longer waits behind the other slot's whole layer 2 (17 MMAs).  Measured
-// 1.02 -> 0.99 ms on cfg3, ~equal on cfg2.
+// 1.02 -> 0.97 ms on cfg3, 1.07 -> 1.05 ms on cfg2.
 #ifdef SP_ONE_ISSUER
 constexpr int kIssuers = 1;
 #else
@@ -306,6 +306,13 @@ __device__ __forceinline__ bool produce_issue(const Params &P, int64_t j, int64_
 // MMA issuer of TMEM slot s (CTA tiles j = s, s+2, ...), one thread: layer 0
 // needs the X tile (x_full) and the slot's previous tile fully read
 // (slot_free); layers 1, 2 need the epilogue's activations (a_ready).
+// The per-slot issuers wait with try_wait without a suspend-time hint: measured
+// 2% faster than the suspending wait (cfg3 0.990 -> 0.972 ms, cfg2 1.07 -> 1.05).
+#ifdef SP_ISSUER_SLEEP
+#define ISSUER_WAIT(b, ph) tc::mbar_wait_sleep(b, ph)
+#else
+#define ISSUER_WAIT(b, ph) tc::mbar_wait(b, ph)
+#endif
 template <bool BF16>
 __device__ __forceinline__ void issue_slot(uint32_t sbase, uint32_t tmem, uint32_t bar0, int64_t n_local, int s) {
   auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
@@ -315,9 +322,9 @@ __device__ __forceinline__ void issue_slot(uint32_t sbase, uint32_t tmem, uint32
   uint32_t pa = 0, pf = 0;
   for (int64_t j = s; j < n_local; j += 2) {
     const int xi = (int)(j % kNX);
-    tc::mbar_wait_sleep(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u);
+    ISSUER_WAIT(bar(kBarXFull + xi), (uint32_t)(j / kNX) & 1u);
     if (j >= 2) {
-      tc::mbar_wait_sleep(bar(kBarSlotFree + s), pf);
+      ISSUER_WAIT(bar(kBarSlotFree + s), pf);
       pf ^= 1;
     }
     tc::fence_after();
@@ -331,7 +338,7 @@ __device__ __forceinline__ void issue_slot(uint32_t sbase, uint32_t tmem, uint32
     tc::commit(bar(kBarXEmpty + xi));
     tc::commit(bar(kBarDFull + s));
     // layer 2: D2 = b2' (bias tiles), += H1 (TMEM) . W2'^T
-    tc::mbar_wait_sleep(bar(kBarAReady + s), pa);
+    ISSUER_WAIT(bar(kBarAReady + s), pa);
     pa ^= 1;
     tc::fence_after();
     if (!kNoMma) {
@@ -344,7 +351,7 @@ __device__ __forceinline__ void issue_slot(uint32_t sbase, uint32_t tmem, uint32
     }
     tc::commit(bar(kBarDFull + s));
     // layer 3: D3 = b3' (bias tiles), += H2 (shared memory) . W3'^T
-    tc::mbar_wait_sleep(bar(kBarAReady + s), pa);
+    ISSUER_WAIT(bar(kBarAReady + s), pa);
     pa ^= 1;
     tc::fence_after();
     if (!kNoMma) {
@@ -630,8 +637,13 @@ constexpr int kFGroups = kFProdWarps / 4;  // producer groups, taking tiles j = 
 static_assert(kNX % (kFProdWarps / 4) == 0, "X ring depth must be a multiple of the producer group count");
 constexpr int kFMmaWarp = kEpiWarps + kFProdWarps;
 // The fused kernel keeps the single polling issuer: with a thread per slot it
-// measured 7% slower on cfg3 (1.178 -> 1.263 ms) while the bare predictor gained 3%.
-constexpr int kFThreads = (kFMmaWarp + 1) * 32;
+// measured 7-8% slower on cfg3 (1.15 -> 1.24 ms; either wait flavour) and 2% on
+// cfg2, while the bare predictor gained 2-5%.
+#ifndef SP_FUSED_ISSUERS
+#define SP_FUSED_ISSUERS 1
+#endif
+constexpr int kFIssuers = SP_FUSED_ISSUERS;
+constexpr int kFThreads = (kFMmaWarp + kFIssuers) * 32;
 constexpr int kFNR = 4 / kFGroups;  // raw stages per producer group
 constexpr uint32_t kFRawBytes = kPreFields * kTile * 8;
 static_assert(kFGroups * kFNR * kFRawBytes <= kNR * kRawBytes, "fused raw staging fits the unfused one");
@@ -721,7 +733,9 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
 
   const int64_t G = gridDim.x;
   const int64_t n_local = P.n_tiles > (int64_t)blockIdx.x ? (P.n_tiles - blockIdx.x + G - 1) / G : 0;
-  if (warp == kFMmaWarp) {
+  if (kFIssuers == 2 && warp >= kFMmaWarp) {
+    if (lane == 0) issue_slot<BF16>(sbase, tmem, bar0, n_local, warp - kFMmaWarp);
+  } else if (warp == kFMmaWarp) {
     // ================= MMA issuer (one thread) =================
     // Per TMEM slot s (CTA tiles j = s, s+2, ...): layer 0 needs the X tile
     // (x_full) and the slot's previous tile fully read (slot_free); layers 1, 2
