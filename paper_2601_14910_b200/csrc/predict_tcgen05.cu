@@ -17,13 +17,13 @@
 // weights (B) stream from shared memory.  The final 64 -> 1 layer is 64 FMAs
 // per row.
 //
-// Warp roles (persistent CTA, one per SM, 21 warps):
+// Warp roles (persistent CTA, one per SM, 22 warps):
 //   producers (4 warps): stream the feature columns of the CTA's tiles into
 //     shared memory with cp.async (kNR tiles ahead), normalise them (a10:
 //     log1p + z-score) and write the 16-bit X tile into a kNX-deep ring;
-//   MMA issuer (1 thread): a small scheduler that issues whichever layer of
-//     either TMEM slot is ready (X tile present + slot free, or activations
-//     written back), so the tensor pipe never idles behind one slot;
+//   MMA issuers (one thread per TMEM slot, in two warps; the fused kernel
+//     below has one thread polling both slots and issuing whichever layer is
+//     ready: X tile present + slot free, or activations written back);
 //   epilogue (16 warps = 2 TMEM slots x 2 column halves x 4 lane quadrants).
 // Keeping the feature decode off the epilogue warps takes it off the
 // layer-to-layer critical path.  TMEM columns of slot s (base B = 256 s):
@@ -32,10 +32,13 @@
 //   D2 [B+64, B+192)     (N = 128 in one MMA per K step: a TS MMA reads its
 //                         4 KB A slice from TMEM at ~64 B/clk, so N = 64 would
 //                         halve the tensor rate; N = 128 matches it)
+//                        -> H2 packed in [B, B+64) (half h: [B+32h, B+32h+32))
 //   D3 [B+192, B+256)
-// H2 is written to shared memory (per slot, UMMA K-major) and layer 3 runs as
-// an SS MMA: the kernel is bound by TMEM reads (epilogue loads + TS operand
-// reads), and moving this 32 KB operand off TMEM measured 2.7% faster.
+// Layers 2 and 3 read their A operand from TMEM.  Until round
+// 2, H2 went to shared memory and layer 3 ran as an SS MMA (then 2.7% faster);
+// once the epilogue's bias presets were gone (bias MMAs, below) the TS form
+// measured 9-12% faster: an SS MMA with N = 64 moves 6 KB of operands per
+// 32-cycle step, more than shared memory delivers, and it took 64 KB of it.
 // Each half writes only columns it has itself read (half 1 packs its D1
 // columns back to front), or columns whose readers the MMA barrier already
 // retired, so the halves need no barrier between them.
@@ -71,7 +74,10 @@ constexpr int kIssuers = 2;
 constexpr int kThreads = (kMmaWarp + kIssuers) * 32;
 constexpr int kK1 = 16;  // n_in padded; column 15 is the constant-1 bias column
 constexpr int kNX = 4;   // X ring depth (tiles)
-constexpr int kNR = 2;   // raw feature staging depth (tiles in flight per producer thread)
+#ifndef SP_NR
+#define SP_NR 2
+#endif
+constexpr int kNR = SP_NR;  // raw feature staging depth (tiles in flight per producer thread)
 
 // Shared-memory image, bytes.  Operand layout (K-major, no swizzle):
 //   off(r, k) = (r / 8) * SBO + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2,  SBO = 16 * K
@@ -108,12 +114,7 @@ constexpr uint32_t kOffX = kWBytes;
 constexpr uint32_t kOffRaw = kOffX + kNX * kXBytes;
 constexpr uint32_t kOffVec = kOffRaw + kNR * kRawBytes;
 constexpr uint32_t kOffZx = kOffVec + kVecBytes;  // [2][128] fp32 partial logits
-// H2 per TMEM slot in shared memory (layer 3 as an SS MMA): [128 rows][128 K]
-// 16-bit, K-major.  Measured 2.7% faster than reading it from TMEM (TS); half
-// of H1 in shared memory measured 26% slower (shared-memory bound).
-constexpr uint32_t kH2Bytes = kTile * 128 * 2;  // 32 KB
-constexpr uint32_t kOffH2 = kOffZx + 2 * kTile * 4;
-constexpr uint32_t kOffBar = kOffH2 + 2 * kH2Bytes;
+constexpr uint32_t kOffBar = kOffZx + 2 * kTile * 4;
 // barriers: x_full[kNX] x_empty[kNX] d_full[2] a_ready[2] slot_free[2], then the TMEM base
 constexpr int kBarXFull = 0, kBarXEmpty = kNX, kBarDFull = 2 * kNX, kBarAReady = 2 * kNX + 2,
               kBarSlotFree = 2 * kNX + 4, kBarRawFull = 2 * kNX + 6, kNumBars = 2 * kNX + 6 + kNR;
@@ -237,24 +238,6 @@ __device__ __forceinline__ void epi_hidden_tmem(uint32_t tmem_row, uint32_t src,
   }
 }
 
-// Hidden epilogue to shared memory: fp32 TMEM columns [src, src + 64) of this
-// lane's row -> ReLU -> 16-bit -> K columns [k0, k0 + 64) of the row in the
-// UMMA K-major layout (K = 128): eight 16-byte core-matrix rows.
-template <bool BF16>
-__device__ __forceinline__ void epi_hidden_smem64(uint32_t tmem_row, uint32_t src, uint32_t hbuf, uint32_t row,
-                                                  uint32_t k0) {
-  uint32_t v[64];
-  tc::tmem_ld32(tmem_row + src, *reinterpret_cast<uint32_t(*)[32]>(v));
-  tc::tmem_ld32(tmem_row + src + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-  tc::tmem_wait_ld();
-  uint32_t w[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) w[j] = tc::relu_x2<BF16>(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-#pragma unroll
-  for (int c = 0; c < 8; ++c)
-    tc::st_shared_v4(hbuf + op_off(row, k0 + 8 * c, 128), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-}
-
 // ---- producer: features of CTA tile j -> raw stage j % kNR (cp.async; each
 // thread copies, and later reads, only its own row: no barrier needed).
 // Raw stage layout: feature f of row r at byte f * kTile * 8 + r * 8 (int64 slots)
@@ -350,7 +333,7 @@ __device__ __forceinline__ void issue_slot(uint32_t sbase, uint32_t tmem, uint32
       }
     }
     tc::commit(bar(kBarDFull + s));
-    // layer 3: D3 = b3' (bias tiles), += H2 (shared memory) . W3'^T
+    // layer 3: D3 = b3' (bias tiles), += H2 (TMEM) . W3'^T
     ISSUER_WAIT(bar(kBarAReady + s), pa);
     pa ^= 1;
     tc::fence_after();
@@ -358,7 +341,7 @@ __device__ __forceinline__ void issue_slot(uint32_t sbase, uint32_t tmem, uint32
       tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffOnes, 128, 0), tc::smem_desc(sbase + kOffB3b, 0, 128), i64, 0);
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks)
-        tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
+        tc::mma_f16kind_ts(B + 192, B + 8 * ks,
                         tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64, 1);
     }
     tc::commit(bar(kBarDFull + s));
@@ -452,14 +435,14 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
                 if (!kNoMma)
                   tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
-            } else {  // D3 = b3' (bias tiles), += H2 (shared memory) . W3'^T
+            } else {  // D3 = b3' (bias tiles), += H2 (TMEM) . W3'^T
               if (!kNoMma)
                 tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffOnes, 128, 0), tc::smem_desc(sbase + kOffB3b, 0, 128),
                                 i64, 0);
 #pragma unroll
               for (int ks = 0; ks < 8; ++ks) {
                 if (!kNoMma)
-                  tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
+                  tc::mma_f16kind_ts(B + 192, B + 8 * ks,
                                   tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64, 1);
               }
             }
@@ -563,13 +546,14 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
-      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 (shared memory, K 64h..64h+63)
+      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 K 64h..64h+63
       EPI_WAIT(bar_d, pd);
       EPT(4);
       pd ^= 1;
       tc::fence_after();
-      epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
-      tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
+      // H2 packed into TMEM [32h, 32h + 32): H1's half-0 columns, retired with layer 2
+      epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
+      tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(5);
@@ -780,14 +764,14 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
                 if (!kNoMma)
                   tc::mma_f16kind_ts(B + 64, a, tc::smem_desc(sbase + kOffW2 + ks * 256, 128, 16 * 256), i128, 1);
               }
-            } else {  // D3 = b3' (bias tiles), += H2 (shared memory) . W3'^T
+            } else {  // D3 = b3' (bias tiles), += H2 (TMEM) . W3'^T
               if (!kNoMma)
                 tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffOnes, 128, 0), tc::smem_desc(sbase + kOffB3b, 0, 128),
                                 i64, 0);
 #pragma unroll
               for (int ks = 0; ks < 8; ++ks) {
                 if (!kNoMma)
-                  tc::mma_f16kind(B + 192, tc::smem_desc(sbase + kOffH2 + s * kH2Bytes + ks * 256, 128, 16 * 128),
+                  tc::mma_f16kind_ts(B + 192, B + 8 * ks,
                                   tc::smem_desc(sbase + kOffW3 + ks * 256, 128, 16 * 128), i64, 1);
               }
             }
@@ -974,13 +958,14 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(3);
-      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 (shared memory, K 64h..64h+63)
+      // layer 2: D2 columns 64h.. [64+64h, 128+64h) -> H2 K 64h..64h+63
       EPI_WAIT(bar_d, pd);
       EPT(4);
       pd ^= 1;
       tc::fence_after();
-      epi_hidden_smem64<BF16>(tmem_row, 64 + 64 * h, sbase + kOffH2 + s * kH2Bytes, row, 64 * h);
-      tc::fence_proxy_async();  // generic-proxy H2 writes -> visible to the tensor core
+      // H2 packed into TMEM [32h, 32h + 32): H1's half-0 columns, retired with layer 2
+      epi_hidden_tmem<64, BF16>(tmem_row, 64 + 64 * h, 32 * h);
+      tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(bar_a);
       EPT(5);
