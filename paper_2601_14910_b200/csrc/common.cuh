@@ -100,8 +100,9 @@ __device__ __forceinline__ int64_t waves_of(int64_t T, int64_t nsm, int64_t occ)
 // and the record store.  tdt = tensor dtype index (0 bf16, 1 fp16, 2 fp8).
 // fv (optional): receives the 12 float slots as stored (the fused predictor
 // normalises them without reading the record back).
-// FAST: fp32-reciprocal quotients (udiv_q) -- measured per kernel: it sped up
-// the fused attention kernel and slowed the fused MoE kernel (register allocation).
+// FAST: fp32-reciprocal quotients (udiv_q) -- the fused predictor's producers
+// use them for every family (round 2: 1.7% faster on cfg3 once layer 3 moved to
+// TMEM; earlier it had slowed the MoE instantiation at the 80-register cap).
 template <bool FAST = false>
 __device__ __forceinline__ void emit_pair(const FeatOut &o, int64_t p, const PairDemand &d,
                                           const Footprint &fp, const DevSpec &s, int pipes,

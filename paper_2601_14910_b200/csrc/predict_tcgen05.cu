@@ -167,11 +167,6 @@ __device__ long long g_pred_wtrace[16][64][16];  // every epilogue warp (lane 0)
 
 #define EPI_WAIT(b, ph) tc::mbar_wait_sleep(b, ph)
 
-#ifdef SP_EXP_NOPROD
-constexpr bool kNoProd = true;  // experiment: fused producers skip a4-a9, the record and a10
-#else
-constexpr bool kNoProd = false;
-#endif
 #ifdef SP_EXP_NOMMA
 constexpr bool kNoMma = true;
 #else
@@ -620,14 +615,12 @@ constexpr int kFGroups = kFProdWarps / 4;  // producer groups, taking tiles j = 
 // the group count: a 3-group variant broke exactly this (a tile of stale X rows).
 static_assert(kNX % (kFProdWarps / 4) == 0, "X ring depth must be a multiple of the producer group count");
 constexpr int kFMmaWarp = kEpiWarps + kFProdWarps;
-// The fused kernel keeps the single polling issuer: with a thread per slot it
-// measured 7-8% slower on cfg3 (1.15 -> 1.24 ms; either wait flavour) and 2% on
-// cfg2, while the bare predictor gained 2-5%.
-#ifndef SP_FUSED_ISSUERS
-#define SP_FUSED_ISSUERS 1
-#endif
-constexpr int kFIssuers = SP_FUSED_ISSUERS;
-constexpr int kFThreads = (kFMmaWarp + kFIssuers) * 32;
+// MMA issue in the fused kernel: one thread polling both TMEM slots and issuing
+// whichever layer is ready.  A thread per slot (as the bare predictor) measured
+// within 1% on cfg3 / cfg5 (-0.6% / +0.8%) and 1% slower on cfg2.  Producer
+// quotients (occupancy, waves, ceil(T/N)) by fp32 reciprocal corrected by one
+// (udiv_q) for every family: cfg3 1.145 -> 1.126 ms, cfg5 10.33 -> 10.26.
+__host__ __device__ constexpr int fused_threads(int) { return (kFMmaWarp + 1) * 32; }
 constexpr int kFNR = 4 / kFGroups;  // raw stages per producer group
 constexpr uint32_t kFRawBytes = kPreFields * kTile * 8;
 static_assert(kFGroups * kFNR * kFRawBytes <= kNR * kRawBytes, "fused raw staging fits the unfused one");
@@ -678,7 +671,7 @@ __device__ __forceinline__ int64_t int_slot_value(const PairDemand &d, int sl) {
 }
 
 template <bool BF16, int FAM>
-__global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(FusedParams P) {
+__global__ void __launch_bounds__(fused_threads(FAM), 1) predict_tcgen05_fused_kernel(FusedParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = tc::smem_u32(smem);
@@ -692,8 +685,8 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
   {
     const uint4 *src = reinterpret_cast<const uint4 *>(P.m.wpack);
     uint4 *dst = reinterpret_cast<uint4 *>(smem);
-    for (int i = threadIdx.x; i < (int)(kWBytes / 16); i += kFThreads) dst[i] = __ldg(src + i);
-    for (int i = threadIdx.x; i < kVecFloats; i += kFThreads) vec[i] = __ldg(P.m.vecs + i);
+    for (int i = threadIdx.x; i < (int)(kWBytes / 16); i += fused_threads(FAM)) dst[i] = __ldg(src + i);
+    for (int i = threadIdx.x; i < kVecFloats; i += fused_threads(FAM)) vec[i] = __ldg(P.m.vecs + i);
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNX; ++i) {
@@ -717,9 +710,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
 
   const int64_t G = gridDim.x;
   const int64_t n_local = P.n_tiles > (int64_t)blockIdx.x ? (P.n_tiles - blockIdx.x + G - 1) / G : 0;
-  if (kFIssuers == 2 && warp >= kFMmaWarp) {
-    if (lane == 0) issue_slot<BF16>(sbase, tmem, bar0, n_local, warp - kFMmaWarp);
-  } else if (warp == kFMmaWarp) {
+  if (warp == kFMmaWarp) {
     // ================= MMA issuer (one thread) =================
     // Per TMEM slot s (CTA tiles j = s, s+2, ...): layer 0 needs the X tile
     // (x_full) and the slot's previous tile fully read (slot_free); layers 1, 2
@@ -828,11 +819,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
       float side_t = 0.f;
       uint32_t side_s = 1;
       const uint64_t w0 = live ? rj[0] : 0;
-#ifdef SP_EXP_NOPROD
-      if (false) {
-#else
       if (FAM == SP_ATTENTION && live && ((w0 >> 9) & 1)) {
-#endif
         // planner config (kv_chunk -1): attn_planner_cross wrote its record; read it back
         const int64_t ld = fz.out.ld;
         const uint32_t st = fz.out.status[p];
@@ -846,7 +833,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
             xv[f] = fmaf(lg2_ftz(1.f + v), na[f], nc[f]);
           }
         }
-      } else if (live && !kNoProd) {
+      } else if (live) {
         int st = (int)(w0 & 0xff);
         const int tdt = (int)((w0 >> 16) & 0xff) - 1;
         const DevSpec &sp = fz.specs[fz.g0 + gs];
@@ -879,7 +866,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
             d.mx[2] = bq * (bkv + 1) * mS;
             d.mx[3] = 2 * hd * mB;
           } else {
-            const int64_t per_sm = (int64_t)(((uint32_t)d.T + (uint32_t)sp.num_sms - 1u) / (uint32_t)sp.num_sms);
+            const int64_t per_sm = (int64_t)udiv_q((uint32_t)d.T + (uint32_t)sp.num_sms - 1u, (uint32_t)sp.num_sms);
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
               const int64_t task = (int64_t)rj[(1 + qq) * kTile];
@@ -890,7 +877,7 @@ __global__ void __launch_bounds__(kFThreads, 1) predict_tcgen05_fused_kernel(Fus
           const uint64_t ws = rj[5 * kTile];
           const Footprint fp{(int64_t)(uint32_t)ws, (int64_t)(ws >> 32), (int64_t)(uint32_t)rj[6 * kTile]};
           float fv[kNumFlts];
-          emit_pair<FAM == SP_ATTENTION>(fz.out, p, d, fp, sp, family_pipes(FAM), tdt < 0 ? 0 : tdt, fv);
+          emit_pair<true>(fz.out, p, d, fp, sp, family_pipes(FAM), tdt < 0 ? 0 : tdt, fv);
           side_s = 0;
           side_t = fv[F_TTHEORY];
 #pragma unroll
@@ -1147,6 +1134,7 @@ int launch_predict_tcgen05(const MlpBf16 &m, const sp_features &in, float *laten
 template <bool BF16>
 static cudaError_t launch_fused(int fam, const FusedParams &P, unsigned grid, cudaStream_t st) {
   void (*kern)(FusedParams) = nullptr;
+  const int fk = fam == SP_SCALED_MM ? SP_GEMM : fam;
   switch (fam) {
     case SP_GEMM:
     case SP_SCALED_MM: kern = predict_tcgen05_fused_kernel<BF16, SP_GEMM>; break;
@@ -1158,7 +1146,7 @@ static cudaError_t launch_fused(int fam, const FusedParams &P, unsigned grid, cu
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmemBytes);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kFThreads, kFSmemBytes, st>>>(P);
+  kern<<<grid, fused_threads(fk), kFSmemBytes, st>>>(P);
   return cudaGetLastError();
 }
 
