@@ -810,12 +810,25 @@ __global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults re
         units((uint32_t)kv, su, mu);
         U += (uint64_t)nqb * su;
         um = max(um, mu);
-      } else {
-        for (uint32_t i = 0; i < nqb; ++i) {  // <= min_n tasks in all
-          units(kv_need(i, bq, rows, (uint32_t)q, (uint32_t)kv, true, dv.g), su, mu);
-          U += su;
-          um = max(um, mu);
+      } else {  // causal, unsplit (csplit is the warp's): q-block i has ceil(kv_need(i)/BKV) units
+        // <= min_n tasks in all.  32-bit forms (kv_need >= 1, so ceil(n/BKV) = (n-1)/BKV + 1
+        // with n - 1 < 2^31; (i+1) BQ < rows + BQ < 2^32); the last q-block needs the whole kv
+        // (q_last = q - 1), so it holds the request's largest unit.
+        const uint32_t qu = (uint32_t)q, kvu = (uint32_t)kv;
+        uint64_t usum = 0;
+        if (bq % g == 0 && bq < (1 << 30)) {
+          // kv_need(i) = kv - max(t_i, 0), t_i = q - (i+1) BQ/g (R10-R11, as the schedule kernel)
+          const int32_t a_per = bq / g;
+          int32_t t = (int32_t)qu - a_per;
+          for (uint32_t i = 0; i < nqb; ++i, t -= a_per) usum += dv.bkv.div31(kvu - 1u - (uint32_t)max(t, 0)) + 1u;
+        } else {
+          for (uint32_t i = 0, e1 = (uint32_t)bq; i < nqb; ++i, e1 += (uint32_t)bq) {
+            const uint32_t q_last = dv.g.div31(min(e1, rows) - 1u);
+            usum += dv.bkv.div31(min(kvu, kvu - qu + q_last + 1u) - 1u) + 1u;
+          }
         }
+        U += usum;
+        um = max(um, dv.bkv.div31(kvu - 1u) + 1u);
       }
     }
     if (!st) {
