@@ -321,9 +321,12 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
     return warp_sum_u64(us);
   }
   const FastDiv &fbq = dv.bq;
-  // causal without split-KV and g | BQ: kv_need is affine in the q-block index
+  // causal without split-KV and g | BQ: kv_need is affine in the q-block index, and
+  // when BKV divides 32 BQ/g the units of q-blocks 32 apart differ by a constant
   const uint32_t a_per = (uint32_t)(a.bq / a.g);
-  const bool lin = !split && a.causal && a.bq % a.g == 0 && (int64_t)a.bq * 33 < (1ll << 30);
+  const bool lin = !split && a.causal && a.bq % a.g == 0 && (int64_t)a.bq * 33 < (1ll << 30) &&
+                   (32u * a_per) % (uint32_t)a.bkv == 0;
+  const uint32_t dlt = lin ? (32u * a_per) / (uint32_t)a.bkv : 0u;
   const FastDiv &fchunk = dv.chunk;
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc);  // shared-window byte address
   const uint32_t lm_le = lanemask_le();
@@ -438,23 +441,23 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       const uint32_t nxt = bcur + 1 < nreq ? s_start[bcur + 1] : total;
       if (k0 + 32 <= nxt) {
         const uint32_t r1 = s_a1[bcur], r2 = s_a2[bcur], r3 = s_a3[bcur], ruf = s_uf[bcur], rul = s_ul[bcur];
-        if (lin && r2 < (1u << 30)) {
-          // causal, g | BQ: kv_need(kl) = min(kv, kv - q + (kl+1)*BQ/g) = kv - max(t, 0) with
-          // t = q - (kl+1)*BQ/g stepping by -32*BQ/g (R10-R11; exact for the last q-block too,
-          // where the min takes kv).  q < 2^30 and 33*BQ < 2^30 keep t in int32.
-          int32_t t = (int32_t)r2 - (int32_t)(k0 + lane - st + 1u) * (int32_t)a_per;
+        if (lin && r3 < (1u << 30)) {
+          // causal, g | BQ: kv_need(kl) = min(kv, kv - q + (kl+1)*BQ/g) (R10-R11; exact for the
+          // last q-block too, where the min takes kv), so u(kl) = min(v(kl), ceil(kv/BKV)) with
+          // v(kl) = ceil((kv - q + (kl+1)*BQ/g) / BKV); BKV | 32*BQ/g makes v(kl + 32) = v(kl) + dlt
+          // exactly: a lane's next unit is an add and a min.  kv < 2^30 and (kl+1)*BQ/g <= q + BQ/g
+          // keep every operand below 2^31.
+          const uint32_t ucap = fbkv.div31(r3 - 1u) + 1u;
+          uint32_t v = fbkv.div31(r3 - r2 + (k0 + lane - st + 1u) * a_per - 1u) + 1u;  // argument >= kv - q + a_per - 1 >= 0
           for (; k0 + 64 <= nxt; k0 += 64) {
-            const uint32_t need0 = r3 - (uint32_t)max(t, 0);  // >= kv - q + 1 >= 1
-            add(k0 + lane, fbkv.div31(need0 - 1u) + 1u, true);
-            t -= 32 * (int32_t)a_per;
-            const uint32_t need1 = r3 - (uint32_t)max(t, 0);
-            add(k0 + 32 + lane, fbkv.div31(need1 - 1u) + 1u, true);
-            t -= 32 * (int32_t)a_per;
+            add(k0 + lane, min(v, ucap), true);
+            v += dlt;
+            add(k0 + 32 + lane, min(v, ucap), true);
+            v += dlt;
             wrap();
           }
           if (k0 + 32 <= nxt) {
-            const uint32_t need = r3 - (uint32_t)max(t, 0);
-            add(k0 + lane, fbkv.div31(need - 1u) + 1u, true);
+            add(k0 + lane, min(v, ucap), true);
             wrap();
             k0 += 32;
           }
