@@ -103,7 +103,7 @@ extern "C" sp_status sp_create(int device, sp_ctx **out) {
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
   cudaSetDevice(device);
-  e = cudaMalloc(&c->counters, kAttnMaxGroups * sizeof(int));
+  e = cudaMalloc(&c->counters, kAttnCounterInts * sizeof(int));
   if (e != cudaSuccess) {
     c->counters = nullptr;
     delete c;
@@ -310,7 +310,7 @@ static sp_status grow_buf(sp_ctx *ctx, void *&p, size_t &bytes, size_t need, con
 static sp_status grow_attn_res(sp_ctx *ctx, int64_t C, int n_slots) {
   const int64_t ld = (C + 31) & ~(int64_t)31;
   return grow_buf(ctx, ctx->attn_res, ctx->attn_res_bytes,
-                  (size_t)ld * (4 + 8 + 8 + 16 * (size_t)n_slots + 4 * (size_t)kAttnPreWords),
+                  (size_t)ld * (4 + 8 + 8 + 16 * (size_t)n_slots + 4 * (size_t)kAttnPreWords + 4),
                   "attention result scratch");
 }
 static sp_status grow_pre(sp_ctx *ctx, int64_t C) {
@@ -366,6 +366,9 @@ static sp_status attn_cross(sp_ctx *ctx, sp_specs *specs, const sp_pairing *pair
   res.mB = res.mS + (size_t)run.n_slots * ld;
   res.st = (int32_t *)(res.mB + (size_t)run.n_slots * ld);
   res.pre = (uint32_t *)(res.st + ld);
+  res.order = (int32_t *)(res.pre + (size_t)kAttnPreWords * ld);
+  res.chunk_b = (int8_t *)(res.order + ld / 32);
+  res.hist = ctx->counters + run.n_groups;
   const int e = launch_featurize_attention(cv, (const DevSpec *)specs->dev.p, pairs->spec_begin, pairs->spec_end,
                                            specs->n, run, res, n_pairs, nullptr, nullptr, specs->max_sms, fo,
                                            ctx->num_sms, stream, ctx->hook(), emit);

@@ -747,9 +747,11 @@ static_assert(kAttnScratchWords >= kFoldDupMax + 32, "fold duplicate overruns th
 // per q-block) leave L to the warp.
 enum : uint32_t { kPreWarp = 1u, kPreWarpCounts = 2u };
 
-__global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults res, int32_t min_n, int32_t n_slots) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= v.n_configs) return;
+// Returns the config's cost for attn_order (its task count, clamped at 2^26), -1 if the
+// warps have nothing to do for it.
+__device__ __forceinline__ int attn_prepass_config(const ConfigView &v, const AttnResults &res, int32_t min_n,
+                                                   int32_t n_slots, int64_t c) {
+  if (c >= v.n_configs) return -1;
   int32_t f[12];
 #pragma unroll
   for (int k = 0; k < 12; ++k) f[k] = __ldg(v.fields + (int64_t)k * v.ld + c);
@@ -874,6 +876,49 @@ __global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults re
     pr[8 * ld] = dv.chunk.m;
     pr[9 * ld] = dv.chunk.s;
   }
+  // cost estimate for attn_order: the task count, clamped (a chunk's sum stays below 2^31);
+  // causal split-KV configs (L counted by the warp) count as the largest
+  return !flags ? -1 : (flags & kPreWarpCounts) ? (1 << 26) : (int)min(L * (int64_t)nkv, (int64_t)1 << 26);
+}
+
+__global__ void __launch_bounds__(256) attn_prepass(ConfigView v, AttnResults res, int32_t min_n, int32_t n_slots) {
+  __shared__ int s_hist[kAttnCostBuckets];
+  if (threadIdx.x < kAttnCostBuckets) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = attn_prepass_config(v, res, min_n, n_slots, c);
+  // a chunk of 32 configs (this warp's) costs the sum of its configs' tasks: class floor(log2 sum)
+  const uint32_t sum = __reduce_add_sync(0xffffffffu, (uint32_t)max(t, 0));
+  const bool any = __any_sync(0xffffffffu, t >= 0);
+  const int cb = any ? 31 - __clz((int)max(sum, 1u)) : -1;
+  if ((threadIdx.x & 31) == 0 && c < v.n_configs) {
+    res.chunk_b[c >> 5] = (int8_t)cb;
+    if (cb >= 0) atomicAdd(s_hist + cb, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < kAttnCostBuckets && s_hist[threadIdx.x]) atomicAdd(res.hist + threadIdx.x, s_hist[threadIdx.x]);
+}
+
+// The chunks of 32 configs with warp work, heaviest cost class first (res.order;
+// see kAttnCostBuckets).  Thread per chunk: its class (attn_prepass), a
+// block-local slot by a shared atomic, a per-(block, class) range from the
+// global cursors.
+__global__ void __launch_bounds__(256) attn_order(AttnResults res, int64_t n_chunks) {
+  __shared__ int s_cnt[kAttnCostBuckets], s_base[kAttnCostBuckets];
+  if (threadIdx.x < kAttnCostBuckets) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = k < n_chunks ? (int)res.chunk_b[k] : -1;
+  const int slot = b >= 0 ? atomicAdd(&s_cnt[b], 1) : 0;
+  __syncthreads();
+  if (threadIdx.x < kAttnCostBuckets) {
+    const int bb = threadIdx.x;
+    int start = 0;  // chunks of the heavier classes
+    for (int x = kAttnCostBuckets - 1; x > bb; --x) start += res.hist[x];
+    s_base[bb] = s_cnt[bb] ? start + atomicAdd(res.hist + kAttnCostBuckets + bb, s_cnt[bb]) : 0;
+  }
+  __syncthreads();
+  if (b >= 0) res.order[s_base[b] + slot] = (int32_t)k;
 }
 
 // A flagged config for the warp: its fields (lanes 0..11, one load each) and the
@@ -933,16 +978,17 @@ __global__ void __launch_bounds__(kWarps * 32, SP_ATTN_MINB) attn_schedule_cross
   // warp region: [accumulators: words_per_warp - kAttnScratchWords][request scratch]
   uint32_t *acc = smem + (size_t)warp * plan.words_per_warp;
   uint32_t *scr = acc + (plan.words_per_warp - kAttnScratchWords);
-  const int64_t C = cfg.n_configs;
-  const int64_t n_chunks = (C + 31) / 32;
   int *counter = plan.counters + blockIdx.y;
   int64_t *mS = res.mS + (int64_t)grp.distinct_first * res.ld, *mB = res.mB + (int64_t)grp.distinct_first * res.ld;
+  // chunks of 32 configs with work for the warps, heaviest cost class first (attn_order)
+  const int64_t F = __reduce_add_sync(0xffffffffu, lane < kAttnCostBuckets ? (uint32_t)__ldg(res.hist + lane) : 0u);
+  const int64_t C = cfg.n_configs;
   for (;;) {
-    int64_t chunk = 0;
-    if (lane == 0) chunk = atomicAdd(counter, 1);
-    chunk = __shfl_sync(0xffffffffu, chunk, 0);
-    if (chunk >= n_chunks) break;
-    const int64_t c0 = chunk * 32;
+    int64_t item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= F) break;
+    const int64_t c0 = (int64_t)__ldg(res.order + item) * 32;
     // configs the pre-pass left to the warps (invalid and sparse ones are done)
     const bool mine = c0 + lane < C && (__ldg(res.pre + c0 + lane) & kPreWarp);
     uint32_t todo = __ballot_sync(0xffffffffu, mine);
@@ -1505,10 +1551,17 @@ int launch_featurize_attention(const ConfigView &cfg, const DevSpec *specs, int 
   if (cfg_idx == nullptr) {
     if (cfg.n_configs == 0 || plan.n_groups == 0) return 0;
     // one launch per run of groups with the same (distinct count, small-N) shape
-    cudaError_t me = cudaMemsetAsync(plan.counters, 0, (size_t)plan.n_groups * sizeof(int), st);
+    // work counters, then the cost-bucket counts and cursors (contiguous: api.cu attn_cross)
+    cudaError_t me = cudaMemsetAsync(plan.counters, 0, (size_t)(plan.n_groups + 2 * kAttnCostBuckets) * sizeof(int), st);
     if (me != cudaSuccess) return (int)me;
     hook.on_begin("attn_prepass", st);
     attn_prepass<<<(unsigned)((cfg.n_configs + 255) / 256), 256, 0, st>>>(cfg, res, plan.min_n, plan.n_slots);
+    hook.on_end(st);
+    me = cudaGetLastError();
+    if (me != cudaSuccess) return (int)me;
+    hook.on_begin("attn_order", st);
+    const int64_t n_chunks = (cfg.n_configs + 31) / 32;
+    attn_order<<<(unsigned)((n_chunks + 255) / 256), 256, 0, st>>>(res, n_chunks);
     hook.on_end(st);
     me = cudaGetLastError();
     if (me != cudaSuccess) return (int)me;

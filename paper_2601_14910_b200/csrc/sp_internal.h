@@ -126,8 +126,20 @@ struct AttnResults {
   int64_t *mS, *mB;
   int64_t ld;
   uint32_t *pre;  // attn_prepass record [kAttnPreWords][ld]: flags, g, FastDiv (m, s) of g, BKV, BQ, chunk
+  int8_t *chunk_b;  // [ld / 32] cost class of each chunk of 32 configs: its heaviest config's floor(log2 T), -1 none
+  int32_t *order;   // [ld / 32] the chunks with warp work, heaviest class first (attn_order)
+  int *hist;        // DEVICE [2 kAttnCostBuckets]: chunks per class, then scatter cursors (zeroed per launch)
 };
 constexpr int kAttnPreWords = 10;
+// The schedule kernel takes its chunks of 32 configs heaviest cost class first:
+// per-config cost is heavy-tailed (cfg2: T up to ~2e5 tasks, mean ~2.4e3), and
+// in input order the last configs drawn by the warps leave a tail of a few busy
+// warps (cfg2 featurize measured 3.33 ms in the bench's shuffled order, 3.10 ms
+// with the configs grouped by floor(log2 T) descending on the host, 3.88 ms
+// lightest first).
+constexpr int kAttnCostBuckets = 32;
+// ctx->counters: [work counters: n_groups][bucket counts + cursors: 2 kAttnCostBuckets]
+constexpr int kAttnCounterInts = kAttnMaxGroups + 2 * kAttnCostBuckets;
 // Optional per-launch hook (kernel accounting, sp_set_profiling): begin/end
 // bracket one kernel launch on the launch stream.
 struct LaunchHook {
