@@ -89,8 +89,13 @@ __global__ void __launch_bounds__(256) e2e_expand_kernel(ExpandArgs a) {
     int32_t my_bs = 0;
     bool my_pf = false;
     int64_t my_roff = 0;
+    // entries of the trace's decode steps before step k: sum_b min(out_b - 1, k - 1), which
+    // grows by the decode batch of step k-1 (min(o-1, k) - min(o-1, k-1) = [o > k]); summed
+    // over the requests only at the warp's first step when that step is mid-trace
+    int64_t run_before = -1;
     for (int64_t s = s_first; s < s_last; ++s) {
       while (s >= t_end) {  // next trace (steps of a trace are contiguous; empty traces cannot occur)
+        run_before = -1;
         ++r;
         t_begin = t_end;
         t_end = __ldg(a.step_off + r + 1);
@@ -107,15 +112,19 @@ __global__ void __launch_bounds__(256) e2e_expand_kernel(ExpandArgs a) {
           *reinterpret_cast<int2 *>(a.attn_ragged + roff + 2 * b) = make_int2(q, q);
         }
         bs = (int32_t)nb;
+        run_before = 0;  // step 1: no decode entries before it
       } else {
         // entries before this step: nb (prefill) + sum_b min(out_b - 1, k - 1) (decode steps 1..k-1)
-        int64_t before = 0;
-        for (int64_t b = lane; b < nb; b += 32) {
-          const int32_t o = b < 32 ? out0 : (b < 64 ? out1 : __ldg(a.out_len + b0 + b));
-          before += min(o - 1, k - 1);
-        }
+        int64_t before = run_before;
+        if (before < 0) {
+          before = 0;
+          for (int64_t b = lane; b < nb; b += 32) {
+            const int32_t o = b < 32 ? out0 : (b < 64 ? out1 : __ldg(a.out_len + b0 + b));
+            before += min(o - 1, k - 1);
+          }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+          for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+        }
         roff += 2 * (nb + before);
         int32_t pos = 0;
         for (int64_t b = 0; b < nb; b += 32) {
@@ -132,6 +141,7 @@ __global__ void __launch_bounds__(256) e2e_expand_kernel(ExpandArgs a) {
           pos += __popc(m);
         }
         bs = pos;
+        run_before = before + pos;
       }
       if (lane == (int)(s - s_first)) {  // lane j keeps step s_first + j's fields for one coalesced store
         my_bs = bs;
