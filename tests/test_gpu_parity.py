@@ -225,6 +225,30 @@ def test_uniform_edge_cases(sp, ctx, orc):
     assert_feature_parity(g, o, "moe edges")
 
 
+def test_attention_records_independent_of_config_order(sp, ctx):
+    """The schedule kernel takes chunks of 32 configs heaviest cost class first
+    (attn_prepass + attn_order): a config's record must not depend on the order
+    or neighbours its chunk gives it.  Records of a batch, of the same batch
+    reversed and of it sorted by cost, compared bit for bit after undoing the
+    permutation (every integer, float and status slot)."""
+    b = gen.gen_attention(2000, 2000, 61, max_bs=8, qlen_max=6000, kvlen_max=9000)
+    sa = specs.paper_gpu_specs()
+    C = b.n_configs
+    _, (gi, gf, gs) = gpu_features(sp, ctx, b, sa)
+    rev = np.arange(C)[::-1].copy()
+    rows = b.ragged[0::2].astype(np.int64)
+    cost = np.bincount(np.repeat(np.arange(C), b.field("BS")), weights=rows, minlength=C)
+    for perm in (rev, np.argsort(-cost, kind="stable")):
+        _, (pi, pf, ps) = gpu_features(sp, ctx, b.subset(perm), sa)
+        inv = np.empty(C, np.int64)
+        inv[perm] = np.arange(C)
+        # pair p = g * C + c (CROSS, spec-major): undo the config permutation per spec
+        idx = (np.arange(len(sa))[:, None] * C + inv[None, :]).ravel()
+        assert np.array_equal(ps[idx], gs)
+        assert np.array_equal(pi[:, idx], gi)
+        assert np.array_equal(pf[:, idx].view(np.uint32), gf.view(np.uint32))
+
+
 def test_moe_histogram_edge_cases(sp, ctx, orc):
     """Fused-MoE histograms the warp pass reduces in 32-bit partials (R16, status 4
     = SP_PAIR_E_HIST): a negative count, counts whose exact sum is 2^32 + M topk
