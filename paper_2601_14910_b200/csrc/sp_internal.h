@@ -126,7 +126,7 @@ struct AttnResults {
   int64_t *mS, *mB;
   int64_t ld;
   uint32_t *pre;  // attn_prepass record [kAttnPreWords][ld]: flags, g, FastDiv (m, s) of g, BKV, BQ, chunk
-  int8_t *chunk_b;  // [ld / 32] cost class of each chunk of 32 configs: its heaviest config's floor(log2 T), -1 none
+  int8_t *chunk_b;  // [ld / 32] cost class of each chunk of 32 configs: floor(log2 of its task-count sum), -1 none
   int32_t *order;   // [ld / 32] the chunks with warp work, heaviest class first (attn_order)
   int *hist;        // DEVICE [2 kAttnCostBuckets]: chunks per class, then scatter cursors (zeroed per launch)
 };
