@@ -354,10 +354,12 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
       } else {  // non-causal split-KV: chunks of one q-block share kv_need = kvlen
         const uint32_t n_ch = fchunk.div(kv + (uint32_t)a.chunk - 1u);
         tasks = nqb * n_ch;
-        const FastDiv f = make_fd(n_ch);
         a1 = n_ch;
-        a2 = f.m;
-        a3 = f.s;
+        if (nqb > 1) {  // chunk index = task mod n_ch (make_fd: an fp64 division)
+          const FastDiv f = make_fd(n_ch);
+          a2 = f.m;
+          a3 = f.s;
+        }  // one q-block (decode): the chunk index is the task index; a2 = 0 marks it
         uf = fbkv.div(min((uint32_t)a.chunk, kv) + (uint32_t)a.bkv - 1u);
         ul = fbkv.div(kv - (n_ch - 1u) * (uint32_t)a.chunk + (uint32_t)a.bkv - 1u);
       }
@@ -392,8 +394,9 @@ __device__ uint64_t accumulate(const AttnCfg &a, uint32_t *acc, int words, uint3
         const uint32_t need = min(r3, r3 - r2 + fg.div(e) + 1u);
         return fbkv.div(need + (uint32_t)a.bkv - 1u);
       }
-      const FastDiv f{r1, r2, r3};  // chunk index kl mod n_ch: full chunks, then the last one
-      return f.mod(kl) == f.d - 1u ? rul : ruf;
+      // chunk index kl mod n_ch (kl itself for one q-block): full chunks, then the last one
+      const uint32_t ch = r2 ? FastDiv{r1, r2, r3}.mod(kl) : kl;
+      return ch == r1 - 1u ? rul : ruf;
     };
     // one step: lane task base + k0 + lane gets u (0 for idle lanes).  The
     // residue pointers wrap lazily: each region has kAttnSlack words past N, so
