@@ -601,9 +601,9 @@ __global__ void __launch_bounds__(kThreads, 1) predict_tcgen05_kernel(Params P) 
 // ---- fused feature + predictor kernel (sp_featurize_predict): the same MMA
 // issuer and epilogue, with 8 producer warps in two groups that take alternate
 // tiles and derive each pair's record from its config pre-pass and spec.
-// Layout: as the kernel above up to H2 (raw staging: 2 groups x kFNR stages of
-// kPreFields u64 per row = 42 KB of the 48 KB), then the producer -> epilogue side
-// ring (t_theory, status per row of kNS tiles) and the barriers.
+// Layout: as the kernel above up to the partial logits (raw staging: 2 groups x
+// kFNR stages of kPreFields u64 per row = 28 KB of the 32 KB), then the producer ->
+// epilogue side ring (t_theory, status per row of kNS tiles) and the barriers.
 #ifndef SP_FPROD_WARPS
 #define SP_FPROD_WARPS 8
 #endif
