@@ -442,7 +442,7 @@ sp_status sp_featurize_predict(sp_ctx *ctx, const sp_config_batch *cfg, const sp
  *                 three streams (H2D of slice i+1 and D2H of slice i-1 overlap
  *                 the kernels of slice i).  NULL weights: n_slices equal
  *                 slices (0: the default, 8; attention defaults to the
- *                 weights (1, 3, 3, 1)); otherwise n_slices relative weights.
+ *                 weights (1, 2, 3, 2)); otherwise n_slices relative weights.
  *                 A wide spec axis (>= 64 specs and >= 4 slices per spec)
  *                 is sliced by spec instead (configs uploaded once).
  *   stream:       the kernels run on it; the copies on two library streams

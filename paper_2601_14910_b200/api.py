@@ -663,7 +663,7 @@ class Context:
         featurize + predict / D2H inside the library -> fp32 latencies in
         spec-major order [spec][config] (a numpy view of `out`, pinned by
         default).  `chunks`: a slice count, or relative slice weights such as
-        (1, 3, 3, 1); None = the library default."""
+        (1, 2, 3, 2); None = the library default."""
         g0, g1 = spec_range if spec_range is not None else (0, len(specs))
         fam = int(batch.family)
 
