@@ -122,8 +122,8 @@ def test_featurize_odd_sm_counts(sp, ctx, orc, fam):
 
 
 def test_attention_edge_cases(sp, ctx, orc):
-    """qlen = 1, kvlen < BKV, nkv = nh, causal + split-KV, T < N, T multiple of N,
-    long single requests, domain errors."""
+    """qlen = 1, kvlen < BKV, nkv = nh, causal + split-KV, non-causal split-KV with one and
+    several q-blocks per request, T < N, T multiple of N, long single requests, domain errors."""
     cols = {k: [] for k in gen.FIELDS[gen.ATTENTION]}
     rag, off = [], []
 
@@ -143,6 +143,10 @@ def test_attention_edge_cases(sp, ctx, orc):
     add([(300, 5000), (2000, 2000)], KV_CHUNK=512)   # causal + split-KV (generic path)
     add([(77, 77)] * 5, KV_CHUNK=64, BQ=16)    # many small chunks
     add([(1, 20481)] * 16, NH=128, NKV=8, BQ=16, KV_CHUNK=2048, CAUSAL=0)  # decode, split
+    # non-causal split-KV with several q-blocks per request (chunk index = task mod n_ch, a
+    # FastDiv of n_ch = 5) next to one-q-block requests (chunk index = task index) in one config
+    add([(300, 5000), (40, 3000), (1, 700), (64, 1024)], NH=8, NKV=2, BQ=64, KV_CHUNK=1024, CAUSAL=0)
+    add([(1, 3000)] * 12 + [(33, 2500)], NH=8, NKV=2, BQ=16, KV_CHUNK=512, CAUSAL=0)
     add([(20097, 20481)], NH=32, NKV=8, BQ=128, BKV=32)   # long prefill
     add([(108 * 64, 108 * 64)], NH=1, NKV=1, CAUSAL=0)    # T = 108 q-blocks (multiple of N=108)
     add([(5, 9)], NH=6, NKV=4)                 # nh % nkv != 0 -> status 3
